@@ -1,0 +1,221 @@
+"""Python face of the CPU oracle (``usp_oracle.c``).
+
+TEST INFRASTRUCTURE ONLY -- only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this.
+It imports nothing from the CUDA product (``paper_2207_14222_b200``) and the
+product imports nothing from here.
+
+What it computes (PAPER.md = /root/reference/PAPER.md):
+
+* ``fftn`` / ``ifftn``             -- the DFT the method's F denotes (L171).
+* ``apply_Linv``                   -- (L+1)^-1 via Eq. 12 (L168-172).
+* ``canonical``                    -- §2.2 / §3.1 canonical form: smallest
+  enclosing circle of the medium values (L167) -> bias; scale c so that
+  max|V| = target_norm (L99, L167).
+* ``fixed_point``                  -- Algorithm 1 (L80-89), x-form, or the
+  Delta-form recurrence (L613) for the R-17 cross-check.
+
+Pins: see tests/test_oracle_*.py.  Parity status per function is listed in
+DESIGN.md ("Oracle and its pins"); every function here is pinned.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "usp_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C11 + OpenMP)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared", _SRC, "-o", _LIB, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        dp = ctypes.POINTER(ctypes.c_double)
+        lp = ctypes.POINTER(ctypes.c_long)
+        L.orc_fft1d.argtypes = [dp, ctypes.c_long, ctypes.c_int]
+        L.orc_fftn.argtypes = [dp, ctypes.c_int, lp, ctypes.c_int]
+        L.orc_apply_Linv.argtypes = [dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 4
+        L.orc_setup.argtypes = [dp, dp, ctypes.c_long] + [ctypes.c_double] * 4 + [dp, dp, dp]
+        L.orc_fixed_point.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double]
+                                      + [ctypes.c_double] * 4
+                                      + [ctypes.c_double, ctypes.c_double, ctypes.c_long, ctypes.c_int,
+                                         dp, dp, lp, dp])
+        L.orc_mec.argtypes = [dp, dp, ctypes.c_long, dp, dp, dp]
+        L.orc_num_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _dims(shape: Sequence[int]):
+    arr = (ctypes.c_long * len(shape))(*shape)
+    return arr
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=np.complex128)
+
+
+def num_threads() -> int:
+    return int(lib().orc_num_threads())
+
+
+# ------------------------------------------------------------------- DFT --
+def fft1d(a, inverse: bool = False) -> np.ndarray:
+    x = _c128(a).copy()
+    rc = lib().orc_fft1d(_dp(x.view(np.float64)), x.size, int(inverse))
+    if rc:
+        raise ValueError(f"orc_fft1d rc={rc}")
+    return x
+
+
+def fftn(a, inverse: bool = False) -> np.ndarray:
+    x = _c128(a).copy()
+    rc = lib().orc_fftn(_dp(x.view(np.float64)), x.ndim, _dims(x.shape), int(inverse))
+    if rc:
+        raise ValueError(f"orc_fftn rc={rc}")
+    return x
+
+
+def ifftn(a) -> np.ndarray:
+    return fftn(a, inverse=True)
+
+
+# ------------------------------------------------------------- operators --
+@dataclass
+class Split:
+    """Canonical-form parameters in the unified reading R-1."""
+
+    D: float
+    sigma: complex
+    c: complex
+    bias: complex          # centre of the smallest enclosing circle of the medium
+    radius: float
+
+
+def apply_Linv(u, h: Sequence[float], D: float, sigma: complex, c: complex) -> np.ndarray:
+    x = _c128(u).copy()
+    hh = np.ascontiguousarray(h, dtype=np.float64)
+    rc = lib().orc_apply_Linv(_dp(x.view(np.float64)), x.ndim, _dims(x.shape), _dp(hh), float(D),
+                              float(np.real(sigma)), float(np.imag(sigma)), float(np.real(c)),
+                              float(np.imag(c)))
+    if rc:
+        raise ValueError(f"orc_apply_Linv rc={rc}")
+    return x
+
+
+def setup(w, S, sigma: complex, c: complex):
+    """V, B, s of the canonical system."""
+    wc, Sc = _c128(w), _c128(S)
+    V = np.empty_like(wc)
+    B = np.empty_like(wc)
+    s = np.empty_like(wc)
+    lib().orc_setup(_dp(wc.view(np.float64)), _dp(Sc.view(np.float64)), wc.size,
+                    float(np.real(sigma)), float(np.imag(sigma)), float(np.real(c)), float(np.imag(c)),
+                    _dp(V.view(np.float64)), _dp(B.view(np.float64)), _dp(s.view(np.float64)))
+    return V, B, s
+
+
+def mec(points) -> Tuple[complex, float]:
+    """Smallest enclosing circle of complex points."""
+    p = np.asarray(points).ravel()
+    re = np.ascontiguousarray(np.real(p), dtype=np.float64)
+    im = np.ascontiguousarray(np.imag(p), dtype=np.float64)
+    cr, ci, r = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    rc = lib().orc_mec(_dp(re), _dp(im), re.size, ctypes.byref(cr), ctypes.byref(ci), ctypes.byref(r))
+    if rc:
+        raise ValueError(f"orc_mec rc={rc}")
+    return complex(cr.value, ci.value), float(r.value)
+
+
+def medium_to_w(kind: str, medium) -> np.ndarray:
+    """w(r) of the unified form: Helmholtz w = -k^2 (Eq. 8 times -1), diffusion w = mu_a."""
+    m = _c128(medium)
+    return -m if kind == "helmholtz" else m
+
+
+def canonical(kind: str, medium, target_norm: float = 0.95, D: float = 1.0) -> Split:
+    """Canonical form of §2.2 / §3.1.
+
+    Helmholtz: kbar^2 = centre of the smallest circle enclosing the k^2 values,
+    c_paper = -(1/(0.95 i)) r = i r / 0.95 (L167); in the unified form
+    sigma = -kbar^2, c = -c_paper.  Diffusion (§3.2 scalar, reading R-15):
+    mu0 = centre (mid-range) of mu_a, c = r / 0.95 (real, so A stays accretive).
+    """
+    centre, r = mec(_c128(medium))
+    if r == 0.0:
+        raise ValueError("homogeneous medium: smallest circle has radius 0; pass sigma, c explicitly")
+    if kind == "helmholtz":
+        c_paper = -(1.0 / (target_norm * 1j)) * r
+        return Split(D=D, sigma=-centre, c=-c_paper, bias=centre, radius=r)
+    if kind == "diffusion":
+        return Split(D=D, sigma=centre, c=complex(r / target_norm), bias=centre, radius=r)
+    raise ValueError(kind)
+
+
+@dataclass
+class Result:
+    x: np.ndarray
+    n_done: int
+    hist: np.ndarray
+    n0: float
+    rc: int
+
+
+def fixed_point(w, S, h: Sequence[float], D: float, sigma: complex, c: complex, alpha: float,
+                tol: float, n_max: int, form: str = "x") -> Result:
+    """Algorithm 1; ``form='delta'`` runs the Neumann
+    recurrence of L613 instead (same iterates in exact arithmetic)."""
+    wc, Sc = _c128(w), _c128(S)
+    if wc.shape != Sc.shape:
+        raise ValueError("w and S shapes differ")
+    x = np.zeros_like(wc)
+    hist = np.zeros(n_max, dtype=np.float64)
+    hh = np.ascontiguousarray(h, dtype=np.float64)
+    nd = ctypes.c_long(0)
+    n0 = ctypes.c_double(0.0)
+    rc = lib().orc_fixed_point(_dp(wc.view(np.float64)), _dp(Sc.view(np.float64)), wc.ndim,
+                               _dims(wc.shape), _dp(hh), float(D), float(np.real(sigma)),
+                               float(np.imag(sigma)), float(np.real(c)), float(np.imag(c)),
+                               float(alpha), float(tol), int(n_max), 0 if form == "x" else 1,
+                               _dp(x.view(np.float64)), _dp(hist), ctypes.byref(nd), ctypes.byref(n0))
+    if rc < 0:
+        raise ValueError(f"orc_fixed_point rc={rc}")
+    return Result(x=x, n_done=int(nd.value), hist=hist[: nd.value].copy(), n0=float(n0.value), rc=rc)
+
+
+def solve_problem(p, target_norm: float = 0.95, form: str = "x", n_iter: Optional[int] = None,
+                  tol: Optional[float] = None, alpha: Optional[float] = None, split: Optional[Split] = None,
+                  medium=None):
+    """Convenience: canonical form + Algorithm 1 for a ``synth`` Problem.
+    ``medium`` may override p.medium (e.g. the complex64-rounded values the
+    GPU receives, so both sides see identical inputs)."""
+    med = p.medium if medium is None else medium
+    med = np.asarray(med)
+    sp = split if split is not None else canonical(p.kind, med, target_norm, D=p.D)
+    w = medium_to_w(p.kind, med)
+    res = fixed_point(w, np.asarray(p.source), p.h, sp.D, sp.sigma, sp.c,
+                      p.alpha if alpha is None else alpha,
+                      p.tol if tol is None else tol,
+                      p.n_iter if n_iter is None else n_iter, form=form)
+    return sp, res

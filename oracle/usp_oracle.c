@@ -1,0 +1,371 @@
+/*
+ * usp_oracle.c -- plain, slow, obviously-correct CPU oracle for the hot path
+ * of the universal split preconditioner (Vettenburg & Vellekoop,
+ * arXiv 2207.14222, /root/reference/PAPER.md).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant with the CUDA product in
+ * paper_2207_14222_b200/ and includes nothing from it.
+ *
+ * Precision: complex128 / float64 throughout (the paper fixes no precision
+ * for the method; its own runs were fp32).
+ *
+ * Unified form (reading R-1):
+ *     A_raw = -D lap + w(r),   L_raw = -D lap + sigma,   V_raw = w - sigma
+ *     A = A_raw / c,  L = L_raw / c,  V = V_raw / c,  s = S_raw / c
+ * (§2.2 "divide the original problem by a complex scalar c").
+ * Helmholtz (Eq. 8) is D = 1, w = -k^2, sigma = -kbar^2,
+ * c = -i r / 0.95 (the paper's c = i r/0.95 with the equation times -1).
+ *
+ * Functions (each cites the passage it follows):
+ *   orc_fft1d     radix-2 DFT, forward e^{-2 pi i jk/N} unnormalised,
+ *                 inverse e^{+...} with 1/N (reading R-8).
+ *   orc_fftn      n-D DFT = 1-D DFT along every axis (PAPER.md L171:
+ *                 "the Fourier transform over all spatial dimensions").
+ *   orc_apply_Linv  (L+1)^-1 = F^-1 c/(D|p|^2 + sigma + c) F   (Eq. 12,
+ *                 PAPER.md L168-172; p = 2 pi fftfreq(N, h), reading R-7).
+ *   orc_setup     V = (w - sigma)/c, B = 1 - V, s = S/c.
+ *   orc_fixed_point  Algorithm 1 literally (x-form), or
+ *                 the Neumann recurrence Delta_i = (1 - Gamma^-1 A) Delta_{i-1}
+ *                 (the Delta-form) for the R-17 cross-check.
+ *   orc_mec       smallest enclosing circle ("smallest circle
+ *                 problem"), Welzl's randomised incremental algorithm.
+ *
+ * Error behaviour: every entry point returns 0 on success, a negative code on
+ * bad arguments (-1 non-power-of-two extent, -2 bad ndim/size, -3 alloc).
+ */
+#include <complex.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef double complex cplx;
+
+static const double ORC_PI = 3.14159265358979323846264338327950288;
+
+static int is_pow2(long n) { return n >= 1 && (n & (n - 1)) == 0; }
+
+/* ---------------------------------------------------------------- FFT -- */
+
+/* In-place iterative radix-2 decimation-in-time DFT of length n (power of 2).
+ * tw[k] = exp(-2 pi i k / n), k < n/2 (forward); the inverse conjugates and
+ * divides by n at the end.  Textbook Cooley-Tukey: bit-reverse, then log2 n
+ * butterfly sweeps. */
+static void fft1d_with_table(cplx *a, long n, const cplx *tw, int inverse) {
+    if (n <= 1) return;
+    for (long i = 1, j = 0; i < n; ++i) {           /* bit reversal */
+        long bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) { cplx t = a[i]; a[i] = a[j]; a[j] = t; }
+    }
+    for (long len = 2; len <= n; len <<= 1) {
+        long half = len >> 1, step = n / len;
+        for (long i = 0; i < n; i += len) {
+            for (long j = 0; j < half; ++j) {
+                cplx w = tw[j * step];
+                if (inverse) w = conj(w);
+                cplx u = a[i + j];
+                cplx v = a[i + j + half] * w;
+                a[i + j] = u + v;
+                a[i + j + half] = u - v;
+            }
+        }
+    }
+    if (inverse) {
+        double inv = 1.0 / (double)n;
+        for (long i = 0; i < n; ++i) a[i] *= inv;
+    }
+}
+
+static cplx *make_twiddles(long n) {
+    long m = n / 2 > 0 ? n / 2 : 1;
+    cplx *tw = (cplx *)malloc(sizeof(cplx) * (size_t)m);
+    if (!tw) return NULL;
+    for (long k = 0; k < m; ++k) {
+        double ang = -2.0 * ORC_PI * (double)k / (double)n;
+        tw[k] = cos(ang) + I * sin(ang);
+    }
+    return tw;
+}
+
+int orc_fft1d(double *data, long n, int inverse) {
+    if (!is_pow2(n)) return -1;
+    cplx *tw = make_twiddles(n);
+    if (!tw) return -3;
+    fft1d_with_table((cplx *)data, n, tw, inverse);
+    free(tw);
+    return 0;
+}
+
+/* n-D DFT of a C-ordered array (dims[ndim-1] contiguous): a 1-D DFT along
+ * each axis in turn.  Lines are independent, so they are spread over OpenMP
+ * threads; each thread gathers a line into its own scratch buffer. */
+int orc_fftn(double *data, int ndim, const long *dims, int inverse) {
+    if (ndim < 1 || ndim > 3) return -2;
+    long total = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (!is_pow2(dims[a])) return -1;
+        total *= dims[a];
+    }
+    cplx *x = (cplx *)data;
+    for (int a = 0; a < ndim; ++a) {
+        long n = dims[a];
+        if (n == 1) continue;
+        long stride = 1;
+        for (int b = a + 1; b < ndim; ++b) stride *= dims[b];
+        long outer = total / (n * stride);
+        long nlines = outer * stride;
+        cplx *tw = make_twiddles(n);
+        if (!tw) return -3;
+        int err = 0;
+#pragma omp parallel
+        {
+            cplx *line = (cplx *)malloc(sizeof(cplx) * (size_t)n);
+            if (!line) {
+#pragma omp atomic write
+                err = 1;
+            } else {
+#pragma omp for schedule(static)
+                for (long l = 0; l < nlines; ++l) {
+                    long o = l / stride, i = l % stride;
+                    cplx *base = x + o * n * stride + i;
+                    for (long t = 0; t < n; ++t) line[t] = base[t * stride];
+                    fft1d_with_table(line, n, tw, inverse);
+                    for (long t = 0; t < n; ++t) base[t * stride] = line[t];
+                }
+                free(line);
+            }
+        }
+        free(tw);
+        if (err) return -3;
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------- (L + 1)^{-1} -- */
+
+/* Angular frequency p_a(m) = 2 pi fftfreq(n, h)[m] (reading R-7). */
+static double freq(long m, long n, double h) {
+    long mm = (m < (n + 1) / 2) ? m : m - n;   /* numpy.fft.fftfreq ordering */
+    if (n % 2 == 0 && m == n / 2) mm = -n / 2;
+    return 2.0 * ORC_PI * (double)mm / ((double)n * h);
+}
+
+/* g(p) = c / (D |p|^2 + sigma + c): the Fourier multiplier of (L+1)^-1 in the
+ * unified form; Eq. 12 L170 is the Helmholtz case
+ * c/(-|p|^2 + kbar^2 + c) with (D, sigma, c) -> (1, -kbar^2, -c). */
+static cplx g_of(double p2, double D, cplx sigma, cplx c) {
+    return c / (D * p2 + sigma + c);
+}
+
+/* u <- (L+1)^{-1} u = F^{-1} g F u   (Eq. 12). */
+int orc_apply_Linv(double *u, int ndim, const long *dims, const double *h, double D,
+                   double sig_re, double sig_im, double c_re, double c_im) {
+    int rc = orc_fftn(u, ndim, dims, 0);
+    if (rc) return rc;
+    cplx sigma = sig_re + I * sig_im, c = c_re + I * c_im;
+    long nx = dims[ndim - 1];
+    long ny = ndim >= 2 ? dims[ndim - 2] : 1;
+    long nz = ndim >= 3 ? dims[ndim - 3] : 1;
+    double hx = h[ndim - 1];
+    double hy = ndim >= 2 ? h[ndim - 2] : 1.0;
+    double hz = ndim >= 3 ? h[ndim - 3] : 1.0;
+    cplx *x = (cplx *)u;
+#pragma omp parallel for schedule(static)
+    for (long l = 0; l < nz; ++l) {
+        double pz = ndim >= 3 ? freq(l, nz, hz) : 0.0;
+        for (long j = 0; j < ny; ++j) {
+            double py = ndim >= 2 ? freq(j, ny, hy) : 0.0;
+            for (long i = 0; i < nx; ++i) {
+                double px = freq(i, nx, hx);
+                double p2 = px * px + py * py + pz * pz;
+                x[(l * ny + j) * nx + i] *= g_of(p2, D, sigma, c);
+            }
+        }
+    }
+    return orc_fftn(u, ndim, dims, 1);
+}
+
+/* ----------------------------------------------------------- splitting -- */
+
+/* V = (w - sigma)/c, B = 1 - V, s = S/c   ("B := 1 - V",
+ * L92-97 "A := c^-1 A_raw ... b := c^-1 b_raw", V := A - L). */
+int orc_setup(const double *w, const double *S, long n, double sig_re, double sig_im,
+              double c_re, double c_im, double *V_out, double *B_out, double *s_out) {
+    cplx sigma = sig_re + I * sig_im, c = c_re + I * c_im;
+    const cplx *wc = (const cplx *)w, *Sc = (const cplx *)S;
+    for (long i = 0; i < n; ++i) {
+        cplx V = (wc[i] - sigma) / c;
+        if (V_out) ((cplx *)V_out)[i] = V;
+        if (B_out) ((cplx *)B_out)[i] = 1.0 - V;
+        if (s_out) ((cplx *)s_out)[i] = Sc[i] / c;
+    }
+    return 0;
+}
+
+/* Plain l2 norm in a fixed sequential order (reading R-21). */
+static double norm2(const cplx *a, long n) {
+    double acc = 0.0;
+    for (long i = 0; i < n; ++i) acc += creal(a[i]) * creal(a[i]) + cimag(a[i]) * cimag(a[i]);
+    return sqrt(acc);
+}
+
+/* ---------------------------------------------------------- Algorithm 1 -- */
+/*
+ * form = 0 (x-form): Algorithm 1 literally:
+ *     x <- 0
+ *     repeat
+ *        Delta <- B[(L+1)^-1 (B x + s) - x]            (line 3, "residual")
+ *        x <- x + alpha Delta                           (line 4, "update")
+ *     until ||Delta|| / ||Gamma^-1 s|| < eps            (line 5)
+ *   with ||Gamma^-1 s|| read alpha-free as ||B (L+1)^-1 s|| (reading R-4).
+ * form = 1 (Delta-form): Delta_0 = B (L+1)^-1 s and
+ *     Delta_{k+1} = Delta_k + alpha B[(L+1)^-1 (B Delta_k) - Delta_k]
+ *   i.e. Delta_{k+1} = (1 - Gamma^-1 A) Delta_k, same x_k.
+ * Stop (reading R-5): after the update of iteration k (0-based) test
+ * r_k = ||Delta_k|| / n0; return x_{k+1}, n_done = k + 1.  tol <= 0 runs
+ * exactly n_max iterations.  hist[k] = r_k (if hist != NULL).
+ * Returns 0 (converged or ran n_max), 1 if the residual became non-finite,
+ * negative on argument errors.
+ */
+int orc_fixed_point(const double *w, const double *S, int ndim, const long *dims,
+                    const double *h, double D, double sig_re, double sig_im, double c_re,
+                    double c_im, double alpha, double tol, long n_max, int form,
+                    double *x_out, double *hist, long *n_done, double *n0_out) {
+    if (ndim < 1 || ndim > 3 || n_max < 1) return -2;
+    long n = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (!is_pow2(dims[a])) return -1;
+        n *= dims[a];
+    }
+    size_t bytes = sizeof(cplx) * (size_t)n;
+    cplx *B = (cplx *)malloc(bytes), *s = (cplx *)malloc(bytes);
+    cplx *u = (cplx *)malloc(bytes), *Dl = (cplx *)malloc(bytes);
+    cplx *x = (cplx *)x_out;
+    if (!B || !s || !u || !Dl) { free(B); free(s); free(u); free(Dl); return -3; }
+    orc_setup(w, S, n, sig_re, sig_im, c_re, c_im, NULL, (double *)B, (double *)s);
+
+    /* n0 = ||B (L+1)^-1 s|| */
+    memcpy(u, s, bytes);
+    int rc = orc_apply_Linv((double *)u, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+    if (rc) goto done;
+    for (long i = 0; i < n; ++i) Dl[i] = B[i] * u[i];
+    double n0 = norm2(Dl, n);
+    if (n0_out) *n0_out = n0;
+    for (long i = 0; i < n; ++i) x[i] = 0.0;
+    *n_done = 0;
+    if (n0 == 0.0) goto done;   /* zero source: x = 0 is exact */
+
+    for (long k = 0; k < n_max; ++k) {
+        if (form == 0) {
+            for (long i = 0; i < n; ++i) u[i] = B[i] * x[i] + s[i];
+            rc = orc_apply_Linv((double *)u, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+            if (rc) goto done;
+            for (long i = 0; i < n; ++i) Dl[i] = B[i] * (u[i] - x[i]);
+            for (long i = 0; i < n; ++i) x[i] = x[i] + alpha * Dl[i];
+        } else {
+            /* Dl holds Delta_k here */
+            for (long i = 0; i < n; ++i) x[i] = x[i] + alpha * Dl[i];
+        }
+        double r = norm2(Dl, n) / n0;
+        if (hist) hist[k] = r;
+        *n_done = k + 1;
+        if (!isfinite(r)) { rc = 1; goto done; }
+        if (tol > 0.0 && r < tol) break;
+        if (form == 1 && k + 1 < n_max) {
+            for (long i = 0; i < n; ++i) u[i] = B[i] * Dl[i];
+            rc = orc_apply_Linv((double *)u, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+            if (rc) goto done;
+            for (long i = 0; i < n; ++i) Dl[i] = Dl[i] + alpha * B[i] * (u[i] - Dl[i]);
+        }
+    }
+done:
+    free(B); free(s); free(u); free(Dl);
+    return rc;
+}
+
+/* ---------------------------------------- smallest enclosing circle -- */
+
+typedef struct { double x, y; } pt;
+
+static double dist(pt a, pt b) { return hypot(a.x - b.x, a.y - b.y); }
+
+static int inside(pt p, pt c, double r) {
+    double scale = fabs(c.x) + fabs(c.y) + r + 1e-300;
+    return dist(p, c) <= r + 1e-14 * scale;
+}
+
+static void circle2(pt a, pt b, pt *c, double *r) {
+    c->x = 0.5 * (a.x + b.x);
+    c->y = 0.5 * (a.y + b.y);
+    *r = 0.5 * dist(a, b);
+}
+
+/* Circumcircle of a, b, c; collinear triples fall back to the diameter of
+ * the farthest pair (the only enclosing circle through two of them). */
+static void circle3(pt a, pt b, pt c, pt *o, double *r) {
+    double bx = b.x - a.x, by = b.y - a.y, cx = c.x - a.x, cy = c.y - a.y;
+    double d = 2.0 * (bx * cy - by * cx);
+    double scale = (fabs(bx) + fabs(by)) * (fabs(cx) + fabs(cy));
+    if (fabs(d) <= 1e-14 * scale || d == 0.0) {
+        double dab = dist(a, b), dac = dist(a, c), dbc = dist(b, c);
+        if (dab >= dac && dab >= dbc) circle2(a, b, o, r);
+        else if (dac >= dbc) circle2(a, c, o, r);
+        else circle2(b, c, o, r);
+        return;
+    }
+    double b2 = bx * bx + by * by, c2 = cx * cx + cy * cy;
+    double ux = (cy * b2 - by * c2) / d, uy = (bx * c2 - cx * b2) / d;
+    o->x = a.x + ux;
+    o->y = a.y + uy;
+    *r = hypot(ux, uy);
+}
+
+/* Welzl's randomised incremental smallest-enclosing-circle (the paper cites
+ * Megiddo [Megiddo83] for the same problem; the result is
+ * unique).  Points are shuffled with a fixed-seed LCG so the run is
+ * deterministic. */
+int orc_mec(const double *re, const double *im, long n, double *cre, double *cim, double *rad) {
+    if (n < 1) return -2;
+    pt *p = (pt *)malloc(sizeof(pt) * (size_t)n);
+    if (!p) return -3;
+    for (long i = 0; i < n; ++i) { p[i].x = re[i]; p[i].y = im ? im[i] : 0.0; }
+    uint64_t st = 0x9E3779B97F4A7C15ull;
+    for (long i = n - 1; i > 0; --i) {
+        st = st * 6364136223846793005ull + 1442695040888963407ull;
+        long j = (long)((st >> 33) % (uint64_t)(i + 1));
+        pt t = p[i]; p[i] = p[j]; p[j] = t;
+    }
+    pt c = p[0];
+    double r = 0.0;
+    for (long i = 1; i < n; ++i) {
+        if (inside(p[i], c, r)) continue;
+        c = p[i]; r = 0.0;
+        for (long j = 0; j < i; ++j) {
+            if (inside(p[j], c, r)) continue;
+            circle2(p[i], p[j], &c, &r);
+            for (long k = 0; k < j; ++k) {
+                if (inside(p[k], c, r)) continue;
+                circle3(p[i], p[j], p[k], &c, &r);
+            }
+        }
+    }
+    *cre = c.x; *cim = c.y; *rad = r;
+    free(p);
+    return 0;
+}
+
+int orc_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
