@@ -1,0 +1,189 @@
+/*
+ * usp.h -- C-ABI of libusp: the B200 hot path of the universal split
+ * preconditioner (Vettenburg & Vellekoop, arXiv 2207.14222; PAPER.md =
+ * /root/reference/PAPER.md, cited by line).
+ *
+ * The library runs the preconditioned fixed-point (Richardson) iteration of
+ * Algorithm 1 with the forward operator eliminated (Eq. 5,
+ * L73-77):
+ *
+ *     Delta_k = B [ (L+1)^-1 (B x_k + s) - x_k ],   x_{k+1} = x_k + alpha Delta_k,
+ *     stop when ||Delta_k|| / ||B (L+1)^-1 s|| < tol          (L87, reading R-4)
+ *
+ * with B = 1 - V (L73), (L+1)^-1 applied as a Fourier multiplier (Eq. 12,
+ * L168-172) by hand-written sm_100a FFT kernels (no cuFFT), in complex64.
+ * Internally the mathematically identical Delta-recurrence of L613 is used
+ * (reading R-17):  Delta_{k+1} = Delta_k + alpha B[(L+1)^-1(B Delta_k) - Delta_k].
+ *
+ * Problem form (reading R-1, §2.2):
+ *     A_raw = -D lap + w(r),   L_raw = -D lap + sigma,   V_raw = w - sigma,
+ *     A = A_raw / c,  L = L_raw / c,  V = V_raw / c,  s = S / c,
+ *     (L+1)^-1 = F^-1 [ c / (D |p|^2 + sigma + c) ] F,   p = 2 pi fftfreq(n, h).
+ * Helmholtz (Eq. 8, lap psi + k^2 psi = -S): the medium is
+ * k^2(r) and w = -k^2, sigma = -kbar^2, D = 1, c = -i r / target_norm (the
+ * paper's c = i r/0.95 for the equation multiplied by -1).  Steady diffusion
+ * (§3.2, scalar D, -D lap u + mu_a u = S): the medium is w = mu_a,
+ * sigma = mu0, c = r / target_norm.
+ *
+ * Layout: every field is C-ordered [z][y][x], x fastest; n[0] = nx, n[1] = ny,
+ * n[2] = nz (unused extents = 1).  Complex values are interleaved
+ * (re, im) float32 pairs ("complex64").  Extents must be powers of two in
+ * [16, 2048] (1-D: [16, 2048]; a 1-D grid is one line, solved by one CTA).
+ *
+ * Ownership: input pointers are borrowed for the duration of the call only
+ * (their contents are copied into the workspace or consumed).  The workspace
+ * is caller-owned device memory (e.g. a torch uint8 tensor), >= the size
+ * usp_plan_workspace_size reports, 256-byte aligned, and must outlive the
+ * plan.  The plan itself only allocates small tables and state (< 1 MiB).
+ * All device work is enqueued on desc.stream.  Calls are not thread-safe per
+ * plan; distinct plans are independent.
+ *
+ * Errors: every call returns a usp_status; nothing aborts, exits or throws
+ * across the ABI.  On error usp_last_error() returns a thread-local message.
+ */
+#ifndef USP_H
+#define USP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define USP_VERSION_MAJOR 0
+#define USP_VERSION_MINOR 1
+
+typedef struct usp_plan_s *usp_plan_t;
+
+typedef enum {
+    USP_OK = 0,
+    USP_ERR_ARG = 1,             /* bad argument (NULL, size, alignment, tol...)      */
+    USP_ERR_STATE = 2,           /* call out of order (e.g. iterate before source)    */
+    USP_ERR_NOT_CONTRACTIVE = 3, /* max |V| >= 1: Theorem 1 needs ||V|| < 1 (L58)      */
+    USP_ERR_NOT_ACCRETIVE = 4,   /* Re(w/c) < 0 somewhere or D Re(c) < 0 (Eq. 1)  */
+    USP_ERR_UNSUPPORTED = 5,     /* extent not a power of two in [16,2048], ...        */
+    USP_ERR_NOMEM = 6,           /* workspace too small / allocation failed            */
+    USP_ERR_CUDA = 7,            /* a CUDA runtime call failed                         */
+    USP_ERR_NCCL = 8,            /* an NCCL call failed                                */
+    USP_ERR_NONFINITE = 9        /* non-finite values in the medium or source          */
+} usp_status;
+
+typedef enum {
+    USP_CONVERGED = 0, /* r_k < tol: Algorithm 1's "until" fired (L87)                  */
+    USP_MAX_ITER = 1,  /* n_max iterations ran (always the outcome when tol <= 0)       */
+    USP_DIVERGED = 2   /* r_k non-finite or > 1e6 (cannot happen for valid input, Cor.1) */
+} usp_term;
+
+typedef enum {
+    USP_MEDIUM_K2 = 0, /* medium array holds k^2(r) (Helmholtz); w = -k^2               */
+    USP_MEDIUM_W = 1   /* medium array holds w(r) directly (diffusion: mu_a)              */
+} usp_medium;
+
+typedef enum {
+    USP_C64 = 0, /* medium / source / field arrays are complex64 (interleaved float32)    */
+    USP_R32 = 1  /* real float32 arrays (imaginary part 0); the field returned is real    */
+} usp_dtype;
+
+typedef enum { USP_DEVICE = 0, USP_HOST = 1 } usp_where;
+
+typedef struct { double re, im; } usp_c128;
+
+typedef struct {
+    int ndim;            /* 1, 2 or 3                                                     */
+    int64_t n[3];        /* extents, n[0] = x (fastest)                                   */
+    double h[3];         /* grid spacing per axis (p_a = 2 pi m / (n_a h_a))               */
+    usp_medium medium;   /* how set_potential interprets its array                        */
+    usp_dtype dtype;     /* element type of medium, source and field arrays               */
+    double D;            /* coefficient of -lap in A_raw and L_raw (> 0)                   */
+    usp_c128 sigma;      /* shift of L_raw (ignored when set_potential auto-scales)       */
+    usp_c128 c;          /* scale c (ignored when set_potential auto-scales)              */
+    void *stream;        /* cudaStream_t; NULL = legacy default stream                    */
+    void *nccl_comm;     /* reserved for the slab-decomposed multi-GPU path; must be NULL */
+} usp_plan_desc;
+
+/* Create a plan for the grid and problem described by *desc (copied).
+ * Errors: USP_ERR_ARG (NULL, ndim, D <= 0), USP_ERR_UNSUPPORTED (extent),
+ * USP_ERR_CUDA. */
+usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out);
+
+/* Bytes of device workspace the plan needs: 4 complex64 fields
+ * (x, Delta, B, work) = 32 bytes per voxel plus reduction scratch. */
+usp_status usp_plan_workspace_size(usp_plan_t plan, size_t *bytes);
+
+/* Attach caller-owned device memory (>= workspace_size bytes, 256-B aligned).
+ * Errors: USP_ERR_ARG (NULL, misaligned), USP_ERR_NOMEM (too small). */
+usp_status usp_plan_set_workspace(usp_plan_t plan, void *dev, size_t bytes);
+
+/* Local z-slab of this rank: z0 = 0, nz_local = nz on a single GPU. */
+usp_status usp_local_extent(usp_plan_t plan, int64_t *z0, int64_t *nz_local);
+
+/* Set the medium (k^2 or w, see desc.medium / desc.dtype; [z][y][x]) and form
+ * V = (w - sigma)/c and B = 1 - V on the device.
+ * where: whether `medium` is a host or a device pointer.
+ * target_norm > 0: canonical form (§2.2, §3.1): sigma, c are
+ *   derived from the smallest circle enclosing the medium values (centre =
+ *   bias, radius r), c = -i r/target_norm (K2) or r/target_norm (W), so that
+ *   max|V| = target_norm; they replace desc.sigma / desc.c.
+ * target_norm <= 0: use desc.sigma, desc.c as given.
+ * Validation (Theorem 1 hypotheses, L58; Eq. 1): USP_ERR_NOT_CONTRACTIVE if
+ * max|V| >= 1; USP_ERR_NOT_ACCRETIVE if Re(w/c) < -1e-6 |w/c| at some voxel
+ * or D Re(c) < 0; USP_ERR_NONFINITE on NaN/Inf.  Invalidates the source. */
+usp_status usp_set_potential(usp_plan_t plan, const void *medium, usp_where where,
+                             double target_norm);
+
+/* Read back the split in use: sigma, c, smallest-circle centre and radius of
+ * the medium values (0 if not auto-scaled), and max |V|. */
+usp_status usp_get_split(usp_plan_t plan, usp_c128 *sigma, usp_c128 *c, usp_c128 *centre,
+                         double *radius, double *max_abs_V);
+
+/* Set the physical source S ([z][y][x], desc.dtype) and reset the state:
+ * s = S/c, x_0 = 0, k = 0, Delta_0 = B (L+1)^-1 s, n0 = ||Delta_0|| (one FFT
+ * round trip).  Requires set_potential first (USP_ERR_STATE). */
+usp_status usp_set_source(usp_plan_t plan, const void *src, usp_where where);
+
+/* Run at most n_max iterations of Algorithm 1 from the current state
+ * (resumable; alpha may change between calls).  tol > 0: stop after the
+ * first iteration k (0-based, counted from the last set_source) whose
+ * r_k = ||Delta_k|| / n0 < tol; the returned field includes that update
+ * (reading R-5).  tol <= 0: exactly n_max iterations.  Returns after the
+ * termination decision (synchronises on the plan stream).
+ * n_done: iterations done by this call; term: why it stopped.
+ * Errors: USP_ERR_STATE (no source), USP_ERR_ARG (n_max < 0, alpha <= 0). */
+usp_status usp_iterate(usp_plan_t plan, int64_t n_max, double alpha, double tol,
+                       int64_t *n_done, usp_term *term);
+
+/* Current residual: rel = ||Delta_k|| / n0 of the last Delta the iteration
+ * used, abs_norm = n0 * rel, k = iterations since set_source. */
+usp_status usp_residual(usp_plan_t plan, double *rel, double *abs_norm, int64_t *k);
+
+/* Copy r_0 .. r_{n-1} (fp64) into host[0..cap); *n = number available
+ * (ring of the most recent 65536 iterations). */
+usp_status usp_residual_history(usp_plan_t plan, double *host, int64_t cap, int64_t *n);
+
+/* Copy the current iterate x_k into `out` ([z][y][x], desc.dtype). */
+usp_status usp_get_field(usp_plan_t plan, void *out, usp_where where);
+
+/* Kernel timing (CUDA events on the plan stream, per kernel class) for the
+ * roofline report.  enable != 0 starts accumulating; usp_profile_read copies
+ * up to cap entries of (name, total ms, launches) for the kernel classes. */
+usp_status usp_profile_enable(usp_plan_t plan, int enable);
+usp_status usp_profile_read(usp_plan_t plan, int cap, char (*names)[32], double *ms,
+                            int64_t *launches, int *n);
+
+/* Number of kernel launches the library issued since plan creation. */
+usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
+
+/* Release the plan (not the caller's workspace).  NULL is a no-op. */
+void usp_plan_destroy(usp_plan_t plan);
+
+/* Thread-local message describing the last error ("" if none). */
+const char *usp_last_error(void);
+
+/* "major.minor sm_100a" */
+const char *usp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* USP_H */

@@ -1,0 +1,94 @@
+"""ctypes loader for libusp.so (the in-tree C-ABI library, include/usp.h).
+
+There is no fallback: if the library is missing or fails to load, importing
+the package's solver API raises.  Every computation goes through libusp's
+CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libusp.so")
+
+USP_OK = 0
+STATUS_NAMES = {0: "USP_OK", 1: "USP_ERR_ARG", 2: "USP_ERR_STATE", 3: "USP_ERR_NOT_CONTRACTIVE",
+                4: "USP_ERR_NOT_ACCRETIVE", 5: "USP_ERR_UNSUPPORTED", 6: "USP_ERR_NOMEM",
+                7: "USP_ERR_CUDA", 8: "USP_ERR_NCCL", 9: "USP_ERR_NONFINITE"}
+TERM_NAMES = {0: "converged", 1: "max_iter", 2: "diverged"}
+MEDIUM_K2, MEDIUM_W = 0, 1
+C64, R32 = 0, 1
+DEVICE, HOST = 0, 1
+
+
+class c128(ctypes.Structure):
+    _fields_ = [("re", ctypes.c_double), ("im", ctypes.c_double)]
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_int64 * 3), ("h", ctypes.c_double * 3),
+                ("medium", ctypes.c_int), ("dtype", ctypes.c_int), ("D", ctypes.c_double),
+                ("sigma", c128), ("c", c128), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p)]
+
+
+class USPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+        super().__init__(f"{self.name}: {msg}")
+
+
+_lib = None
+
+# name -> (restype, argtypes) for every entry point of include/usp.h
+SIGNATURES = {
+    "usp_plan_create": (ctypes.c_int, [ctypes.POINTER(PlanDesc), ctypes.POINTER(ctypes.c_void_p)]),
+    "usp_plan_workspace_size": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
+    "usp_plan_set_workspace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
+    "usp_local_extent": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "usp_set_potential": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double]),
+    "usp_get_split": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(c128), ctypes.POINTER(c128),
+                                     ctypes.POINTER(c128), ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_double)]),
+    "usp_set_source": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "usp_iterate": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                   ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
+    "usp_residual": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double),
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)]),
+    "usp_residual_history": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
+                                            ctypes.POINTER(ctypes.c_int64)]),
+    "usp_get_field": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "usp_profile_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "usp_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                        ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
+                                        ctypes.POINTER(ctypes.c_int)]),
+    "usp_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
+    "usp_plan_destroy": (None, [ctypes.c_void_p]),
+    "usp_last_error": (ctypes.c_char_p, []),
+    "usp_version": (ctypes.c_char_p, []),
+}
+
+
+def load():
+    """Load libusp.so (building it first if it is absent).  Raises on failure."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        from .build import build
+
+        build()
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int):
+    if status != USP_OK:
+        msg = load().usp_last_error().decode(errors="replace")
+        raise USPError(status, msg)

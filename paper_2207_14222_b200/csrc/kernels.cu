@@ -1,0 +1,604 @@
+// kernels.cu -- sm_100a kernels of the universal-split-preconditioner hot path.
+//
+// One iteration of Algorithm 1 in the Delta-form of L613
+// (reading R-17) is a chain of FFT passes over the field:
+//
+//   3-D:  K_B  y forward            (strided, k_strided<S_FWD>)
+//         K_C  z forward, x g(p), z inverse  (k_strided<S_FWD_MUL_INV>)  Eq. 12
+//         K_D  y inverse            (k_strided<S_INV>)
+//         K_A  x inverse -> epilogue -> prologue -> x forward  (k_xpass<X_ITER>)
+//   2-D:  K_Y  y forward, x g, y inverse; K_A as above.
+//   1-D:  one CTA runs the whole solve (k_solve1d).
+//
+// K_A's epilogue is the update of Algorithm 1 lines 3-4 in Delta-form:
+//     y = (L+1)^-1 (B Delta_k)            (the chain that just completed)
+//     x_{k+1}     = x_k + alpha Delta_k                       (line 4)
+//     Delta_{k+1} = Delta_k + alpha B (y - Delta_k)           (L613)
+//     r_{k+1}     = ||Delta_{k+1}|| / n0                      (line 5, reading R-4)
+// and its prologue starts the next chain: u = B Delta_{k+1}, forward x-FFT.
+// The residual is reduced per CTA (fp32 per line -> fp64), and the last CTA
+// to finish sums the CTA partials in a fixed order (deterministic) and
+// updates the device-side IterState (stop flag, counter, history).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fft_core.cuh"
+#include "usp_internal.h"
+
+namespace usp {
+
+// ------------------------------------------------------------ helpers --
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-order CTA reduction of one double per thread; result valid in tid 0.
+template <int NT>
+__device__ __forceinline__ double block_sum_d(double v, double *sh) {
+    v = warp_sum_d(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) s += sh[i];
+    }
+    __syncthreads();
+    return s;
+}
+
+// Last-CTA-done reduction: every CTA contributes `mine` (valid in tid 0);
+// returns true in the last CTA, where *total holds the fixed-order sum.
+template <int NT>
+__device__ bool last_block_total(double mine, IterState *st, double *partials, double *sh,
+                                 double *total) {
+    __shared__ int am_last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = mine;
+        __threadfence();
+        const unsigned t = atomicAdd(&st->counter, 1u);
+        am_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return false;
+    __threadfence();
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) s += __ldcg(&partials[i]);
+    s = block_sum_d<NT>(s, sh);
+    if (threadIdx.x == 0) {
+        *total = s;
+        st->counter = 0u;
+    }
+    return true;
+}
+
+// Fourier multiplier g(p)/N_vox of (L+1)^-1 (Eq. 12, unified form R-1):
+//   g = c / (D |p|^2 + sigma + c)
+__device__ __forceinline__ float2 multiplier(const MulParams &mp, float p2) {
+    const float dr = fmaf(mp.D, p2, mp.sc.x), di = mp.sc.y;
+    const float inv = 1.0f / fmaf(dr, dr, di * di);
+    return make_float2((mp.cn.x * dr + mp.cn.y * di) * inv, (mp.cn.y * dr - mp.cn.x * di) * inv);
+}
+
+__device__ __forceinline__ float freq_m(int k, int n) { return (float)(k < (n >> 1) ? k : k - n); }
+
+// ================================================================ x pass ==
+template <int N>
+struct XGeo {
+    using G = LineGeo<N>;
+    static constexpr int NT = 256;
+    static constexpr int LPC = NT / G::N1;   // lines per CTA
+    static constexpr int SMEM = LPC * LayRow<N>::kFloat2PerLine * (int)sizeof(float2);
+};
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(256) k_xpass(XParams p) {
+    using G = LineGeo<N>;
+    using XG = XGeo<N>;
+    extern __shared__ float2 smem[];
+    __shared__ double sh_red[XG::NT / 32];
+    const int tid = threadIdx.x;
+    const int lq = tid / G::N1, j = tid % G::N1;
+    const LayRow<N> lay{smem + lq * LayRow<N>::kFloat2PerLine};
+
+    bool xonly = false;
+    float alpha = 0.f;
+    if (MODE == X_ITER) {
+        const int status = p.st->status;
+        const long long k = p.st->k, kmax = p.st->kmax;
+        if (k >= kmax || (status != ST_RUNNING && status != ST_STOP_PENDING)) return;
+        xonly = (status == ST_STOP_PENDING);
+        alpha = (float)p.st->alpha;
+    }
+
+    double acc = 0.0;
+    const long long ngroups = (p.nlines + XG::LPC - 1) / XG::LPC;
+    for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const long long line = g * XG::LPC + lq;
+        const bool valid = line < p.nlines;
+        const long long base = line * (long long)N + j;
+        float2 v[G::N2];
+
+        if (MODE == X_ITER && xonly) {   // final x update after convergence (reading R-5)
+            if (valid) {
+#pragma unroll
+                for (int m = 0; m < G::N2; ++m) {
+                    const long long i = base + (long long)G::N1 * m;
+                    const float2 d = p.delta[i];
+                    float2 xx = p.x[i];
+                    xx.x = fmaf(alpha, d.x, xx.x);
+                    xx.y = fmaf(alpha, d.y, xx.y);
+                    p.x[i] = xx;
+                }
+            }
+            continue;
+        }
+
+        if (MODE == X_SRC_FWD) {
+            // s = S / c, staged raw source in the x buffer
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) {
+                const long long i = base + (long long)G::N1 * m;
+                float2 sv = make_float2(0.f, 0.f);
+                if (valid) sv = p.src_real ? make_float2(reinterpret_cast<const float *>(p.x)[i], 0.f) : p.x[i];
+                v[m] = cmul(sv, p.inv_c);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m)
+                v[m] = valid ? p.work[base + (long long)G::N1 * m] : make_float2(0.f, 0.f);
+            fft_line<N, true, 0>(v, lay, j, p.tw);   // x inverse: v = (L+1)^-1 u
+            float lacc = 0.f;
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) {
+                const long long i = base + (long long)G::N1 * m;
+                const float2 b = valid ? p.B[i] : make_float2(0.f, 0.f);
+                float2 dn;
+                if (MODE == X_SRC_EPI) {
+                    dn = cmul(b, v[m]);                       // Delta_0 = B (L+1)^-1 s
+                    if (valid) {
+                        p.x[i] = make_float2(0.f, 0.f);       // x_0 = 0 (L83)
+                        p.delta[i] = dn;
+                    }
+                } else {
+                    const float2 d = valid ? p.delta[i] : make_float2(0.f, 0.f);
+                    const float2 xx = valid ? p.x[i] : make_float2(0.f, 0.f);
+                    // x_{k+1} = x_k + alpha Delta_k ; Delta_{k+1} = Delta_k + alpha B (y - Delta_k)
+                    const float2 t = cmul(b, csub(v[m], d));
+                    dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
+                    if (valid) {
+                        p.x[i] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                        p.delta[i] = dn;
+                    }
+                }
+                lacc += cabs2(dn);
+                v[m] = cmul(b, dn);                           // next chain: u = B Delta
+            }
+            acc += (double)lacc;
+        }
+        fft_line<N, false, 0>(v, lay, j, p.tw);   // x forward
+        if (valid) {
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) p.work[base + (long long)G::N1 * m] = v[m];
+        }
+    }
+
+    if (MODE == X_SRC_FWD) return;
+    double total;
+    const double mine = block_sum_d<XG::NT>(acc, sh_red);
+    if (!last_block_total<XG::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
+    if (threadIdx.x != 0) return;
+    IterState *st = p.st;
+    if (MODE == X_SRC_EPI) {
+        const double n0 = sqrt(total);
+        st->n0 = n0;
+        st->r = (n0 > 0.0) ? 1.0 : 0.0;
+        st->k = 0;
+        st->status = (n0 > 0.0) ? ST_RUNNING : ST_DONE_CONV;
+        if (n0 > 0.0 && st->tol > 0.0 && 1.0 < st->tol) st->status = ST_STOP_PENDING;
+        p.red.hist[0] = st->r;
+        return;
+    }
+    const long long k1 = st->k + 1;
+    st->k = k1;
+    if (xonly) {
+        st->status = ST_DONE_CONV;
+        return;
+    }
+    const double r = sqrt(total) / st->n0;
+    st->r = r;
+    p.red.hist[k1 % p.red.hist_cap] = r;
+    if (!(r <= 1e6)) st->status = ST_DIVERGED;            // NaN, Inf or r > 1e6
+    else if (st->tol > 0.0 && r < st->tol) st->status = ST_STOP_PENDING;
+}
+
+// ========================================================== strided pass ==
+template <int N>
+struct SGeo {
+    using G = LineGeo<N>;
+    static constexpr int COLS = (N >= 2048) ? 8 : 16;
+    static constexpr int NT = COLS * G::N1;
+    static constexpr int PITCH = G::N2 * COLS + (COLS == 16 ? 0 : 8);   // float2 per n1 row
+    static constexpr int SMEM = G::N1 * PITCH * (int)sizeof(float2);
+};
+
+template <int N, int COLS, int PAD>
+struct LayColP {
+    float2 *base;
+    int c;
+    __device__ __forceinline__ int off(int n1, int k2) const {
+        return n1 * (LineGeo<N>::N2 * COLS + PAD) + k2 * COLS + c;
+    }
+};
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(SGeo<N>::NT) k_strided(SParams p) {
+    using G = LineGeo<N>;
+    using SG = SGeo<N>;
+    constexpr int COLS = SG::COLS;
+    extern __shared__ float2 smem[];
+    const int tid = threadIdx.x;
+    const int c = tid % COLS, j = tid / COLS;
+    if (p.check_state) {
+        const int status = p.st->status;
+        if (status != ST_RUNNING || p.st->k >= p.st->kmax) return;
+    }
+    const LayColP<N, COLS, (COLS == 16 ? 0 : 8)> lay{smem, c};
+    const long long tpo = p.ncols / COLS;
+    const long long ntiles = tpo * p.nouter;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long o = tile / tpo;
+        const long long col = (tile - o * tpo) * COLS + c;
+        const long long base = o * p.ostride + col;
+        float2 v[G::N2];
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) v[m] = p.data[base + (long long)(j + G::N1 * m) * p.stride];
+        fft_line<N, MODE == S_INV, 1>(v, lay, j, p.tw);
+        if (MODE == S_FWD_MUL_INV) {
+            // (L+1)^-1 multiplier, Eq. 12: |p|^2 = px^2 + py^2 + p_line^2
+            float pt2;
+            if (p.line_axis == 2) {
+                const int ix = (int)(col % p.mp.nx), iy = (int)(col / p.mp.nx);
+                const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
+                pt2 = fmaf(px, px, py * py);
+            } else {
+                const float px = p.mp.kx * freq_m((int)col, p.mp.nx);
+                pt2 = px * px;
+            }
+            const float kl = (p.line_axis == 2) ? p.mp.kz : p.mp.ky;
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) {
+                const float pl = kl * freq_m(j + G::N1 * m, N);
+                v[m] = cmul(v[m], multiplier(p.mp, fmaf(pl, pl, pt2)));
+            }
+            fft_line<N, true, 1>(v, lay, j, p.tw);
+        }
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) p.data[base + (long long)(j + G::N1 * m) * p.stride] = v[m];
+    }
+}
+
+// =================================================================== 1-D ==
+// The whole 1-D solve in one CTA (one line; latency bound):
+// O_SETUP computes Delta_0 = B (L+1)^-1 (S/c), n0, x_0 = 0; O_ITER loops the
+// iteration on-chip until the stop test or kmax, then writes the state back.
+template <int N>
+__device__ __forceinline__ void mul_line(float2 (&v)[LineGeo<N>::N2], const MulParams &mp, int j) {
+    using G = LineGeo<N>;
+#pragma unroll
+    for (int m = 0; m < G::N2; ++m) {
+        const float pl = mp.kx * freq_m(j + G::N1 * m, N);
+        v[m] = cmul(v[m], multiplier(mp, pl * pl));
+    }
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(LineGeo<N>::N1) k_solve1d(OneParams p) {
+    using G = LineGeo<N>;
+    __shared__ float2 smem[LayRow<N>::kFloat2PerLine];
+    const int j = threadIdx.x;
+    const LayRow<N> lay{smem};
+    float2 b[G::N2], d[G::N2], xx[G::N2], v[G::N2];
+#pragma unroll
+    for (int m = 0; m < G::N2; ++m) b[m] = p.B[j + G::N1 * m];
+    IterState *st = p.st;
+
+    if constexpr (MODE == O_SETUP) {
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) {
+            const int i = j + G::N1 * m;
+            const float2 sv = p.src_real ? make_float2(reinterpret_cast<const float *>(p.x)[i], 0.f) : p.x[i];
+            v[m] = cmul(sv, p.inv_c);
+        }
+        fft_line<N, false, 0>(v, lay, j, p.tw);
+        mul_line<N>(v, p.mp, j);
+        fft_line<N, true, 0>(v, lay, j, p.tw);
+        float lacc = 0.f;
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) {
+            d[m] = cmul(b[m], v[m]);
+            lacc += cabs2(d[m]);
+            p.delta[j + G::N1 * m] = d[m];
+            p.x[j + G::N1 * m] = make_float2(0.f, 0.f);
+        }
+        const double n0 = sqrt(warp_sum_d((double)lacc));
+        if (j == 0) {
+            st->n0 = n0;
+            st->r = n0 > 0.0 ? 1.0 : 0.0;
+            st->k = 0;
+            st->status = n0 > 0.0 ? ST_RUNNING : ST_DONE_CONV;
+            if (n0 > 0.0 && st->tol > 0.0 && 1.0 < st->tol) st->status = ST_STOP_PENDING;
+            p.red.hist[0] = st->r;
+        }
+        return;
+    } else {
+
+#pragma unroll
+    for (int m = 0; m < G::N2; ++m) {
+        d[m] = p.delta[j + G::N1 * m];
+        xx[m] = p.x[j + G::N1 * m];
+    }
+    const float alpha = (float)st->alpha;
+    const double tol = st->tol, n0 = st->n0;
+    long long k = st->k;
+    const long long kmax = st->kmax;
+    int status = st->status;
+    double r = st->r;
+    while (k < kmax && status == ST_RUNNING) {
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) v[m] = cmul(b[m], d[m]);
+        fft_line<N, false, 0>(v, lay, j, p.tw);
+        mul_line<N>(v, p.mp, j);
+        fft_line<N, true, 0>(v, lay, j, p.tw);
+        float lacc = 0.f;
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) {
+            xx[m] = make_float2(fmaf(alpha, d[m].x, xx[m].x), fmaf(alpha, d[m].y, xx[m].y));
+            const float2 t = cmul(b[m], csub(v[m], d[m]));
+            d[m] = make_float2(fmaf(alpha, t.x, d[m].x), fmaf(alpha, t.y, d[m].y));
+            lacc += cabs2(d[m]);
+        }
+        r = sqrt(warp_sum_d((double)lacc)) / n0;
+        ++k;
+        if (j == 0) p.red.hist[k % p.red.hist_cap] = r;
+        if (!(r <= 1e6)) status = ST_DIVERGED;
+        else if (tol > 0.0 && r < tol) status = ST_STOP_PENDING;
+    }
+    if (status == ST_STOP_PENDING && k < kmax) {
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) xx[m] = make_float2(fmaf(alpha, d[m].x, xx[m].x), fmaf(alpha, d[m].y, xx[m].y));
+        ++k;
+        status = ST_DONE_CONV;
+    }
+#pragma unroll
+    for (int m = 0; m < G::N2; ++m) {
+        p.delta[j + G::N1 * m] = d[m];
+        p.x[j + G::N1 * m] = xx[m];
+    }
+    if (j == 0) {
+        st->k = k;
+        st->r = r;
+        st->status = status;
+    }
+    }
+}
+
+// ================================================================= setup ==
+// V = (w - sigma)/c, B = 1 - V, with the Theorem 1
+// hypotheses checked pointwise: |V| < 1 and Re(w/c) >= 0 (accretive A for
+// D Re(c) >= 0, Eq. 1).
+__global__ void __launch_bounds__(256) k_potential(PotParams p) {
+    float vmax = 0.f;
+    unsigned nacc = 0, nnf = 0;
+    const double cr = p.c_re, ci = p.c_im, inv_c2 = 1.0 / (cr * cr + ci * ci);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double mr, mi;
+        if (p.medium_real) {
+            mr = reinterpret_cast<const float *>(p.medium)[i];
+            mi = 0.0;
+        } else {
+            const float2 m = reinterpret_cast<const float2 *>(p.medium)[i];
+            mr = m.x;
+            mi = m.y;
+        }
+        const double wr = p.medium_is_k2 ? -mr : mr, wi = p.medium_is_k2 ? -mi : mi;
+        const double ar = wr - p.sig_re, ai = wi - p.sig_im;
+        // V = (w - sigma)/c = (w - sigma) conj(c) / |c|^2
+        const double vr = (ar * cr + ai * ci) * inv_c2, vi = (ai * cr - ar * ci) * inv_c2;
+        const double av = sqrt(vr * vr + vi * vi);
+        if (!isfinite(vr) || !isfinite(vi)) ++nnf;
+        vmax = fmaxf(vmax, (float)av);
+        if (av >= 1.0) vmax = fmaxf(vmax, 1.0f);
+        // Re(w/c)
+        const double wcr = (wr * cr + wi * ci) * inv_c2, wci = (wi * cr - wr * ci) * inv_c2;
+        if (wcr < -1e-6 * sqrt(wcr * wcr + wci * wci)) ++nacc;
+        p.B[i] = make_float2((float)(1.0 - vr), (float)(-vi));
+    }
+    // CTA reduce then one atomic each
+    __shared__ float smax[8];
+    __shared__ unsigned sacc[8], snf[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+        nnf += __shfl_xor_sync(0xffffffffu, nnf, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        smax[w] = vmax;
+        sacc[w] = nacc;
+        snf[w] = nnf;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            smax[0] = fmaxf(smax[0], smax[i]);
+            sacc[0] += sacc[i];
+            snf[0] += snf[i];
+        }
+        atomicMax(p.max_absV_bits, __float_as_uint(smax[0]));
+        if (sacc[0]) atomicAdd(p.n_nonaccretive, sacc[0]);
+        if (snf[0]) atomicAdd(p.n_nonfinite, snf[0]);
+    }
+}
+
+// Farthest medium value from (cre, cim) -- one pass of the smallest-circle
+// driver (usp_api.cu).  Exact double distances of the complex64 values.
+__global__ void __launch_bounds__(256) k_farthest(FarParams p) {
+    double best = -1.0;
+    long long bi = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double mr, mi;
+        if (p.medium_real) {
+            mr = reinterpret_cast<const float *>(p.medium)[i];
+            mi = 0.0;
+        } else {
+            const float2 m = reinterpret_cast<const float2 *>(p.medium)[i];
+            mr = m.x;
+            mi = m.y;
+        }
+        const double dx = mr - p.cre, dy = mi - p.cim, d2 = dx * dx + dy * dy;
+        if (d2 > best) {
+            best = d2;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    __shared__ double sb[8];
+    __shared__ long long si[8];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        sb[w] = best;
+        si[w] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i)
+            if (sb[i] > sb[0] || (sb[i] == sb[0] && si[i] < si[0])) {
+                sb[0] = sb[i];
+                si[0] = si[i];
+            }
+        p.best_d2[blockIdx.x] = sb[0];
+        p.best_idx[blockIdx.x] = si[0];
+    }
+}
+
+__global__ void k_set_state(IterState *st, double alpha, double tol, long long kmax) {
+    st->alpha = alpha;
+    st->tol = tol;
+    st->kmax = kmax;
+    st->counter = 0u;
+    const bool below = tol > 0.0 && st->r < tol;
+    if (st->status == ST_RUNNING && below) st->status = ST_STOP_PENDING;
+    if (st->status == ST_STOP_PENDING && !below) st->status = ST_RUNNING;
+}
+
+// ============================================================= launchers ==
+#define USP_FOR_EACH_N(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
+
+bool supported_n(long long n) { return n >= 16 && n <= 2048 && (n & (n - 1)) == 0; }
+
+template <int N, int MODE>
+static cudaError_t xpass_t(const XParams &p, int grid, cudaStream_t s) {
+    constexpr int SM = XGeo<N>::SMEM;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_xpass<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_xpass<N, MODE><<<grid, XGeo<N>::NT, SM, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStream_t s) {
+#define X_CASE(n)                                                  \
+    case n:                                                        \
+        if (mode == X_SRC_FWD) return xpass_t<n, X_SRC_FWD>(p, grid, s); \
+        if (mode == X_SRC_EPI) return xpass_t<n, X_SRC_EPI>(p, grid, s); \
+        return xpass_t<n, X_ITER>(p, grid, s);
+    switch (N) { USP_FOR_EACH_N(X_CASE) default: return cudaErrorInvalidValue; }
+#undef X_CASE
+}
+
+cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_t s) {
+    (void)p; (void)nvox; (void)grid; (void)s;
+    return cudaSuccess;   // x-only update is folded into k_xpass<X_ITER>
+}
+
+template <int N, int MODE>
+static cudaError_t strided_t(const SParams &p, int grid, cudaStream_t s) {
+    constexpr int SM = SGeo<N>::SMEM;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_strided<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_strided<N, MODE><<<grid, SGeo<N>::NT, SM, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s) {
+#define S_CASE(n)                                                    \
+    case n:                                                          \
+        if (mode == S_FWD) return strided_t<n, S_FWD>(p, grid, s);   \
+        if (mode == S_INV) return strided_t<n, S_INV>(p, grid, s);   \
+        return strided_t<n, S_FWD_MUL_INV>(p, grid, s);
+    switch (N) { USP_FOR_EACH_N(S_CASE) default: return cudaErrorInvalidValue; }
+#undef S_CASE
+}
+
+cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s) {
+#define O_CASE(n)                                                                   \
+    case n:                                                                         \
+        if (mode == O_SETUP) k_solve1d<n, O_SETUP><<<1, LineGeo<n>::N1, 0, s>>>(p); \
+        else k_solve1d<n, O_ITER><<<1, LineGeo<n>::N1, 0, s>>>(p);                  \
+        return cudaGetLastError();
+    switch (N) { USP_FOR_EACH_N(O_CASE) default: return cudaErrorInvalidValue; }
+#undef O_CASE
+}
+
+cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s) {
+    k_potential<<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s) {
+    k_farthest<<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s) {
+    k_set_state<<<1, 1, 0, s>>>(st, alpha, tol, kmax);
+    return cudaGetLastError();
+}
+
+int xpass_threads(int) { return 256; }
+int xpass_lines_per_cta(int N) { return 256 / (1 << (ilog2(N) / 2)); }
+size_t xpass_smem(int N) {
+    const int n1 = 1 << (ilog2(N) / 2), n2 = N / n1;
+    return (size_t)(256 / n1) * n1 * (n2 + 1) * sizeof(float2);
+}
+int strided_cols() { return 16; }
+int strided_threads(int N) { return (N >= 2048 ? 8 : 16) * (1 << (ilog2(N) / 2)); }
+size_t strided_smem(int N) {
+    const int n1 = 1 << (ilog2(N) / 2), n2 = N / n1, cols = N >= 2048 ? 8 : 16;
+    return (size_t)n1 * (n2 * cols + (cols == 16 ? 0 : 8)) * sizeof(float2);
+}
+
+}  // namespace usp

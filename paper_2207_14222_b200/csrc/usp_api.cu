@@ -1,0 +1,710 @@
+// usp_api.cu -- the C-ABI of include/usp.h: plan, workspace, setup and the
+// iteration driver.  All arithmetic of the method runs in kernels.cu; this
+// file only sequences launches, validates, and moves bytes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "usp.h"
+#include "usp_internal.h"
+
+using namespace usp;
+
+namespace {
+
+thread_local std::string g_err;
+
+usp_status fail(usp_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CU(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(USP_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                             \
+    } while (0)
+
+enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
+              KC_FARTHEST, KC_SETSTATE, KC_N };
+const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
+                              "solve1d", "potential", "farthest", "set_state"};
+
+struct Timed {
+    int cls;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct usp_plan_s {
+    usp_plan_desc d{};
+    int ndim = 0;
+    long long nx = 1, ny = 1, nz = 1, nvox = 0;
+    cudaStream_t stream = nullptr;
+    int nsm = 148;
+    // workspace
+    char *ws = nullptr;
+    size_t ws_bytes = 0;
+    float2 *x = nullptr, *delta = nullptr, *B = nullptr, *work = nullptr;
+    // plan-owned small device memory
+    IterState *st = nullptr;
+    double *partials = nullptr;
+    int partials_cap = 0;
+    double *hist = nullptr;
+    int hist_cap = 65536;
+    float2 *tw[3] = {nullptr, nullptr, nullptr};
+    unsigned int *red_u = nullptr;  // [0] max|V| bits, [1] non-accretive, [2] non-finite
+    double *far_d = nullptr;
+    long long *far_i = nullptr;
+    int far_cap = 0;
+    IterState *st_host = nullptr;   // pinned mirror
+    // split
+    usp_c128 sigma{}, c{}, centre{};
+    double radius = 0.0, vmax = 0.0;
+    bool have_potential = false, have_source = false;
+    // launch configuration
+    int grid_x = 0, grid_y = 0, grid_z = 0;
+    // profiling
+    bool prof = false;
+    std::vector<Timed> timed;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[KC_N] = {0};
+    long long prof_n[KC_N] = {0};
+    long long launches = 0;
+};
+
+namespace {
+
+cudaEvent_t get_event(usp_plan_s *p) {
+    if (!p->ev_pool.empty()) {
+        cudaEvent_t e = p->ev_pool.back();
+        p->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct Tick {   // brackets one launch with events when profiling
+    usp_plan_s *p;
+    int cls;
+    cudaEvent_t a = nullptr;
+    Tick(usp_plan_s *pl, int c) : p(pl), cls(c) {
+        ++p->launches;
+        if (p->prof) {
+            a = get_event(p);
+            cudaEventRecord(a, p->stream);
+        }
+    }
+    ~Tick() {
+        if (p->prof) {
+            cudaEvent_t b = get_event(p);
+            cudaEventRecord(b, p->stream);
+            p->timed.push_back({cls, a, b});
+        }
+    }
+};
+
+void drain_timing(usp_plan_s *p) {
+    if (p->timed.empty()) return;
+    cudaStreamSynchronize(p->stream);
+    for (auto &t : p->timed) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        p->prof_ms[t.cls] += ms;
+        p->prof_n[t.cls] += 1;
+        p->ev_pool.push_back(t.a);
+        p->ev_pool.push_back(t.b);
+    }
+    p->timed.clear();
+}
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+std::vector<float2> twiddle_table(int n) {
+    // tw[k2*N1 + j] = W_n^(j*k2) = exp(-2 pi i j k2 / n), computed in double
+    int lg = 0;
+    while ((1 << lg) < n) ++lg;
+    const int n1 = 1 << (lg / 2), n2 = n / n1;
+    std::vector<float2> t((size_t)n);
+    for (int k2 = 0; k2 < n2; ++k2)
+        for (int j = 0; j < n1; ++j) {
+            const long long e = ((long long)j * k2) % n;
+            const double a = -2.0 * M_PI * (double)e / (double)n;
+            double cr = std::cos(a), ci = std::sin(a);
+            if (4 * e == n) { cr = 0.0; ci = -1.0; }
+            if (2 * e == n) { cr = -1.0; ci = 0.0; }
+            if (4 * e == 3 * n) { cr = 0.0; ci = 1.0; }
+            if (e == 0) { cr = 1.0; ci = 0.0; }
+            t[(size_t)k2 * n1 + j] = make_float2((float)cr, (float)ci);
+        }
+    return t;
+}
+
+int occ_grid(usp_plan_s *p, long long units, int per_sm) {
+    long long g = (long long)p->nsm * per_sm;
+    return (int)std::max(1LL, std::min(units, g));
+}
+
+// ---------------------------------------------------------------- MEC --
+struct P2 { double x, y; };
+
+bool in_circle(P2 q, P2 c, double r) {
+    const double sc = std::fabs(c.x) + std::fabs(c.y) + r + 1e-300;
+    return std::hypot(q.x - c.x, q.y - c.y) <= r + 1e-13 * sc;
+}
+
+void circ2(P2 a, P2 b, P2 &c, double &r) {
+    c = {0.5 * (a.x + b.x), 0.5 * (a.y + b.y)};
+    r = 0.5 * std::hypot(a.x - b.x, a.y - b.y);
+}
+
+void circ3(P2 a, P2 b, P2 q, P2 &c, double &r) {
+    const double bx = b.x - a.x, by = b.y - a.y, cx = q.x - a.x, cy = q.y - a.y;
+    const double d = 2.0 * (bx * cy - by * cx);
+    const double sc = (std::fabs(bx) + std::fabs(by)) * (std::fabs(cx) + std::fabs(cy));
+    if (d == 0.0 || std::fabs(d) <= 1e-14 * sc) {   // collinear: farthest pair's diameter
+        const double ab = std::hypot(bx, by), aq = std::hypot(cx, cy), bq = std::hypot(q.x - b.x, q.y - b.y);
+        if (ab >= aq && ab >= bq) circ2(a, b, c, r);
+        else if (aq >= bq) circ2(a, q, c, r);
+        else circ2(b, q, c, r);
+        return;
+    }
+    const double b2 = bx * bx + by * by, c2 = cx * cx + cy * cy;
+    const double ux = (cy * b2 - by * c2) / d, uy = (bx * c2 - cx * b2) / d;
+    c = {a.x + ux, a.y + uy};
+    r = std::hypot(ux, uy);
+}
+
+// Smallest circle of a small support set (incremental construction with
+// two / three boundary points; exact for the handful of support points the
+// device-side farthest-point loop collects).
+void mec_small(const std::vector<P2> &pts, P2 &c, double &r) {
+    c = pts[0];
+    r = 0.0;
+    for (size_t i = 1; i < pts.size(); ++i) {
+        if (in_circle(pts[i], c, r)) continue;
+        c = pts[i];
+        r = 0.0;
+        for (size_t j = 0; j < i; ++j) {
+            if (in_circle(pts[j], c, r)) continue;
+            circ2(pts[i], pts[j], c, r);
+            for (size_t k = 0; k < j; ++k) {
+                if (in_circle(pts[k], c, r)) continue;
+                circ3(pts[i], pts[j], pts[k], c, r);
+            }
+        }
+    }
+}
+
+usp_status read_point(usp_plan_s *p, const void *medium_dev, long long idx, P2 &out) {
+    if (p->d.dtype == USP_R32) {
+        float v = 0.f;
+        CU(cudaMemcpyAsync(&v, (const float *)medium_dev + idx, sizeof(float), cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        out = {v, 0.0};
+    } else {
+        float2 v{};
+        CU(cudaMemcpyAsync(&v, (const float2 *)medium_dev + idx, sizeof(float2), cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        out = {v.x, v.y};
+    }
+    return USP_OK;
+}
+
+// Smallest enclosing circle of all medium values: grow a
+// support set with the farthest point from the current circle (one device
+// pass each) until every value is inside.  The result is the MEC of a subset
+// that encloses all points, i.e. the MEC of the full set.
+usp_status device_mec(usp_plan_s *p, const void *medium_dev, P2 &centre, double &radius) {
+    std::vector<P2> sup;
+    P2 q;
+    usp_status s = read_point(p, medium_dev, 0, q);
+    if (s) return s;
+    sup.push_back(q);
+    centre = q;
+    radius = 0.0;
+    const int grid = std::min(p->far_cap, occ_grid(p, (p->nvox + 255) / 256, 8));
+    std::vector<double> bd(grid);
+    std::vector<long long> bi(grid);
+    for (int it = 0; it < 200; ++it) {
+        FarParams fp{medium_dev, p->d.dtype == USP_R32, p->nvox, centre.x, centre.y, p->far_d, p->far_i};
+        {
+            Tick t(p, KC_FARTHEST);
+            CU(launch_farthest(fp, grid, p->stream));
+        }
+        CU(cudaMemcpyAsync(bd.data(), p->far_d, sizeof(double) * grid, cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaMemcpyAsync(bi.data(), p->far_i, sizeof(long long) * grid, cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        int b = 0;
+        for (int i = 1; i < grid; ++i)
+            if (bd[i] > bd[b] || (bd[i] == bd[b] && bi[i] < bi[b])) b = i;
+        s = read_point(p, medium_dev, bi[b], q);
+        if (s) return s;
+        if (in_circle(q, centre, radius)) return USP_OK;
+        sup.push_back(q);
+        mec_small(sup, centre, radius);
+    }
+    return fail(USP_ERR_CUDA, "smallest-circle search did not converge");
+}
+
+usp_status stage(usp_plan_s *p, void *dst, const void *src, size_t bytes, usp_where where) {
+    CU(cudaMemcpyAsync(dst, src, bytes, where == USP_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       p->stream));
+    return USP_OK;
+}
+
+size_t elem_bytes(const usp_plan_s *p) { return p->d.dtype == USP_R32 ? 4 : 8; }
+
+MulParams mul_params(const usp_plan_s *p) {
+    MulParams mp{};
+    const double cr = p->c.re / (double)p->nvox, ci = p->c.im / (double)p->nvox;
+    mp.cn = make_float2((float)cr, (float)ci);
+    mp.sc = make_float2((float)(p->sigma.re + p->c.re), (float)(p->sigma.im + p->c.im));
+    mp.D = (float)p->d.D;
+    mp.kx = (float)(2.0 * M_PI / ((double)p->nx * p->d.h[0]));
+    mp.ky = (float)(2.0 * M_PI / ((double)p->ny * p->d.h[1]));
+    mp.kz = (float)(2.0 * M_PI / ((double)p->nz * p->d.h[2]));
+    mp.nx = (int)p->nx;
+    mp.ny = (int)p->ny;
+    mp.nz = (int)p->nz;
+    return mp;
+}
+
+XParams x_params(usp_plan_s *p) {
+    XParams xp{};
+    xp.work = p->work;
+    xp.delta = p->delta;
+    xp.x = p->x;
+    xp.B = p->B;
+    xp.tw = p->tw[0];
+    xp.nlines = p->ny * p->nz;
+    xp.src_real = p->d.dtype == USP_R32;
+    const double m = p->c.re * p->c.re + p->c.im * p->c.im;
+    xp.inv_c = make_float2((float)(p->c.re / m), (float)(-p->c.im / m));
+    xp.st = p->st;
+    xp.red = Red{p->partials, p->hist, p->hist_cap};
+    return xp;
+}
+
+// The middle of the chain: every FFT pass between the x forward and the x
+// inverse, with the (L+1)^-1 multiplier on the last axis.
+usp_status chain_mid(usp_plan_s *p, int check_state) {
+    const MulParams mp = mul_params(p);
+    if (p->ndim == 2) {
+        SParams sp{p->work, p->tw[1], p->nx, p->nx, 1, 0, 1, check_state, mp, p->st};
+        Tick t(p, KC_YMUL2D);
+        CU(launch_strided((int)p->ny, S_FWD_MUL_INV, sp, p->grid_y, p->stream));
+        return USP_OK;
+    }
+    SParams yf{p->work, p->tw[1], p->nx, p->nx, p->nz, p->nx * p->ny, 1, check_state, mp, p->st};
+    SParams zm{p->work, p->tw[2], p->nx * p->ny, p->nx * p->ny, 1, 0, 2, check_state, mp, p->st};
+    {
+        Tick t(p, KC_YFWD);
+        CU(launch_strided((int)p->ny, S_FWD, yf, p->grid_y, p->stream));
+    }
+    {
+        Tick t(p, KC_ZMUL);
+        CU(launch_strided((int)p->nz, S_FWD_MUL_INV, zm, p->grid_z, p->stream));
+    }
+    {
+        Tick t(p, KC_YINV);
+        CU(launch_strided((int)p->ny, S_INV, yf, p->grid_y, p->stream));
+    }
+    return USP_OK;
+}
+
+usp_status sync_state(usp_plan_s *p) {
+    CU(cudaMemcpyAsync(p->st_host, p->st, sizeof(IterState), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    return USP_OK;
+}
+
+}  // namespace
+
+// =================================================================== ABI ==
+extern "C" {
+
+const char *usp_last_error(void) { return g_err.c_str(); }
+
+const char *usp_version(void) { return "0.1 sm_100a"; }
+
+usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
+    if (!desc || !out) return fail(USP_ERR_ARG, "NULL argument");
+    *out = nullptr;
+    if (desc->ndim < 1 || desc->ndim > 3) return fail(USP_ERR_ARG, "ndim must be 1..3 (got %d)", desc->ndim);
+    if (!(desc->D > 0.0)) return fail(USP_ERR_ARG, "D must be > 0");
+    if (desc->nccl_comm) return fail(USP_ERR_UNSUPPORTED, "multi-GPU plans are not available in this build");
+    if (desc->dtype != USP_C64 && desc->dtype != USP_R32) return fail(USP_ERR_ARG, "bad dtype");
+    if (desc->medium != USP_MEDIUM_K2 && desc->medium != USP_MEDIUM_W) return fail(USP_ERR_ARG, "bad medium");
+    for (int a = 0; a < desc->ndim; ++a) {
+        if (!supported_n(desc->n[a]))
+            return fail(USP_ERR_UNSUPPORTED, "extent n[%d]=%lld must be a power of two in [16, 2048]", a,
+                        (long long)desc->n[a]);
+        if (!(desc->h[a] > 0.0)) return fail(USP_ERR_ARG, "h[%d] must be > 0", a);
+    }
+    usp_plan_s *p = new usp_plan_s();
+    p->d = *desc;
+    p->ndim = desc->ndim;
+    p->nx = desc->n[0];
+    p->ny = desc->ndim >= 2 ? desc->n[1] : 1;
+    p->nz = desc->ndim >= 3 ? desc->n[2] : 1;
+    for (int a = desc->ndim; a < 3; ++a) p->d.h[a] = 1.0;
+    p->nvox = p->nx * p->ny * p->nz;
+    p->stream = (cudaStream_t)desc->stream;
+    p->sigma = desc->sigma;
+    p->c = desc->c;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) {
+        delete p;
+        return fail(USP_ERR_CUDA, "no CUDA device: %s", cudaGetErrorString(e));
+    }
+    // launch grids: one resident wave, persistent grid-stride loops
+    {
+        const long long xgroups = (p->ny * p->nz + xpass_lines_per_cta((int)p->nx) - 1) / xpass_lines_per_cta((int)p->nx);
+        p->grid_x = occ_grid(p, xgroups, 2);
+        if (p->ndim >= 2) p->grid_y = occ_grid(p, (p->nx / (p->ny >= 2048 ? 8 : 16)) * p->nz, 2);
+        if (p->ndim >= 3) p->grid_z = occ_grid(p, (p->nx * p->ny) / (p->nz >= 2048 ? 8 : 16), 2);
+    }
+    p->partials_cap = std::max(1, p->grid_x);
+    p->far_cap = p->nsm * 8;
+    std::vector<float2> twh[3];
+    const long long ext[3] = {p->nx, p->ny, p->nz};
+#define TRY(call)                                                                         \
+    do {                                                                                  \
+        cudaError_t e2 = (call);                                                          \
+        if (e2 != cudaSuccess) {                                                          \
+            usp_plan_destroy(p);                                                          \
+            return fail(USP_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e2));          \
+        }                                                                                 \
+    } while (0)
+    TRY(cudaMalloc(&p->st, sizeof(IterState)));
+    TRY(cudaMalloc(&p->partials, sizeof(double) * p->partials_cap));
+    TRY(cudaMalloc(&p->hist, sizeof(double) * p->hist_cap));
+    TRY(cudaMalloc(&p->red_u, sizeof(unsigned) * 4));
+    TRY(cudaMalloc(&p->far_d, sizeof(double) * p->far_cap));
+    TRY(cudaMalloc(&p->far_i, sizeof(long long) * p->far_cap));
+    TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
+    for (int a = 0; a < p->ndim; ++a) {
+        twh[a] = twiddle_table((int)ext[a]);
+        TRY(cudaMalloc(&p->tw[a], sizeof(float2) * twh[a].size()));
+        TRY(cudaMemcpy(p->tw[a], twh[a].data(), sizeof(float2) * twh[a].size(), cudaMemcpyHostToDevice));
+    }
+    IterState s0{};
+    s0.status = ST_NO_SOURCE;
+    TRY(cudaMemcpy(p->st, &s0, sizeof s0, cudaMemcpyHostToDevice));
+#undef TRY
+    *out = p;
+    return USP_OK;
+}
+
+usp_status usp_plan_workspace_size(usp_plan_t p, size_t *bytes) {
+    if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
+    *bytes = 4 * align256((size_t)p->nvox * sizeof(float2));
+    return USP_OK;
+}
+
+usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
+    if (!p || !dev) return fail(USP_ERR_ARG, "NULL argument");
+    if (((uintptr_t)dev) & 255) return fail(USP_ERR_ARG, "workspace must be 256-byte aligned");
+    size_t need = 0;
+    usp_plan_workspace_size(p, &need);
+    if (bytes < need) return fail(USP_ERR_NOMEM, "workspace %zu bytes < required %zu", bytes, need);
+    const size_t f = align256((size_t)p->nvox * sizeof(float2));
+    p->ws = (char *)dev;
+    p->ws_bytes = bytes;
+    p->x = (float2 *)(p->ws);
+    p->delta = (float2 *)(p->ws + f);
+    p->B = (float2 *)(p->ws + 2 * f);
+    p->work = (float2 *)(p->ws + 3 * f);
+    p->have_potential = p->have_source = false;
+    return USP_OK;
+}
+
+usp_status usp_local_extent(usp_plan_t p, int64_t *z0, int64_t *nz_local) {
+    if (!p || !z0 || !nz_local) return fail(USP_ERR_ARG, "NULL argument");
+    *z0 = 0;
+    *nz_local = p->ndim == 3 ? p->nz : (p->ndim == 2 ? p->ny : p->nx);
+    return USP_OK;
+}
+
+usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, double target_norm) {
+    if (!p || !medium) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p->ws) return fail(USP_ERR_STATE, "workspace not set");
+    if (where != USP_HOST && where != USP_DEVICE) return fail(USP_ERR_ARG, "bad where");
+    // stage the medium in the chain buffer (the source resets it later)
+    usp_status s = stage(p, p->work, medium, (size_t)p->nvox * elem_bytes(p), where);
+    if (s) return s;
+    p->have_source = false;
+    p->have_potential = false;
+    if (target_norm > 0.0) {
+        if (!(target_norm < 1.0)) return fail(USP_ERR_ARG, "target_norm must be in (0, 1)");
+        P2 cen;
+        double r;
+        s = device_mec(p, p->work, cen, r);
+        if (s) return s;
+        if (!(r > 0.0))
+            return fail(USP_ERR_ARG, "homogeneous medium: smallest circle has radius 0; give sigma and c explicitly");
+        p->centre = {cen.x, cen.y};
+        p->radius = r;
+        if (p->d.medium == USP_MEDIUM_K2) {   // sigma = -kbar^2, c = -i r / 0.95 (R-1)
+            p->sigma = {-cen.x, -cen.y};
+            p->c = {0.0, -r / target_norm};
+        } else {                              // diffusion: sigma = centre, c = r / 0.95 (R-15)
+            p->sigma = {cen.x, cen.y};
+            p->c = {r / target_norm, 0.0};
+        }
+    } else {
+        p->sigma = p->d.sigma;
+        p->c = p->d.c;
+        p->centre = {0.0, 0.0};
+        p->radius = 0.0;
+    }
+    if (p->c.re == 0.0 && p->c.im == 0.0) return fail(USP_ERR_ARG, "c must be non-zero");
+    if (p->d.D * p->c.re < 0.0)
+        return fail(USP_ERR_NOT_ACCRETIVE, "D Re(c) < 0: -D lap / c is not accretive (Eq. 1)");
+    CU(cudaMemsetAsync(p->red_u, 0, sizeof(unsigned) * 4, p->stream));
+    PotParams pp{p->work, p->d.dtype == USP_R32, p->d.medium == USP_MEDIUM_K2, p->B, p->nvox,
+                 p->sigma.re, p->sigma.im, p->c.re, p->c.im, p->red_u, p->red_u + 1, p->red_u + 2};
+    {
+        Tick t(p, KC_POTENTIAL);
+        CU(launch_potential(pp, occ_grid(p, (p->nvox + 255) / 256, 8), p->stream));
+    }
+    unsigned red[4];
+    CU(cudaMemcpyAsync(red, p->red_u, sizeof red, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    float vmax;
+    std::memcpy(&vmax, &red[0], sizeof vmax);
+    p->vmax = vmax;
+    if (red[2]) return fail(USP_ERR_NONFINITE, "%u non-finite medium values", red[2]);
+    if (!(vmax < 1.0f))
+        return fail(USP_ERR_NOT_CONTRACTIVE, "max|V| = %g >= 1: Theorem 1 needs ||V|| < 1", (double)vmax);
+    if (red[1])
+        return fail(USP_ERR_NOT_ACCRETIVE, "Re(w/c) < 0 at %u voxels: A is not accretive (Eq. 1)", red[1]);
+    p->have_potential = true;
+    return USP_OK;
+}
+
+usp_status usp_get_split(usp_plan_t p, usp_c128 *sigma, usp_c128 *c, usp_c128 *centre, double *radius,
+                         double *max_abs_V) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    if (sigma) *sigma = p->sigma;
+    if (c) *c = p->c;
+    if (centre) *centre = p->centre;
+    if (radius) *radius = p->radius;
+    if (max_abs_V) *max_abs_V = p->vmax;
+    return USP_OK;
+}
+
+usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
+    if (!p || !src) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p->have_potential) return fail(USP_ERR_STATE, "set_potential must succeed first");
+    usp_status s = stage(p, p->x, src, (size_t)p->nvox * elem_bytes(p), where);
+    if (s) return s;
+    IterState s0{};
+    s0.status = ST_NO_SOURCE;
+    s0.alpha = 0.75;
+    CU(cudaMemcpyAsync(p->st, &s0, sizeof s0, cudaMemcpyHostToDevice, p->stream));
+    if (p->ndim == 1) {
+        OneParams op{};
+        op.delta = p->delta;
+        op.x = p->x;
+        op.B = p->B;
+        op.tw = p->tw[0];
+        op.src_real = p->d.dtype == USP_R32;
+        const double m = p->c.re * p->c.re + p->c.im * p->c.im;
+        op.inv_c = make_float2((float)(p->c.re / m), (float)(-p->c.im / m));
+        op.mp = mul_params(p);
+        op.st = p->st;
+        op.red = Red{p->partials, p->hist, p->hist_cap};
+        Tick t(p, KC_SOLVE1D);
+        CU(launch_solve1d((int)p->nx, O_SETUP, op, p->stream));
+    } else {
+        XParams xp = x_params(p);
+        {
+            Tick t(p, KC_XPASS);
+            CU(launch_xpass((int)p->nx, X_SRC_FWD, xp, p->grid_x, p->stream));
+        }
+        s = chain_mid(p, 0);
+        if (s) return s;
+        {
+            Tick t(p, KC_XPASS);
+            CU(launch_xpass((int)p->nx, X_SRC_EPI, xp, p->grid_x, p->stream));
+        }
+    }
+    s = sync_state(p);
+    if (s) return s;
+    p->have_source = true;
+    return USP_OK;
+}
+
+usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, int64_t *n_done, usp_term *term) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
+    if (n_max < 0 || !(alpha > 0.0)) return fail(USP_ERR_ARG, "need n_max >= 0 and alpha > 0");
+    usp_status s = sync_state(p);
+    if (s) return s;
+    const long long k0 = p->st_host->k;
+    const long long kmax = k0 + n_max;
+    {
+        Tick t(p, KC_SETSTATE);
+        CU(launch_set_state(p->st, alpha, tol, kmax, p->stream));
+    }
+    if (p->ndim == 1) {
+        OneParams op{};
+        op.delta = p->delta;
+        op.x = p->x;
+        op.B = p->B;
+        op.tw = p->tw[0];
+        op.mp = mul_params(p);
+        op.st = p->st;
+        op.red = Red{p->partials, p->hist, p->hist_cap};
+        Tick t(p, KC_SOLVE1D);
+        CU(launch_solve1d((int)p->nx, O_ITER, op, p->stream));
+    } else {
+        const XParams xp = x_params(p);
+        const long long batch = 16;
+        long long launched = 0;
+        // with tol > 0 the device stops itself; +1 covers the final x-only update
+        const long long total = n_max;
+        while (launched < total) {
+            const long long nb = std::min(batch, total - launched);
+            for (long long i = 0; i < nb; ++i) {
+                s = chain_mid(p, 1);
+                if (s) return s;
+                Tick t(p, KC_XPASS);
+                CU(launch_xpass((int)p->nx, X_ITER, xp, p->grid_x, p->stream));
+            }
+            launched += nb;
+            if (tol > 0.0 || p->prof) {
+                s = sync_state(p);
+                if (s) return s;
+                drain_timing(p);
+                const int stt = p->st_host->status;
+                if (stt == ST_DONE_CONV || stt == ST_DIVERGED) break;
+            }
+        }
+    }
+    s = sync_state(p);
+    if (s) return s;
+    drain_timing(p);
+    const IterState &h = *p->st_host;
+    if (n_done) *n_done = h.k - k0;
+    if (term) {
+        if (h.status == ST_DONE_CONV) *term = USP_CONVERGED;
+        else if (h.status == ST_DIVERGED) *term = USP_DIVERGED;
+        else *term = USP_MAX_ITER;
+    }
+    return USP_OK;
+}
+
+usp_status usp_residual(usp_plan_t p, double *rel, double *abs_norm, int64_t *k) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    if (!p->have_source) return fail(USP_ERR_STATE, "no source");
+    usp_status s = sync_state(p);
+    if (s) return s;
+    if (rel) *rel = p->st_host->r;
+    if (abs_norm) *abs_norm = p->st_host->r * p->st_host->n0;
+    if (k) *k = p->st_host->k;
+    return USP_OK;
+}
+
+usp_status usp_residual_history(usp_plan_t p, double *host, int64_t cap, int64_t *n) {
+    if (!p || !n) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p->have_source) return fail(USP_ERR_STATE, "no source");
+    usp_status s = sync_state(p);
+    if (s) return s;
+    const long long avail = std::min<long long>(p->st_host->k + 1, p->hist_cap);
+    *n = avail;
+    if (host && cap > 0) {
+        std::vector<double> all(p->hist_cap);
+        CU(cudaMemcpy(all.data(), p->hist, sizeof(double) * p->hist_cap, cudaMemcpyDeviceToHost));
+        const long long first = p->st_host->k + 1 - avail;
+        for (long long i = 0; i < std::min<long long>(cap, avail); ++i) host[i] = all[(first + i) % p->hist_cap];
+    }
+    return USP_OK;
+}
+
+usp_status usp_get_field(usp_plan_t p, void *out, usp_where where) {
+    if (!p || !out) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p->have_source) return fail(USP_ERR_STATE, "no source");
+    const cudaMemcpyKind kind = where == USP_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (p->d.dtype == USP_C64) {
+        CU(cudaMemcpyAsync(out, p->x, (size_t)p->nvox * sizeof(float2), kind, p->stream));
+    } else {
+        // real field: take the real parts (strided copy, pitch 8 -> 4 bytes)
+        CU(cudaMemcpy2DAsync(out, sizeof(float), p->x, sizeof(float2), sizeof(float), (size_t)p->nvox, kind,
+                             p->stream));
+    }
+    if (where == USP_HOST) CU(cudaStreamSynchronize(p->stream));
+    return USP_OK;
+}
+
+usp_status usp_profile_enable(usp_plan_t p, int enable) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    drain_timing(p);
+    p->prof = enable != 0;
+    if (enable) {
+        for (int i = 0; i < KC_N; ++i) {
+            p->prof_ms[i] = 0.0;
+            p->prof_n[i] = 0;
+        }
+    }
+    return USP_OK;
+}
+
+usp_status usp_profile_read(usp_plan_t p, int cap, char (*names)[32], double *ms, int64_t *launches, int *n) {
+    if (!p || !n) return fail(USP_ERR_ARG, "NULL argument");
+    drain_timing(p);
+    int k = 0;
+    for (int i = 0; i < KC_N && k < cap; ++i) {
+        if (!p->prof_n[i]) continue;
+        if (names) std::snprintf(names[k], 32, "%s", kc_names[i]);
+        if (ms) ms[k] = p->prof_ms[i];
+        if (launches) launches[k] = p->prof_n[i];
+        ++k;
+    }
+    *n = k;
+    return USP_OK;
+}
+
+usp_status usp_launch_count(usp_plan_t p, int64_t *launches) {
+    if (!p || !launches) return fail(USP_ERR_ARG, "NULL argument");
+    *launches = p->launches;
+    return USP_OK;
+}
+
+void usp_plan_destroy(usp_plan_t p) {
+    if (!p) return;
+    if (p->stream || true) cudaStreamSynchronize(p->stream);
+    drain_timing(p);
+    for (auto e : p->ev_pool) cudaEventDestroy(e);
+    cudaFree(p->st);
+    cudaFree(p->partials);
+    cudaFree(p->hist);
+    cudaFree(p->red_u);
+    cudaFree(p->far_d);
+    cudaFree(p->far_i);
+    for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
+    cudaFreeHost(p->st_host);
+    delete p;
+}
+
+}  // extern "C"

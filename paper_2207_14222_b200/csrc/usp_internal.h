@@ -1,0 +1,131 @@
+// usp_internal.h -- structures shared by the kernels (kernels.cu) and the
+// plan/driver (usp_api.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace usp {
+
+// Iteration status kept on the device so launched batches can stop
+// themselves without a host round trip.
+enum : int {
+    ST_RUNNING = 0,      // iterate: full iteration (chain + update)
+    ST_STOP_PENDING = 1, // r_k < tol: the next iteration only applies x += alpha Delta_k
+    ST_DONE_CONV = 2,    // converged, final update applied
+    ST_DIVERGED = 3,     // non-finite or r > 1e6
+    ST_NO_SOURCE = 4
+};
+
+struct IterState {
+    double alpha;        // step size (Algorithm 1 line 4)
+    double tol;          // stop threshold (<= 0: none)
+    double n0;           // ||Delta_0|| = ||B (L+1)^-1 s||  (reading R-4)
+    double r;            // r_k = ||Delta_k|| / n0 of the current Delta_k
+    long long k;         // iterations done since set_source (x_k is current)
+    long long kmax;      // absolute iteration limit of the running iterate call
+    int status;
+    unsigned int counter;  // last-block-done counter (reset by the last block)
+};
+
+struct Red {             // reduction scratch (device)
+    double *partials;    // one per CTA of the reducing kernel
+    double *hist;        // residual ring
+    int hist_cap;
+};
+
+// Fourier multiplier data of (L+1)^-1 = F^-1 [c/(D|p|^2 + sigma + c)] F (Eq. 12),
+// with the inverse DFT's 1/N_vox folded into the numerator.
+struct MulParams {
+    float2 cn;           // c / N_vox
+    float2 sc;           // sigma + c
+    float D;
+    float kx, ky, kz;    // 2 pi / (n_a h_a): p_a = k_a * m_a
+    int nx, ny, nz;
+};
+
+// ---------------------------------------------------------------- x pass --
+enum XMode : int { X_SRC_FWD = 0, X_SRC_EPI = 1, X_ITER = 2 };
+
+struct XParams {
+    float2 *work;        // chain buffer (complex64, [z][y][x])
+    float2 *delta;       // Delta_k
+    float2 *x;           // x_k (also the staging area of the raw source S)
+    const float2 *B;     // B = 1 - V
+    const float2 *tw;    // four-step twiddles for nx
+    long long nlines;    // ny * nz (local)
+    int src_real;        // staged source is float32 (else complex64)
+    float2 inv_c;        // 1/c (s = S/c)
+    IterState *st;
+    Red red;
+};
+
+// ---------------------------------------------------------- strided pass --
+enum SMode : int { S_FWD = 0, S_INV = 1, S_FWD_MUL_INV = 2 };
+
+struct SParams {
+    float2 *data;
+    const float2 *tw;    // four-step twiddles for the line length
+    long long stride;    // elements between consecutive line points
+    long long ncols;     // columns per outer slab (contiguous)
+    long long nouter;    // outer slabs
+    long long ostride;   // elements between outer slabs
+    int line_axis;       // 1 = y (2-D, columns = x), 2 = z (3-D, columns = (y, x))
+    int check_state;     // 1: skip unless status == RUNNING && k < kmax
+    MulParams mp;
+    IterState *st;
+};
+
+// ------------------------------------------------------------------ 1-D --
+enum OneMode : int { O_SETUP = 0, O_ITER = 1 };
+struct OneParams {
+    float2 *delta, *x;
+    const float2 *B;
+    const float2 *tw;
+    int src_real;
+    float2 inv_c;
+    MulParams mp;
+    IterState *st;
+    Red red;
+};
+
+// --------------------------------------------------------------- setup --
+struct PotParams {
+    const void *medium;  // staged medium (device)
+    int medium_real;     // float32 (else complex64)
+    int medium_is_k2;    // w = -k^2 (else w = medium)
+    float2 *B;           // out: B = 1 - V
+    long long n;
+    double sig_re, sig_im, c_re, c_im;
+    // outputs (atomics)
+    unsigned int *max_absV_bits;  // float bits of max |V| (non-negative -> int order)
+    unsigned int *n_nonaccretive;
+    unsigned int *n_nonfinite;
+};
+
+struct FarParams {       // farthest medium value from a centre (smallest circle)
+    const void *medium;
+    int medium_real;
+    long long n;
+    double cre, cim;
+    double *best_d2;     // per CTA
+    long long *best_idx; // per CTA
+};
+
+// launchers (kernels.cu); all return cudaGetLastError()
+cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);
+cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s);
+cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s);
+cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_t s);
+cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
+cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
+cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
+
+int xpass_threads(int N);          // threads per CTA of the x pass
+int xpass_lines_per_cta(int N);
+int strided_threads(int N);
+int strided_cols();
+size_t xpass_smem(int N);
+size_t strided_smem(int N);
+bool supported_n(long long n);
+
+}  // namespace usp

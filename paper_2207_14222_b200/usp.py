@@ -1,0 +1,184 @@
+"""Thin Python binding of libusp (include/usp.h): argument marshalling only.
+
+PyTorch supplies device memory (the workspace and field tensors) and the
+stream; every step of the method runs in libusp's sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib as L
+
+_TERM = L.TERM_NAMES
+
+
+@dataclass
+class Split:
+    sigma: complex
+    c: complex
+    centre: complex
+    radius: float
+    max_abs_V: float
+
+
+def _ptr_where(a, want_dtype):
+    """(pointer, where, keepalive) for a torch tensor or numpy array."""
+    try:
+        import torch
+    except Exception:  # pragma: no cover
+        torch = None
+    if torch is not None and isinstance(a, torch.Tensor):
+        tdt = {"c64": torch.complex64, "r32": torch.float32}[want_dtype]
+        if a.dtype != tdt:
+            raise TypeError(f"expected {tdt}, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(a.data_ptr()), (L.DEVICE if a.is_cuda else L.HOST), a
+    arr = np.asarray(a)
+    ndt = {"c64": np.complex64, "r32": np.float32}[want_dtype]
+    if arr.dtype != ndt or not arr.flags.c_contiguous:
+        raise TypeError(f"expected a C-contiguous {np.dtype(ndt)} array, got {arr.dtype}")
+    return ctypes.c_void_p(arr.ctypes.data), L.HOST, arr
+
+
+class Plan:
+    """One solver plan for a grid of ``shape`` (C order, x last).
+
+    kind='helmholtz': medium is k^2(r) (Eq. 8); kind='diffusion':
+    medium is mu_a(r) (§3.2, scalar D).  dtype 'c64' (complex64 arrays) or
+    'r32' (float32 arrays, diffusion with real data).
+    """
+
+    def __init__(self, shape: Sequence[int], kind: str = "helmholtz", h: Optional[Sequence[float]] = None,
+                 D: float = 1.0, sigma: complex = 0j, c: complex = 1 + 0j, dtype: str = "c64",
+                 stream=None, device=None):
+        import torch
+
+        self.lib = L.load()
+        self.shape = tuple(int(s) for s in shape)
+        self.ndim = len(self.shape)
+        self.kind = kind
+        self.dtype = dtype
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        d = L.PlanDesc()
+        d.ndim = self.ndim
+        rev = list(reversed(self.shape)) + [1] * (3 - self.ndim)
+        hh = list(reversed(h)) if h is not None else [1.0] * self.ndim
+        hh += [1.0] * (3 - self.ndim)
+        for a in range(3):
+            d.n[a] = rev[a]
+            d.h[a] = float(hh[a])
+        d.medium = L.MEDIUM_K2 if kind == "helmholtz" else L.MEDIUM_W
+        d.dtype = L.C64 if dtype == "c64" else L.R32
+        d.D = float(D)
+        d.sigma = L.c128(float(np.real(sigma)), float(np.imag(sigma)))
+        d.c = L.c128(float(np.real(c)), float(np.imag(c)))
+        d.stream = ctypes.c_void_p(self.stream.cuda_stream)
+        d.nccl_comm = None
+        self.desc = d
+        h_ = ctypes.c_void_p()
+        L.check(self.lib.usp_plan_create(ctypes.byref(d), ctypes.byref(h_)))
+        self.handle = h_
+        nbytes = ctypes.c_size_t()
+        L.check(self.lib.usp_plan_workspace_size(self.handle, ctypes.byref(nbytes)))
+        self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+        L.check(self.lib.usp_plan_set_workspace(self.handle, ctypes.c_void_p(self.workspace.data_ptr()),
+                                                int(nbytes.value)))
+
+    # -- setup ---------------------------------------------------------------
+    def set_potential(self, medium, target_norm: float = 0.95):
+        ptr, where, keep = _ptr_where(medium, self.dtype)
+        L.check(self.lib.usp_set_potential(self.handle, ptr, where, float(target_norm)))
+        del keep
+        return self.split
+
+    @property
+    def split(self) -> Split:
+        s, c, ce = L.c128(), L.c128(), L.c128()
+        r, v = ctypes.c_double(), ctypes.c_double()
+        L.check(self.lib.usp_get_split(self.handle, ctypes.byref(s), ctypes.byref(c), ctypes.byref(ce),
+                                       ctypes.byref(r), ctypes.byref(v)))
+        return Split(complex(s.re, s.im), complex(c.re, c.im), complex(ce.re, ce.im), r.value, v.value)
+
+    def set_source(self, src):
+        ptr, where, keep = _ptr_where(src, self.dtype)
+        L.check(self.lib.usp_set_source(self.handle, ptr, where))
+        del keep
+
+    # -- iteration -----------------------------------------------------------
+    def iterate(self, n_max: int, alpha: float = 0.75, tol: float = 0.0) -> Tuple[int, str]:
+        nd = ctypes.c_int64()
+        term = ctypes.c_int()
+        L.check(self.lib.usp_iterate(self.handle, int(n_max), float(alpha), float(tol), ctypes.byref(nd),
+                                     ctypes.byref(term)))
+        return int(nd.value), _TERM[term.value]
+
+    def residual(self) -> Tuple[float, float, int]:
+        r, a, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        L.check(self.lib.usp_residual(self.handle, ctypes.byref(r), ctypes.byref(a), ctypes.byref(k)))
+        return r.value, a.value, int(k.value)
+
+    def history(self) -> np.ndarray:
+        n = ctypes.c_int64()
+        L.check(self.lib.usp_residual_history(self.handle, None, 0, ctypes.byref(n)))
+        buf = np.zeros(int(n.value), dtype=np.float64)
+        L.check(self.lib.usp_residual_history(self.handle, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                              buf.size, ctypes.byref(n)))
+        return buf
+
+    def get_field(self, out=None):
+        import torch
+
+        if out is None:
+            tdt = torch.complex64 if self.dtype == "c64" else torch.float32
+            out = torch.empty(self.shape, dtype=tdt, device=self.device)
+        ptr, where, keep = _ptr_where(out, self.dtype)
+        L.check(self.lib.usp_get_field(self.handle, ptr, where))
+        return out
+
+    # -- instrumentation -----------------------------------------------------
+    def profile(self, enable: bool = True):
+        L.check(self.lib.usp_profile_enable(self.handle, int(enable)))
+
+    def profile_read(self):
+        cap = 16
+        names = (ctypes.c_char * 32 * cap)()
+        ms = (ctypes.c_double * cap)()
+        cnt = (ctypes.c_int64 * cap)()
+        n = ctypes.c_int()
+        L.check(self.lib.usp_profile_read(self.handle, cap, names, ms, cnt, ctypes.byref(n)))
+        return {bytes(names[i]).split(b"\0", 1)[0].decode(): (ms[i], int(cnt[i])) for i in range(n.value)}
+
+    def launch_count(self) -> int:
+        n = ctypes.c_int64()
+        L.check(self.lib.usp_launch_count(self.handle, ctypes.byref(n)))
+        return int(n.value)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.usp_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve(medium, source, kind: str = "helmholtz", alpha: float = 0.75, tol: float = 0.0, n_iter: int = 100,
+          target_norm: float = 0.95, h=None, D: float = 1.0, dtype: str = "c64", sigma=None, c=None):
+    """Convenience: plan + canonical form + source + Algorithm 1.  Returns
+    (x, n_done, term, plan)."""
+    shape = tuple(np.shape(medium)) if not hasattr(medium, "shape") else tuple(medium.shape)
+    plan = Plan(shape, kind=kind, h=h, D=D, dtype=dtype,
+                sigma=0j if sigma is None else sigma, c=1 + 0j if c is None else c)
+    plan.set_potential(medium, target_norm if sigma is None else -1.0)
+    plan.set_source(source)
+    n, term = plan.iterate(n_iter, alpha, tol)
+    return plan.get_field(), n, term, plan

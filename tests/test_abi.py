@@ -1,0 +1,77 @@
+"""The C-ABI library builds, loads, exports every symbol include/usp.h
+declares, and rejects bad arguments with a status (no GPU needed: no
+compute call is made)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "usp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(usp_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2207_14222_b200 import build as B
+
+    B.build()
+    from paper_2207_14222_b200 import _lib
+
+    return _lib.load()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 17
+    for s in syms:
+        assert hasattr(lib, s), s
+    from paper_2207_14222_b200 import _lib
+
+    assert set(syms) == set(_lib.SIGNATURES), "binding must cover exactly the header"
+
+
+def test_version_and_error_strings(lib):
+    assert lib.usp_version().startswith(b"0.1")
+    assert isinstance(lib.usp_last_error(), bytes)
+
+
+def test_argument_errors_return_status(lib):
+    from paper_2207_14222_b200 import _lib
+
+    h = ctypes.c_void_p()
+    assert lib.usp_plan_create(None, ctypes.byref(h)) == 1            # USP_ERR_ARG
+    d = _lib.PlanDesc()
+    d.ndim = 0
+    assert lib.usp_plan_create(ctypes.byref(d), ctypes.byref(h)) == 1
+    d.ndim, d.D = 2, 1.0
+    d.n[0], d.n[1] = 48, 64                                           # 48: not a power of two
+    d.h[0] = d.h[1] = 1.0
+    assert lib.usp_plan_create(ctypes.byref(d), ctypes.byref(h)) == 5  # USP_ERR_UNSUPPORTED
+    assert b"power of two" in lib.usp_last_error()
+    d.n[0] = 4096
+    assert lib.usp_plan_create(ctypes.byref(d), ctypes.byref(h)) == 5
+    d.n[0], d.D = 64, -1.0
+    assert lib.usp_plan_create(ctypes.byref(d), ctypes.byref(h)) == 1
+    lib.usp_plan_destroy(None)                                        # no-op
+
+
+def test_product_does_not_touch_oracle():
+    """The CUDA product and the oracle share no code and neither imports the
+    other."""
+    pkg = os.path.join(ROOT, "paper_2207_14222_b200")
+    bad_prod = re.compile(r"^\s*(from\s+oracle|import\s+oracle|#\s*include\s+\"[^\"]*oracle)", re.M)
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f), errors="replace").read()
+                assert not bad_prod.search(txt), f
+    bad_orc = re.compile(r"^\s*(from\s+paper_2207_14222_b200|import\s+paper_2207_14222_b200|#\s*include\s+\"[^\"]*(usp\.h|fft_core|kernels))", re.M)
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c", ".h")):
+            assert not bad_orc.search(open(os.path.join(ROOT, "oracle", f)).read()), f
