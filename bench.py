@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""Benchmark of the universal-split-preconditioner hot path on B200.
+
+Metric (BASELINE.json): voxel-iterations/s (device-timed) and % of HBM
+roofline.  Workload at N=1: BASELINE.json configs[4] "C5" -- 3-D Helmholtz
+1024^3 complex64, 100 iterations of Algorithm 1 (the config the north star's
+roofline target is quoted on; it fits one GPU).
+
+One step = the whole hot path over one synthetic input:
+canonical form + V/B setup (a0), source setup (s, Delta_0, n0), and 100
+iterations (a1..a10), inputs resident in HBM.  Inputs (8 GiB each) are far
+larger than L2 (126 MB), so no explicit flush is needed.
+
+--impl reference runs the CPU oracle (oracle/, complex128, plain C + OpenMP)
+on a bounded sample of the same workload on the host cores (this tier has no
+installable reference implementation; the oracle is the reference arm).
+
+Multi-GPU (torchrun, one process per GPU): the slab-decomposed NCCL path is
+not built yet; N>1 runs one independent C5 solve per GPU ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxel-iterations/s (device-timed) and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "voxel-iterations/s"
+
+# Algorithmic HBM bytes per voxel and launch of each kernel class (DESIGN.md
+# "Kernels and their rooflines"): complex64 = 8 B per value.
+KERNEL_BYTES = {
+    "xpass": 56,            # read work, Delta, x, B; write Delta, x, work
+    "y_fwd": 16,            # read + write work
+    "z_fwd_mul_inv": 16,
+    "y_inv": 16,
+    "y_fwd_mul_inv": 16,
+}
+ITER_BYTES_3D = 104         # 56 + 3 * 16 (SURVEY.md §8 geometry table)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl" if args.impl == "usp" else "gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(world, v: float) -> float:
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    --set full capture summary (profiles/), if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------- oracle --
+def cpu_oracle_sample(shape=(256, 256, 256), iters=2):
+    """The oracle as it stands (x-form Alg. 1, c128) on a bounded sample of the
+    C5 recipe; returns (vox-it/s, seconds, threads, description)."""
+    from oracle import oracle as O
+    from synth import make
+
+    O.build()
+    p = make("C5", shape)
+    med = p.medium.astype("complex64").astype("complex128")
+    sp = O.canonical(p.kind, med)
+    w = O.medium_to_w(p.kind, med)
+    t0 = time.perf_counter()
+    res = O.fixed_point(w, p.source, p.h, sp.D, sp.sigma, sp.c, 0.75, 0.0, iters)
+    dt = time.perf_counter() - t0
+    nvox = p.n_vox
+    return nvox * res.n_done / dt, dt, O.num_threads(), (
+        f"oracle x-form Alg. 1 (complex128) on the C5 recipe at {shape[0]}^3 "
+        f"(lambda=8, GRF ell=4, seed 3), {iters} iterations incl. its setup FFT round trip")
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    cfg = {"workload": "C5 recipe sample for the CPU oracle", "grid": [256, 256, 256], "iterations_per_step": 1}
+    from oracle import oracle as O
+    from synth import make
+
+    O.build()
+    p = make("C5", (256, 256, 256))
+    med = p.medium.astype("complex64").astype("complex128")
+    sp = O.canonical(p.kind, med)
+    w = O.medium_to_w(p.kind, med)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.fixed_point(w, p.source, p.h, sp.D, sp.sigma, sp.c, 0.75, 0.0, 1)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    # one oracle call = setup round trip + 1 iteration = 2 applications of (L+1)^-1
+    value = p.n_vox * args.steps / tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+                             "sample": "1 iteration of Alg. 1 (x-form, complex128) incl. the n0 setup FFT round "
+                                       "trip on the C5 recipe at 256^3 per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------------- GPU --
+def run_usp(args, world, rank, local):
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2207_14222_b200 import Plan
+    from synth import make
+
+    name = args.config
+    p = make(name, None if args.size is None else (args.size,) * 3, device=str(dev))
+    shape = p.shape
+    n_iter = args.iters if args.iters else p.n_iter
+    med = p.medium.to(torch.complex64)
+    src = p.source.to(torch.complex64)
+    del p.medium, p.source
+    torch.cuda.empty_cache()
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        plan = Plan(shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev)
+    nvox = int(np.prod(shape))
+
+    def step(m, s, where_host=False, out=None):
+        plan.set_potential(m, 0.95)
+        plan.set_source(s)
+        n, term = plan.iterate(n_iter, p.alpha, 0.0)
+        assert n == n_iter, (n, term)
+        if out is not None:
+            plan.get_field(out)
+
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step(med, src)
+    # ------------------------------------------------ timed region (device)
+    sampler = ClockSampler(local)
+    plan.profile(True)
+    l0 = plan.launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(med, src)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    launches = plan.launch_count() - l0
+    prof = plan.profile_read()
+    plan.profile(False)
+    ms_max = max_over_ranks(world, ms)
+    value = nvox * n_iter * args.steps * world / (ms_max / 1e3)
+
+    # dominant kernel roofline (algorithmic bytes / its average launch time)
+    hbm, peak_kind = peaks()
+    dom = max(((k, v) for k, v in prof.items() if k in KERNEL_BYTES), key=lambda kv: kv[1][0])
+    dname, (dms, dcount) = dom
+    dbytes = KERNEL_BYTES[dname] * nvox
+    achieved = dbytes / (dms / dcount / 1e3) / 1e9
+    traffic = ncu_traffic().get(dname)
+    iter_ms = sum(v[0] for k, v in prof.items() if k in KERNEL_BYTES) / (n_iter * args.steps + args.steps)
+    kernel_share = {k: round(v[0] / sum(x[0] for x in prof.values()), 4) for k, v in prof.items()}
+
+    # ------------------------------------------------ e2e (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        h_med = torch.empty(shape, dtype=torch.complex64, pin_memory=True)
+        h_src = torch.empty(shape, dtype=torch.complex64, pin_memory=True)
+        h_out = torch.empty(shape, dtype=torch.complex64, pin_memory=True)
+        h_med.copy_(med)
+        h_src.copy_(src)
+        del med, src
+        torch.cuda.empty_cache()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        step(h_med, h_src, out=h_out)   # warm the host path
+        barrier(world)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(e2e_steps):
+            step(h_med, h_src, out=h_out)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(world, f0.elapsed_time(f1))
+        e2e = {"value": nvox * n_iter * e2e_steps * world / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * nvox * 8, "d2h_bytes_per_step": nvox * 8, "steps": e2e_steps}
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, dt, thr, desc = cpu_oracle_sample()
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
+    it_bytes = ITER_BYTES_3D * nvox
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "config": {"workload": f"{name} 3-D Helmholtz {shape[2]}x{shape[1]}x{shape[0]} complex64, "
+                               f"{n_iter} iterations of Alg. 1 per step (setup + iterations), alpha=0.75",
+                   "grid": list(shape), "iterations_per_step": n_iter,
+                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas",
+                   "l2": "inputs (8 GiB fields) larger than L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": dbytes, "avg_launch_ms": dms / dcount},
+        "iteration_roofline": {"bytes_per_voxel": ITER_BYTES_3D, "iter_ms": iter_ms,
+                               "achieved_gbs": it_bytes / (iter_ms / 1e3) / 1e9,
+                               "frac": it_bytes / (iter_ms / 1e3) / 1e9 / hbm},
+        "kernel_share": kernel_share,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="usp", choices=["usp", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--size", type=int, default=None, help="override cubic grid edge (debug)")
+    ap.add_argument("--iters", type=int, default=None)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        rc = run_reference(args, world, rank)
+    else:
+        rc = run_usp(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

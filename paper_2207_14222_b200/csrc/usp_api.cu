@@ -593,10 +593,9 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
                 CU(launch_xpass((int)p->nx, X_ITER, xp, p->grid_x, p->stream));
             }
             launched += nb;
-            if (tol > 0.0 || p->prof) {
+            if (tol > 0.0) {
                 s = sync_state(p);
                 if (s) return s;
-                drain_timing(p);
                 const int stt = p->st_host->status;
                 if (stt == ST_DONE_CONV || stt == ST_DIVERGED) break;
             }
