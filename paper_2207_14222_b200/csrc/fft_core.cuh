@@ -129,29 +129,42 @@ __device__ __forceinline__ void dft(float2 *v) {
     }
 }
 
-// Shared-memory layouts for the exchange step.
+// Shared-memory layouts for the exchange step.  A layout maps (n1, k2) of
+// the calling thread's line to a float2 offset and knows which threads share
+// the line (sync()).
 // Contiguous lines (x axis): one buffer per line, rows n1 padded to N2+1
-// float2 (odd stride: conflict-free 64-bit phases of 16 lanes).
+// float2 (odd stride: conflict-free 64-bit phases of 16 lanes); the line
+// lives inside one warp, so __syncwarp orders the exchange.
 template <int N>
 struct LayRow {
     float2 *base;  // this line's buffer: N1*(N2+1) float2
     __device__ __forceinline__ int off(int n1, int k2) const { return n1 * (LineGeo<N>::N2 + 1) + k2; }
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
     static constexpr int kFloat2PerLine = LineGeo<N>::N1 * (LineGeo<N>::N2 + 1);
 };
 // Strided lines (y, z axes): COLS columns interleaved innermost, so the 16
-// lanes of a 64-bit phase hit 16 consecutive float2.
-template <int N, int COLS>
+// lanes of a 64-bit phase hit consecutive float2; PAD float2 per n1 row keep
+// two rows of an 8-column tile on different banks.  BAR = 0: the whole CTA
+// shares the tile (__syncthreads); BAR = NT > 0: named barrier 1 over NT
+// consumer threads.
+template <int N, int COLS, int PAD, int BAR>
 struct LayCol {
-    float2 *base;  // tile buffer: N*COLS float2
+    float2 *base;
     int c;
-    __device__ __forceinline__ int off(int n1, int k2) const { return (n1 * LineGeo<N>::N2 + k2) * COLS + c; }
+    __device__ __forceinline__ int off(int n1, int k2) const {
+        return n1 * (LineGeo<N>::N2 * COLS + PAD) + k2 * COLS + c;
+    }
+    __device__ __forceinline__ void sync() const {
+        if constexpr (BAR == 0) __syncthreads();
+        else asm volatile("bar.sync 1, %0;" ::"n"(BAR) : "memory");
+    }
+    static constexpr int kFloat2 = LineGeo<N>::N1 * (LineGeo<N>::N2 * COLS + PAD);
 };
 
 // Four-step FFT of one line.  On entry v[n2] = x[j + N1*n2]; on exit
 // v[m] = X[j + N1*m] (unnormalised DFT, sign - for forward, + for INV).
 // tw[k2*N1 + j] = W_N^(j*k2) (forward); the inverse uses its conjugate.
-// SYNC: 0 -> __syncwarp (line within one warp), 1 -> __syncthreads.
-template <int N, bool INV, int SYNC, class Lay>
+template <int N, bool INV, class Lay>
 __device__ __forceinline__ void fft_line(float2 (&v)[LineGeo<N>::N2], const Lay &lay, int j,
                                          const float2 *__restrict__ tw) {
     using G = LineGeo<N>;
@@ -163,12 +176,12 @@ __device__ __forceinline__ void fft_line(float2 (&v)[LineGeo<N>::N2], const Lay 
     }
 #pragma unroll
     for (int k2 = 0; k2 < G::N2; ++k2) lay.base[lay.off(j, k2)] = v[k2];
-    if (SYNC) __syncthreads(); else __syncwarp();
+    lay.sync();
 #pragma unroll
     for (int t = 0; t < G::R; ++t)
 #pragma unroll
         for (int n1 = 0; n1 < G::N1; ++n1) v[t * G::N1 + n1] = lay.base[lay.off(n1, j + G::N1 * t)];
-    if (SYNC) __syncthreads(); else __syncwarp();
+    lay.sync();
 #pragma unroll
     for (int t = 0; t < G::R; ++t) dft<G::N1, INV>(v + t * G::N1);
     if constexpr (G::R > 1) {

@@ -1,0 +1,96 @@
+// kcommon.cuh -- device helpers shared by the pass kernels: deterministic
+// reductions, the last-CTA-done residual reduction, and the Fourier
+// multiplier of (L+1)^-1 (Eq. 12).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fft_core.cuh"
+#include "usp_internal.h"
+
+namespace usp {
+
+// ------------------------------------------------------------ helpers --
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-order CTA reduction of one double per thread; result valid in tid 0.
+template <int NT>
+__device__ __forceinline__ double block_sum_d(double v, double *sh) {
+    v = warp_sum_d(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) s += sh[i];
+    }
+    __syncthreads();
+    return s;
+}
+
+// Last-CTA-done reduction: every CTA contributes `mine` (valid in tid 0);
+// returns true in the last CTA, where *total holds the fixed-order sum.
+template <int NT>
+__device__ __forceinline__ bool last_block_total(double mine, IterState *st, double *partials, double *sh,
+                                 double *total) {
+    __shared__ int am_last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = mine;
+        __threadfence();
+        const unsigned t = atomicAdd(&st->counter, 1u);
+        am_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!am_last) return false;
+    __threadfence();
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) s += __ldcg(&partials[i]);
+    s = block_sum_d<NT>(s, sh);
+    if (threadIdx.x == 0) {
+        *total = s;
+        st->counter = 0u;
+    }
+    return true;
+}
+
+// Fourier multiplier g(p)/N_vox of (L+1)^-1 (Eq. 12, unified form R-1):
+//   g = c / (D |p|^2 + sigma + c)
+__device__ __forceinline__ float2 multiplier(const MulParams &mp, float p2) {
+    const float dr = fmaf(mp.D, p2, mp.sc.x), di = mp.sc.y;
+    const float inv = 1.0f / fmaf(dr, dr, di * di);
+    return make_float2((mp.cn.x * dr + mp.cn.y * di) * inv, (mp.cn.y * dr - mp.cn.x * di) * inv);
+}
+
+__device__ __forceinline__ float freq_m(int k, int n) { return (float)(k < (n >> 1) ? k : k - n); }
+
+// Thread 0 of the last CTA of an x pass: publish n0 (source setup) or
+// r_{k+1} and the stop decision (iteration), see kernels.cu header.
+__device__ __forceinline__ void finish_xpass(bool src_epi, bool xonly, double total, IterState *st,
+                                             const Red &red) {
+    if (src_epi) {
+        const double n0 = sqrt(total);
+        st->n0 = n0;
+        st->r = (n0 > 0.0) ? 1.0 : 0.0;
+        st->k = 0;
+        st->status = (n0 > 0.0) ? ST_RUNNING : ST_DONE_CONV;
+        red.hist[0] = st->r;
+        return;
+    }
+    const long long k1 = st->k + 1;
+    st->k = k1;
+    if (xonly) {                       // the final update x_{k+1} = x_k + alpha Delta_k
+        st->status = ST_DONE_CONV;
+        return;
+    }
+    const double r = sqrt(total) / st->n0;
+    st->r = r;
+    red.hist[k1 % red.hist_cap] = r;
+    if (!(r <= 1e6)) st->status = ST_DIVERGED;            // NaN, Inf or r > 1e6
+    else if (st->tol > 0.0 && r < st->tol) st->status = ST_STOP_PENDING;
+}
+
+}  // namespace usp

@@ -24,67 +24,10 @@
 #include <stdint.h>
 
 #include "fft_core.cuh"
+#include "kcommon.cuh"
 #include "usp_internal.h"
 
 namespace usp {
-
-// ------------------------------------------------------------ helpers --
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Fixed-order CTA reduction of one double per thread; result valid in tid 0.
-template <int NT>
-__device__ __forceinline__ double block_sum_d(double v, double *sh) {
-    v = warp_sum_d(v);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) sh[w] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int i = 0; i < NT / 32; ++i) s += sh[i];
-    }
-    __syncthreads();
-    return s;
-}
-
-// Last-CTA-done reduction: every CTA contributes `mine` (valid in tid 0);
-// returns true in the last CTA, where *total holds the fixed-order sum.
-template <int NT>
-__device__ bool last_block_total(double mine, IterState *st, double *partials, double *sh,
-                                 double *total) {
-    __shared__ int am_last;
-    if (threadIdx.x == 0) {
-        partials[blockIdx.x] = mine;
-        __threadfence();
-        const unsigned t = atomicAdd(&st->counter, 1u);
-        am_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!am_last) return false;
-    __threadfence();
-    double s = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) s += __ldcg(&partials[i]);
-    s = block_sum_d<NT>(s, sh);
-    if (threadIdx.x == 0) {
-        *total = s;
-        st->counter = 0u;
-    }
-    return true;
-}
-
-// Fourier multiplier g(p)/N_vox of (L+1)^-1 (Eq. 12, unified form R-1):
-//   g = c / (D |p|^2 + sigma + c)
-__device__ __forceinline__ float2 multiplier(const MulParams &mp, float p2) {
-    const float dr = fmaf(mp.D, p2, mp.sc.x), di = mp.sc.y;
-    const float inv = 1.0f / fmaf(dr, dr, di * di);
-    return make_float2((mp.cn.x * dr + mp.cn.y * di) * inv, (mp.cn.y * dr - mp.cn.x * di) * inv);
-}
-
-__device__ __forceinline__ float freq_m(int k, int n) { return (float)(k < (n >> 1) ? k : k - n); }
 
 // ================================================================ x pass ==
 template <int N>
@@ -151,7 +94,7 @@ __global__ void __launch_bounds__(256) k_xpass(XParams p) {
 #pragma unroll
             for (int m = 0; m < G::N2; ++m)
                 v[m] = valid ? p.work[base + (long long)G::N1 * m] : make_float2(0.f, 0.f);
-            fft_line<N, true, 0>(v, lay, j, p.tw);   // x inverse: v = (L+1)^-1 u
+            fft_line<N, true>(v, lay, j, p.tw);   // x inverse: v = (L+1)^-1 u
             float lacc = 0.f;
 #pragma unroll
             for (int m = 0; m < G::N2; ++m) {
@@ -180,7 +123,7 @@ __global__ void __launch_bounds__(256) k_xpass(XParams p) {
             }
             acc += (double)lacc;
         }
-        fft_line<N, false, 0>(v, lay, j, p.tw);   // x forward
+        fft_line<N, false>(v, lay, j, p.tw);   // x forward
         if (valid) {
 #pragma unroll
             for (int m = 0; m < G::N2; ++m) p.work[base + (long long)G::N1 * m] = v[m];
@@ -192,28 +135,7 @@ __global__ void __launch_bounds__(256) k_xpass(XParams p) {
     const double mine = block_sum_d<XG::NT>(acc, sh_red);
     if (!last_block_total<XG::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
     if (threadIdx.x != 0) return;
-    IterState *st = p.st;
-    if (MODE == X_SRC_EPI) {
-        const double n0 = sqrt(total);
-        st->n0 = n0;
-        st->r = (n0 > 0.0) ? 1.0 : 0.0;
-        st->k = 0;
-        st->status = (n0 > 0.0) ? ST_RUNNING : ST_DONE_CONV;
-        if (n0 > 0.0 && st->tol > 0.0 && 1.0 < st->tol) st->status = ST_STOP_PENDING;
-        p.red.hist[0] = st->r;
-        return;
-    }
-    const long long k1 = st->k + 1;
-    st->k = k1;
-    if (xonly) {
-        st->status = ST_DONE_CONV;
-        return;
-    }
-    const double r = sqrt(total) / st->n0;
-    st->r = r;
-    p.red.hist[k1 % p.red.hist_cap] = r;
-    if (!(r <= 1e6)) st->status = ST_DIVERGED;            // NaN, Inf or r > 1e6
-    else if (st->tol > 0.0 && r < st->tol) st->status = ST_STOP_PENDING;
+    finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red);
 }
 
 // ========================================================== strided pass ==
@@ -224,15 +146,6 @@ struct SGeo {
     static constexpr int NT = COLS * G::N1;
     static constexpr int PITCH = G::N2 * COLS + (COLS == 16 ? 0 : 8);   // float2 per n1 row
     static constexpr int SMEM = G::N1 * PITCH * (int)sizeof(float2);
-};
-
-template <int N, int COLS, int PAD>
-struct LayColP {
-    float2 *base;
-    int c;
-    __device__ __forceinline__ int off(int n1, int k2) const {
-        return n1 * (LineGeo<N>::N2 * COLS + PAD) + k2 * COLS + c;
-    }
 };
 
 template <int N, int MODE>
@@ -247,7 +160,7 @@ __global__ void __launch_bounds__(SGeo<N>::NT) k_strided(SParams p) {
         const int status = p.st->status;
         if (status != ST_RUNNING || p.st->k >= p.st->kmax) return;
     }
-    const LayColP<N, COLS, (COLS == 16 ? 0 : 8)> lay{smem, c};
+    const LayCol<N, COLS, (COLS == 16 ? 0 : 8), 0> lay{smem, c};
     const long long tpo = p.ncols / COLS;
     const long long ntiles = tpo * p.nouter;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -257,7 +170,7 @@ __global__ void __launch_bounds__(SGeo<N>::NT) k_strided(SParams p) {
         float2 v[G::N2];
 #pragma unroll
         for (int m = 0; m < G::N2; ++m) v[m] = p.data[base + (long long)(j + G::N1 * m) * p.stride];
-        fft_line<N, MODE == S_INV, 1>(v, lay, j, p.tw);
+        fft_line<N, MODE == S_INV>(v, lay, j, p.tw);
         if (MODE == S_FWD_MUL_INV) {
             // (L+1)^-1 multiplier, Eq. 12: |p|^2 = px^2 + py^2 + p_line^2
             float pt2;
@@ -275,7 +188,7 @@ __global__ void __launch_bounds__(SGeo<N>::NT) k_strided(SParams p) {
                 const float pl = kl * freq_m(j + G::N1 * m, N);
                 v[m] = cmul(v[m], multiplier(p.mp, fmaf(pl, pl, pt2)));
             }
-            fft_line<N, true, 1>(v, lay, j, p.tw);
+            fft_line<N, true>(v, lay, j, p.tw);
         }
 #pragma unroll
         for (int m = 0; m < G::N2; ++m) p.data[base + (long long)(j + G::N1 * m) * p.stride] = v[m];
@@ -314,9 +227,9 @@ __global__ void __launch_bounds__(LineGeo<N>::N1) k_solve1d(OneParams p) {
             const float2 sv = p.src_real ? make_float2(reinterpret_cast<const float *>(p.x)[i], 0.f) : p.x[i];
             v[m] = cmul(sv, p.inv_c);
         }
-        fft_line<N, false, 0>(v, lay, j, p.tw);
+        fft_line<N, false>(v, lay, j, p.tw);
         mul_line<N>(v, p.mp, j);
-        fft_line<N, true, 0>(v, lay, j, p.tw);
+        fft_line<N, true>(v, lay, j, p.tw);
         float lacc = 0.f;
 #pragma unroll
         for (int m = 0; m < G::N2; ++m) {
@@ -351,9 +264,9 @@ __global__ void __launch_bounds__(LineGeo<N>::N1) k_solve1d(OneParams p) {
     while (k < kmax && status == ST_RUNNING) {
 #pragma unroll
         for (int m = 0; m < G::N2; ++m) v[m] = cmul(b[m], d[m]);
-        fft_line<N, false, 0>(v, lay, j, p.tw);
+        fft_line<N, false>(v, lay, j, p.tw);
         mul_line<N>(v, p.mp, j);
-        fft_line<N, true, 0>(v, lay, j, p.tw);
+        fft_line<N, true>(v, lay, j, p.tw);
         float lacc = 0.f;
 #pragma unroll
         for (int m = 0; m < G::N2; ++m) {

@@ -1,9 +1,11 @@
 // usp_api.cu -- the C-ABI of include/usp.h: plan, workspace, setup and the
 // iteration driver.  All arithmetic of the method runs in kernels.cu; this
 // file only sequences launches, validates, and moves bytes.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -78,6 +80,11 @@ struct usp_plan_s {
     bool have_potential = false, have_source = false;
     // launch configuration
     int grid_x = 0, grid_y = 0, grid_z = 0;
+    // TMA-pipelined kernels (default); USP_LEGACY=1 selects the register-staged ones
+    bool pipe = true, pipe_xk = true;
+    bool pipe_y = false, pipe_z = false;
+    int gridp_x = 0, gridp_y = 0, gridp_z = 0;
+    CUtensorMap map_y{}, map_z{};
     // profiling
     bool prof = false;
     std::vector<Timed> timed;
@@ -135,6 +142,43 @@ void drain_timing(usp_plan_s *p) {
 }
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+int log2ll(long long n) {
+    int l = 0;
+    while ((1LL << l) < n) ++l;
+    return l;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+// Tensor map over the complex64 work field viewed with 8-byte elements.
+bool make_map(CUtensorMap *m, void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides_bytes,
+              const cuuint32_t *box) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapL2promotion promo = (box[0] * 8 >= 128) ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                              : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, base, dims, strides_bytes, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 std::vector<float2> twiddle_table(int n) {
     // tw[k2*N1 + j] = W_n^(j*k2) = exp(-2 pi i j k2 / n), computed in double
@@ -302,36 +346,45 @@ XParams x_params(usp_plan_s *p) {
     return xp;
 }
 
+usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
+    Tick t(p, KC_XPASS);
+    if (p->pipe_xk) CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream));
+    else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
+    return USP_OK;
+}
+
+usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, bool use_pipe, int rank, const CUtensorMap &map,
+                       const SParams &sp, int grid_legacy, int grid_pipe) {
+    Tick t(p, cls);
+    if (use_pipe) CU(launch_strided_pipe(n, mode, rank, map, sp, grid_pipe, p->stream));
+    else CU(launch_strided(n, mode, sp, grid_legacy, p->stream));
+    return USP_OK;
+}
+
 // The middle of the chain: every FFT pass between the x forward and the x
 // inverse, with the (L+1)^-1 multiplier on the last axis.
 usp_status chain_mid(usp_plan_s *p, int check_state) {
     const MulParams mp = mul_params(p);
     if (p->ndim == 2) {
         SParams sp{p->work, p->tw[1], p->nx, p->nx, 1, 0, 1, check_state, mp, p->st};
-        Tick t(p, KC_YMUL2D);
-        CU(launch_strided((int)p->ny, S_FWD_MUL_INV, sp, p->grid_y, p->stream));
-        return USP_OK;
+        return run_strided(p, KC_YMUL2D, (int)p->ny, S_FWD_MUL_INV, p->pipe_y, 2, p->map_y, sp, p->grid_y,
+                           p->gridp_y);
     }
     SParams yf{p->work, p->tw[1], p->nx, p->nx, p->nz, p->nx * p->ny, 1, check_state, mp, p->st};
     SParams zm{p->work, p->tw[2], p->nx * p->ny, p->nx * p->ny, 1, 0, 2, check_state, mp, p->st};
-    {
-        Tick t(p, KC_YFWD);
-        CU(launch_strided((int)p->ny, S_FWD, yf, p->grid_y, p->stream));
-    }
-    {
-        Tick t(p, KC_ZMUL);
-        CU(launch_strided((int)p->nz, S_FWD_MUL_INV, zm, p->grid_z, p->stream));
-    }
-    {
-        Tick t(p, KC_YINV);
-        CU(launch_strided((int)p->ny, S_INV, yf, p->grid_y, p->stream));
-    }
-    return USP_OK;
+    usp_status s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, p->pipe_y, 3, p->map_y, yf, p->grid_y, p->gridp_y);
+    if (s) return s;
+    s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, p->pipe_z, 2, p->map_z, zm, p->grid_z, p->gridp_z);
+    if (s) return s;
+    return run_strided(p, KC_YINV, (int)p->ny, S_INV, p->pipe_y, 3, p->map_y, yf, p->grid_y, p->gridp_y);
 }
 
 usp_status sync_state(usp_plan_s *p) {
     CU(cudaMemcpyAsync(p->st_host, p->st, sizeof(IterState), cudaMemcpyDeviceToHost, p->stream));
     CU(cudaStreamSynchronize(p->stream));
+    if (p->st_host->err)
+        return fail(USP_ERR_CUDA, "pipeline watchdog: a kernel gave up waiting (code %d, unit %d)",
+                    p->st_host->err, p->st_host->err_info);
     return USP_OK;
 }
 
@@ -383,7 +436,19 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (p->ndim >= 2) p->grid_y = occ_grid(p, (p->nx / (p->ny >= 2048 ? 8 : 16)) * p->nz, 2);
         if (p->ndim >= 3) p->grid_z = occ_grid(p, (p->nx * p->ny) / (p->nz >= 2048 ? 8 : 16), 2);
     }
-    p->partials_cap = std::max(1, p->grid_x);
+    {
+        const char *leg = std::getenv("USP_LEGACY");
+        p->pipe = !(leg && leg[0] == '1');
+        const char *px = std::getenv("USP_PIPE_X");
+        p->pipe_xk = p->pipe && !(px && px[0] == '0');
+        const int u = 32 / (1 << (log2ll(p->nx) / 2));   // x lines per warp unit (32 / N1)
+        p->gridp_x = occ_grid(p, (p->ny * p->nz) / u, 1);
+        if (p->ndim >= 2)
+            p->gridp_y = occ_grid(p, (p->nx / strided_pipe_cols((int)p->ny)) * p->nz, 1);
+        if (p->ndim >= 3)
+            p->gridp_z = occ_grid(p, (p->nx * p->ny) / strided_pipe_cols((int)p->nz), 1);
+    }
+    p->partials_cap = std::max(1, std::max(p->grid_x, p->gridp_x));
     p->far_cap = p->nsm * 8;
     std::vector<float2> twh[3];
     const long long ext[3] = {p->nx, p->ny, p->nz};
@@ -435,6 +500,28 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     p->B = (float2 *)(p->ws + 2 * f);
     p->work = (float2 *)(p->ws + 3 * f);
     p->have_potential = p->have_source = false;
+    p->pipe_y = p->pipe_z = false;
+    if (p->pipe && p->ndim >= 2 && strided_pipe_supported(p->ny)) {
+        const cuuint32_t cy = (cuuint32_t)strided_pipe_cols((int)p->ny), by = (cuuint32_t)strided_pipe_box((int)p->ny);
+        if (p->ndim == 2) {
+            const cuuint64_t dims[2] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny};
+            const cuuint64_t str[1] = {(cuuint64_t)p->nx * 8};
+            const cuuint32_t box[2] = {cy, by};
+            p->pipe_y = make_map(&p->map_y, p->work, 2, dims, str, box);
+        } else {
+            const cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)p->nz};
+            const cuuint64_t str[2] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nx * p->ny) * 8};
+            const cuuint32_t box[3] = {cy, by, 1};
+            p->pipe_y = make_map(&p->map_y, p->work, 3, dims, str, box);
+        }
+    }
+    if (p->pipe && p->ndim == 3 && strided_pipe_supported(p->nz)) {
+        const cuuint32_t cz = (cuuint32_t)strided_pipe_cols((int)p->nz), bz = (cuuint32_t)strided_pipe_box((int)p->nz);
+        const cuuint64_t dims[2] = {(cuuint64_t)(p->nx * p->ny), (cuuint64_t)p->nz};
+        const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};
+        const cuuint32_t box[2] = {cz, bz};
+        p->pipe_z = make_map(&p->map_z, p->work, 2, dims, str, box);
+    }
     return USP_OK;
 }
 
@@ -538,16 +625,12 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         CU(launch_solve1d((int)p->nx, O_SETUP, op, p->stream));
     } else {
         XParams xp = x_params(p);
-        {
-            Tick t(p, KC_XPASS);
-            CU(launch_xpass((int)p->nx, X_SRC_FWD, xp, p->grid_x, p->stream));
-        }
+        s = run_xpass(p, X_SRC_FWD, xp);
+        if (s) return s;
         s = chain_mid(p, 0);
         if (s) return s;
-        {
-            Tick t(p, KC_XPASS);
-            CU(launch_xpass((int)p->nx, X_SRC_EPI, xp, p->grid_x, p->stream));
-        }
+        s = run_xpass(p, X_SRC_EPI, xp);
+        if (s) return s;
     }
     s = sync_state(p);
     if (s) return s;
@@ -589,8 +672,8 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
             for (long long i = 0; i < nb; ++i) {
                 s = chain_mid(p, 1);
                 if (s) return s;
-                Tick t(p, KC_XPASS);
-                CU(launch_xpass((int)p->nx, X_ITER, xp, p->grid_x, p->stream));
+                s = run_xpass(p, X_ITER, xp);
+                if (s) return s;
             }
             launched += nb;
             if (tol > 0.0) {

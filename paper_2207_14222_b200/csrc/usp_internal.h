@@ -1,6 +1,7 @@
 // usp_internal.h -- structures shared by the kernels (kernels.cu) and the
 // plan/driver (usp_api.cu).  Not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,6 +26,8 @@ struct IterState {
     long long kmax;      // absolute iteration limit of the running iterate call
     int status;
     unsigned int counter;  // last-block-done counter (reset by the last block)
+    int err;               // pipeline watchdog: non-zero = a kernel gave up waiting (see tma.cuh)
+    int err_info;
 };
 
 struct Red {             // reduction scratch (device)
@@ -119,6 +122,14 @@ cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_
 cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
+
+// TMA-pipelined variants (kernels_pipe.cu)
+cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);
+cudaError_t launch_strided_pipe(int N, SMode mode, int rank, const CUtensorMap &map, const SParams &p, int grid,
+                                cudaStream_t s);
+bool strided_pipe_supported(long long n);
+int strided_pipe_cols(int N);
+int strided_pipe_box(int N);
 
 int xpass_threads(int N);          // threads per CTA of the x pass
 int xpass_lines_per_cta(int N);
