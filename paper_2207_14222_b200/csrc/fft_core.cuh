@@ -129,6 +129,14 @@ __device__ __forceinline__ void dft(float2 *v) {
     }
 }
 
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+
+// Copy the N-entry four-step twiddle table into shared memory (all threads).
+template <int N>
+__device__ __forceinline__ void load_twiddles(float2 *sm_tw, const float2 *__restrict__ tw) {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) sm_tw[i] = __ldg(&tw[i]);
+}
+
 // Shared-memory layouts for the exchange step.  A layout maps (n1, k2) of
 // the calling thread's line to a float2 offset and knows which threads share
 // the line (sync()).
@@ -164,14 +172,16 @@ struct LayCol {
 // Four-step FFT of one line.  On entry v[n2] = x[j + N1*n2]; on exit
 // v[m] = X[j + N1*m] (unnormalised DFT, sign - for forward, + for INV).
 // tw[k2*N1 + j] = W_N^(j*k2) (forward); the inverse uses its conjugate.
-template <int N, bool INV, class Lay>
+// TWS: the twiddle table lives in shared memory (plain loads) instead of
+// global memory (read-only path).
+template <int N, bool INV, class Lay, bool TWS = false>
 __device__ __forceinline__ void fft_line(float2 (&v)[LineGeo<N>::N2], const Lay &lay, int j,
                                          const float2 *__restrict__ tw) {
     using G = LineGeo<N>;
     dft<G::N2, INV>(v);
 #pragma unroll
     for (int k2 = 1; k2 < G::N2; ++k2) {
-        const float2 w = __ldg(&tw[k2 * G::N1 + j]);
+        const float2 w = TWS ? tw[k2 * G::N1 + j] : __ldg(&tw[k2 * G::N1 + j]);
         v[k2] = INV ? cmulc(v[k2], w) : cmul(v[k2], w);
     }
 #pragma unroll

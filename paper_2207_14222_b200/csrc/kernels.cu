@@ -139,59 +139,86 @@ __global__ void __launch_bounds__(256) k_xpass(XParams p) {
 }
 
 // ========================================================== strided pass ==
-template <int N>
+// Strided axes (y: stride nx, z: stride nx*ny).  A CTA transforms tiles of
+// COLS adjacent columns x N rows; thread (c, j) owns column c and rows
+// j + N1*m.  A warp load/store touches 32/COLS rows of COLS*8 contiguous
+// bytes.  COLS = 8 with N1 = 32 gives 256-thread CTAs, two per SM, so one
+// CTA's loads overlap the other's FFT arithmetic.  The inverse transform is
+// computed as conj(DFT(conj(.))) so a single FFT body is compiled and the
+// kernel stays inside the instruction cache; twiddles are read from smem.
+template <int N, int COLS>
 struct SGeo {
     using G = LineGeo<N>;
-    static constexpr int COLS = (N >= 2048) ? 8 : 16;
     static constexpr int NT = COLS * G::N1;
-    static constexpr int PITCH = G::N2 * COLS + (COLS == 16 ? 0 : 8);   // float2 per n1 row
-    static constexpr int SMEM = G::N1 * PITCH * (int)sizeof(float2);
+    static constexpr int PAD = (COLS == 16 || COLS == 32) ? 0 : 8;
+    static constexpr int PITCH = G::N2 * COLS + PAD;                    // float2 per n1 row
+    static constexpr int SMEM = (G::N1 * PITCH + N) * (int)sizeof(float2);   // exchange + twiddles
+    static constexpr int MINB = (NT <= 256) ? 2 : 1;
 };
 
-template <int N, int MODE>
-__global__ void __launch_bounds__(SGeo<N>::NT) k_strided(SParams p) {
+template <int N, int MODE, int COLS>
+__global__ void __launch_bounds__(SGeo<N, COLS>::NT, SGeo<N, COLS>::MINB) k_strided(SParams p) {
     using G = LineGeo<N>;
-    using SG = SGeo<N>;
-    constexpr int COLS = SG::COLS;
+    using SG = SGeo<N, COLS>;
     extern __shared__ float2 smem[];
+    float2 *sm_tw = smem + G::N1 * SG::PITCH;
     const int tid = threadIdx.x;
     const int c = tid % COLS, j = tid / COLS;
     if (p.check_state) {
         const int status = p.st->status;
         if (status != ST_RUNNING || p.st->k >= p.st->kmax) return;
     }
-    const LayCol<N, COLS, (COLS == 16 ? 0 : 8), 0> lay{smem, c};
+    load_twiddles<N>(sm_tw, p.tw);
+    __syncthreads();
+    const LayCol<N, COLS, SG::PAD, 0> lay{smem, c};
     const long long tpo = p.ncols / COLS;
     const long long ntiles = tpo * p.nouter;
+    constexpr int NPASS = (MODE == S_FWD_MUL_INV) ? 2 : 1;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long o = tile / tpo;
         const long long col = (tile - o * tpo) * COLS + c;
-        const long long base = o * p.ostride + col;
+        const float2 *lb = p.data + (o * p.ostride + col) + (long long)j * p.stride;
+        const long long lstep = (long long)G::N1 * p.stride;
         float2 v[G::N2];
 #pragma unroll
-        for (int m = 0; m < G::N2; ++m) v[m] = p.data[base + (long long)(j + G::N1 * m) * p.stride];
-        fft_line<N, MODE == S_INV>(v, lay, j, p.tw);
-        if (MODE == S_FWD_MUL_INV) {
-            // (L+1)^-1 multiplier, Eq. 12: |p|^2 = px^2 + py^2 + p_line^2
-            float pt2;
-            if (p.line_axis == 2) {
-                const int ix = (int)(col % p.mp.nx), iy = (int)(col / p.mp.nx);
-                const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
-                pt2 = fmaf(px, px, py * py);
-            } else {
-                const float px = p.mp.kx * freq_m((int)col, p.mp.nx);
-                pt2 = px * px;
-            }
-            const float kl = (p.line_axis == 2) ? p.mp.kz : p.mp.ky;
-#pragma unroll
-            for (int m = 0; m < G::N2; ++m) {
-                const float pl = kl * freq_m(j + G::N1 * m, N);
-                v[m] = cmul(v[m], multiplier(p.mp, fmaf(pl, pl, pt2)));
-            }
-            fft_line<N, true>(v, lay, j, p.tw);
+        for (int m = 0; m < G::N2; ++m) {
+            const float2 t = lb[m * lstep];
+            v[m] = (MODE == S_INV) ? cconj(t) : t;
         }
+#pragma unroll 1
+        for (int pass = 0; pass < NPASS; ++pass) {
+            fft_line<N, false, LayCol<N, COLS, SG::PAD, 0>, true>(v, lay, j, sm_tw);
+            if (MODE == S_FWD_MUL_INV && pass == 0) {
+                // (L+1)^-1 multiplier, Eq. 12: |p|^2 = px^2 + py^2 + p_line^2; then
+                // conjugate so the second forward DFT computes the inverse.
+                float pt2;
+                if (p.line_axis == 2) {
+                    const int ix = (int)(col % p.mp.nx), iy = (int)(col / p.mp.nx);
+                    const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
+                    pt2 = fmaf(px, px, py * py);
+                } else {
+                    const float px = p.mp.kx * freq_m((int)col, p.mp.nx);
+                    pt2 = px * px;
+                }
+                const float kl = (p.line_axis == 2) ? p.mp.kz : p.mp.ky;
 #pragma unroll
-        for (int m = 0; m < G::N2; ++m) p.data[base + (long long)(j + G::N1 * m) * p.stride] = v[m];
+                for (int m = 0; m < G::N2; ++m) {
+                    const float pl = kl * freq_m(j + G::N1 * m, N);
+                    v[m] = cconj(cmul(v[m], multiplier(p.mp, fmaf(pl, pl, pt2))));
+                }
+            }
+        }
+        // recompute the store addresses (an opaque stride keeps the compiler from
+        // holding 32 load addresses live across the FFT, which would spill)
+        long long stride = p.stride;
+        asm volatile("" : "+l"(stride));
+        float2 *sb = p.data + (o * p.ostride + col) + (long long)j * stride;
+        const long long step = (long long)G::N1 * stride;
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) {
+            sb[0] = (MODE == S_FWD) ? v[m] : cconj(v[m]);
+            sb += step;
+        }
     }
 }
 
@@ -453,27 +480,42 @@ cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_
     return cudaSuccess;   // x-only update is folded into k_xpass<X_ITER>
 }
 
-template <int N, int MODE>
+template <int N, int MODE, int COLS>
 static cudaError_t strided_t(const SParams &p, int grid, cudaStream_t s) {
-    constexpr int SM = SGeo<N>::SMEM;
+    constexpr int SM = SGeo<N, COLS>::SMEM;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_strided<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+        cudaError_t e = cudaFuncSetAttribute(k_strided<N, MODE, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_strided<N, MODE><<<grid, SGeo<N>::NT, SM, s>>>(p);
+    k_strided<N, MODE, COLS><<<grid, SGeo<N, COLS>::NT, SM, s>>>(p);
     return cudaGetLastError();
 }
 
-cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s) {
-#define S_CASE(n)                                                    \
-    case n:                                                          \
-        if (mode == S_FWD) return strided_t<n, S_FWD>(p, grid, s);   \
-        if (mode == S_INV) return strided_t<n, S_INV>(p, grid, s);   \
-        return strided_t<n, S_FWD_MUL_INV>(p, grid, s);
-    switch (N) { USP_FOR_EACH_N(S_CASE) default: return cudaErrorInvalidValue; }
-#undef S_CASE
+template <int N, int COLS>
+static cudaError_t strided_mode(SMode mode, const SParams &p, int grid, cudaStream_t s) {
+    if (mode == S_FWD) return strided_t<N, S_FWD, COLS>(p, grid, s);
+    if (mode == S_INV) return strided_t<N, S_INV, COLS>(p, grid, s);
+    return strided_t<N, S_FWD_MUL_INV, COLS>(p, grid, s);
+}
+
+// Columns per tile: 8 for N1 = 32 (N >= 1024: 256-thread CTAs, 2 per SM), else 16.
+int strided_cols_for(int N) { return N >= 1024 ? 8 : 16; }
+
+cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s, int cols) {
+    if (cols == 16 && N == 1024) return strided_mode<1024, 16>(mode, p, grid, s);
+    switch (N) {
+    case 16: return strided_mode<16, 16>(mode, p, grid, s);
+    case 32: return strided_mode<32, 16>(mode, p, grid, s);
+    case 64: return strided_mode<64, 16>(mode, p, grid, s);
+    case 128: return strided_mode<128, 16>(mode, p, grid, s);
+    case 256: return strided_mode<256, 16>(mode, p, grid, s);
+    case 512: return strided_mode<512, 16>(mode, p, grid, s);
+    case 1024: return strided_mode<1024, 8>(mode, p, grid, s);
+    case 2048: return strided_mode<2048, 8>(mode, p, grid, s);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s) {
@@ -507,11 +549,6 @@ size_t xpass_smem(int N) {
     const int n1 = 1 << (ilog2(N) / 2), n2 = N / n1;
     return (size_t)(256 / n1) * n1 * (n2 + 1) * sizeof(float2);
 }
-int strided_cols() { return 16; }
-int strided_threads(int N) { return (N >= 2048 ? 8 : 16) * (1 << (ilog2(N) / 2)); }
-size_t strided_smem(int N) {
-    const int n1 = 1 << (ilog2(N) / 2), n2 = N / n1, cols = N >= 2048 ? 8 : 16;
-    return (size_t)n1 * (n2 * cols + (cols == 16 ? 0 : 8)) * sizeof(float2);
-}
+int strided_threads(int N) { return strided_cols_for(N) * (1 << (ilog2(N) / 2)); }
 
 }  // namespace usp

@@ -37,7 +37,7 @@ struct XPipe {
     using G = LineGeo<N>;
     static constexpr int U = 32 / G::N1;                    // lines per warp unit
     static constexpr int UE = 32 * G::N2;                   // elements per unit (= U * N)
-    static constexpr int XC = (N >= 2048) ? 2 : 4;          // consumer warps
+    static constexpr int XC = (N >= 2048) ? 2 : 5;          // consumer warps
     static constexpr int NT = 32 * (XC + 1);
     static constexpr int XBUF = U * LayRow<N>::kFloat2PerLine;   // float2 per consumer warp
     static constexpr int STAGE = 4 * UE;                    // float2 per stage (4 slots)
@@ -45,11 +45,11 @@ struct XPipe {
     // warp that consumed it: S = XC * SPW and unit i -> stage i % S, warp
     // i % XC.  A consumer at unit i has itself finished unit i - S, so the
     // mbarrier it tests is never one phase behind (no parity ABA).
-    static constexpr int SPW0 = (kSmemBudget - XC * XBUF * 8) / (XC * STAGE * 8);
+    static constexpr int SPW0 = (kSmemBudget - XC * XBUF * 8 - N * 8) / (XC * STAGE * 8);
     static constexpr int SPW = SPW0 > 2 ? 2 : SPW0;
     static constexpr int S = XC * SPW;
     static_assert(SPW >= 1, "x pipeline needs >= 1 stage per consumer warp");
-    static constexpr int SMEM = (S * STAGE + XC * XBUF) * 8 + 2 * S * 8;
+    static constexpr int SMEM = (S * STAGE + XC * XBUF + N) * 8 + 2 * S * 8;   // stages, exchange, twiddles, barriers
 };
 
 template <int N, int MODE>
@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stages = reinterpret_cast<float2 *>(smem_raw);
     float2 *xbufs = stages + T::S * T::STAGE;
-    uint64_t *full = reinterpret_cast<uint64_t *>(xbufs + T::XC * T::XBUF);
+    float2 *sm_tw = xbufs + T::XC * T::XBUF;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N);
     uint64_t *empty = full + T::S;
     __shared__ double sh_red[T::NT / 32];
 
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
             }
             fence_mbar_init();
         }
+        load_twiddles<N>(sm_tw, p.tw);
         __syncthreads();
         const long long nunits = p.nlines / T::U;
         const int nloc = (int)((nunits - blockIdx.x + gridDim.x - 1) / gridDim.x);
@@ -154,35 +156,42 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                     if (lane == 0) mbar_arrive(&empty[s]);   // the warp's stage can refill now
                 } else {
 #pragma unroll
-                    for (int m = 0; m < G::N2; ++m) v[m] = st[sbase + G::N1 * m];
-                    fft_line<N, true>(v, lay, j, p.tw);        // x inverse: (L+1)^-1 u complete
-                    float lacc = 0.f;
-#pragma unroll
-                    for (int m = 0; m < G::N2; ++m) {
-                        const int e = sbase + G::N1 * m;
-                        const long long gi = gb + G::N1 * m;
-                        const float2 b = st[3 * T::UE + e];
-                        float2 dn;
-                        if (MODE == X_SRC_EPI) {
-                            dn = cmul(b, v[m]);                 // Delta_0 = B (L+1)^-1 s
-                            p.x[gi] = make_float2(0.f, 0.f);    // x_0 = 0 (L83)
-                        } else {
-                            const float2 d = st[1 * T::UE + e];
-                            const float2 xx = st[2 * T::UE + e];
-                            const float2 t = cmul(b, csub(v[m], d));
-                            dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
-                            p.x[gi] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
-                        }
-                        p.delta[gi] = dn;
-                        lacc += cabs2(dn);
-                        v[m] = cmul(b, dn);                     // next chain: u = B Delta
-                    }
-                    acc += (double)lacc;
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[s]);
+                    for (int m = 0; m < G::N2; ++m) v[m] = cconj(st[sbase + G::N1 * m]);
                 }
-                fft_line<N, false>(v, lay, j, p.tw);           // x forward
+                // pass 0: x inverse as conj(DFT(conj(u))) + update; pass 1: x forward.
+                // One FFT body in the binary keeps the kernel inside the I-cache.
+#pragma unroll 1
+                for (int pass = (MODE == X_SRC_FWD) ? 1 : 0; pass < 2; ++pass) {
+                    fft_line<N, false, LayRow<N>, true>(v, lay, j, sm_tw);
+                    if (pass == 0) {
+                        float lacc = 0.f;
+#pragma unroll
+                        for (int m = 0; m < G::N2; ++m) {
+                            const int e = sbase + G::N1 * m;
+                            const long long gi = gb + G::N1 * m;
+                            const float2 y = cconj(v[m]);           // (L+1)^-1 u, chain complete
+                            const float2 b = st[3 * T::UE + e];
+                            float2 dn;
+                            if (MODE == X_SRC_EPI) {
+                                dn = cmul(b, y);                    // Delta_0 = B (L+1)^-1 s
+                                p.x[gi] = make_float2(0.f, 0.f);    // x_0 = 0 (L83)
+                            } else {
+                                const float2 d = st[1 * T::UE + e];
+                                const float2 xx = st[2 * T::UE + e];
+                                const float2 t = cmul(b, csub(y, d));
+                                dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
+                                p.x[gi] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                            }
+                            p.delta[gi] = dn;
+                            lacc += cabs2(dn);
+                            v[m] = cmul(b, dn);                     // next chain: u = B Delta
+                        }
+                        acc += (double)lacc;
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[s]);
+                    }
+                }
 #pragma unroll
                 for (int m = 0; m < G::N2; ++m) p.work[gb + G::N1 * m] = v[m];
             }

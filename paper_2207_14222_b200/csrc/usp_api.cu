@@ -81,7 +81,7 @@ struct usp_plan_s {
     // launch configuration
     int grid_x = 0, grid_y = 0, grid_z = 0;
     // TMA-pipelined kernels (default); USP_LEGACY=1 selects the register-staged ones
-    bool pipe = true, pipe_xk = true;
+    bool pipe = true, pipe_xk = true, pipe_sk = false;
     bool pipe_y = false, pipe_z = false;
     int gridp_x = 0, gridp_y = 0, gridp_z = 0;
     CUtensorMap map_y{}, map_z{};
@@ -356,8 +356,13 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
 usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, bool use_pipe, int rank, const CUtensorMap &map,
                        const SParams &sp, int grid_legacy, int grid_pipe) {
     Tick t(p, cls);
+    // z pass (two FFTs + multiplier, the most arithmetic per byte): 16-column
+    // tiles of 512 threads measured faster than two 256-thread CTAs per SM
+    // (7.2 vs 7.9 ms at 1024^3); USP_ZCOLS=8 selects the latter.
+    static const char *zc = std::getenv("USP_ZCOLS");
+    const int cols = (cls == KC_ZMUL) ? (zc ? std::atoi(zc) : 16) : 0;
     if (use_pipe) CU(launch_strided_pipe(n, mode, rank, map, sp, grid_pipe, p->stream));
-    else CU(launch_strided(n, mode, sp, grid_legacy, p->stream));
+    else CU(launch_strided(n, mode, sp, cols == 16 ? p->nsm : grid_legacy, p->stream, cols));
     return USP_OK;
 }
 
@@ -433,14 +438,21 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     {
         const long long xgroups = (p->ny * p->nz + xpass_lines_per_cta((int)p->nx) - 1) / xpass_lines_per_cta((int)p->nx);
         p->grid_x = occ_grid(p, xgroups, 2);
-        if (p->ndim >= 2) p->grid_y = occ_grid(p, (p->nx / (p->ny >= 2048 ? 8 : 16)) * p->nz, 2);
-        if (p->ndim >= 3) p->grid_z = occ_grid(p, (p->nx * p->ny) / (p->nz >= 2048 ? 8 : 16), 2);
+        // strided passes: CTAs per SM = 2 when the tile has 256 threads, else 1; two waves
+        auto sgrid = [&](long long n, long long ncol_units) {
+            const int per_sm = strided_threads((int)n) <= 256 ? 2 : 1;
+            return occ_grid(p, ncol_units, per_sm);
+        };
+        if (p->ndim >= 2) p->grid_y = sgrid(p->ny, (p->nx / strided_cols_for((int)p->ny)) * p->nz);
+        if (p->ndim >= 3) p->grid_z = sgrid(p->nz, (p->nx * p->ny) / strided_cols_for((int)p->nz));
     }
     {
         const char *leg = std::getenv("USP_LEGACY");
         p->pipe = !(leg && leg[0] == '1');
         const char *px = std::getenv("USP_PIPE_X");
         p->pipe_xk = p->pipe && !(px && px[0] == '0');
+        const char *ps = std::getenv("USP_PIPE_S");   // TMA strided passes (experimental, off by default)
+        p->pipe_sk = p->pipe && ps && ps[0] == '1';
         const int u = 32 / (1 << (log2ll(p->nx) / 2));   // x lines per warp unit (32 / N1)
         p->gridp_x = occ_grid(p, (p->ny * p->nz) / u, 1);
         if (p->ndim >= 2)
@@ -501,7 +513,7 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     p->work = (float2 *)(p->ws + 3 * f);
     p->have_potential = p->have_source = false;
     p->pipe_y = p->pipe_z = false;
-    if (p->pipe && p->ndim >= 2 && strided_pipe_supported(p->ny)) {
+    if (p->pipe_sk && p->ndim >= 2 && strided_pipe_supported(p->ny)) {
         const cuuint32_t cy = (cuuint32_t)strided_pipe_cols((int)p->ny), by = (cuuint32_t)strided_pipe_box((int)p->ny);
         if (p->ndim == 2) {
             const cuuint64_t dims[2] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny};
@@ -515,7 +527,7 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
             p->pipe_y = make_map(&p->map_y, p->work, 3, dims, str, box);
         }
     }
-    if (p->pipe && p->ndim == 3 && strided_pipe_supported(p->nz)) {
+    if (p->pipe_sk && p->ndim == 3 && strided_pipe_supported(p->nz)) {
         const cuuint32_t cz = (cuuint32_t)strided_pipe_cols((int)p->nz), bz = (cuuint32_t)strided_pipe_box((int)p->nz);
         const cuuint64_t dims[2] = {(cuuint64_t)(p->nx * p->ny), (cuuint64_t)p->nz};
         const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};

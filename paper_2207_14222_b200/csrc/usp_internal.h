@@ -116,7 +116,7 @@ struct FarParams {       // farthest medium value from a centre (smallest circle
 
 // launchers (kernels.cu); all return cudaGetLastError()
 cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);
-cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s);
+cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s, int cols = 0);
 cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s);
 cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_t s);
 cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
@@ -134,9 +134,8 @@ int strided_pipe_box(int N);
 int xpass_threads(int N);          // threads per CTA of the x pass
 int xpass_lines_per_cta(int N);
 int strided_threads(int N);
-int strided_cols();
+int strided_cols_for(int N);
 size_t xpass_smem(int N);
-size_t strided_smem(int N);
 bool supported_n(long long n);
 
 }  // namespace usp
