@@ -327,6 +327,7 @@ def run_usp(args, world, rank, local):
                                "achieved_gbs": it_bytes / (iter_ms / 1e3) / 1e9,
                                "frac": it_bytes / (iter_ms / 1e3) / 1e9 / hbm},
         "kernel_share": kernel_share,
+        "kernel_ms_per_launch": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,

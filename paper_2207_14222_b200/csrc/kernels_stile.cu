@@ -1,0 +1,324 @@
+// kernels_stile.cu -- strided-axis FFT passes with a TMA-prefetched tile
+// (the default y/z passes for line lengths 64..1024 on sm_100a).
+//
+// A CTA owns COLS = 16 adjacent columns (128-byte rows) x N rows of a strided
+// axis (y: stride nx; z: stride nx*ny) per tile and walks its tiles in a
+// persistent loop.  One thread issues the tensor-map TMA boxes
+// (cp.async.bulk.tensor, SASS UTMALDG) of tile i+1 into the single stage as
+// soon as every thread has copied tile i into registers, so the load of the
+// next tile overlaps the whole FFT arithmetic of the current one; results are
+// stored straight from registers (128-byte rows).  Thread (c, j) owns column
+// c, rows j + N1*m (the four-step layout of fft_core.cuh).
+//
+// Shared memory per CTA: stage (COLS*N float2) + exchange buffer + twiddles.
+// For N = 1024 the exchange buffer is HALF a tile (64 KB), so stage +
+// exchange fit one SM (200 KB): the transpose of the four-step FFT runs in
+// two rounds.  Round r moves, for every writer row n1, the half of its k2
+// values with k2 >> (L2-1) == r ^ b(n1), b(n1) = top bit of n1; to keep the
+// register indices compile-time, the half a thread writes/reads first is
+// selected by DFT shift identities instead of register swaps:
+//   x'[n] = (-1)^n x[n]        =>  DFT(x')[s] = X[s ^ N/2]      (input flip)
+//   y[s]  = x[s ^ N/2]         =>  DFT(y)[k]  = (-1)^k DFT(x)[k] (output flip)
+// so a thread with b = 1 negates its odd inputs before the first DFT and its
+// odd outputs after the last one; nothing else changes.  (N1 = N2 only.)
+//
+// Modes (Eq. 12; the multiplier is the Fourier symbol of
+// (L+1)^-1 with 1/N_vox folded in):
+//   S_FWD          y forward                       (K_B)
+//   S_INV          y inverse  = conj(DFT(conj(.))) (K_D)
+//   S_FWD_MUL_INV  z (or 2-D y) forward, x g(p), inverse (K_C)
+// The inverse is always computed as conj(DFT(conj(.))) so ONE FFT body is
+// compiled per kernel (the unrolled body of two would overflow the I-cache).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fft_core.cuh"
+#include "kcommon.cuh"
+#include "tma.cuh"
+#include "usp_internal.h"
+
+namespace usp {
+
+template <int N>
+struct STile {
+    using G = LineGeo<N>;
+    static constexpr int COLS = 16;
+    static constexpr int NT = COLS * G::N1;
+    static constexpr int TILE = COLS * N;                       // float2 per stage
+    // two-round exchange only where a full buffer would not fit next to the stage
+    static constexpr bool HALFX = (N >= 512);
+    static constexpr bool FLIP = HALFX && G::R == 1;   // N1 == N2: halves chosen by shift flips
+    static constexpr int XPITCH = HALFX ? (G::N2 / 2) * COLS : G::N2 * COLS;   // float2 per writer row
+    static constexpr int XB = G::N1 * XPITCH;
+    static constexpr int BOXN = N < 256 ? N : 256;
+    static constexpr int SMEM = (TILE + XB + N) * 8 + 16;
+    static constexpr int FIT_SMEM = 232448 / (SMEM + 1024);
+    static constexpr int FIT_REGS = 65536 / (NT * 96);            // keep >= 96 registers per thread
+    static constexpr int FIT_THR = 2048 / NT;
+    static constexpr int MINB0 = FIT_SMEM < FIT_REGS ? FIT_SMEM : FIT_REGS;
+    static constexpr int MINB1 = MINB0 < FIT_THR ? MINB0 : FIT_THR;
+    static constexpr int MINB = MINB1 < 1 ? 1 : MINB1;
+};
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// One forward four-step DFT of the thread's line (the shared body).
+// v[n2] = x[j + N1 n2] on entry; v[m] = X[j + N1 m] on exit (up to the
+// shift flips of HALFX, which the caller applies).
+template <int N>
+__device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *xb, const float2 *sm_tw, int c,
+                                          int j) {
+    using G = LineGeo<N>;
+    using T = STile<N>;
+    dft<G::N2, false>(v);
+    if constexpr (T::FLIP) {
+        constexpr int H = G::N2 / 2;
+        const int b = (j >> (ilog2(G::N1) - 1)) & 1;
+        // slot s holds k2 = s ^ (H b): twiddle W_N^(j k2)
+        const float2 *tw0 = sm_tw + (H * b) * G::N1 + j;
+        const float2 *tw1 = sm_tw + (H * (1 - b)) * G::N1 + j;
+#pragma unroll
+        for (int s = 0; s < G::N2; ++s) {
+            const float2 w = (s < H) ? tw0[s * G::N1] : tw1[(s - H) * G::N1];
+            v[s] = cmul(v[s], w);
+        }
+        float2 *wb = xb + j * T::XPITCH + c;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+            for (int q = 0; q < H; ++q) wb[q * T::COLS] = v[r * H + q];
+            __syncthreads();
+            const float2 *rb = xb + (H * (r ^ b)) * T::XPITCH + (j & (H - 1)) * T::COLS + c;
+#pragma unroll
+            for (int q = 0; q < H; ++q) v[r * H + q] = rb[q * T::XPITCH];
+            __syncthreads();
+        }
+        dft<G::N1, false>(v);
+    } else if constexpr (T::HALFX) {
+        // N2 = 2 N1: round t moves the k2-half t; thread j reads k2 = j + N1 t
+#pragma unroll
+        for (int k2 = 1; k2 < G::N2; ++k2) v[k2] = cmul(v[k2], sm_tw[k2 * G::N1 + j]);
+        float2 *wb = xb + j * T::XPITCH + c;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+#pragma unroll
+            for (int q = 0; q < G::N1; ++q) wb[q * T::COLS] = v[t * G::N1 + q];
+            __syncthreads();
+#pragma unroll
+            for (int n1 = 0; n1 < G::N1; ++n1) v[t * G::N1 + n1] = xb[n1 * T::XPITCH + j * T::COLS + c];
+            __syncthreads();
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) dft<G::N1, false>(v + t * G::N1);
+        float2 o[G::N2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int k1 = 0; k1 < G::N1; ++k1) o[t + 2 * k1] = v[t * G::N1 + k1];
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) v[m] = o[m];
+    } else {
+#pragma unroll
+        for (int k2 = 1; k2 < G::N2; ++k2) v[k2] = cmul(v[k2], sm_tw[k2 * G::N1 + j]);
+        float2 *wb = xb + j * T::XPITCH + c;
+#pragma unroll
+        for (int k2 = 0; k2 < G::N2; ++k2) wb[k2 * T::COLS] = v[k2];
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < G::R; ++t)
+#pragma unroll
+            for (int n1 = 0; n1 < G::N1; ++n1)
+                v[t * G::N1 + n1] = xb[n1 * T::XPITCH + (j + G::N1 * t) * T::COLS + c];
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < G::R; ++t) dft<G::N1, false>(v + t * G::N1);
+        if constexpr (G::R > 1) {
+            float2 o[G::N2];
+#pragma unroll
+            for (int t = 0; t < G::R; ++t)
+#pragma unroll
+                for (int k1 = 0; k1 < G::N1; ++k1) o[t + G::R * k1] = v[t * G::N1 + k1];
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) v[m] = o[m];
+        }
+    }
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
+    k_stile(const __grid_constant__ CUtensorMap tmap, SParams p) {
+    using G = LineGeo<N>;
+    using T = STile<N>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2 *stage = reinterpret_cast<float2 *>(smem_raw);
+    float2 *xb = stage + T::TILE;
+    float2 *sm_tw = xb + T::XB;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N);
+    if (p.check_state) {
+        if (p.st->status != ST_RUNNING || p.st->k >= p.st->kmax) return;
+    }
+    const int tid = threadIdx.x;
+    const int c = tid % T::COLS, j = tid / T::COLS;
+    const long long tpo = p.ncols / T::COLS;
+    const long long ntiles = tpo * p.nouter;
+    const int nloc = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const bool rank3 = p.line_axis == 1 && p.nouter > 1;
+
+    auto issue = [&](int i) {   // thread 0: TMA boxes of local tile i
+        const long long t = blockIdx.x + (long long)i * gridDim.x;
+        const long long o = t / tpo;
+        const int c0 = (int)((t - o * tpo) * T::COLS);
+        mbar_arrive_expect_tx(full, T::TILE * 8);
+#pragma unroll
+        for (int bx = 0; bx < N / T::BOXN; ++bx) {
+            if (rank3) tma_load_3d(stage + bx * T::BOXN * T::COLS, &tmap, c0, bx * T::BOXN, (int)o, full);
+            else tma_load_2d(stage + bx * T::BOXN * T::COLS, &tmap, c0, bx * T::BOXN, full);
+        }
+    };
+    if (tid == 0) {
+        prefetch_tmap(&tmap);
+        mbar_init(full, 1);
+        fence_mbar_init();
+        if (nloc > 0) issue(0);
+    }
+    load_twiddles<N>(sm_tw, p.tw);
+    __syncthreads();
+
+    // HALFX shift flips: threads whose top row bit is set negate odd inputs /
+    // outputs (see header)
+    float sg = 1.f;
+    if constexpr (T::FLIP) sg = ((j >> (ilog2(G::N1) - 1)) & 1) ? -1.f : 1.f;
+
+    for (int i = 0; i < nloc; ++i) {
+        if (!mbar_wait(full, i & 1)) {
+            if (tid == 0 && atomicCAS(&p.st->err, 0, 5) == 0) p.st->err_info = i;
+            return;
+        }
+        float2 v[G::N2];
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) {
+            float2 a = stage[(j + G::N1 * m) * T::COLS + c];
+            if (MODE == S_INV) a = cconj(a);
+            if (T::FLIP && (m & 1)) a = cscale(a, sg);
+            v[m] = a;
+        }
+        fence_proxy_async_smem();
+        __syncthreads();                 // stage consumed: prefetch the next tile
+        if (tid == 0 && i + 1 < nloc) issue(i + 1);
+
+        if constexpr (MODE == S_FWD_MUL_INV) {
+            float base;   // D (p_x^2 + p_y^2) + Re(sigma + c) of this thread's column
+            {
+                const long long t = blockIdx.x + (long long)i * gridDim.x;
+                const long long o = t / tpo;
+                const long long col = (t - o * tpo) * T::COLS + c;
+                float pt2;
+                if (p.line_axis == 2) {
+                    const int ix = (int)(col % p.mp.nx), iy = (int)(col / p.mp.nx);
+                    const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
+                    pt2 = fmaf(px, px, py * py);
+                } else {
+                    const float px = p.mp.kx * freq_m((int)col, p.mp.nx);
+                    pt2 = px * px;
+                }
+                base = fmaf(p.mp.D, pt2, p.mp.sc.x);
+            }
+#pragma unroll 1
+            for (int pass = 0; pass < 2; ++pass) {
+                stile_fft<N>(v, xb, sm_tw, c, j);
+                if (pass == 0) {
+                    // (L+1)^-1 symbol (Eq. 12) at the signed frequency of k = j + N1 m:
+                    //   g = cn (dr - i di) / (dr^2 + di^2),  dr = D |p|^2 + Re(sigma + c),
+                    //   di = Im(sigma + c);  then conj so the second forward DFT inverts.
+                    // (constants are re-derived here, opaque to hoisting, to keep them
+                    // out of the registers live across the FFT)
+                    float di = p.mp.sc.y, kl = (p.line_axis == 2) ? p.mp.kz : p.mp.ky;
+                    asm volatile("" : "+f"(di), "+f"(kl));
+                    const float di2 = di * di, cyd = p.mp.cn.y * di, cxd = p.mp.cn.x * di;
+                    const float klj = kl * (float)j, Dm = p.mp.D;
+#pragma unroll
+                    for (int m = 0; m < G::N2; ++m) {
+                        const float cm = (float)(G::N1 * m - ((m >= G::N2 / 2) ? N : 0));
+                        const float pl = fmaf(kl, cm, klj);
+                        const float dr = fmaf(Dm * pl, pl, base);
+                        const float inv = rcp_approx(fmaf(dr, dr, di2));
+                        const float gr = fmaf(p.mp.cn.x, dr, cyd) * inv;
+                        const float gi = fmaf(p.mp.cn.y, dr, -cxd) * inv;
+                        v[m] = cconj(cmul(v[m], make_float2(gr, gi)));
+                    }
+                }
+            }
+        } else {
+            stile_fft<N>(v, xb, sm_tw, c, j);
+        }
+        long long t = blockIdx.x + (long long)i * gridDim.x;
+        asm volatile("" : "+l"(t));
+        const long long o = t / tpo;
+        const long long col = (t - o * tpo) * T::COLS + c;
+        long long stride = p.stride;
+        asm volatile("" : "+l"(stride));
+        float2 *sb = p.data + (o * p.ostride + col) + (long long)j * stride;
+        const long long step = (long long)G::N1 * stride;
+#pragma unroll
+        for (int m = 0; m < G::N2; ++m) {
+            float2 a = v[m];
+            if (T::FLIP && (m & 1)) a = cscale(a, sg);
+            sb[0] = (MODE == S_FWD) ? a : cconj(a);
+            sb += step;
+        }
+    }
+}
+
+// ========================================================= launchers ====
+template <int N, int MODE>
+static cudaError_t stile_t(const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(k_stile<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, STile<N>::SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_stile<N, MODE><<<grid, STile<N>::NT, STile<N>::SMEM, s>>>(map, p);
+    return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t stile_mode(SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
+    if (mode == S_FWD) return stile_t<N, S_FWD>(map, p, grid, s);
+    if (mode == S_INV) return stile_t<N, S_INV>(map, p, grid, s);
+    return stile_t<N, S_FWD_MUL_INV>(map, p, grid, s);
+}
+
+bool stile_supported(long long n) { return n >= 64 && n <= 1024 && (n & (n - 1)) == 0; }
+int stile_cols(int) { return 16; }
+int stile_box(int N) { return N < 256 ? N : 256; }
+int stile_ctas_per_sm(int N) {
+    switch (N) {
+    case 64: return STile<64>::MINB;
+    case 128: return STile<128>::MINB;
+    case 256: return STile<256>::MINB;
+    case 512: return STile<512>::MINB;
+    case 1024: return STile<1024>::MINB;
+    default: return 1;
+    }
+}
+
+cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
+    switch (N) {
+    case 64: return stile_mode<64>(mode, map, p, grid, s);
+    case 128: return stile_mode<128>(mode, map, p, grid, s);
+    case 256: return stile_mode<256>(mode, map, p, grid, s);
+    case 512: return stile_mode<512>(mode, map, p, grid, s);
+    case 1024: return stile_mode<1024>(mode, map, p, grid, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace usp

@@ -85,6 +85,10 @@ struct usp_plan_s {
     bool pipe_y = false, pipe_z = false;
     int gridp_x = 0, gridp_y = 0, gridp_z = 0;
     CUtensorMap map_y{}, map_z{};
+    // TMA-prefetched 16-column strided passes (kernels_stile.cu; default, USP_STILE=0 disables)
+    bool stile = true, stile_y = false, stile_z = false;
+    int grids_y = 0, grids_z = 0;
+    CUtensorMap smap_y{}, smap_z{};
     // profiling
     bool prof = false;
     std::vector<Timed> timed;
@@ -356,6 +360,11 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
 usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, bool use_pipe, int rank, const CUtensorMap &map,
                        const SParams &sp, int grid_legacy, int grid_pipe) {
     Tick t(p, cls);
+    const bool is_z = (cls == KC_ZMUL);
+    if (is_z ? p->stile_z : p->stile_y) {
+        CU(launch_stile(n, mode, is_z ? p->smap_z : p->smap_y, sp, is_z ? p->grids_z : p->grids_y, p->stream));
+        return USP_OK;
+    }
     // z pass (two FFTs + multiplier, the most arithmetic per byte): 16-column
     // tiles of 512 threads measured faster than two 256-thread CTAs per SM
     // (7.2 vs 7.9 ms at 1024^3); USP_ZCOLS=8 selects the latter.
@@ -453,6 +462,12 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         p->pipe_xk = p->pipe && !(px && px[0] == '0');
         const char *ps = std::getenv("USP_PIPE_S");   // TMA strided passes (experimental, off by default)
         p->pipe_sk = p->pipe && ps && ps[0] == '1';
+        const char *stl = std::getenv("USP_STILE");
+        p->stile = p->pipe && !(stl && stl[0] == '0');
+        if (p->ndim >= 2 && stile_supported(p->ny))
+            p->grids_y = occ_grid(p, (p->nx / stile_cols((int)p->ny)) * p->nz, stile_ctas_per_sm((int)p->ny));
+        if (p->ndim >= 3 && stile_supported(p->nz))
+            p->grids_z = occ_grid(p, (p->nx * p->ny) / stile_cols((int)p->nz), stile_ctas_per_sm((int)p->nz));
         const int u = 32 / (1 << (log2ll(p->nx) / 2));   // x lines per warp unit (32 / N1)
         p->gridp_x = occ_grid(p, (p->ny * p->nz) / u, 1);
         if (p->ndim >= 2)
@@ -513,6 +528,28 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     p->work = (float2 *)(p->ws + 3 * f);
     p->have_potential = p->have_source = false;
     p->pipe_y = p->pipe_z = false;
+    p->stile_y = p->stile_z = false;
+    if (p->stile && p->ndim >= 2 && stile_supported(p->ny)) {
+        const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
+        if (p->ndim == 2) {
+            const cuuint64_t dims[2] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny};
+            const cuuint64_t str[1] = {(cuuint64_t)p->nx * 8};
+            const cuuint32_t box[2] = {cy, by};
+            p->stile_y = make_map(&p->smap_y, p->work, 2, dims, str, box);
+        } else {
+            const cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)p->nz};
+            const cuuint64_t str[2] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nx * p->ny) * 8};
+            const cuuint32_t box[3] = {cy, by, 1};
+            p->stile_y = make_map(&p->smap_y, p->work, 3, dims, str, box);
+        }
+    }
+    if (p->stile && p->ndim == 3 && stile_supported(p->nz)) {
+        const cuuint32_t cz = (cuuint32_t)stile_cols((int)p->nz), bz = (cuuint32_t)stile_box((int)p->nz);
+        const cuuint64_t dims[2] = {(cuuint64_t)(p->nx * p->ny), (cuuint64_t)p->nz};
+        const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};
+        const cuuint32_t box[2] = {cz, bz};
+        p->stile_z = make_map(&p->smap_z, p->work, 2, dims, str, box);
+    }
     if (p->pipe_sk && p->ndim >= 2 && strided_pipe_supported(p->ny)) {
         const cuuint32_t cy = (cuuint32_t)strided_pipe_cols((int)p->ny), by = (cuuint32_t)strided_pipe_box((int)p->ny);
         if (p->ndim == 2) {

@@ -128,6 +128,13 @@ cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cud
 cudaError_t launch_strided_pipe(int N, SMode mode, int rank, const CUtensorMap &map, const SParams &p, int grid,
                                 cudaStream_t s);
 bool strided_pipe_supported(long long n);
+
+// TMA-prefetched 16-column strided passes (kernels_stile.cu)
+cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s);
+bool stile_supported(long long n);
+int stile_cols(int N);
+int stile_box(int N);
+int stile_ctas_per_sm(int N);
 int strided_pipe_cols(int N);
 int strided_pipe_box(int N);
 
