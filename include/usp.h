@@ -52,7 +52,7 @@ extern "C" {
 #endif
 
 #define USP_VERSION_MAJOR 0
-#define USP_VERSION_MINOR 1
+#define USP_VERSION_MINOR 2
 
 typedef struct usp_plan_s *usp_plan_t;
 
@@ -99,23 +99,41 @@ typedef struct {
     usp_c128 sigma;      /* shift of L_raw (ignored when set_potential auto-scales)       */
     usp_c128 c;          /* scale c (ignored when set_potential auto-scales)              */
     void *stream;        /* cudaStream_t; NULL = legacy default stream                    */
-    void *nccl_comm;     /* reserved for the slab-decomposed multi-GPU path; must be NULL */
+    void *nccl_comm;     /* NULL = one GPU; else an ncclComm_t (usp_comm_init): the 3-D grid
+                            is split into z-slabs over its ranks, one GPU per rank           */
+    int virtual_ranks;   /* > 1 (with nccl_comm NULL): run the same slab decomposition with
+                            this many slabs on ONE GPU, the transposes as device copies
+                            (a test mode: every kernel, layout and index of the multi-GPU
+                            path, no second GPU needed); 0 or 1 = off                        */
 } usp_plan_desc;
 
 /* Create a plan for the grid and problem described by *desc (copied).
- * Errors: USP_ERR_ARG (NULL, ndim, D <= 0), USP_ERR_UNSUPPORTED (extent),
- * USP_ERR_CUDA. */
+ *
+ * Slab decomposition (desc.nccl_comm or virtual_ranks > 1,
+ * P slabs): a 3-D grid is split into P z-slabs of nz/P planes.  The x and y
+ * FFT passes are slab-local; the z pass runs on y-slabs reached by an
+ * all-to-all transpose (and back), and the residual norm is one all-gather
+ * of P doubles summed in rank order, so every rank takes the same stop
+ * decision.  With nccl_comm, the arrays passed to
+ * set_potential / set_source / get_field are the rank's slab
+ * [nz/P][ny][nx] (usp_local_extent gives z0); every call is collective.
+ * Requires P a power of two dividing ny and nz, ny and nz in [64, 1024].
+ *
+ * Errors: USP_ERR_ARG (NULL, ndim, D <= 0), USP_ERR_UNSUPPORTED (extent,
+ * decomposition), USP_ERR_NCCL, USP_ERR_CUDA. */
 usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out);
 
 /* Bytes of device workspace the plan needs: 4 complex64 fields
- * (x, Delta, B, work) = 32 bytes per voxel plus reduction scratch. */
+ * (x, Delta, B, work) = 32 bytes per local voxel; 6 (+ send and receive
+ * buffers of the transposes) = 48 bytes per local voxel when P > 1. */
 usp_status usp_plan_workspace_size(usp_plan_t plan, size_t *bytes);
 
 /* Attach caller-owned device memory (>= workspace_size bytes, 256-B aligned).
  * Errors: USP_ERR_ARG (NULL, misaligned), USP_ERR_NOMEM (too small). */
 usp_status usp_plan_set_workspace(usp_plan_t plan, void *dev, size_t bytes);
 
-/* Local z-slab of this rank: z0 = 0, nz_local = nz on a single GPU. */
+/* Local z-slab of this rank: first plane z0 and number of planes held
+ * (z0 = 0, nz_local = nz on a single GPU and in virtual mode). */
 usp_status usp_local_extent(usp_plan_t plan, int64_t *z0, int64_t *nz_local);
 
 /* Set the medium (k^2 or w, see desc.medium / desc.dtype; [z][y][x]) and form
@@ -173,6 +191,16 @@ usp_status usp_profile_read(usp_plan_t plan, int cap, char (*names)[32], double 
 
 /* Number of kernel launches the library issued since plan creation. */
 usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
+
+/* NCCL communicator for the slab decomposition (one process per GPU).
+ * Rank 0 calls usp_comm_unique_id and broadcasts the 128 bytes (e.g. with
+ * torch.distributed); every rank then calls usp_comm_init with the same id,
+ * the rank count and its rank (collective; the current CUDA device is the
+ * rank's GPU).  libnccl.so.2 is opened at run time (USP_NCCL_LIB overrides
+ * the path).  Errors: USP_ERR_ARG, USP_ERR_NCCL. */
+usp_status usp_comm_unique_id(unsigned char id[128]);
+usp_status usp_comm_init(const unsigned char id[128], int nranks, int rank, void **comm);
+usp_status usp_comm_destroy(void *comm);
 
 /* Release the plan (not the caller's workspace).  NULL is a no-op. */
 void usp_plan_destroy(usp_plan_t plan);

@@ -29,7 +29,8 @@ class c128(ctypes.Structure):
 class PlanDesc(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_int64 * 3), ("h", ctypes.c_double * 3),
                 ("medium", ctypes.c_int), ("dtype", ctypes.c_int), ("D", ctypes.c_double),
-                ("sigma", c128), ("c", c128), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p)]
+                ("sigma", c128), ("c", c128), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
+                ("virtual_ranks", ctypes.c_int)]
 
 
 class USPError(RuntimeError):
@@ -65,9 +66,30 @@ SIGNATURES = {
                                         ctypes.POINTER(ctypes.c_int)]),
     "usp_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "usp_plan_destroy": (None, [ctypes.c_void_p]),
+    "usp_comm_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
+    "usp_comm_init": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int, ctypes.c_int,
+                                     ctypes.POINTER(ctypes.c_void_p)]),
+    "usp_comm_destroy": (ctypes.c_int, [ctypes.c_void_p]),
     "usp_last_error": (ctypes.c_char_p, []),
     "usp_version": (ctypes.c_char_p, []),
 }
+
+
+def _nccl_path_hint():
+    """Point libusp's run-time NCCL loader at the torch wheel's libnccl.so.2
+    (used only by multi-GPU plans)."""
+    if "USP_NCCL_LIB" in os.environ:
+        return
+    try:
+        import nvidia.nccl as nn
+
+        for d in nn.__path__:
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["USP_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
 
 
 def load():
@@ -79,6 +101,7 @@ def load():
         from .build import build
 
         build()
+    _nccl_path_hint()
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)

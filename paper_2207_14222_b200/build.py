@@ -20,6 +20,23 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
+def _nccl_include():
+    """nccl.h for the types of the run-time-loaded NCCL (torch wheel's copy first)."""
+    try:
+        import nvidia.nccl as nn
+
+        for d in nn.__path__:
+            inc = os.path.join(d, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
+FLAGS += ["-I", _nccl_include()]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
@@ -50,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -135,6 +135,10 @@ __global__ void __launch_bounds__(256) k_xpass(XParams p) {
     const double mine = block_sum_d<XG::NT>(acc, sh_red);
     if (!last_block_total<XG::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
     if (threadIdx.x != 0) return;
+    if (p.red.local_sum) {   // slab-decomposed: k_finish sums the ranks' totals after the all-gather
+        *p.red.local_sum = total;
+        return;
+    }
     finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red);
 }
 
@@ -437,6 +441,21 @@ __global__ void __launch_bounds__(256) k_farthest(FarParams p) {
     }
 }
 
+// Slab-decomposed runs: after the all-gather of the ranks' x-pass totals,
+// every rank sums them in rank order (deterministic, identical on all ranks)
+// and takes the same stop decision (reading R-4).
+__global__ void k_finish(IterState *st, const double *sums, int P, int src_epi, Red red) {
+    bool xonly = false;
+    if (!src_epi) {
+        const int status = st->status;
+        if (st->k >= st->kmax || (status != ST_RUNNING && status != ST_STOP_PENDING)) return;
+        xonly = (status == ST_STOP_PENDING);
+    }
+    double total = 0.0;
+    for (int q = 0; q < P; ++q) total += sums[q];
+    finish_xpass(src_epi != 0, xonly, total, st, red);
+}
+
 __global__ void k_set_state(IterState *st, double alpha, double tol, long long kmax) {
     st->alpha = alpha;
     st->tol = tol;
@@ -535,6 +554,11 @@ cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s) {
 
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s) {
     k_farthest<<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s) {
+    k_finish<<<1, 1, 0, s>>>(st, sums, P, src_epi, red);
     return cudaGetLastError();
 }
 

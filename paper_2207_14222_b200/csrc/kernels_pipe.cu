@@ -8,10 +8,7 @@
 //                   i.e. one warp's lines) of up to four fields -- work,
 //                   Delta, x, B -- fetched with cp.async.bulk (1-D, 8 KiB per
 //                   field for N = 1024).  Consumer warps each own a unit.
-//   k_strided_pipe: each stage holds a COLS x N tile of a strided axis
-//                   (y: stride nx; z: stride nx*ny), fetched with tensor-map
-//                   TMA boxes (cp.async.bulk.tensor, <= 256 rows per box).
-//                   All consumer warps transform one tile together.
+// (The strided y/z passes are in kernels_stile.cu.)
 //
 // Loads therefore cost no registers and keep up to S stages in flight per SM
 // (Little's law needs ~35 KB/SM at 6.5 TB/s; a stage is 32-64 KB), while the
@@ -203,124 +200,15 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
     const double mine = block_sum_d<T::NT>(acc, sh_red);
     if (!last_block_total<T::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
     if (threadIdx.x != 0) return;
+    if (p.red.local_sum) {   // slab-decomposed: k_finish sums the ranks' totals after the all-gather
+        *p.red.local_sum = total;
+        return;
+    }
     finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red);
-}
-
-// ====================================================== strided pass ====
-template <int N>
-struct SPipe {
-    using G = LineGeo<N>;
-    static constexpr int COLS = (G::N1 >= 32) ? 8 : 16;     // columns per tile (64 / 128-byte rows)
-    static constexpr int PAD = (COLS == 8) ? 8 : 0;
-    static constexpr int CT = COLS * G::N1;                 // consumer threads
-    static constexpr int CW = CT / 32;
-    static constexpr int NT = CT + 32;
-    static constexpr int TILE = COLS * N;                   // float2 per stage
-    static constexpr int XB = LayCol<N, COLS, PAD, CT>::kFloat2;
-    static constexpr int BOXN = N < 256 ? N : 256;
-    static constexpr int S0 = (kSmemBudget - XB * 8) / (TILE * 8);
-    static constexpr int S = S0 > 4 ? 4 : S0;
-    static_assert(S >= 2, "strided pipeline needs >= 2 stages");
-    static constexpr int SMEM = (S * TILE + XB) * 8 + 2 * S * 8;
-};
-
-template <int N, int MODE, int RANK>
-__global__ void __launch_bounds__(SPipe<N>::NT, 1) k_strided_pipe(const __grid_constant__ CUtensorMap tmap,
-                                                                  SParams p) {
-    using G = LineGeo<N>;
-    using T = SPipe<N>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float2 *stages = reinterpret_cast<float2 *>(smem_raw);
-    float2 *xbuf = stages + T::S * T::TILE;
-    uint64_t *full = reinterpret_cast<uint64_t *>(xbuf + T::XB);
-    uint64_t *empty = full + T::S;
-    if (p.check_state) {
-        if (p.st->status != ST_RUNNING || p.st->k >= p.st->kmax) return;
-    }
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < T::S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], T::CW);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const long long tpo = p.ncols / T::COLS;
-    const long long ntiles = tpo * p.nouter;
-    const int nloc = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
-    if (warp == T::CW) {
-        // ---------------------------------------------------- producer warp
-        if (lane == 0) {
-            prefetch_tmap(&tmap);
-            for (int i = 0; i < nloc; ++i) {
-                const int s = i % T::S;
-                if (i >= T::S && !mbar_wait(&empty[s], ((i / T::S) - 1) & 1)) {
-                    if (atomicCAS(&p.st->err, 0, 3) == 0) p.st->err_info = i;
-                    break;
-                }
-                const long long t = blockIdx.x + (long long)i * gridDim.x;
-                const long long o = t / tpo;
-                const int c0 = (int)((t - o * tpo) * T::COLS);
-                float2 *st = stages + s * T::TILE;
-                mbar_arrive_expect_tx(&full[s], T::TILE * 8);
-#pragma unroll
-                for (int b = 0; b < N / T::BOXN; ++b) {
-                    if (RANK == 3) tma_load_3d(st + b * T::BOXN * T::COLS, &tmap, c0, b * T::BOXN, (int)o, &full[s]);
-                    else tma_load_2d(st + b * T::BOXN * T::COLS, &tmap, c0, b * T::BOXN, &full[s]);
-                }
-            }
-        }
-        return;   // the producer takes no part in the consumers' named barriers
-    }
-    // -------------------------------------------------------- consumers
-    const int c = threadIdx.x % T::COLS, j = threadIdx.x / T::COLS;
-    const LayCol<N, T::COLS, T::PAD, T::CT> lay{xbuf, c};
-    for (int i = 0; i < nloc; ++i) {
-        const int s = i % T::S;
-        if (!mbar_wait(&full[s], (i / T::S) & 1)) {
-            if (threadIdx.x == 0 && atomicCAS(&p.st->err, 0, 4) == 0) p.st->err_info = i;
-            return;
-        }
-        const long long t = blockIdx.x + (long long)i * gridDim.x;
-        const long long o = t / tpo;
-        const long long col = (t - o * tpo) * T::COLS + c;
-        const float2 *st = stages + s * T::TILE;
-        float2 v[G::N2];
-#pragma unroll
-        for (int m = 0; m < G::N2; ++m) v[m] = st[(j + G::N1 * m) * T::COLS + c];
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        fft_line<N, MODE == S_INV>(v, lay, j, p.tw);
-        if (MODE == S_FWD_MUL_INV) {
-            // (L+1)^-1 multiplier, Eq. 12: |p|^2 = p_x^2 + p_y^2 + p_line^2
-            float pt2;
-            if (p.line_axis == 2) {
-                const int ix = (int)(col % p.mp.nx), iy = (int)(col / p.mp.nx);
-                const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
-                pt2 = fmaf(px, px, py * py);
-            } else {
-                const float px = p.mp.kx * freq_m((int)col, p.mp.nx);
-                pt2 = px * px;
-            }
-            const float kl = (p.line_axis == 2) ? p.mp.kz : p.mp.ky;
-#pragma unroll
-            for (int m = 0; m < G::N2; ++m) {
-                const float pl = kl * freq_m(j + G::N1 * m, N);
-                v[m] = cmul(v[m], multiplier(p.mp, fmaf(pl, pl, pt2)));
-            }
-            fft_line<N, true>(v, lay, j, p.tw);
-        }
-        float2 *dst = p.data + (o * p.ostride + col);
-#pragma unroll
-        for (int m = 0; m < G::N2; ++m) dst[(long long)(j + G::N1 * m) * p.stride] = v[m];
-    }
 }
 
 // ========================================================= launchers ====
 #define USP_PIPE_X_N(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
-#define USP_PIPE_S_N(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
 template <int N, int MODE>
 static cudaError_t xpipe_t(const XParams &p, int grid, cudaStream_t s) {
@@ -343,44 +231,6 @@ cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cud
         return xpipe_t<n, X_ITER>(p, grid, s);
     switch (N) { USP_PIPE_X_N(XP_CASE) default: return cudaErrorInvalidValue; }
 #undef XP_CASE
-}
-
-template <int N, int MODE, int RANK>
-static cudaError_t spipe_t(const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_strided_pipe<N, MODE, RANK>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SPipe<N>::SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    k_strided_pipe<N, MODE, RANK><<<grid, SPipe<N>::NT, SPipe<N>::SMEM, s>>>(map, p);
-    return cudaGetLastError();
-}
-
-template <int N>
-static cudaError_t spipe_mode(SMode mode, int rank, const CUtensorMap &map, const SParams &p, int grid,
-                              cudaStream_t s) {
-    if (rank == 3) {
-        if (mode == S_FWD) return spipe_t<N, S_FWD, 3>(map, p, grid, s);
-        if (mode == S_INV) return spipe_t<N, S_INV, 3>(map, p, grid, s);
-        return spipe_t<N, S_FWD_MUL_INV, 3>(map, p, grid, s);
-    }
-    if (mode == S_FWD) return spipe_t<N, S_FWD, 2>(map, p, grid, s);
-    if (mode == S_INV) return spipe_t<N, S_INV, 2>(map, p, grid, s);
-    return spipe_t<N, S_FWD_MUL_INV, 2>(map, p, grid, s);
-}
-
-bool strided_pipe_supported(long long n) { return n >= 16 && n <= 1024; }
-int strided_pipe_cols(int N) { return (1 << (ilog2(N) / 2)) >= 32 ? 8 : 16; }
-int strided_pipe_box(int N) { return N < 256 ? N : 256; }
-
-cudaError_t launch_strided_pipe(int N, SMode mode, int rank, const CUtensorMap &map, const SParams &p, int grid,
-                                cudaStream_t s) {
-#define SP_CASE(n) \
-    case n: return spipe_mode<n>(mode, rank, map, p, grid, s);
-    switch (N) { USP_PIPE_S_N(SP_CASE) default: return cudaErrorInvalidValue; }
-#undef SP_CASE
 }
 
 }  // namespace usp

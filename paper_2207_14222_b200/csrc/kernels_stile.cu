@@ -168,17 +168,26 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     const long long tpo = p.ncols / T::COLS;
     const long long ntiles = tpo * p.nouter;
     const int nloc = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
-    const bool rank3 = p.line_axis == 1 && p.nouter > 1;
 
     auto issue = [&](int i) {   // thread 0: TMA boxes of local tile i
         const long long t = blockIdx.x + (long long)i * gridDim.x;
         const long long o = t / tpo;
         const int c0 = (int)((t - o * tpo) * T::COLS);
         mbar_arrive_expect_tx(full, T::TILE * 8);
+        if (p.map_rank == 5) {
+            // K_D after the return transpose: the line's rows live in P blocks of
+            // the send layout [r][q][z_loc][y_loc][x] (5-D map {x, y_loc, z_loc, q, r})
+            const int r = (int)(o / p.nz_loc), zl = (int)(o - (long long)r * p.nz_loc);
+            const int lg = p.nyl_lg < ilog2(T::BOXN) ? p.nyl_lg : ilog2(T::BOXN);
+            const int nyl_mask = (1 << p.nyl_lg) - 1;
+            for (int y0 = 0; y0 < N; y0 += (1 << lg))
+                tma_load_5d(stage + y0 * T::COLS, &tmap, c0, y0 & nyl_mask, zl, y0 >> p.nyl_lg, r, full);
+        } else {
 #pragma unroll
-        for (int bx = 0; bx < N / T::BOXN; ++bx) {
-            if (rank3) tma_load_3d(stage + bx * T::BOXN * T::COLS, &tmap, c0, bx * T::BOXN, (int)o, full);
-            else tma_load_2d(stage + bx * T::BOXN * T::COLS, &tmap, c0, bx * T::BOXN, full);
+            for (int bx = 0; bx < N / T::BOXN; ++bx) {
+                if (p.map_rank == 3) tma_load_3d(stage + bx * T::BOXN * T::COLS, &tmap, c0, bx * T::BOXN, (int)o, full);
+                else tma_load_2d(stage + bx * T::BOXN * T::COLS, &tmap, c0, (int)o * N + bx * T::BOXN, full);
+            }
         }
     };
     if (tid == 0) {
@@ -190,10 +199,10 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     load_twiddles<N>(sm_tw, p.tw);
     __syncthreads();
 
-    // HALFX shift flips: threads whose top row bit is set negate odd inputs /
-    // outputs (see header)
-    float sg = 1.f;
-    if constexpr (T::FLIP) sg = ((j >> (ilog2(G::N1) - 1)) & 1) ? -1.f : 1.f;
+    // FLIP shift flips: threads whose top row bit is set negate odd inputs /
+    // outputs (see header).  The bit is uniform per warp (a warp holds rows
+    // j = 2w, 2w+1), so the flips are a non-divergent branch.
+    const bool flip = T::FLIP && ((j >> (ilog2(G::N1) - 1)) & 1);
 
     for (int i = 0; i < nloc; ++i) {
         if (!mbar_wait(full, i & 1)) {
@@ -203,10 +212,12 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         float2 v[G::N2];
 #pragma unroll
         for (int m = 0; m < G::N2; ++m) {
-            float2 a = stage[(j + G::N1 * m) * T::COLS + c];
-            if (MODE == S_INV) a = cconj(a);
-            if (T::FLIP && (m & 1)) a = cscale(a, sg);
-            v[m] = a;
+            const float2 a = stage[(j + G::N1 * m) * T::COLS + c];
+            v[m] = (MODE == S_INV) ? cconj(a) : a;
+        }
+        if (flip) {
+#pragma unroll
+            for (int m = 1; m < G::N2; m += 2) v[m] = cscale(v[m], -1.f);
         }
         fence_proxy_async_smem();
         __syncthreads();                 // stage consumed: prefetch the next tile
@@ -220,7 +231,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 const long long col = (t - o * tpo) * T::COLS + c;
                 float pt2;
                 if (p.line_axis == 2) {
-                    const int ix = (int)(col % p.mp.nx), iy = (int)(col / p.mp.nx);
+                    // column (x, y) of the (possibly y-sliced) z pass; y global
+                    const long long gc = o * p.ncols + col;
+                    const int ix = (int)(gc % p.mp.nx), iy = (int)(p.y0 + gc / p.mp.nx);
                     const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
                     pt2 = fmaf(px, px, py * py);
                 } else {
@@ -238,15 +251,17 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                     //   di = Im(sigma + c);  then conj so the second forward DFT inverts.
                     // (constants are re-derived here, opaque to hoisting, to keep them
                     // out of the registers live across the FFT)
+                    // (kl is pre-scaled by sqrt(D): dr = (sqrt(D) p_line)^2 + base)
                     float di = p.mp.sc.y, kl = (p.line_axis == 2) ? p.mp.kz : p.mp.ky;
                     asm volatile("" : "+f"(di), "+f"(kl));
+                    kl *= p.mp.sqrtD;
                     const float di2 = di * di, cyd = p.mp.cn.y * di, cxd = p.mp.cn.x * di;
-                    const float klj = kl * (float)j, Dm = p.mp.D;
+                    const float klj = kl * (float)j;
 #pragma unroll
                     for (int m = 0; m < G::N2; ++m) {
                         const float cm = (float)(G::N1 * m - ((m >= G::N2 / 2) ? N : 0));
                         const float pl = fmaf(kl, cm, klj);
-                        const float dr = fmaf(Dm * pl, pl, base);
+                        const float dr = fmaf(pl, pl, base);
                         const float inv = rcp_approx(fmaf(dr, dr, di2));
                         const float gr = fmaf(p.mp.cn.x, dr, cyd) * inv;
                         const float gi = fmaf(p.mp.cn.y, dr, -cxd) * inv;
@@ -263,14 +278,30 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         const long long col = (t - o * tpo) * T::COLS + c;
         long long stride = p.stride;
         asm volatile("" : "+l"(stride));
-        float2 *sb = p.data + (o * p.ostride + col) + (long long)j * stride;
-        const long long step = (long long)G::N1 * stride;
+        if (flip) {
 #pragma unroll
-        for (int m = 0; m < G::N2; ++m) {
-            float2 a = v[m];
-            if (T::FLIP && (m & 1)) a = cscale(a, sg);
-            sb[0] = (MODE == S_FWD) ? a : cconj(a);
-            sb += step;
+            for (int m = 1; m < G::N2; m += 2) v[m] = cscale(v[m], -1.f);
+        }
+        if (MODE == S_FWD && p.send_layout) {
+            // K_B before the forward transpose: row y of plane o goes to block
+            // (r, q = y / ny_loc) of the send layout [r][q][z_loc][y_loc][x]
+            const long long r = o / p.nz_loc, zl = o - r * p.nz_loc;
+            const long long nyl = 1LL << p.nyl_lg;
+            const long long bk = (long long)p.nz_loc * nyl * p.ncols;
+            float2 *sb = p.dst + r * p.P * bk + zl * nyl * p.ncols + col;
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) {
+                const int y = j + G::N1 * m;
+                sb[(y >> p.nyl_lg) * bk + (long long)(y & (nyl - 1)) * stride] = v[m];
+            }
+        } else {
+            float2 *sb = p.dst + (o * p.ostride + col) + (long long)j * stride;
+            const long long step = (long long)G::N1 * stride;
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) {
+                sb[0] = (MODE == S_FWD) ? v[m] : cconj(v[m]);
+                sb += step;
+            }
         }
     }
 }

@@ -1,8 +1,25 @@
 // usp_api.cu -- the C-ABI of include/usp.h: plan, workspace, setup and the
-// iteration driver.  All arithmetic of the method runs in kernels.cu; this
-// file only sequences launches, validates, and moves bytes.
+// iteration driver.  All arithmetic of the method runs in the kernels
+// (kernels*.cu); this file only sequences launches and collectives,
+// validates, and moves bytes.
+//
+// Slab decomposition: a 3-D grid is split into P z-slabs.
+// The x pass (K_A) and the y passes (K_B, K_D) are local to a slab; the z
+// pass (K_C) needs whole z-lines, so K_B stores its output in the "send
+// layout" [q][z_loc][y_loc][x] (block q = the y-range of slab q), an
+// all-to-all turns it into y-slabs [z][y_loc][x] on which K_C runs, and the
+// reverse all-to-all brings the blocks back for K_D, which reads them through
+// a 5-D tensor map.  The residual is one all-gather of P doubles summed in
+// rank order, so every rank takes the same stop decision.
+//   * NCCL mode (desc.nccl_comm): one GPU per rank, the all-to-alls are
+//     grouped ncclSend/ncclRecv over NVLink.
+//   * virtual mode (desc.virtual_ranks = P): all P slabs on one GPU, the
+//     all-to-alls are device copies -- the same kernels, layouts and index
+//     arithmetic, so the decomposition is testable on a single GPU.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -40,10 +57,78 @@ usp_status fail(usp_status s, const char *fmt, ...) {
                         __FILE__, __LINE__);                                             \
     } while (0)
 
+// ------------------------------------------------------------ NCCL shim --
+// libnccl.so.2 is opened at run time (the torch wheel's copy when torch has
+// loaded it, else the path in USP_NCCL_LIB), so single-GPU use of libusp
+// needs no NCCL at all.  nccl.h supplies the types only.
+struct Nccl {
+    bool ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*CommCount)(const ncclComm_t, int *);
+    ncclResult_t (*CommUserRank)(const ncclComm_t, int *);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    const char *(*GetErrorString)(ncclResult_t);
+};
+
+Nccl &nccl() {
+    static Nccl n;
+    static bool tried = false;
+    if (tried) return n;
+    tried = true;
+    void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        const char *path = std::getenv("USP_NCCL_LIB");
+        if (path) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) {
+        n.why = "libnccl.so.2 not found (set USP_NCCL_LIB)";
+        return n;
+    }
+    bool all = true;
+    auto sym = [&](const char *name) {
+        void *f = dlsym(h, name);
+        if (!f) all = false;
+        return f;
+    };
+    n.GetUniqueId = (decltype(n.GetUniqueId))sym("ncclGetUniqueId");
+    n.CommInitRank = (decltype(n.CommInitRank))sym("ncclCommInitRank");
+    n.CommDestroy = (decltype(n.CommDestroy))sym("ncclCommDestroy");
+    n.CommCount = (decltype(n.CommCount))sym("ncclCommCount");
+    n.CommUserRank = (decltype(n.CommUserRank))sym("ncclCommUserRank");
+    n.GroupStart = (decltype(n.GroupStart))sym("ncclGroupStart");
+    n.GroupEnd = (decltype(n.GroupEnd))sym("ncclGroupEnd");
+    n.Send = (decltype(n.Send))sym("ncclSend");
+    n.Recv = (decltype(n.Recv))sym("ncclRecv");
+    n.AllGather = (decltype(n.AllGather))sym("ncclAllGather");
+    n.AllReduce = (decltype(n.AllReduce))sym("ncclAllReduce");
+    n.GetErrorString = (decltype(n.GetErrorString))sym("ncclGetErrorString");
+    n.ok = all;
+    if (!all) n.why = "libnccl.so.2 lacks an entry point";
+    return n;
+}
+
+#define NC(call)                                                                                   \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess)                                                                     \
+            return fail(USP_ERR_NCCL, "%s failed: %s (%s:%d)", #call, nccl().GetErrorString(r_), __FILE__, \
+                        __LINE__);                                                                 \
+    } while (0)
+
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
-              KC_FARTHEST, KC_SETSTATE, KC_N };
+              KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_N };
 const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
-                              "solve1d", "potential", "farthest", "set_state"};
+                              "solve1d", "potential", "farthest", "set_state", "xpass_setup",
+                              "all_to_all", "finish"};
 
 struct Timed {
     int cls;
@@ -55,13 +140,22 @@ struct Timed {
 struct usp_plan_s {
     usp_plan_desc d{};
     int ndim = 0;
-    long long nx = 1, ny = 1, nz = 1, nvox = 0;
+    long long nx = 1, ny = 1, nz = 1, nvox = 0;   // global grid
     cudaStream_t stream = nullptr;
     int nsm = 148;
+    // slab decomposition
+    int P = 1, rank = 0;          // slabs, this rank
+    bool virt = false;            // all P slabs on this GPU (device-copy transposes)
+    ncclComm_t comm = nullptr;    // NCCL mode
+    long long nzs = 1;            // z planes per slab (nz / P)
+    long long nzh = 1;            // z planes this plan holds (nzs, or nz in virtual / 1-GPU mode)
+    long long nyl = 1;            // y rows per y block (ny / P)
+    long long nloc = 0;           // voxels this plan holds
     // workspace
     char *ws = nullptr;
     size_t ws_bytes = 0;
     float2 *x = nullptr, *delta = nullptr, *B = nullptr, *work = nullptr;
+    float2 *sendb = nullptr, *recvb = nullptr;   // P > 1
     // plan-owned small device memory
     IterState *st = nullptr;
     double *partials = nullptr;
@@ -73,6 +167,7 @@ struct usp_plan_s {
     double *far_d = nullptr;
     long long *far_i = nullptr;
     int far_cap = 0;
+    double *coll = nullptr;         // collective scratch: [0] local x-pass total, [8..] gathers
     IterState *st_host = nullptr;   // pinned mirror
     // split
     usp_c128 sigma{}, c{}, centre{};
@@ -80,15 +175,13 @@ struct usp_plan_s {
     bool have_potential = false, have_source = false;
     // launch configuration
     int grid_x = 0, grid_y = 0, grid_z = 0;
-    // TMA-pipelined kernels (default); USP_LEGACY=1 selects the register-staged ones
-    bool pipe = true, pipe_xk = true, pipe_sk = false;
-    bool pipe_y = false, pipe_z = false;
-    int gridp_x = 0, gridp_y = 0, gridp_z = 0;
-    CUtensorMap map_y{}, map_z{};
+    // TMA-pipelined x pass (default); USP_LEGACY=1 selects the register-staged kernels
+    bool pipe = true, pipe_xk = true;
+    int gridp_x = 0;
     // TMA-prefetched 16-column strided passes (kernels_stile.cu; default, USP_STILE=0 disables)
     bool stile = true, stile_y = false, stile_z = false;
     int grids_y = 0, grids_z = 0;
-    CUtensorMap smap_y{}, smap_z{};
+    CUtensorMap smap_y{}, smap_z{}, smap_kd{};
     // profiling
     bool prof = false;
     std::vector<Timed> timed;
@@ -99,6 +192,8 @@ struct usp_plan_s {
 };
 
 namespace {
+
+bool multi_rank(const usp_plan_s *p) { return p->P > 1 && !p->virt; }
 
 cudaEvent_t get_event(usp_plan_s *p) {
     if (!p->ev_pool.empty()) {
@@ -115,8 +210,8 @@ struct Tick {   // brackets one launch with events when profiling
     usp_plan_s *p;
     int cls;
     cudaEvent_t a = nullptr;
-    Tick(usp_plan_s *pl, int c) : p(pl), cls(c) {
-        ++p->launches;
+    Tick(usp_plan_s *pl, int c, bool count = true) : p(pl), cls(c) {
+        if (count) ++p->launches;
         if (p->prof) {
             a = get_event(p);
             cudaEventRecord(a, p->stream);
@@ -171,12 +266,12 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// Tensor map over the complex64 work field viewed with 8-byte elements.
+// Tensor map over a complex64 field viewed with 8-byte elements.
 bool make_map(CUtensorMap *m, void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides_bytes,
               const cuuint32_t *box) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
-    const cuuint32_t es[3] = {1, 1, 1};
+    const cuuint32_t es[5] = {1, 1, 1, 1, 1};
     const CUtensorMapL2promotion promo = (box[0] * 8 >= 128) ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                               : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, base, dims, strides_bytes, box, es,
@@ -207,6 +302,22 @@ std::vector<float2> twiddle_table(int n) {
 int occ_grid(usp_plan_s *p, long long units, int per_sm) {
     long long g = (long long)p->nsm * per_sm;
     return (int)std::max(1LL, std::min(units, g));
+}
+
+// ------------------------------------------------------- collectives --
+// Gather `n` host doubles from every rank (rank order) into out[P*n].
+usp_status gather_host(usp_plan_s *p, const double *mine, int n, std::vector<double> &out) {
+    out.assign((size_t)p->P * n, 0.0);
+    if (!multi_rank(p)) {
+        std::copy(mine, mine + n, out.begin());
+        return USP_OK;
+    }
+    double *snd = p->coll + 8, *rcv = p->coll + 16;
+    CU(cudaMemcpyAsync(snd, mine, sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    NC(nccl().AllGather(snd, rcv, (size_t)n, ncclDouble, p->comm, p->stream));
+    CU(cudaMemcpyAsync(out.data(), rcv, sizeof(double) * n * p->P, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    return USP_OK;
 }
 
 // ---------------------------------------------------------------- MEC --
@@ -277,21 +388,29 @@ usp_status read_point(usp_plan_s *p, const void *medium_dev, long long idx, P2 &
 
 // Smallest enclosing circle of all medium values: grow a
 // support set with the farthest point from the current circle (one device
-// pass each) until every value is inside.  The result is the MEC of a subset
-// that encloses all points, i.e. the MEC of the full set.
+// pass each; across ranks the farthest of the ranks' farthest points, ties
+// to the lowest rank) until every value is inside.  The result is the MEC of
+// a subset that encloses all points, i.e. the MEC of the full set, and it is
+// identical on every rank.
 usp_status device_mec(usp_plan_s *p, const void *medium_dev, P2 &centre, double &radius) {
     std::vector<P2> sup;
     P2 q;
     usp_status s = read_point(p, medium_dev, 0, q);
     if (s) return s;
+    std::vector<double> g;
+    {
+        const double mine[3] = {0.0, q.x, q.y};
+        if ((s = gather_host(p, mine, 3, g))) return s;
+        q = {g[1], g[2]};   // rank 0's first value
+    }
     sup.push_back(q);
     centre = q;
     radius = 0.0;
-    const int grid = std::min(p->far_cap, occ_grid(p, (p->nvox + 255) / 256, 8));
+    const int grid = std::min(p->far_cap, occ_grid(p, (p->nloc + 255) / 256, 8));
     std::vector<double> bd(grid);
     std::vector<long long> bi(grid);
     for (int it = 0; it < 200; ++it) {
-        FarParams fp{medium_dev, p->d.dtype == USP_R32, p->nvox, centre.x, centre.y, p->far_d, p->far_i};
+        FarParams fp{medium_dev, p->d.dtype == USP_R32, p->nloc, centre.x, centre.y, p->far_d, p->far_i};
         {
             Tick t(p, KC_FARTHEST);
             CU(launch_farthest(fp, grid, p->stream));
@@ -304,6 +423,14 @@ usp_status device_mec(usp_plan_s *p, const void *medium_dev, P2 &centre, double 
             if (bd[i] > bd[b] || (bd[i] == bd[b] && bi[i] < bi[b])) b = i;
         s = read_point(p, medium_dev, bi[b], q);
         if (s) return s;
+        {
+            const double mine[3] = {bd[b], q.x, q.y};
+            if ((s = gather_host(p, mine, 3, g))) return s;
+            int best = 0;
+            for (int r = 1; r < p->P && multi_rank(p); ++r)
+                if (g[3 * r] > g[3 * best]) best = r;
+            q = {g[3 * best + 1], g[3 * best + 2]};
+        }
         if (in_circle(q, centre, radius)) return USP_OK;
         sup.push_back(q);
         mec_small(sup, centre, radius);
@@ -321,10 +448,11 @@ size_t elem_bytes(const usp_plan_s *p) { return p->d.dtype == USP_R32 ? 4 : 8; }
 
 MulParams mul_params(const usp_plan_s *p) {
     MulParams mp{};
-    const double cr = p->c.re / (double)p->nvox, ci = p->c.im / (double)p->nvox;
+    const double cr = p->c.re / (double)p->nvox, ci = p->c.im / (double)p->nvox;   // 1/N_vox of the global F^-1
     mp.cn = make_float2((float)cr, (float)ci);
     mp.sc = make_float2((float)(p->sigma.re + p->c.re), (float)(p->sigma.im + p->c.im));
     mp.D = (float)p->d.D;
+    mp.sqrtD = (float)std::sqrt(p->d.D);
     mp.kx = (float)(2.0 * M_PI / ((double)p->nx * p->d.h[0]));
     mp.ky = (float)(2.0 * M_PI / ((double)p->ny * p->d.h[1]));
     mp.kz = (float)(2.0 * M_PI / ((double)p->nz * p->d.h[2]));
@@ -334,6 +462,12 @@ MulParams mul_params(const usp_plan_s *p) {
     return mp;
 }
 
+Red red_params(usp_plan_s *p) {
+    Red r{p->partials, p->hist, p->hist_cap, nullptr};
+    if (multi_rank(p)) r.local_sum = p->coll;
+    return r;
+}
+
 XParams x_params(usp_plan_s *p) {
     XParams xp{};
     xp.work = p->work;
@@ -341,56 +475,129 @@ XParams x_params(usp_plan_s *p) {
     xp.x = p->x;
     xp.B = p->B;
     xp.tw = p->tw[0];
-    xp.nlines = p->ny * p->nz;
+    xp.nlines = p->ny * p->nzh;
     xp.src_real = p->d.dtype == USP_R32;
     const double m = p->c.re * p->c.re + p->c.im * p->c.im;
     xp.inv_c = make_float2((float)(p->c.re / m), (float)(-p->c.im / m));
     xp.st = p->st;
-    xp.red = Red{p->partials, p->hist, p->hist_cap};
+    xp.red = red_params(p);
     return xp;
 }
 
+// x pass; with P ranks the CTA total is all-gathered and k_finish sums the
+// ranks' totals in rank order (X_SRC_FWD reduces nothing).
 usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
-    Tick t(p, KC_XPASS);
-    if (p->pipe_xk) CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream));
-    else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
+    {
+        Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
+        if (p->pipe_xk) CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream));
+        else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
+    }
+    if (mode != X_SRC_FWD && multi_rank(p)) {
+        {
+            Tick t(p, KC_A2A, false);
+            NC(nccl().AllGather(p->coll, p->coll + 8, 1, ncclDouble, p->comm, p->stream));
+        }
+        Tick t(p, KC_FINISH);
+        CU(launch_finish(p->st, p->coll + 8, p->P, mode == X_SRC_EPI, red_params(p), p->stream));
+    }
     return USP_OK;
 }
 
-usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, bool use_pipe, int rank, const CUtensorMap &map,
-                       const SParams &sp, int grid_legacy, int grid_pipe) {
+usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, const SParams &sp, const CUtensorMap &map,
+                       bool use_stile, int grid_legacy) {
     Tick t(p, cls);
-    const bool is_z = (cls == KC_ZMUL);
-    if (is_z ? p->stile_z : p->stile_y) {
-        CU(launch_stile(n, mode, is_z ? p->smap_z : p->smap_y, sp, is_z ? p->grids_z : p->grids_y, p->stream));
+    if (use_stile) {
+        CU(launch_stile(n, mode, map, sp, cls == KC_ZMUL ? p->grids_z : p->grids_y, p->stream));
         return USP_OK;
     }
-    // z pass (two FFTs + multiplier, the most arithmetic per byte): 16-column
-    // tiles of 512 threads measured faster than two 256-thread CTAs per SM
-    // (7.2 vs 7.9 ms at 1024^3); USP_ZCOLS=8 selects the latter.
+    // legacy register-staged passes (line lengths the TMA tiles do not cover):
+    // the z pass (two FFTs + multiplier) runs 16-column tiles of 512 threads
     static const char *zc = std::getenv("USP_ZCOLS");
     const int cols = (cls == KC_ZMUL) ? (zc ? std::atoi(zc) : 16) : 0;
-    if (use_pipe) CU(launch_strided_pipe(n, mode, rank, map, sp, grid_pipe, p->stream));
-    else CU(launch_strided(n, mode, sp, cols == 16 ? p->nsm : grid_legacy, p->stream, cols));
+    CU(launch_strided(n, mode, sp, cols == 16 ? p->nsm : grid_legacy, p->stream, cols));
+    return USP_OK;
+}
+
+SParams sparams(usp_plan_s *p, float2 *data, float2 *dst, const float2 *tw, long long stride, long long ncols,
+                long long nouter, long long ostride, int line_axis, int check_state, int map_rank) {
+    SParams sp{};
+    sp.data = data;
+    sp.dst = dst;
+    sp.tw = tw;
+    sp.stride = stride;
+    sp.ncols = ncols;
+    sp.nouter = nouter;
+    sp.ostride = ostride;
+    sp.line_axis = line_axis;
+    sp.check_state = check_state;
+    sp.mp = mul_params(p);
+    sp.st = p->st;
+    sp.map_rank = map_rank;
+    sp.send_layout = 0;
+    sp.P = p->P;
+    sp.nz_loc = (int)p->nzs;
+    sp.nyl_lg = log2ll(p->nyl);
+    sp.y0 = 0;
+    return sp;
+}
+
+// The two transposes of the slab decomposition.  Block (r, q) of the send
+// layout holds slab r's rows for y block q; block (r, q) of the receive
+// layout holds y block r's planes of slab q.  forward: recv(r,q) <- send(q,r);
+// back: send(q,r) <- recv(r,q).
+usp_status exchange(usp_plan_s *p, bool forward) {
+    const long long bk = p->nzs * p->nyl * p->nx;   // elements per block
+    const size_t bytes = (size_t)bk * sizeof(float2);
+    Tick t(p, KC_A2A, false);
+    if (p->virt) {
+        for (int r = 0; r < p->P; ++r)
+            for (int q = 0; q < p->P; ++q) {
+                float2 *rv = p->recvb + ((long long)r * p->P + q) * bk;
+                float2 *sd = p->sendb + ((long long)q * p->P + r) * bk;
+                if (forward) CU(cudaMemcpyAsync(rv, sd, bytes, cudaMemcpyDeviceToDevice, p->stream));
+                else CU(cudaMemcpyAsync(sd, rv, bytes, cudaMemcpyDeviceToDevice, p->stream));
+            }
+        return USP_OK;
+    }
+    Nccl &n = nccl();
+    float2 *from = forward ? p->sendb : p->recvb, *to = forward ? p->recvb : p->sendb;
+    NC(n.GroupStart());
+    for (int q = 0; q < p->P; ++q) {
+        NC(n.Send(from + q * bk, (size_t)bk * 2, ncclFloat, q, p->comm, p->stream));
+        NC(n.Recv(to + q * bk, (size_t)bk * 2, ncclFloat, q, p->comm, p->stream));
+    }
+    NC(n.GroupEnd());
     return USP_OK;
 }
 
 // The middle of the chain: every FFT pass between the x forward and the x
-// inverse, with the (L+1)^-1 multiplier on the last axis.
+// inverse, with the (L+1)^-1 multiplier on the last axis (Eq. 12).
 usp_status chain_mid(usp_plan_s *p, int check_state) {
-    const MulParams mp = mul_params(p);
     if (p->ndim == 2) {
-        SParams sp{p->work, p->tw[1], p->nx, p->nx, 1, 0, 1, check_state, mp, p->st};
-        return run_strided(p, KC_YMUL2D, (int)p->ny, S_FWD_MUL_INV, p->pipe_y, 2, p->map_y, sp, p->grid_y,
-                           p->gridp_y);
+        SParams sp = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, 1, 0, 1, check_state, 2);
+        return run_strided(p, KC_YMUL2D, (int)p->ny, S_FWD_MUL_INV, sp, p->smap_y, p->stile_y, p->grid_y);
     }
-    SParams yf{p->work, p->tw[1], p->nx, p->nx, p->nz, p->nx * p->ny, 1, check_state, mp, p->st};
-    SParams zm{p->work, p->tw[2], p->nx * p->ny, p->nx * p->ny, 1, 0, 2, check_state, mp, p->st};
-    usp_status s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, p->pipe_y, 3, p->map_y, yf, p->grid_y, p->gridp_y);
-    if (s) return s;
-    s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, p->pipe_z, 2, p->map_z, zm, p->grid_z, p->gridp_z);
-    if (s) return s;
-    return run_strided(p, KC_YINV, (int)p->ny, S_INV, p->pipe_y, 3, p->map_y, yf, p->grid_y, p->gridp_y);
+    usp_status s;
+    if (p->P == 1) {
+        SParams yf = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, p->nz, p->nx * p->ny, 1, check_state, 3);
+        SParams zm = sparams(p, p->work, p->work, p->tw[2], p->nx * p->ny, p->nx * p->ny, 1, 0, 2, check_state, 2);
+        if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, p->stile_y, p->grid_y))) return s;
+        if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, p->stile_z, p->grid_z))) return s;
+        return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, p->stile_y, p->grid_y);
+    }
+    // slab decomposition: K_B -> transpose -> K_C -> transpose -> K_D
+    const long long pv = p->virt ? p->P : 1;   // y blocks held here
+    SParams yb = sparams(p, p->work, p->sendb, p->tw[1], p->nx, p->nx, p->nzh, p->nx * p->ny, 1, check_state, 3);
+    yb.send_layout = 1;
+    SParams zm = sparams(p, p->recvb, p->recvb, p->tw[2], p->nyl * p->nx, p->nyl * p->nx, pv,
+                         p->nz * p->nyl * p->nx, 2, check_state, 2);
+    zm.y0 = p->virt ? 0 : (long long)p->rank * p->nyl;
+    SParams yd = sparams(p, p->sendb, p->work, p->tw[1], p->nx, p->nx, p->nzh, p->nx * p->ny, 1, check_state, 5);
+    if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0))) return s;
+    if ((s = exchange(p, true))) return s;
+    if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, true, 0))) return s;
+    if ((s = exchange(p, false))) return s;
+    return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_kd, true, 0);
 }
 
 usp_status sync_state(usp_plan_s *p) {
@@ -402,6 +609,53 @@ usp_status sync_state(usp_plan_s *p) {
     return USP_OK;
 }
 
+// Tensor maps of the strided passes (they embed the workspace addresses).
+void build_maps(usp_plan_s *p) {
+    p->stile_y = p->stile_z = false;
+    if (!p->stile || p->ndim < 2 || !stile_supported(p->ny)) return;
+    const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
+    if (p->ndim == 2) {
+        const cuuint64_t dims[2] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny};
+        const cuuint64_t str[1] = {(cuuint64_t)p->nx * 8};
+        const cuuint32_t box[2] = {cy, by};
+        p->stile_y = make_map(&p->smap_y, p->work, 2, dims, str, box);
+        return;
+    }
+    {   // y pass over the planes held here: {x, y, z}
+        const cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)p->nzh};
+        const cuuint64_t str[2] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nx * p->ny) * 8};
+        const cuuint32_t box[3] = {cy, by, 1};
+        p->stile_y = make_map(&p->smap_y, p->work, 3, dims, str, box);
+    }
+    if (!stile_supported(p->nz)) return;
+    const cuuint32_t cz = (cuuint32_t)stile_cols((int)p->nz), bz = (cuuint32_t)stile_box((int)p->nz);
+    if (p->P == 1) {   // z pass: {x*y columns, z}
+        const cuuint64_t dims[2] = {(cuuint64_t)(p->nx * p->ny), (cuuint64_t)p->nz};
+        const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};
+        const cuuint32_t box[2] = {cz, bz};
+        p->stile_z = make_map(&p->smap_z, p->work, 2, dims, str, box);
+        return;
+    }
+    const long long pv = p->virt ? p->P : 1;
+    bool ok;
+    {   // z pass on the y-slabs of the receive buffer: {x*y_loc columns, z * (y blocks)}
+        const cuuint64_t dims[2] = {(cuuint64_t)(p->nyl * p->nx), (cuuint64_t)(p->nz * pv)};
+        const cuuint64_t str[1] = {(cuuint64_t)(p->nyl * p->nx) * 8};
+        const cuuint32_t box[2] = {cz, bz};
+        ok = make_map(&p->smap_z, p->recvb, 2, dims, str, box);
+    }
+    {   // K_D reads the send layout [r][q][z_loc][y_loc][x]: {x, y_loc, z_loc, q, r}
+        const cuuint64_t dims[5] = {(cuuint64_t)p->nx, (cuuint64_t)p->nyl, (cuuint64_t)p->nzs, (cuuint64_t)p->P,
+                                    (cuuint64_t)pv};
+        const cuuint64_t bk = (cuuint64_t)(p->nzs * p->nyl * p->nx) * 8;
+        const cuuint64_t str[4] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nyl * p->nx) * 8, bk, bk * p->P};
+        const cuuint32_t box[5] = {cy, std::min<cuuint32_t>(by, (cuuint32_t)p->nyl), 1, 1, 1};
+        ok = ok && make_map(&p->smap_kd, p->sendb, 5, dims, str, box);
+    }
+    p->stile_z = ok;
+    p->stile_y = p->stile_y && ok;
+}
+
 }  // namespace
 
 // =================================================================== ABI ==
@@ -409,14 +663,45 @@ extern "C" {
 
 const char *usp_last_error(void) { return g_err.c_str(); }
 
-const char *usp_version(void) { return "0.1 sm_100a"; }
+const char *usp_version(void) { return "0.2 sm_100a"; }
+
+usp_status usp_comm_unique_id(unsigned char id[128]) {
+    if (!id) return fail(USP_ERR_ARG, "NULL argument");
+    Nccl &n = nccl();
+    if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
+    ncclUniqueId u;
+    NC(n.GetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(id, &u, 128);
+    return USP_OK;
+}
+
+usp_status usp_comm_init(const unsigned char id[128], int nranks, int rank, void **comm) {
+    if (!id || !comm) return fail(USP_ERR_ARG, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(USP_ERR_ARG, "bad rank %d of %d", rank, nranks);
+    Nccl &n = nccl();
+    if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclComm_t c = nullptr;
+    NC(n.CommInitRank(&c, nranks, u, rank));
+    *comm = c;
+    return USP_OK;
+}
+
+usp_status usp_comm_destroy(void *comm) {
+    if (!comm) return USP_OK;
+    Nccl &n = nccl();
+    if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
+    NC(n.CommDestroy((ncclComm_t)comm));
+    return USP_OK;
+}
 
 usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     if (!desc || !out) return fail(USP_ERR_ARG, "NULL argument");
     *out = nullptr;
     if (desc->ndim < 1 || desc->ndim > 3) return fail(USP_ERR_ARG, "ndim must be 1..3 (got %d)", desc->ndim);
     if (!(desc->D > 0.0)) return fail(USP_ERR_ARG, "D must be > 0");
-    if (desc->nccl_comm) return fail(USP_ERR_UNSUPPORTED, "multi-GPU plans are not available in this build");
     if (desc->dtype != USP_C64 && desc->dtype != USP_R32) return fail(USP_ERR_ARG, "bad dtype");
     if (desc->medium != USP_MEDIUM_K2 && desc->medium != USP_MEDIUM_W) return fail(USP_ERR_ARG, "bad medium");
     for (int a = 0; a < desc->ndim; ++a) {
@@ -424,6 +709,29 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
             return fail(USP_ERR_UNSUPPORTED, "extent n[%d]=%lld must be a power of two in [16, 2048]", a,
                         (long long)desc->n[a]);
         if (!(desc->h[a] > 0.0)) return fail(USP_ERR_ARG, "h[%d] must be > 0", a);
+    }
+    int P = 1, rank = 0;
+    bool virt = false;
+    if (desc->nccl_comm && desc->virtual_ranks > 1)
+        return fail(USP_ERR_ARG, "nccl_comm and virtual_ranks are exclusive");
+    if (desc->nccl_comm) {
+        Nccl &n = nccl();
+        if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
+        NC(n.CommCount((ncclComm_t)desc->nccl_comm, &P));
+        NC(n.CommUserRank((ncclComm_t)desc->nccl_comm, &rank));
+    } else if (desc->virtual_ranks > 1) {
+        P = desc->virtual_ranks;
+        virt = true;
+    }
+    if (P > 1) {
+        // z-slabs over P ranks: 3-D, P | nz, P | ny, and the
+        // TMA-tiled strided passes for both y and z
+        if (desc->ndim != 3) return fail(USP_ERR_UNSUPPORTED, "slab decomposition needs a 3-D grid");
+        if (P & (P - 1)) return fail(USP_ERR_UNSUPPORTED, "rank count %d must be a power of two", P);
+        if (desc->n[2] % P || desc->n[1] % P)
+            return fail(USP_ERR_UNSUPPORTED, "rank count %d must divide ny and nz", P);
+        if (!stile_supported(desc->n[1]) || !stile_supported(desc->n[2]))
+            return fail(USP_ERR_UNSUPPORTED, "slab decomposition needs ny, nz in [64, 1024]");
     }
     usp_plan_s *p = new usp_plan_s();
     p->d = *desc;
@@ -433,6 +741,14 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     p->nz = desc->ndim >= 3 ? desc->n[2] : 1;
     for (int a = desc->ndim; a < 3; ++a) p->d.h[a] = 1.0;
     p->nvox = p->nx * p->ny * p->nz;
+    p->P = P;
+    p->rank = rank;
+    p->virt = virt;
+    p->comm = (ncclComm_t)desc->nccl_comm;
+    p->nzs = p->nz / P;
+    p->nzh = (P > 1 && !virt) ? p->nzs : p->nz;
+    p->nyl = p->ny / P;
+    p->nloc = p->nx * p->ny * p->nzh;
     p->stream = (cudaStream_t)desc->stream;
     p->sigma = desc->sigma;
     p->c = desc->c;
@@ -445,35 +761,28 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     }
     // launch grids: one resident wave, persistent grid-stride loops
     {
-        const long long xgroups = (p->ny * p->nz + xpass_lines_per_cta((int)p->nx) - 1) / xpass_lines_per_cta((int)p->nx);
-        p->grid_x = occ_grid(p, xgroups, 2);
-        // strided passes: CTAs per SM = 2 when the tile has 256 threads, else 1; two waves
+        const long long xl = p->ny * p->nzh;
+        p->grid_x = occ_grid(p, (xl + xpass_lines_per_cta((int)p->nx) - 1) / xpass_lines_per_cta((int)p->nx), 2);
         auto sgrid = [&](long long n, long long ncol_units) {
             const int per_sm = strided_threads((int)n) <= 256 ? 2 : 1;
             return occ_grid(p, ncol_units, per_sm);
         };
-        if (p->ndim >= 2) p->grid_y = sgrid(p->ny, (p->nx / strided_cols_for((int)p->ny)) * p->nz);
+        if (p->ndim >= 2) p->grid_y = sgrid(p->ny, (p->nx / strided_cols_for((int)p->ny)) * p->nzh);
         if (p->ndim >= 3) p->grid_z = sgrid(p->nz, (p->nx * p->ny) / strided_cols_for((int)p->nz));
-    }
-    {
         const char *leg = std::getenv("USP_LEGACY");
         p->pipe = !(leg && leg[0] == '1');
         const char *px = std::getenv("USP_PIPE_X");
         p->pipe_xk = p->pipe && !(px && px[0] == '0');
-        const char *ps = std::getenv("USP_PIPE_S");   // TMA strided passes (experimental, off by default)
-        p->pipe_sk = p->pipe && ps && ps[0] == '1';
         const char *stl = std::getenv("USP_STILE");
-        p->stile = p->pipe && !(stl && stl[0] == '0');
+        p->stile = (P > 1) || (p->pipe && !(stl && stl[0] == '0'));
         if (p->ndim >= 2 && stile_supported(p->ny))
-            p->grids_y = occ_grid(p, (p->nx / stile_cols((int)p->ny)) * p->nz, stile_ctas_per_sm((int)p->ny));
-        if (p->ndim >= 3 && stile_supported(p->nz))
-            p->grids_z = occ_grid(p, (p->nx * p->ny) / stile_cols((int)p->nz), stile_ctas_per_sm((int)p->nz));
+            p->grids_y = occ_grid(p, (p->nx / stile_cols((int)p->ny)) * p->nzh, stile_ctas_per_sm((int)p->ny));
+        if (p->ndim >= 3 && stile_supported(p->nz)) {
+            const long long zcols = (P > 1) ? p->nyl * p->nx * (virt ? P : 1) : p->nx * p->ny;
+            p->grids_z = occ_grid(p, zcols / stile_cols((int)p->nz), stile_ctas_per_sm((int)p->nz));
+        }
         const int u = 32 / (1 << (log2ll(p->nx) / 2));   // x lines per warp unit (32 / N1)
-        p->gridp_x = occ_grid(p, (p->ny * p->nz) / u, 1);
-        if (p->ndim >= 2)
-            p->gridp_y = occ_grid(p, (p->nx / strided_pipe_cols((int)p->ny)) * p->nz, 1);
-        if (p->ndim >= 3)
-            p->gridp_z = occ_grid(p, (p->nx * p->ny) / strided_pipe_cols((int)p->nz), 1);
+        p->gridp_x = occ_grid(p, xl / u, 1);
     }
     p->partials_cap = std::max(1, std::max(p->grid_x, p->gridp_x));
     p->far_cap = p->nsm * 8;
@@ -493,6 +802,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->red_u, sizeof(unsigned) * 4));
     TRY(cudaMalloc(&p->far_d, sizeof(double) * p->far_cap));
     TRY(cudaMalloc(&p->far_i, sizeof(long long) * p->far_cap));
+    TRY(cudaMalloc(&p->coll, sizeof(double) * (16 + 3 * 64)));
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     for (int a = 0; a < p->ndim; ++a) {
         twh[a] = twiddle_table((int)ext[a]);
@@ -509,7 +819,8 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
 
 usp_status usp_plan_workspace_size(usp_plan_t p, size_t *bytes) {
     if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
-    *bytes = 4 * align256((size_t)p->nvox * sizeof(float2));
+    const int fields = p->P > 1 ? 6 : 4;
+    *bytes = fields * align256((size_t)p->nloc * sizeof(float2));
     return USP_OK;
 }
 
@@ -519,65 +830,33 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     size_t need = 0;
     usp_plan_workspace_size(p, &need);
     if (bytes < need) return fail(USP_ERR_NOMEM, "workspace %zu bytes < required %zu", bytes, need);
-    const size_t f = align256((size_t)p->nvox * sizeof(float2));
+    const size_t f = align256((size_t)p->nloc * sizeof(float2));
     p->ws = (char *)dev;
     p->ws_bytes = bytes;
     p->x = (float2 *)(p->ws);
     p->delta = (float2 *)(p->ws + f);
     p->B = (float2 *)(p->ws + 2 * f);
     p->work = (float2 *)(p->ws + 3 * f);
+    if (p->P > 1) {
+        p->sendb = (float2 *)(p->ws + 4 * f);
+        p->recvb = (float2 *)(p->ws + 5 * f);
+    }
     p->have_potential = p->have_source = false;
-    p->pipe_y = p->pipe_z = false;
-    p->stile_y = p->stile_z = false;
-    if (p->stile && p->ndim >= 2 && stile_supported(p->ny)) {
-        const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
-        if (p->ndim == 2) {
-            const cuuint64_t dims[2] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny};
-            const cuuint64_t str[1] = {(cuuint64_t)p->nx * 8};
-            const cuuint32_t box[2] = {cy, by};
-            p->stile_y = make_map(&p->smap_y, p->work, 2, dims, str, box);
-        } else {
-            const cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)p->nz};
-            const cuuint64_t str[2] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nx * p->ny) * 8};
-            const cuuint32_t box[3] = {cy, by, 1};
-            p->stile_y = make_map(&p->smap_y, p->work, 3, dims, str, box);
-        }
-    }
-    if (p->stile && p->ndim == 3 && stile_supported(p->nz)) {
-        const cuuint32_t cz = (cuuint32_t)stile_cols((int)p->nz), bz = (cuuint32_t)stile_box((int)p->nz);
-        const cuuint64_t dims[2] = {(cuuint64_t)(p->nx * p->ny), (cuuint64_t)p->nz};
-        const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};
-        const cuuint32_t box[2] = {cz, bz};
-        p->stile_z = make_map(&p->smap_z, p->work, 2, dims, str, box);
-    }
-    if (p->pipe_sk && p->ndim >= 2 && strided_pipe_supported(p->ny)) {
-        const cuuint32_t cy = (cuuint32_t)strided_pipe_cols((int)p->ny), by = (cuuint32_t)strided_pipe_box((int)p->ny);
-        if (p->ndim == 2) {
-            const cuuint64_t dims[2] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny};
-            const cuuint64_t str[1] = {(cuuint64_t)p->nx * 8};
-            const cuuint32_t box[2] = {cy, by};
-            p->pipe_y = make_map(&p->map_y, p->work, 2, dims, str, box);
-        } else {
-            const cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)p->nz};
-            const cuuint64_t str[2] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nx * p->ny) * 8};
-            const cuuint32_t box[3] = {cy, by, 1};
-            p->pipe_y = make_map(&p->map_y, p->work, 3, dims, str, box);
-        }
-    }
-    if (p->pipe_sk && p->ndim == 3 && strided_pipe_supported(p->nz)) {
-        const cuuint32_t cz = (cuuint32_t)strided_pipe_cols((int)p->nz), bz = (cuuint32_t)strided_pipe_box((int)p->nz);
-        const cuuint64_t dims[2] = {(cuuint64_t)(p->nx * p->ny), (cuuint64_t)p->nz};
-        const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};
-        const cuuint32_t box[2] = {cz, bz};
-        p->pipe_z = make_map(&p->map_z, p->work, 2, dims, str, box);
-    }
+    build_maps(p);
+    if (p->P > 1 && !(p->stile_y && p->stile_z))
+        return fail(USP_ERR_CUDA, "could not encode the tensor maps of the slab decomposition");
     return USP_OK;
 }
 
 usp_status usp_local_extent(usp_plan_t p, int64_t *z0, int64_t *nz_local) {
     if (!p || !z0 || !nz_local) return fail(USP_ERR_ARG, "NULL argument");
-    *z0 = 0;
-    *nz_local = p->ndim == 3 ? p->nz : (p->ndim == 2 ? p->ny : p->nx);
+    if (p->ndim == 3) {
+        *z0 = (p->P > 1 && !p->virt) ? (int64_t)p->rank * p->nzs : 0;
+        *nz_local = p->nzh;
+    } else {
+        *z0 = 0;
+        *nz_local = p->ndim == 2 ? p->ny : p->nx;
+    }
     return USP_OK;
 }
 
@@ -586,7 +865,7 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
     if (!p->ws) return fail(USP_ERR_STATE, "workspace not set");
     if (where != USP_HOST && where != USP_DEVICE) return fail(USP_ERR_ARG, "bad where");
     // stage the medium in the chain buffer (the source resets it later)
-    usp_status s = stage(p, p->work, medium, (size_t)p->nvox * elem_bytes(p), where);
+    usp_status s = stage(p, p->work, medium, (size_t)p->nloc * elem_bytes(p), where);
     if (s) return s;
     p->have_source = false;
     p->have_potential = false;
@@ -617,11 +896,15 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
     if (p->d.D * p->c.re < 0.0)
         return fail(USP_ERR_NOT_ACCRETIVE, "D Re(c) < 0: -D lap / c is not accretive (Eq. 1)");
     CU(cudaMemsetAsync(p->red_u, 0, sizeof(unsigned) * 4, p->stream));
-    PotParams pp{p->work, p->d.dtype == USP_R32, p->d.medium == USP_MEDIUM_K2, p->B, p->nvox,
+    PotParams pp{p->work, p->d.dtype == USP_R32, p->d.medium == USP_MEDIUM_K2, p->B, p->nloc,
                  p->sigma.re, p->sigma.im, p->c.re, p->c.im, p->red_u, p->red_u + 1, p->red_u + 2};
     {
         Tick t(p, KC_POTENTIAL);
-        CU(launch_potential(pp, occ_grid(p, (p->nvox + 255) / 256, 8), p->stream));
+        CU(launch_potential(pp, occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
+    }
+    if (multi_rank(p)) {   // the Theorem 1 checks over the whole grid
+        NC(nccl().AllReduce(p->red_u, p->red_u, 1, ncclUint32, ncclMax, p->comm, p->stream));
+        NC(nccl().AllReduce(p->red_u + 1, p->red_u + 1, 2, ncclUint32, ncclSum, p->comm, p->stream));
     }
     unsigned red[4];
     CU(cudaMemcpyAsync(red, p->red_u, sizeof red, cudaMemcpyDeviceToHost, p->stream));
@@ -652,7 +935,7 @@ usp_status usp_get_split(usp_plan_t p, usp_c128 *sigma, usp_c128 *c, usp_c128 *c
 usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
     if (!p || !src) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->have_potential) return fail(USP_ERR_STATE, "set_potential must succeed first");
-    usp_status s = stage(p, p->x, src, (size_t)p->nvox * elem_bytes(p), where);
+    usp_status s = stage(p, p->x, src, (size_t)p->nloc * elem_bytes(p), where);
     if (s) return s;
     IterState s0{};
     s0.status = ST_NO_SOURCE;
@@ -669,7 +952,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         op.inv_c = make_float2((float)(p->c.re / m), (float)(-p->c.im / m));
         op.mp = mul_params(p);
         op.st = p->st;
-        op.red = Red{p->partials, p->hist, p->hist_cap};
+        op.red = Red{p->partials, p->hist, p->hist_cap, nullptr};
         Tick t(p, KC_SOLVE1D);
         CU(launch_solve1d((int)p->nx, O_SETUP, op, p->stream));
     } else {
@@ -707,14 +990,15 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         op.tw = p->tw[0];
         op.mp = mul_params(p);
         op.st = p->st;
-        op.red = Red{p->partials, p->hist, p->hist_cap};
+        op.red = Red{p->partials, p->hist, p->hist_cap, nullptr};
         Tick t(p, KC_SOLVE1D);
         CU(launch_solve1d((int)p->nx, O_ITER, op, p->stream));
     } else {
         const XParams xp = x_params(p);
         const long long batch = 16;
         long long launched = 0;
-        // with tol > 0 the device stops itself; +1 covers the final x-only update
+        // with tol > 0 the device stops itself (every kernel checks the state);
+        // the host looks once per batch
         const long long total = n_max;
         while (launched < total) {
             const long long nb = std::min(batch, total - launched);
@@ -778,10 +1062,10 @@ usp_status usp_get_field(usp_plan_t p, void *out, usp_where where) {
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
     const cudaMemcpyKind kind = where == USP_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (p->d.dtype == USP_C64) {
-        CU(cudaMemcpyAsync(out, p->x, (size_t)p->nvox * sizeof(float2), kind, p->stream));
+        CU(cudaMemcpyAsync(out, p->x, (size_t)p->nloc * sizeof(float2), kind, p->stream));
     } else {
         // real field: take the real parts (strided copy, pitch 8 -> 4 bytes)
-        CU(cudaMemcpy2DAsync(out, sizeof(float), p->x, sizeof(float2), sizeof(float), (size_t)p->nvox, kind,
+        CU(cudaMemcpy2DAsync(out, sizeof(float), p->x, sizeof(float2), sizeof(float), (size_t)p->nloc, kind,
                              p->stream));
     }
     if (where == USP_HOST) CU(cudaStreamSynchronize(p->stream));
@@ -824,7 +1108,7 @@ usp_status usp_launch_count(usp_plan_t p, int64_t *launches) {
 
 void usp_plan_destroy(usp_plan_t p) {
     if (!p) return;
-    if (p->stream || true) cudaStreamSynchronize(p->stream);
+    cudaStreamSynchronize(p->stream);
     drain_timing(p);
     for (auto e : p->ev_pool) cudaEventDestroy(e);
     cudaFree(p->st);
@@ -833,6 +1117,7 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->red_u);
     cudaFree(p->far_d);
     cudaFree(p->far_i);
+    cudaFree(p->coll);
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
     cudaFreeHost(p->st_host);
     delete p;

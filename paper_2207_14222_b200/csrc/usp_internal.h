@@ -34,6 +34,7 @@ struct Red {             // reduction scratch (device)
     double *partials;    // one per CTA of the reducing kernel
     double *hist;        // residual ring
     int hist_cap;
+    double *local_sum;   // slab-decomposed: the x pass stores its total here (else nullptr)
 };
 
 // Fourier multiplier data of (L+1)^-1 = F^-1 [c/(D|p|^2 + sigma + c)] F (Eq. 12),
@@ -42,6 +43,7 @@ struct MulParams {
     float2 cn;           // c / N_vox
     float2 sc;           // sigma + c
     float D;
+    float sqrtD;         // sqrt(D) (the z pass folds it into the line frequency)
     float kx, ky, kz;    // 2 pi / (n_a h_a): p_a = k_a * m_a
     int nx, ny, nz;
 };
@@ -66,7 +68,8 @@ struct XParams {
 enum SMode : int { S_FWD = 0, S_INV = 1, S_FWD_MUL_INV = 2 };
 
 struct SParams {
-    float2 *data;
+    float2 *data;        // field the pass reads (in place unless dst differs)
+    float2 *dst;         // where results are stored (== data for in-place passes)
     const float2 *tw;    // four-step twiddles for the line length
     long long stride;    // elements between consecutive line points
     long long ncols;     // columns per outer slab (contiguous)
@@ -76,6 +79,13 @@ struct SParams {
     int check_state;     // 1: skip unless status == RUNNING && k < kmax
     MulParams mp;
     IterState *st;
+    // slab decomposition (k_stile only; P = 1: natural layout everywhere)
+    int map_rank;        // tensor map rank: 2, 3 (y pass, 3-D) or 5 (send layout)
+    int send_layout;     // S_FWD: store into the send layout [r][q][z_loc][y_loc][x]
+    int P;               // slabs per rank group
+    int nz_loc;          // z planes per slab
+    int nyl_lg;          // log2(ny / P)
+    long long y0;        // global y of this rank's y block (z pass multiplier)
 };
 
 // ------------------------------------------------------------------ 1-D --
@@ -121,6 +131,7 @@ cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t
 cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_t s);
 cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
+cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s);
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
 
 // TMA-pipelined variants (kernels_pipe.cu)

@@ -51,11 +51,17 @@ class Plan:
     kind='helmholtz': medium is k^2(r) (Eq. 8); kind='diffusion':
     medium is mu_a(r) (§3.2, scalar D).  dtype 'c64' (complex64 arrays) or
     'r32' (float32 arrays, diffusion with real data).
+
+    Slab decomposition (3-D): ``comm`` = a communicator from
+    :func:`comm_init` splits the grid into z-slabs over its ranks (one GPU
+    per rank; arrays are the rank's slab, ``local_shape``);
+    ``virtual_ranks=P`` runs the same decomposition with P slabs on one GPU
+    (transposes as device copies; arrays are the full grid).
     """
 
     def __init__(self, shape: Sequence[int], kind: str = "helmholtz", h: Optional[Sequence[float]] = None,
                  D: float = 1.0, sigma: complex = 0j, c: complex = 1 + 0j, dtype: str = "c64",
-                 stream=None, device=None):
+                 stream=None, device=None, comm=None, virtual_ranks: int = 0):
         import torch
 
         self.lib = L.load()
@@ -79,7 +85,9 @@ class Plan:
         d.sigma = L.c128(float(np.real(sigma)), float(np.imag(sigma)))
         d.c = L.c128(float(np.real(c)), float(np.imag(c)))
         d.stream = ctypes.c_void_p(self.stream.cuda_stream)
-        d.nccl_comm = None
+        d.nccl_comm = comm.handle if comm is not None else None
+        d.virtual_ranks = int(virtual_ranks)
+        self.comm = comm
         self.desc = d
         h_ = ctypes.c_void_p()
         L.check(self.lib.usp_plan_create(ctypes.byref(d), ctypes.byref(h_)))
@@ -89,6 +97,10 @@ class Plan:
         self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
         L.check(self.lib.usp_plan_set_workspace(self.handle, ctypes.c_void_p(self.workspace.data_ptr()),
                                                 int(nbytes.value)))
+        z0, nzl = ctypes.c_int64(), ctypes.c_int64()
+        L.check(self.lib.usp_local_extent(self.handle, ctypes.byref(z0), ctypes.byref(nzl)))
+        self.z0 = int(z0.value)
+        self.local_shape = ((int(nzl.value),) + self.shape[1:]) if self.ndim == 3 else self.shape
 
     # -- setup ---------------------------------------------------------------
     def set_potential(self, medium, target_norm: float = 0.95):
@@ -136,7 +148,7 @@ class Plan:
 
         if out is None:
             tdt = torch.complex64 if self.dtype == "c64" else torch.float32
-            out = torch.empty(self.shape, dtype=tdt, device=self.device)
+            out = torch.empty(self.local_shape, dtype=tdt, device=self.device)
         ptr, where, keep = _ptr_where(out, self.dtype)
         L.check(self.lib.usp_get_field(self.handle, ptr, where))
         return out
@@ -169,6 +181,50 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+class Comm:
+    """NCCL communicator of libusp's slab decomposition (usp_comm_init).
+    The 128-byte unique id travels over torch.distributed (any backend)."""
+
+    def __init__(self, handle, nranks: int, rank: int):
+        self.handle = handle
+        self.nranks = nranks
+        self.rank = rank
+
+    def close(self):
+        if getattr(self, "handle", None):
+            L.check(L.load().usp_comm_destroy(self.handle))
+            self.handle = None
+
+
+def broadcast_unique_id(group=None):
+    """Rank 0 of the torch.distributed ``group`` draws an NCCL unique id
+    (usp_comm_unique_id); every rank returns the same 128 bytes."""
+    import torch
+    import torch.distributed as dist
+
+    lib = L.load()
+    idbuf = (ctypes.c_ubyte * 128)()
+    if dist.get_rank(group) == 0:
+        L.check(lib.usp_comm_unique_id(idbuf))
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor(list(bytes(idbuf)), dtype=torch.uint8, device=dev)
+    dist.broadcast(t, src=0, group=group)
+    return (ctypes.c_ubyte * 128)(*t.cpu().tolist())
+
+
+def comm_init(group=None) -> Comm:
+    """Collective over the torch.distributed ``group``: every rank joins the
+    NCCL communicator of libusp's slab decomposition on its current CUDA
+    device."""
+    import torch.distributed as dist
+
+    idbuf = broadcast_unique_id(group)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    h = ctypes.c_void_p()
+    L.check(L.load().usp_comm_init(idbuf, world, rank, ctypes.byref(h)))
+    return Comm(h, world, rank)
 
 
 def solve(medium, source, kind: str = "helmholtz", alpha: float = 0.75, tol: float = 0.0, n_iter: int = 100,
