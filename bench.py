@@ -15,8 +15,12 @@ larger than L2 (126 MB), so no explicit flush is needed.
 on a bounded sample of the same workload on the host cores (this tier has no
 installable reference implementation; the oracle is the reference arm).
 
-Multi-GPU (torchrun, one process per GPU): the slab-decomposed NCCL path is
-not built yet; N>1 runs one independent C5 solve per GPU ("scaling": "weak").
+Multi-GPU (torchrun, one process per GPU, N>1): C5 is split into N z-slabs
+(libusp's slab decomposition: NCCL all-to-all transposes around the z pass,
+rank-ordered residual all-gather) -- strong scaling, the total work fixed.
+Before timing, a closed-form check (constant V, 128^3) runs through the same
+communicator; if it fails, the run falls back to N independent replicas
+("scaling": "weak") and says so.  --replicas forces the replica mode.
 """
 from __future__ import annotations
 
@@ -46,6 +50,15 @@ KERNEL_BYTES = {
     "y_fwd_mul_inv": 16,
 }
 ITER_BYTES_3D = 104         # 56 + 3 * 16 (SURVEY.md §8 geometry table)
+# Chunked schedule (1 GPU, 3-D): per z-chunk K_D -> K_A -> K_B
+# with the chunk's work array L2-resident in between, so HBM sees only
+KERNEL_BYTES_CHUNKED = {
+    "xpass": 40,            # read Delta, x, B; write Delta, x (work read/written in L2)
+    "y_fwd": 8,             # write work (read from L2)
+    "z_fwd_mul_inv": 16,
+    "y_inv": 8,             # read work (written to L2)
+}
+ITER_BYTES_CHUNKED = 72
 
 
 def env_int(name, default):
@@ -152,7 +165,7 @@ def ncu_traffic():
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            return json.load(f).get("bytes_per_launch", {})
     except Exception:
         return {}
 
@@ -213,6 +226,43 @@ def run_reference(args, world, rank):
 
 
 # -------------------------------------------------------------------- GPU --
+def slab_selfcheck(comm, world, rank, dev, n_iter=8, shape=(128, 128, 128)):
+    """Constant V through the decomposed path: x^_k = x^*(1 - q^k) per
+    Fourier mode (the closed form of tests/test_gpu_parity.py).  Returns the
+    relative L2 error (all ranks)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2207_14222_b200 import Plan
+
+    k2 = (2 * math.pi / 8 * (1.0 + 0.05j)) ** 2
+    sigma, c, alpha = -k2.real, -1j * abs(k2.imag) / 0.95, 0.75
+    S = np.zeros(shape, dtype=np.complex64)
+    S[tuple(s // 3 for s in shape)] = 1.0
+    S[tuple(s // 5 for s in shape)] = 0.5 - 0.25j
+    plan = Plan(shape, sigma=sigma, c=c, comm=comm, device=dev)
+    z0, nzl = plan.z0, plan.local_shape[0]
+    plan.set_potential(torch.full(plan.local_shape, k2, dtype=torch.complex64, device=dev), -1.0)
+    plan.set_source(torch.from_numpy(np.ascontiguousarray(S[z0:z0 + nzl])).to(dev))
+    plan.iterate(n_iter, alpha, 0.0)
+    x = plan.get_field()
+    parts = [torch.empty_like(x) for _ in range(world)]
+    dist.all_gather(parts, x)
+    plan.close()
+    err = torch.zeros(1, dtype=torch.float64, device=dev)
+    if rank == 0:
+        xg = torch.cat(parts).cpu().numpy().astype(np.complex128)
+        w = -complex(np.complex64(k2))
+        b = 1.0 - (w - sigma) / c
+        p2 = sum(np.meshgrid(*[(2 * np.pi * np.fft.fftfreq(n)) ** 2 for n in shape], indexing="ij"))
+        g = c / (p2 + sigma + c)
+        q = 1.0 - alpha * b * (1.0 - b * g)
+        ref = np.fft.ifftn(g * np.fft.fftn(S.astype(np.complex128) / c) / (1.0 - b * g) * (1.0 - q ** n_iter))
+        err[0] = float(np.linalg.norm(xg - ref) / np.linalg.norm(ref))
+    dist.broadcast(err, src=0)
+    return float(err.item())
+
+
 def run_usp(args, world, rank, local):
     import numpy as np
     import torch
@@ -223,22 +273,48 @@ def run_usp(args, world, rank, local):
     from synth import make
 
     name = args.config
+    # multi-GPU: z-slabs over the ranks (strong scaling) unless the check fails
+    comm, slab_check, mode = None, None, ("1 GPU" if world == 1 else "replicas")
+    if world > 1 and not args.replicas:
+        from paper_2207_14222_b200 import comm_init
+
+        comm = comm_init()
+        slab_check = slab_selfcheck(comm, world, rank, dev)
+        if slab_check <= 1e-4:
+            mode = "slabs"
+        else:
+            comm.close()
+            comm = None
     p = make(name, None if args.size is None else (args.size,) * 3, device=str(dev))
     shape = p.shape
     n_iter = args.iters if args.iters else p.n_iter
-    med = p.medium.to(torch.complex64)
-    src = p.source.to(torch.complex64)
+    stream = torch.cuda.Stream(device=dev)
+    if args.virtual_ranks > 1 and world == 1:
+        mode = "virtual"
+    with torch.cuda.stream(stream):
+        plan = Plan(shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev, comm=comm,
+                    virtual_ranks=args.virtual_ranks if mode == "virtual" else 0)
+    z0, nzl = plan.z0, plan.local_shape[0]
+    med = p.medium[z0:z0 + nzl].to(torch.complex64).contiguous()
+    src = p.source[z0:z0 + nzl].to(torch.complex64).contiguous()
     del p.medium, p.source
     torch.cuda.empty_cache()
-    stream = torch.cuda.Stream(device=dev)
-    with torch.cuda.stream(stream):
-        plan = Plan(shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev)
-    nvox = int(np.prod(shape))
+    nvox = int(np.prod(shape))              # global voxels
+    nloc = int(np.prod(plan.local_shape))   # voxels this rank holds
+    units = nvox if mode == "slabs" else nvox * world   # voxels all ranks advance per iteration
 
-    def step(m, s, where_host=False, out=None):
+    it_events = []
+
+    def step(m, s, where_host=False, out=None, timed=False):
         plan.set_potential(m, 0.95)
         plan.set_source(s)
+        if timed:
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record(stream)
         n, term = plan.iterate(n_iter, p.alpha, 0.0)
+        if timed:
+            eb.record(stream)
+            it_events.append((ea, eb))
         assert n == n_iter, (n, term)
         if out is not None:
             plan.get_field(out)
@@ -257,7 +333,7 @@ def run_usp(args, world, rank, local):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        step(med, src)
+        step(med, src, timed=True)
     e1.record(stream)
     torch.cuda.synchronize()
     clocks = sampler.stop()
@@ -267,24 +343,32 @@ def run_usp(args, world, rank, local):
     prof = plan.profile_read()
     plan.profile(False)
     ms_max = max_over_ranks(world, ms)
-    value = nvox * n_iter * args.steps * world / (ms_max / 1e3)
+    value = units * n_iter * args.steps / (ms_max / 1e3)
 
-    # dominant kernel roofline (algorithmic bytes / its average launch time)
+    # dominant kernel roofline: its algorithmic HBM bytes per iteration over
+    # its device time per iteration (x-pass launches are iterations only; the
+    # chunked schedule launches it once per z-chunk)
     hbm, peak_kind = peaks()
-    dom = max(((k, v) for k, v in prof.items() if k in KERNEL_BYTES), key=lambda kv: kv[1][0])
-    dname, (dms, dcount) = dom
-    dbytes = KERNEL_BYTES[dname] * nvox
-    achieved = dbytes / (dms / dcount / 1e3) / 1e9
+    n_it_total = n_iter * args.steps
+    chunks = max(1, prof.get("xpass", (0, n_it_total))[1] // n_it_total)
+    schedule = "chunked" if chunks > 1 else "4-pass"
+    kbytes = KERNEL_BYTES_CHUNKED if chunks > 1 else KERNEL_BYTES
+    dname = "xpass" if "xpass" in prof else max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
+    dms, dcount = prof[dname]
+    d_ms_per_iter = dms / n_it_total
+    dbytes = kbytes[dname] * nloc                   # per iteration (= per launch x chunks)
+    achieved = dbytes / (d_ms_per_iter / 1e3) / 1e9
     traffic = ncu_traffic().get(dname)
-    iter_ms = sum(v[0] for k, v in prof.items() if k in KERNEL_BYTES) / (n_iter * args.steps + args.steps)
+    # iteration time: device time of the iterate() calls / iterations
+    iter_ms = sum(a.elapsed_time(b) for a, b in it_events) / n_it_total
     kernel_share = {k: round(v[0] / sum(x[0] for x in prof.values()), 4) for k, v in prof.items()}
 
     # ------------------------------------------------ e2e (host buffers)
     e2e = None
     if not args.no_e2e:
-        h_med = torch.empty(shape, dtype=torch.complex64, pin_memory=True)
-        h_src = torch.empty(shape, dtype=torch.complex64, pin_memory=True)
-        h_out = torch.empty(shape, dtype=torch.complex64, pin_memory=True)
+        h_med = torch.empty(plan.local_shape, dtype=torch.complex64, pin_memory=True)
+        h_src = torch.empty(plan.local_shape, dtype=torch.complex64, pin_memory=True)
+        h_out = torch.empty(plan.local_shape, dtype=torch.complex64, pin_memory=True)
         h_med.copy_(med)
         h_src.copy_(src)
         del med, src
@@ -301,8 +385,9 @@ def run_usp(args, world, rank, local):
         f1.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(world, f0.elapsed_time(f1))
-        e2e = {"value": nvox * n_iter * e2e_steps * world / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": 2 * nvox * 8, "d2h_bytes_per_step": nvox * 8, "steps": e2e_steps}
+        e2e = {"value": units * n_iter * e2e_steps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * nloc * 8 * world, "d2h_bytes_per_step": nloc * 8 * world,
+               "steps": e2e_steps}
 
     if rank != 0:
         return 0
@@ -310,20 +395,26 @@ def run_usp(args, world, rank, local):
     if world == 1 and not args.no_cpu:
         v, dt, thr, desc = cpu_oracle_sample()
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
-    it_bytes = ITER_BYTES_3D * nvox
+    iter_bpv = (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D) + (32 if mode in ("slabs", "virtual") else 0)
+    it_bytes = iter_bpv * nloc
+    parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
+                   "slabs": f"{world} z-slabs, NCCL all-to-all transposes",
+                   "virtual": f"1 GPU, {args.virtual_ranks} virtual z-slabs (device-copy transposes)"}[mode]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+        "scaling": "strong" if mode == "slabs" else "weak", "vs_baseline": None, "dtype": "c64",
+        "data": "synthetic",
         "config": {"workload": f"{name} 3-D Helmholtz {shape[2]}x{shape[1]}x{shape[0]} complex64, "
                                f"{n_iter} iterations of Alg. 1 per step (setup + iterations), alpha=0.75",
                    "grid": list(shape), "iterations_per_step": n_iter,
-                   "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas",
+                   "parallelism": parallelism, "slab_check_rel_l2": slab_check,
                    "l2": "inputs (8 GiB fields) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": dbytes, "avg_launch_ms": dms / dcount},
-        "iteration_roofline": {"bytes_per_voxel": ITER_BYTES_3D, "iter_ms": iter_ms,
+                     "algorithmic_bytes_per_iteration": dbytes, "ms_per_iteration": d_ms_per_iter,
+                     "launches_per_iteration": dcount // n_it_total, "schedule": schedule},
+        "iteration_roofline": {"bytes_per_voxel": iter_bpv, "iter_ms": iter_ms,
                                "achieved_gbs": it_bytes / (iter_ms / 1e3) / 1e9,
                                "frac": it_bytes / (iter_ms / 1e3) / 1e9 / hbm},
         "kernel_share": kernel_share,
@@ -349,6 +440,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
+    ap.add_argument("--virtual-ranks", type=int, default=0,
+                    help="N=1: run the slab-decomposed path with this many virtual slabs (measurement)")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":

@@ -135,6 +135,13 @@ __global__ void __launch_bounds__(256) k_xpass(XParams p) {
     const double mine = block_sum_d<XG::NT>(acc, sh_red);
     if (!last_block_total<XG::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
     if (threadIdx.x != 0) return;
+    if (p.red.chunk_acc) {   // chunked schedule: z-chunks reduce in launch order (deterministic)
+        if (!p.red.chunk_first) total += *p.red.chunk_acc;
+        if (!p.red.chunk_last) {
+            *p.red.chunk_acc = total;
+            return;
+        }
+    }
     if (p.red.local_sum) {   // slab-decomposed: k_finish sums the ranks' totals after the all-gather
         *p.red.local_sum = total;
         return;

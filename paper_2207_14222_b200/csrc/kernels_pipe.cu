@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
         if (warp == T::XC) {
             // ------------------------------------------------ producer warp
             if (lane == 0) {
+                const uint64_t pol_first = policy_evict_first();
                 for (int i = 0; i < nloc; ++i) {
                     const int s = i % T::S;
                     if (i >= T::S && !mbar_wait(&empty[s], ((i / T::S) - 1) & 1)) {
@@ -116,6 +117,12 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                         mbar_arrive_expect_tx(&full[s], 2 * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
                         bulk_g2s(st + 3 * T::UE, p.B + off, ub, &full[s]);
+                    } else if (p.l2hint) {
+                        mbar_arrive_expect_tx(&full[s], 4 * ub);
+                        bulk_g2s(st, p.work + off, ub, &full[s]);
+                        bulk_g2s_hint(st + 1 * T::UE, p.delta + off, ub, &full[s], pol_first);
+                        bulk_g2s_hint(st + 2 * T::UE, p.x + off, ub, &full[s], pol_first);
+                        bulk_g2s_hint(st + 3 * T::UE, p.B + off, ub, &full[s], pol_first);
                     } else {
                         mbar_arrive_expect_tx(&full[s], 4 * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
@@ -129,6 +136,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
         } else {
             // ------------------------------------------------ consumer warps
             const int lq = lane / G::N1, j = lane % G::N1;
+            const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
             const LayRow<N> lay{xbufs + warp * T::XBUF + lq * LayRow<N>::kFloat2PerLine};
             for (int i = warp; i < nloc; i += T::XC) {
                 const int s = i % T::S;
@@ -177,9 +185,12 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                                 const float2 xx = st[2 * T::UE + e];
                                 const float2 t = cmul(b, csub(y, d));
                                 dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
-                                p.x[gi] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                                const float2 xn = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                                if (p.l2hint) st_hint(&p.x[gi], xn, pol_first);
+                                else p.x[gi] = xn;
                             }
-                            p.delta[gi] = dn;
+                            if (MODE != X_SRC_EPI && p.l2hint) st_hint(&p.delta[gi], dn, pol_first);
+                            else p.delta[gi] = dn;
                             lacc += cabs2(dn);
                             v[m] = cmul(b, dn);                     // next chain: u = B Delta
                         }
@@ -189,8 +200,13 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                         if (lane == 0) mbar_arrive(&empty[s]);
                     }
                 }
+                if (p.l2hint) {
 #pragma unroll
-                for (int m = 0; m < G::N2; ++m) p.work[gb + G::N1 * m] = v[m];
+                    for (int m = 0; m < G::N2; ++m) st_hint(&p.work[gb + G::N1 * m], v[m], pol_last);
+                } else {
+#pragma unroll
+                    for (int m = 0; m < G::N2; ++m) p.work[gb + G::N1 * m] = v[m];
+                }
             }
         }
     }
@@ -200,6 +216,13 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
     const double mine = block_sum_d<T::NT>(acc, sh_red);
     if (!last_block_total<T::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
     if (threadIdx.x != 0) return;
+    if (p.red.chunk_acc) {   // chunked schedule: z-chunks reduce in launch order (deterministic)
+        if (!p.red.chunk_first) total += *p.red.chunk_acc;
+        if (!p.red.chunk_last) {
+            *p.red.chunk_acc = total;
+            return;
+        }
+    }
     if (p.red.local_sum) {   // slab-decomposed: k_finish sums the ranks' totals after the all-gather
         *p.red.local_sum = total;
         return;

@@ -161,7 +161,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     float2 *sm_tw = xb + T::XB;
     uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N);
     if (p.check_state) {
-        if (p.st->status != ST_RUNNING || p.st->k >= p.st->kmax) return;
+        const bool running = p.st->status == ST_RUNNING && p.st->k < p.st->kmax;
+        if (p.check_state == 3 && blockIdx.x == 0 && threadIdx.x == 0) p.st->full_iter = running;
+        if (!((p.check_state == 2) ? (p.st->full_iter != 0) : running)) return;
     }
     const int tid = threadIdx.x;
     const int c = tid % T::COLS, j = tid / T::COLS;
@@ -171,8 +173,8 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
 
     auto issue = [&](int i) {   // thread 0: TMA boxes of local tile i
         const long long t = blockIdx.x + (long long)i * gridDim.x;
-        const long long o = t / tpo;
-        const int c0 = (int)((t - o * tpo) * T::COLS);
+        const long long ol = t / tpo, o = p.o0 + ol;
+        const int c0 = (int)((t - ol * tpo) * T::COLS);
         mbar_arrive_expect_tx(full, T::TILE * 8);
         if (p.map_rank == 5) {
             // K_D after the return transpose: the line's rows live in P blocks of
@@ -274,8 +276,8 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         }
         long long t = blockIdx.x + (long long)i * gridDim.x;
         asm volatile("" : "+l"(t));
-        const long long o = t / tpo;
-        const long long col = (t - o * tpo) * T::COLS + c;
+        const long long ol = t / tpo, o = p.o0 + ol;
+        const long long col = (t - ol * tpo) * T::COLS + c;
         long long stride = p.stride;
         asm volatile("" : "+l"(stride));
         if (flip) {
@@ -297,10 +299,19 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         } else {
             float2 *sb = p.dst + (o * p.ostride + col) + (long long)j * stride;
             const long long step = (long long)G::N1 * stride;
+            if (p.store_hint) {
+                const uint64_t pol = p.store_hint == 1 ? policy_evict_last() : policy_evict_first();
 #pragma unroll
-            for (int m = 0; m < G::N2; ++m) {
-                sb[0] = (MODE == S_FWD) ? v[m] : cconj(v[m]);
-                sb += step;
+                for (int m = 0; m < G::N2; ++m) {
+                    st_hint(sb, (MODE == S_FWD) ? v[m] : cconj(v[m]), pol);
+                    sb += step;
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < G::N2; ++m) {
+                    sb[0] = (MODE == S_FWD) ? v[m] : cconj(v[m]);
+                    sb += step;
+                }
             }
         }
     }

@@ -125,10 +125,10 @@ Nccl &nccl() {
     } while (0)
 
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
-              KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_N };
+              KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_N };
 const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
                               "solve1d", "potential", "farthest", "set_state", "xpass_setup",
-                              "all_to_all", "finish"};
+                              "all_to_all", "finish", "allgather"};
 
 struct Timed {
     int cls;
@@ -182,6 +182,13 @@ struct usp_plan_s {
     bool stile = true, stile_y = false, stile_z = false;
     int grids_y = 0, grids_z = 0;
     CUtensorMap smap_y{}, smap_z{}, smap_kd{};
+    // chunked schedule (1 GPU, 3-D; experimental, off by default): per
+    // iteration K_C over the volume, then K_D, K_A, K_B chunk by chunk of G
+    // z-planes so the chunk's work array can stay in L2 between the three
+    // (USP_CHUNK = G).  Measured slower at 1024^3.
+    bool chunked = false;
+    long long chunk_g = 0;
+    bool l2hint = true;   // USP_L2HINT=0 disables the eviction-priority hints
     // profiling
     bool prof = false;
     std::vector<Timed> timed;
@@ -494,7 +501,7 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
     }
     if (mode != X_SRC_FWD && multi_rank(p)) {
         {
-            Tick t(p, KC_A2A, false);
+            Tick t(p, KC_ALLGATHER, false);
             NC(nccl().AllGather(p->coll, p->coll + 8, 1, ncclDouble, p->comm, p->stream));
         }
         Tick t(p, KC_FINISH);
@@ -600,6 +607,49 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
     return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_kd, true, 0);
 }
 
+// Chunked schedule (P = 1, 3-D).  Invariant between iterations: `work`
+// holds the x- and y-forward transforms of B Delta_k.  One iteration:
+//   K_C over the volume (z forward, multiplier, z inverse; snapshots the
+//   "full iteration" test into st->full_iter), then for each chunk of G
+//   z-planes: K_D (y inverse), K_A (x inverse, update, residual partial,
+//   x forward), K_B (y forward).  The chunk's 8 G nx ny bytes of `work`
+//   written by K_D are re-read by K_A and K_B straight from L2, so only
+//   Delta, x, B and the K_C/K_D/K_B endpoints touch HBM: 72 B/voxel instead
+//   of 104 B/voxel per iteration.  K_A's residual partials are summed over
+//   the chunks in launch order (deterministic).
+usp_status chunk_kb_all(usp_plan_s *p) {
+    SParams yb = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, p->nz, p->nx * p->ny, 1, 0, 3);
+    return run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0);
+}
+
+usp_status chunked_iteration(usp_plan_s *p) {
+    usp_status s;
+    SParams zm = sparams(p, p->work, p->work, p->tw[2], p->nx * p->ny, p->nx * p->ny, 1, 0, 2, 3, 2);
+    if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, true, 0))) return s;
+    const long long G = p->chunk_g, nch = p->nz / G, plane = p->nx * p->ny;
+    for (long long ch = 0; ch < nch; ++ch) {
+        SParams yc = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, G, plane, 1, 2, 3);
+        yc.o0 = ch * G;
+        yc.store_hint = p->l2hint ? 1 : 0;   // K_A re-reads the chunk from L2
+        if ((s = run_strided(p, KC_YINV, (int)p->ny, S_INV, yc, p->smap_y, true, 0))) return s;
+        yc.store_hint = 0;
+        XParams xp = x_params(p);
+        const long long off = ch * G * plane;
+        xp.work += off;
+        xp.delta += off;
+        xp.x += off;
+        xp.B += off;
+        xp.nlines = G * p->ny;
+        xp.red.chunk_acc = p->coll + 1;
+        xp.red.chunk_first = ch == 0;
+        xp.red.chunk_last = ch == nch - 1;
+        xp.l2hint = p->l2hint;
+        if ((s = run_xpass(p, X_ITER, xp))) return s;
+        if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yc, p->smap_y, true, 0))) return s;
+    }
+    return USP_OK;
+}
+
 usp_status sync_state(usp_plan_s *p) {
     CU(cudaMemcpyAsync(p->st_host, p->st, sizeof(IterState), cudaMemcpyDeviceToHost, p->stream));
     CU(cudaStreamSynchronize(p->stream));
@@ -612,6 +662,7 @@ usp_status sync_state(usp_plan_s *p) {
 // Tensor maps of the strided passes (they embed the workspace addresses).
 void build_maps(usp_plan_s *p) {
     p->stile_y = p->stile_z = false;
+    p->chunked = false;
     if (!p->stile || p->ndim < 2 || !stile_supported(p->ny)) return;
     const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
     if (p->ndim == 2) {
@@ -634,6 +685,7 @@ void build_maps(usp_plan_s *p) {
         const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};
         const cuuint32_t box[2] = {cz, bz};
         p->stile_z = make_map(&p->smap_z, p->work, 2, dims, str, box);
+        p->chunked = p->stile_y && p->stile_z && p->pipe_xk && p->chunk_g > 0 && p->chunk_g < p->nz;
         return;
     }
     const long long pv = p->virt ? p->P : 1;
@@ -773,6 +825,11 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         p->pipe = !(leg && leg[0] == '1');
         const char *px = std::getenv("USP_PIPE_X");
         p->pipe_xk = p->pipe && !(px && px[0] == '0');
+        const char *l2h = std::getenv("USP_L2HINT");
+        p->l2hint = !(l2h && l2h[0] == '0');
+        const char *chk = std::getenv("USP_CHUNK");
+        if (chk) p->chunk_g = std::atoll(chk);
+        while (p->chunk_g > 0 && (p->nz % p->chunk_g)) p->chunk_g >>= 1;
         const char *stl = std::getenv("USP_STILE");
         p->stile = (P > 1) || (p->pipe && !(stl && stl[0] == '0'));
         if (p->ndim >= 2 && stile_supported(p->ny))
@@ -963,6 +1020,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         if (s) return s;
         s = run_xpass(p, X_SRC_EPI, xp);
         if (s) return s;
+        if (p->chunked && (s = chunk_kb_all(p))) return s;   // establish the chunked invariant
     }
     s = sync_state(p);
     if (s) return s;
@@ -1003,6 +1061,10 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         while (launched < total) {
             const long long nb = std::min(batch, total - launched);
             for (long long i = 0; i < nb; ++i) {
+                if (p->chunked) {
+                    if ((s = chunked_iteration(p))) return s;
+                    continue;
+                }
                 s = chain_mid(p, 1);
                 if (s) return s;
                 s = run_xpass(p, X_ITER, xp);

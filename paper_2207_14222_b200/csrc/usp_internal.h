@@ -28,6 +28,7 @@ struct IterState {
     unsigned int counter;  // last-block-done counter (reset by the last block)
     int err;               // pipeline watchdog: non-zero = a kernel gave up waiting (see tma.cuh)
     int err_info;
+    int full_iter;         // chunked schedule: the running iteration does the full chain (snapshot by K_C)
 };
 
 struct Red {             // reduction scratch (device)
@@ -35,6 +36,8 @@ struct Red {             // reduction scratch (device)
     double *hist;        // residual ring
     int hist_cap;
     double *local_sum;   // slab-decomposed: the x pass stores its total here (else nullptr)
+    double *chunk_acc;   // chunked schedule: running total over the z-chunk launches (else nullptr)
+    int chunk_first, chunk_last;
 };
 
 // Fourier multiplier data of (L+1)^-1 = F^-1 [c/(D|p|^2 + sigma + c)] F (Eq. 12),
@@ -62,6 +65,7 @@ struct XParams {
     float2 inv_c;        // 1/c (s = S/c)
     IterState *st;
     Red red;
+    int l2hint;          // chunked schedule: stream Delta/x/B evict_first, keep work evict_last
 };
 
 // ---------------------------------------------------------- strided pass --
@@ -76,7 +80,9 @@ struct SParams {
     long long nouter;    // outer slabs
     long long ostride;   // elements between outer slabs
     int line_axis;       // 1 = y (2-D, columns = x), 2 = z (3-D, columns = (y, x))
-    int check_state;     // 1: skip unless status == RUNNING && k < kmax
+    int check_state;     // 0: always run; 1: skip unless status == RUNNING && k < kmax;
+                         // 3: as 1, and block 0 snapshots that test into st->full_iter;
+                         // 2: skip unless st->full_iter (chunked schedule, see usp_api.cu)
     MulParams mp;
     IterState *st;
     // slab decomposition (k_stile only; P = 1: natural layout everywhere)
@@ -86,6 +92,8 @@ struct SParams {
     int nz_loc;          // z planes per slab
     int nyl_lg;          // log2(ny / P)
     long long y0;        // global y of this rank's y block (z pass multiplier)
+    long long o0;        // first outer index (plane) of this launch (chunked schedule)
+    int store_hint;      // 0: plain stores; 1: evict_last (K_D: K_A re-reads from L2); 2: evict_first
 };
 
 // ------------------------------------------------------------------ 1-D --
