@@ -59,6 +59,13 @@ KERNEL_BYTES_CHUNKED = {
     "y_inv": 8,             # read work (written to L2)
 }
 ITER_BYTES_CHUNKED = 72
+# Real path (C4 diffusion, float32 fields, half spectra; SURVEY.md §8 geometry
+# table): x pass reads x, Delta, B (4 B each) + half spectrum (4) and writes
+# x, Delta (4 each) + half spectrum (4); each strided pass moves the half
+# spectrum once each way (8).  (The 16 padding columns per spectrum row add
+# 16/(nx/2) to the spectrum bytes; they are counted as overhead, not work.)
+KERNEL_BYTES_REAL = {"xpass": 28, "y_fwd": 8, "z_fwd_mul_inv": 8, "y_inv": 8}
+ITER_BYTES_REAL = 52
 
 
 def env_int(name, default):
@@ -291,12 +298,19 @@ def run_usp(args, world, rank, local):
     stream = torch.cuda.Stream(device=dev)
     if args.virtual_ranks > 1 and world == 1:
         mode = "virtual"
+    real = p.kind == "diffusion"          # C4: float32 data, the real (half-spectrum) path
+    fdt = torch.float32 if real else torch.complex64
+    esz = 4 if real else 8
     with torch.cuda.stream(stream):
         plan = Plan(shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev, comm=comm,
-                    virtual_ranks=args.virtual_ranks if mode == "virtual" else 0)
+                    dtype="r32" if real else "c64", virtual_ranks=args.virtual_ranks if mode == "virtual" else 0)
     z0, nzl = plan.z0, plan.local_shape[0]
-    med = p.medium[z0:z0 + nzl].to(torch.complex64).contiguous()
-    src = p.source[z0:z0 + nzl].to(torch.complex64).contiguous()
+    if real:
+        med = p.medium[z0:z0 + nzl].real.to(fdt).contiguous()
+        src = p.source[z0:z0 + nzl].real.to(fdt).contiguous()
+    else:
+        med = p.medium[z0:z0 + nzl].to(fdt).contiguous()
+        src = p.source[z0:z0 + nzl].to(fdt).contiguous()
     del p.medium, p.source
     torch.cuda.empty_cache()
     nvox = int(np.prod(shape))              # global voxels
@@ -352,7 +366,7 @@ def run_usp(args, world, rank, local):
     n_it_total = n_iter * args.steps
     chunks = max(1, prof.get("xpass", (0, n_it_total))[1] // n_it_total)
     schedule = "chunked" if chunks > 1 else "4-pass"
-    kbytes = KERNEL_BYTES_CHUNKED if chunks > 1 else KERNEL_BYTES
+    kbytes = KERNEL_BYTES_REAL if real else (KERNEL_BYTES_CHUNKED if chunks > 1 else KERNEL_BYTES)
     dname = "xpass" if "xpass" in prof else max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
     dms, dcount = prof[dname]
     d_ms_per_iter = dms / n_it_total
@@ -366,9 +380,9 @@ def run_usp(args, world, rank, local):
     # ------------------------------------------------ e2e (host buffers)
     e2e = None
     if not args.no_e2e:
-        h_med = torch.empty(plan.local_shape, dtype=torch.complex64, pin_memory=True)
-        h_src = torch.empty(plan.local_shape, dtype=torch.complex64, pin_memory=True)
-        h_out = torch.empty(plan.local_shape, dtype=torch.complex64, pin_memory=True)
+        h_med = torch.empty(plan.local_shape, dtype=fdt, pin_memory=True)
+        h_src = torch.empty(plan.local_shape, dtype=fdt, pin_memory=True)
+        h_out = torch.empty(plan.local_shape, dtype=fdt, pin_memory=True)
         h_med.copy_(med)
         h_src.copy_(src)
         del med, src
@@ -386,7 +400,7 @@ def run_usp(args, world, rank, local):
         torch.cuda.synchronize()
         ems = max_over_ranks(world, f0.elapsed_time(f1))
         e2e = {"value": units * n_iter * e2e_steps / (ems / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": 2 * nloc * 8 * world, "d2h_bytes_per_step": nloc * 8 * world,
+               "h2d_bytes_per_step": 2 * nloc * esz * world, "d2h_bytes_per_step": nloc * esz * world,
                "steps": e2e_steps}
 
     if rank != 0:
@@ -395,7 +409,8 @@ def run_usp(args, world, rank, local):
     if world == 1 and not args.no_cpu:
         v, dt, thr, desc = cpu_oracle_sample()
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
-    iter_bpv = (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D) + (32 if mode in ("slabs", "virtual") else 0)
+    iter_bpv = (ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D)) + \
+        ((16 if real else 32) if mode in ("slabs", "virtual") else 0)
     it_bytes = iter_bpv * nloc
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
                    "slabs": f"{world} z-slabs, NCCL all-to-all transposes",
@@ -403,9 +418,10 @@ def run_usp(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong" if mode == "slabs" else "weak", "vs_baseline": None, "dtype": "c64",
+        "scaling": "strong" if mode == "slabs" else "weak", "vs_baseline": None, "dtype": "f32" if real else "c64",
         "data": "synthetic",
-        "config": {"workload": f"{name} 3-D Helmholtz {shape[2]}x{shape[1]}x{shape[0]} complex64, "
+        "config": {"workload": f"{name} 3-D {'diffusion' if real else 'Helmholtz'} {shape[2]}x{shape[1]}x{shape[0]} "
+                               f"{'float32 (half-spectrum path)' if real else 'complex64'}, "
                                f"{n_iter} iterations of Alg. 1 per step (setup + iterations), alpha=0.75",
                    "grid": list(shape), "iterations_per_step": n_iter,
                    "parallelism": parallelism, "slab_check_rel_l2": slab_check,

@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(256) k_potential(PotParams p) {
         // Re(w/c)
         const double wcr = (wr * cr + wi * ci) * inv_c2, wci = (wi * cr - wr * ci) * inv_c2;
         if (wcr < -1e-6 * sqrt(wcr * wcr + wci * wci)) ++nacc;
-        p.B[i] = make_float2((float)(1.0 - vr), (float)(-vi));
+        if (p.b_real) reinterpret_cast<float *>(p.B)[i] = (float)(1.0 - vr);
+        else p.B[i] = make_float2((float)(1.0 - vr), (float)(-vi));
     }
     // CTA reduce then one atomic each
     __shared__ float smax[8];

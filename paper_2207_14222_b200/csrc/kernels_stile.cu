@@ -235,11 +235,11 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 if (p.line_axis == 2) {
                     // column (x, y) of the (possibly y-sliced) z pass; y global
                     const long long gc = o * p.ncols + col;
-                    const int ix = (int)(gc % p.mp.nx), iy = (int)(p.y0 + gc / p.mp.nx);
+                    const int ix = (int)(gc % p.mp.rowc), iy = (int)(p.y0 + gc / p.mp.rowc);
                     const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
                     pt2 = fmaf(px, px, py * py);
                 } else {
-                    const float px = p.mp.kx * freq_m((int)col, p.mp.nx);
+                    const float px = p.mp.kx * freq_m((int)col, p.mp.nx);   // 2-D (complex path only)
                     pt2 = px * px;
                 }
                 base = fmaf(p.mp.D, pt2, p.mp.sc.x);

@@ -151,6 +151,11 @@ struct usp_plan_s {
     long long nzh = 1;            // z planes this plan holds (nzs, or nz in virtual / 1-GPU mode)
     long long nyl = 1;            // y rows per y block (ny / P)
     long long nloc = 0;           // voxels this plan holds
+    // real path (diffusion with float32 data, kernels_real.cu): x, Delta, B
+    // are float32 and `work` holds the half spectrum in rows of rp complex
+    bool real = false;
+    long long rp = 1;             // row pitch of `work` in complex64 (nx, or nx/2 + 16 on the real path)
+    float2 *twr = nullptr;        // real path: W_nx^k, k < nx/2
     // workspace
     char *ws = nullptr;
     size_t ws_bytes = 0;
@@ -466,6 +471,7 @@ MulParams mul_params(const usp_plan_s *p) {
     mp.nx = (int)p->nx;
     mp.ny = (int)p->ny;
     mp.nz = (int)p->nz;
+    mp.rowc = (int)p->rp;
     return mp;
 }
 
@@ -482,6 +488,7 @@ XParams x_params(usp_plan_s *p) {
     xp.x = p->x;
     xp.B = p->B;
     xp.tw = p->tw[0];
+    xp.twr = p->twr;
     xp.nlines = p->ny * p->nzh;
     xp.src_real = p->d.dtype == USP_R32;
     const double m = p->c.re * p->c.re + p->c.im * p->c.im;
@@ -496,7 +503,8 @@ XParams x_params(usp_plan_s *p) {
 usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
     {
         Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
-        if (p->pipe_xk) CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream));
+        if (p->real) CU(launch_xpass_real((int)p->nx, mode, xp, p->gridp_x, p->stream));
+        else if (p->pipe_xk) CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream));
         else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
     }
     if (mode != X_SRC_FWD && multi_rank(p)) {
@@ -553,7 +561,7 @@ SParams sparams(usp_plan_s *p, float2 *data, float2 *dst, const float2 *tw, long
 // layout holds y block r's planes of slab q.  forward: recv(r,q) <- send(q,r);
 // back: send(q,r) <- recv(r,q).
 usp_status exchange(usp_plan_s *p, bool forward) {
-    const long long bk = p->nzs * p->nyl * p->nx;   // elements per block
+    const long long bk = p->nzs * p->nyl * p->rp;   // elements per block
     const size_t bytes = (size_t)bk * sizeof(float2);
     Tick t(p, KC_A2A, false);
     if (p->virt) {
@@ -581,25 +589,25 @@ usp_status exchange(usp_plan_s *p, bool forward) {
 // inverse, with the (L+1)^-1 multiplier on the last axis (Eq. 12).
 usp_status chain_mid(usp_plan_s *p, int check_state) {
     if (p->ndim == 2) {
-        SParams sp = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, 1, 0, 1, check_state, 2);
+        SParams sp = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, 1, 0, 1, check_state, 2);
         return run_strided(p, KC_YMUL2D, (int)p->ny, S_FWD_MUL_INV, sp, p->smap_y, p->stile_y, p->grid_y);
     }
     usp_status s;
     if (p->P == 1) {
-        SParams yf = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, p->nz, p->nx * p->ny, 1, check_state, 3);
-        SParams zm = sparams(p, p->work, p->work, p->tw[2], p->nx * p->ny, p->nx * p->ny, 1, 0, 2, check_state, 2);
+        SParams yf = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, p->nz, p->rp * p->ny, 1, check_state, 3);
+        SParams zm = sparams(p, p->work, p->work, p->tw[2], p->rp * p->ny, p->rp * p->ny, 1, 0, 2, check_state, 2);
         if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, p->stile_y, p->grid_y))) return s;
         if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, p->stile_z, p->grid_z))) return s;
         return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, p->stile_y, p->grid_y);
     }
     // slab decomposition: K_B -> transpose -> K_C -> transpose -> K_D
     const long long pv = p->virt ? p->P : 1;   // y blocks held here
-    SParams yb = sparams(p, p->work, p->sendb, p->tw[1], p->nx, p->nx, p->nzh, p->nx * p->ny, 1, check_state, 3);
+    SParams yb = sparams(p, p->work, p->sendb, p->tw[1], p->rp, p->rp, p->nzh, p->rp * p->ny, 1, check_state, 3);
     yb.send_layout = 1;
-    SParams zm = sparams(p, p->recvb, p->recvb, p->tw[2], p->nyl * p->nx, p->nyl * p->nx, pv,
-                         p->nz * p->nyl * p->nx, 2, check_state, 2);
+    SParams zm = sparams(p, p->recvb, p->recvb, p->tw[2], p->nyl * p->rp, p->nyl * p->rp, pv,
+                         p->nz * p->nyl * p->rp, 2, check_state, 2);
     zm.y0 = p->virt ? 0 : (long long)p->rank * p->nyl;
-    SParams yd = sparams(p, p->sendb, p->work, p->tw[1], p->nx, p->nx, p->nzh, p->nx * p->ny, 1, check_state, 5);
+    SParams yd = sparams(p, p->sendb, p->work, p->tw[1], p->rp, p->rp, p->nzh, p->rp * p->ny, 1, check_state, 5);
     if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0))) return s;
     if ((s = exchange(p, true))) return s;
     if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, true, 0))) return s;
@@ -618,17 +626,17 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
 //   of 104 B/voxel per iteration.  K_A's residual partials are summed over
 //   the chunks in launch order (deterministic).
 usp_status chunk_kb_all(usp_plan_s *p) {
-    SParams yb = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, p->nz, p->nx * p->ny, 1, 0, 3);
+    SParams yb = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, p->nz, p->rp * p->ny, 1, 0, 3);
     return run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0);
 }
 
 usp_status chunked_iteration(usp_plan_s *p) {
     usp_status s;
-    SParams zm = sparams(p, p->work, p->work, p->tw[2], p->nx * p->ny, p->nx * p->ny, 1, 0, 2, 3, 2);
+    SParams zm = sparams(p, p->work, p->work, p->tw[2], p->rp * p->ny, p->rp * p->ny, 1, 0, 2, 3, 2);
     if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, true, 0))) return s;
-    const long long G = p->chunk_g, nch = p->nz / G, plane = p->nx * p->ny;
+    const long long G = p->chunk_g, nch = p->nz / G, plane = p->rp * p->ny;
     for (long long ch = 0; ch < nch; ++ch) {
-        SParams yc = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, G, plane, 1, 2, 3);
+        SParams yc = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, G, plane, 1, 2, 3);
         yc.o0 = ch * G;
         yc.store_hint = p->l2hint ? 1 : 0;   // K_A re-reads the chunk from L2
         if ((s = run_strided(p, KC_YINV, (int)p->ny, S_INV, yc, p->smap_y, true, 0))) return s;
@@ -666,23 +674,23 @@ void build_maps(usp_plan_s *p) {
     if (!p->stile || p->ndim < 2 || !stile_supported(p->ny)) return;
     const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
     if (p->ndim == 2) {
-        const cuuint64_t dims[2] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny};
-        const cuuint64_t str[1] = {(cuuint64_t)p->nx * 8};
+        const cuuint64_t dims[2] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny};
+        const cuuint64_t str[1] = {(cuuint64_t)p->rp * 8};
         const cuuint32_t box[2] = {cy, by};
         p->stile_y = make_map(&p->smap_y, p->work, 2, dims, str, box);
         return;
     }
     {   // y pass over the planes held here: {x, y, z}
-        const cuuint64_t dims[3] = {(cuuint64_t)p->nx, (cuuint64_t)p->ny, (cuuint64_t)p->nzh};
-        const cuuint64_t str[2] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nx * p->ny) * 8};
+        const cuuint64_t dims[3] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny, (cuuint64_t)p->nzh};
+        const cuuint64_t str[2] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->rp * p->ny) * 8};
         const cuuint32_t box[3] = {cy, by, 1};
         p->stile_y = make_map(&p->smap_y, p->work, 3, dims, str, box);
     }
     if (!stile_supported(p->nz)) return;
     const cuuint32_t cz = (cuuint32_t)stile_cols((int)p->nz), bz = (cuuint32_t)stile_box((int)p->nz);
     if (p->P == 1) {   // z pass: {x*y columns, z}
-        const cuuint64_t dims[2] = {(cuuint64_t)(p->nx * p->ny), (cuuint64_t)p->nz};
-        const cuuint64_t str[1] = {(cuuint64_t)(p->nx * p->ny) * 8};
+        const cuuint64_t dims[2] = {(cuuint64_t)(p->rp * p->ny), (cuuint64_t)p->nz};
+        const cuuint64_t str[1] = {(cuuint64_t)(p->rp * p->ny) * 8};
         const cuuint32_t box[2] = {cz, bz};
         p->stile_z = make_map(&p->smap_z, p->work, 2, dims, str, box);
         p->chunked = p->stile_y && p->stile_z && p->pipe_xk && p->chunk_g > 0 && p->chunk_g < p->nz;
@@ -691,16 +699,16 @@ void build_maps(usp_plan_s *p) {
     const long long pv = p->virt ? p->P : 1;
     bool ok;
     {   // z pass on the y-slabs of the receive buffer: {x*y_loc columns, z * (y blocks)}
-        const cuuint64_t dims[2] = {(cuuint64_t)(p->nyl * p->nx), (cuuint64_t)(p->nz * pv)};
-        const cuuint64_t str[1] = {(cuuint64_t)(p->nyl * p->nx) * 8};
+        const cuuint64_t dims[2] = {(cuuint64_t)(p->nyl * p->rp), (cuuint64_t)(p->nz * pv)};
+        const cuuint64_t str[1] = {(cuuint64_t)(p->nyl * p->rp) * 8};
         const cuuint32_t box[2] = {cz, bz};
         ok = make_map(&p->smap_z, p->recvb, 2, dims, str, box);
     }
     {   // K_D reads the send layout [r][q][z_loc][y_loc][x]: {x, y_loc, z_loc, q, r}
-        const cuuint64_t dims[5] = {(cuuint64_t)p->nx, (cuuint64_t)p->nyl, (cuuint64_t)p->nzs, (cuuint64_t)p->P,
+        const cuuint64_t dims[5] = {(cuuint64_t)p->rp, (cuuint64_t)p->nyl, (cuuint64_t)p->nzs, (cuuint64_t)p->P,
                                     (cuuint64_t)pv};
-        const cuuint64_t bk = (cuuint64_t)(p->nzs * p->nyl * p->nx) * 8;
-        const cuuint64_t str[4] = {(cuuint64_t)p->nx * 8, (cuuint64_t)(p->nyl * p->nx) * 8, bk, bk * p->P};
+        const cuuint64_t bk = (cuuint64_t)(p->nzs * p->nyl * p->rp) * 8;
+        const cuuint64_t str[4] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->nyl * p->rp) * 8, bk, bk * p->P};
         const cuuint32_t box[5] = {cy, std::min<cuuint32_t>(by, (cuuint32_t)p->nyl), 1, 1, 1};
         ok = ok && make_map(&p->smap_kd, p->sendb, 5, dims, str, box);
     }
@@ -801,6 +809,12 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     p->nzh = (P > 1 && !virt) ? p->nzs : p->nz;
     p->nyl = p->ny / P;
     p->nloc = p->nx * p->ny * p->nzh;
+    {
+        const char *rl = std::getenv("USP_REAL");
+        p->real = !(rl && rl[0] == '0') && desc->dtype == USP_R32 && desc->medium == USP_MEDIUM_W &&
+                  desc->ndim == 3 && xreal_supported(p->nx) && stile_supported(p->ny) && stile_supported(p->nz);
+        p->rp = p->real ? xreal_row_pitch((int)p->nx) : p->nx;
+    }
     p->stream = (cudaStream_t)desc->stream;
     p->sigma = desc->sigma;
     p->c = desc->c;
@@ -831,15 +845,15 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (chk) p->chunk_g = std::atoll(chk);
         while (p->chunk_g > 0 && (p->nz % p->chunk_g)) p->chunk_g >>= 1;
         const char *stl = std::getenv("USP_STILE");
-        p->stile = (P > 1) || (p->pipe && !(stl && stl[0] == '0'));
+        p->stile = (P > 1) || p->real || (p->pipe && !(stl && stl[0] == '0'));
         if (p->ndim >= 2 && stile_supported(p->ny))
-            p->grids_y = occ_grid(p, (p->nx / stile_cols((int)p->ny)) * p->nzh, stile_ctas_per_sm((int)p->ny));
+            p->grids_y = occ_grid(p, (p->rp / stile_cols((int)p->ny)) * p->nzh, stile_ctas_per_sm((int)p->ny));
         if (p->ndim >= 3 && stile_supported(p->nz)) {
-            const long long zcols = (P > 1) ? p->nyl * p->nx * (virt ? P : 1) : p->nx * p->ny;
+            const long long zcols = (P > 1) ? p->nyl * p->rp * (virt ? P : 1) : p->rp * p->ny;
             p->grids_z = occ_grid(p, zcols / stile_cols((int)p->nz), stile_ctas_per_sm((int)p->nz));
         }
-        const int u = 32 / (1 << (log2ll(p->nx) / 2));   // x lines per warp unit (32 / N1)
-        p->gridp_x = occ_grid(p, xl / u, 1);
+        const int u = p->real ? xreal_lines_per_unit((int)p->nx) : 32 / (1 << (log2ll(p->nx) / 2));
+        p->gridp_x = occ_grid(p, xl / u, 1);   // one CTA per SM, persistent over the warp units
     }
     p->partials_cap = std::max(1, std::max(p->grid_x, p->gridp_x));
     p->far_cap = p->nsm * 8;
@@ -861,8 +875,21 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->far_i, sizeof(long long) * p->far_cap));
     TRY(cudaMalloc(&p->coll, sizeof(double) * (16 + 3 * 64)));
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
+    if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
+        const int n = (int)p->nx, m = n / 2;
+        std::vector<float2> tr(m);
+        for (int k = 0; k < m; ++k) {
+            const double a = -2.0 * M_PI * (double)k / (double)n;
+            double c_ = std::cos(a), s_ = std::sin(a);
+            if (4 * k == n) { c_ = 0.0; s_ = -1.0; }
+            if (k == 0) { c_ = 1.0; s_ = 0.0; }
+            tr[k] = make_float2((float)c_, (float)s_);
+        }
+        TRY(cudaMalloc(&p->twr, sizeof(float2) * m));
+        TRY(cudaMemcpy(p->twr, tr.data(), sizeof(float2) * m, cudaMemcpyHostToDevice));
+    }
     for (int a = 0; a < p->ndim; ++a) {
-        twh[a] = twiddle_table((int)ext[a]);
+        twh[a] = twiddle_table((int)((a == 0 && p->real) ? ext[a] / 2 : ext[a]));
         TRY(cudaMalloc(&p->tw[a], sizeof(float2) * twh[a].size()));
         TRY(cudaMemcpy(p->tw[a], twh[a].data(), sizeof(float2) * twh[a].size(), cudaMemcpyHostToDevice));
     }
@@ -876,8 +903,9 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
 
 usp_status usp_plan_workspace_size(usp_plan_t p, size_t *bytes) {
     if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
-    const int fields = p->P > 1 ? 6 : 4;
-    *bytes = fields * align256((size_t)p->nloc * sizeof(float2));
+    const size_t f = align256((size_t)p->nloc * (p->real ? sizeof(float) : sizeof(float2)));
+    const size_t w = align256((size_t)p->nzh * p->ny * p->rp * sizeof(float2));
+    *bytes = 3 * f + w * (p->P > 1 ? 3 : 1);
     return USP_OK;
 }
 
@@ -887,7 +915,8 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     size_t need = 0;
     usp_plan_workspace_size(p, &need);
     if (bytes < need) return fail(USP_ERR_NOMEM, "workspace %zu bytes < required %zu", bytes, need);
-    const size_t f = align256((size_t)p->nloc * sizeof(float2));
+    const size_t f = align256((size_t)p->nloc * (p->real ? sizeof(float) : sizeof(float2)));
+    const size_t w = align256((size_t)p->nzh * p->ny * p->rp * sizeof(float2));
     p->ws = (char *)dev;
     p->ws_bytes = bytes;
     p->x = (float2 *)(p->ws);
@@ -895,9 +924,11 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     p->B = (float2 *)(p->ws + 2 * f);
     p->work = (float2 *)(p->ws + 3 * f);
     if (p->P > 1) {
-        p->sendb = (float2 *)(p->ws + 4 * f);
-        p->recvb = (float2 *)(p->ws + 5 * f);
+        p->sendb = (float2 *)(p->ws + 3 * f + w);
+        p->recvb = (float2 *)(p->ws + 3 * f + 2 * w);
     }
+    if (p->real)   // the spectrum rows' padding columns are never written by the x pass: keep them 0
+        CU(cudaMemsetAsync(p->work, 0, w * (p->P > 1 ? 3 : 1), p->stream));
     p->have_potential = p->have_source = false;
     build_maps(p);
     if (p->P > 1 && !(p->stile_y && p->stile_z))
@@ -953,8 +984,11 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
     if (p->d.D * p->c.re < 0.0)
         return fail(USP_ERR_NOT_ACCRETIVE, "D Re(c) < 0: -D lap / c is not accretive (Eq. 1)");
     CU(cudaMemsetAsync(p->red_u, 0, sizeof(unsigned) * 4, p->stream));
+    if (p->real && (p->sigma.im != 0.0 || p->c.im != 0.0))
+        return fail(USP_ERR_UNSUPPORTED, "the real (float32 diffusion) path needs real sigma and c");
     PotParams pp{p->work, p->d.dtype == USP_R32, p->d.medium == USP_MEDIUM_K2, p->B, p->nloc,
                  p->sigma.re, p->sigma.im, p->c.re, p->c.im, p->red_u, p->red_u + 1, p->red_u + 2};
+    pp.b_real = p->real;
     {
         Tick t(p, KC_POTENTIAL);
         CU(launch_potential(pp, occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
@@ -1125,6 +1159,8 @@ usp_status usp_get_field(usp_plan_t p, void *out, usp_where where) {
     const cudaMemcpyKind kind = where == USP_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     if (p->d.dtype == USP_C64) {
         CU(cudaMemcpyAsync(out, p->x, (size_t)p->nloc * sizeof(float2), kind, p->stream));
+    } else if (p->real) {
+        CU(cudaMemcpyAsync(out, p->x, (size_t)p->nloc * sizeof(float), kind, p->stream));
     } else {
         // real field: take the real parts (strided copy, pitch 8 -> 4 bytes)
         CU(cudaMemcpy2DAsync(out, sizeof(float), p->x, sizeof(float2), sizeof(float), (size_t)p->nloc, kind,
@@ -1181,6 +1217,7 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->far_i);
     cudaFree(p->coll);
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
+    cudaFree(p->twr);
     cudaFreeHost(p->st_host);
     delete p;
 }

@@ -49,6 +49,7 @@ struct MulParams {
     float sqrtD;         // sqrt(D) (the z pass folds it into the line frequency)
     float kx, ky, kz;    // 2 pi / (n_a h_a): p_a = k_a * m_a
     int nx, ny, nz;
+    int rowc;            // columns per row of the spectrum array (nx; nx/2 + 16 on the real path)
 };
 
 // ---------------------------------------------------------------- x pass --
@@ -59,7 +60,8 @@ struct XParams {
     float2 *delta;       // Delta_k
     float2 *x;           // x_k (also the staging area of the raw source S)
     const float2 *B;     // B = 1 - V
-    const float2 *tw;    // four-step twiddles for nx
+    const float2 *tw;    // four-step twiddles for nx (real path: for nx/2)
+    const float2 *twr;   // real path: W_nx^k, k < nx/2 (split/merge of the half-length FFT)
     long long nlines;    // ny * nz (local)
     int src_real;        // staged source is float32 (else complex64)
     float2 inv_c;        // 1/c (s = S/c)
@@ -121,6 +123,7 @@ struct PotParams {
     unsigned int *max_absV_bits;  // float bits of max |V| (non-negative -> int order)
     unsigned int *n_nonaccretive;
     unsigned int *n_nonfinite;
+    int b_real;          // store B as float32 (real path; V is real there)
 };
 
 struct FarParams {       // farthest medium value from a centre (smallest circle)
@@ -131,6 +134,12 @@ struct FarParams {       // farthest medium value from a centre (smallest circle
     double *best_d2;     // per CTA
     long long *best_idx; // per CTA
 };
+
+// real path (kernels_real.cu)
+cudaError_t launch_xpass_real(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);
+bool xreal_supported(long long n);
+int xreal_row_pitch(int N);
+int xreal_lines_per_unit(int N);
 
 // launchers (kernels.cu); all return cudaGetLastError()
 cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);
