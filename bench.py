@@ -166,13 +166,15 @@ def max_over_ranks(world, v: float) -> float:
     return float(t.item())
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
-    --set full capture summary (profiles/), if present."""
+def ncu_traffic(workload):
+    """Per-launch DRAM bytes of the kernels from the committed ncu --set full
+    capture summary (profiles/ncu_traffic.json) when it was taken on this
+    workload, else {}."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get("bytes_per_launch", {})
+            d = json.load(f)
+        return d.get("bytes_per_launch", {}) if d.get("workload") == workload else {}
     except Exception:
         return {}
 
@@ -372,7 +374,7 @@ def run_usp(args, world, rank, local):
     d_ms_per_iter = dms / n_it_total
     dbytes = kbytes[dname] * nloc                   # per iteration (= per launch x chunks)
     achieved = dbytes / (d_ms_per_iter / 1e3) / 1e9
-    traffic = ncu_traffic().get(dname)
+    traffic = ncu_traffic(name).get(dname) if args.size is None and mode != "virtual" else None
     # iteration time: device time of the iterate() calls / iterations
     iter_ms = sum(a.elapsed_time(b) for a, b in it_events) / n_it_total
     kernel_share = {k: round(v[0] / sum(x[0] for x in prof.values()), 4) for k, v in prof.items()}
