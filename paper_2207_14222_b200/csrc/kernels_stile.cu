@@ -44,16 +44,25 @@ namespace usp {
 template <int N>
 struct STile {
     using G = LineGeo<N>;
-    static constexpr int COLS = 16;
-    static constexpr int NT = COLS * G::N1;
+    // GROUPS independent thread groups per CTA, each with its own stage,
+    // exchange buffer, mbarrier and named barrier.  Two groups of 8 columns at
+    // N = 1024 (one computes while the other waits) measured 1.6x SLOWER than
+    // one group of 16 columns (y 5.0 vs 3.1 ms, z 7.4 vs 4.6 ms: 64-byte TMA
+    // rows), so one group of 16 columns (128-byte rows) is used.
+    static constexpr int GROUPS = 1;
+    static constexpr int COLS = (GROUPS == 2) ? 8 : 16;
+    static constexpr int NTG = COLS * G::N1;                    // threads per group
+    static constexpr int NT = GROUPS * NTG;
     static constexpr int TILE = COLS * N;                       // float2 per stage
     // two-round exchange only where a full buffer would not fit next to the stage
     static constexpr bool HALFX = (N >= 512);
     static constexpr bool FLIP = HALFX && G::R == 1;   // N1 == N2: halves chosen by shift flips
-    static constexpr int XPITCH = HALFX ? (G::N2 / 2) * COLS : G::N2 * COLS;   // float2 per writer row
+    static constexpr int XPAD = (COLS == 8) ? 8 : 0;   // 8-column rows: offset writer rows by 64 B (banks)
+    static constexpr int XPITCH = (HALFX ? (G::N2 / 2) * COLS : G::N2 * COLS) + XPAD;   // float2 per writer row
     static constexpr int XB = G::N1 * XPITCH;
+    static constexpr int GSM = TILE + XB;                       // float2 per group
     static constexpr int BOXN = N < 256 ? N : 256;
-    static constexpr int SMEM = (TILE + XB + N) * 8 + 16;
+    static constexpr int SMEM = (GROUPS * GSM + N) * 8 + 16 * GROUPS;
     static constexpr int FIT_SMEM = 232448 / (SMEM + 1024);
     static constexpr int FIT_REGS = 65536 / (NT * 96);            // keep >= 96 registers per thread
     static constexpr int FIT_THR = 2048 / NT;
@@ -72,8 +81,13 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // v[n2] = x[j + N1 n2] on entry; v[m] = X[j + N1 m] on exit (up to the
 // shift flips of HALFX, which the caller applies).
 template <int N>
+__device__ __forceinline__ void gsync(int bar) {   // the calling thread group (named barrier)
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(STile<N>::NTG) : "memory");
+}
+
+template <int N>
 __device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *xb, const float2 *sm_tw, int c,
-                                          int j) {
+                                          int j, int bar) {
     using G = LineGeo<N>;
     using T = STile<N>;
     dft<G::N2, false>(v);
@@ -93,11 +107,11 @@ __device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *x
         for (int r = 0; r < 2; ++r) {
 #pragma unroll
             for (int q = 0; q < H; ++q) wb[q * T::COLS] = v[r * H + q];
-            __syncthreads();
+            gsync<N>(bar);
             const float2 *rb = xb + (H * (r ^ b)) * T::XPITCH + (j & (H - 1)) * T::COLS + c;
 #pragma unroll
             for (int q = 0; q < H; ++q) v[r * H + q] = rb[q * T::XPITCH];
-            __syncthreads();
+            gsync<N>(bar);
         }
         dft<G::N1, false>(v);
     } else if constexpr (T::HALFX) {
@@ -109,10 +123,10 @@ __device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *x
         for (int t = 0; t < 2; ++t) {
 #pragma unroll
             for (int q = 0; q < G::N1; ++q) wb[q * T::COLS] = v[t * G::N1 + q];
-            __syncthreads();
+            gsync<N>(bar);
 #pragma unroll
             for (int n1 = 0; n1 < G::N1; ++n1) v[t * G::N1 + n1] = xb[n1 * T::XPITCH + j * T::COLS + c];
-            __syncthreads();
+            gsync<N>(bar);
         }
 #pragma unroll
         for (int t = 0; t < 2; ++t) dft<G::N1, false>(v + t * G::N1);
@@ -129,13 +143,13 @@ __device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *x
         float2 *wb = xb + j * T::XPITCH + c;
 #pragma unroll
         for (int k2 = 0; k2 < G::N2; ++k2) wb[k2 * T::COLS] = v[k2];
-        __syncthreads();
+        gsync<N>(bar);
 #pragma unroll
         for (int t = 0; t < G::R; ++t)
 #pragma unroll
             for (int n1 = 0; n1 < G::N1; ++n1)
                 v[t * G::N1 + n1] = xb[n1 * T::XPITCH + (j + G::N1 * t) * T::COLS + c];
-        __syncthreads();
+        gsync<N>(bar);
 #pragma unroll
         for (int t = 0; t < G::R; ++t) dft<G::N1, false>(v + t * G::N1);
         if constexpr (G::R > 1) {
@@ -156,23 +170,27 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     using G = LineGeo<N>;
     using T = STile<N>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float2 *stage = reinterpret_cast<float2 *>(smem_raw);
+    const int tid = threadIdx.x;
+    const int g = tid / T::NTG, tl = tid % T::NTG;     // thread group, thread in group
+    float2 *stage = reinterpret_cast<float2 *>(smem_raw) + g * T::GSM;
     float2 *xb = stage + T::TILE;
-    float2 *sm_tw = xb + T::XB;
-    uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N);
+    float2 *sm_tw = reinterpret_cast<float2 *>(smem_raw) + T::GROUPS * T::GSM;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N) + g;
+    const int bar = 1 + g;
     if (p.check_state) {
         const bool running = p.st->status == ST_RUNNING && p.st->k < p.st->kmax;
         if (p.check_state == 3 && blockIdx.x == 0 && threadIdx.x == 0) p.st->full_iter = running;
         if (!((p.check_state == 2) ? (p.st->full_iter != 0) : running)) return;
     }
-    const int tid = threadIdx.x;
-    const int c = tid % T::COLS, j = tid / T::COLS;
+    const int c = tl % T::COLS, j = tl / T::COLS;
     const long long tpo = p.ncols / T::COLS;
     const long long ntiles = tpo * p.nouter;
-    const int nloc = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    // tiles are dealt to (CTA, group) pairs round-robin
+    const long long vb = (long long)blockIdx.x * T::GROUPS + g, vg = (long long)gridDim.x * T::GROUPS;
+    const int nloc = (int)((ntiles - vb + vg - 1) / vg);
 
-    auto issue = [&](int i) {   // thread 0: TMA boxes of local tile i
-        const long long t = blockIdx.x + (long long)i * gridDim.x;
+    auto issue = [&](int i) {   // thread 0 of the group: TMA boxes of local tile i
+        const long long t = vb + (long long)i * vg;
         const long long ol = t / tpo, o = p.o0 + ol;
         const int c0 = (int)((t - ol * tpo) * T::COLS);
         mbar_arrive_expect_tx(full, T::TILE * 8);
@@ -192,7 +210,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
             }
         }
     };
-    if (tid == 0) {
+    if (tl == 0) {
         prefetch_tmap(&tmap);
         mbar_init(full, 1);
         fence_mbar_init();
@@ -202,13 +220,13 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     __syncthreads();
 
     // FLIP shift flips: threads whose top row bit is set negate odd inputs /
-    // outputs (see header).  The bit is uniform per warp (a warp holds rows
-    // j = 2w, 2w+1), so the flips are a non-divergent branch.
+    // outputs (see header).  The bit is uniform per warp (a warp holds the
+    // rows 32/COLS consecutive j), so the flips are a non-divergent branch.
     const bool flip = T::FLIP && ((j >> (ilog2(G::N1) - 1)) & 1);
 
     for (int i = 0; i < nloc; ++i) {
         if (!mbar_wait(full, i & 1)) {
-            if (tid == 0 && atomicCAS(&p.st->err, 0, 5) == 0) p.st->err_info = i;
+            if (tl == 0 && atomicCAS(&p.st->err, 0, 5) == 0) p.st->err_info = i;
             return;
         }
         float2 v[G::N2];
@@ -222,13 +240,13 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
             for (int m = 1; m < G::N2; m += 2) v[m] = cscale(v[m], -1.f);
         }
         fence_proxy_async_smem();
-        __syncthreads();                 // stage consumed: prefetch the next tile
-        if (tid == 0 && i + 1 < nloc) issue(i + 1);
+        gsync<N>(bar);                   // stage consumed: prefetch the next tile
+        if (tl == 0 && i + 1 < nloc) issue(i + 1);
 
         if constexpr (MODE == S_FWD_MUL_INV) {
             float base;   // D (p_x^2 + p_y^2) + Re(sigma + c) of this thread's column
             {
-                const long long t = blockIdx.x + (long long)i * gridDim.x;
+                const long long t = vb + (long long)i * vg;
                 const long long o = t / tpo;
                 const long long col = (t - o * tpo) * T::COLS + c;
                 float pt2;
@@ -246,7 +264,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
             }
 #pragma unroll 1
             for (int pass = 0; pass < 2; ++pass) {
-                stile_fft<N>(v, xb, sm_tw, c, j);
+                stile_fft<N>(v, xb, sm_tw, c, j, bar);
                 if (pass == 0) {
                     // (L+1)^-1 symbol (Eq. 12) at the signed frequency of k = j + N1 m:
                     //   g = cn (dr - i di) / (dr^2 + di^2),  dr = D |p|^2 + Re(sigma + c),
@@ -272,9 +290,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 }
             }
         } else {
-            stile_fft<N>(v, xb, sm_tw, c, j);
+            stile_fft<N>(v, xb, sm_tw, c, j, bar);
         }
-        long long t = blockIdx.x + (long long)i * gridDim.x;
+        long long t = vb + (long long)i * vg;
         asm volatile("" : "+l"(t));
         const long long ol = t / tpo, o = p.o0 + ol;
         const long long col = (t - ol * tpo) * T::COLS + c;
@@ -339,7 +357,7 @@ static cudaError_t stile_mode(SMode mode, const CUtensorMap &map, const SParams 
 }
 
 bool stile_supported(long long n) { return n >= 64 && n <= 1024 && (n & (n - 1)) == 0; }
-int stile_cols(int) { return 16; }
+int stile_cols(int N) { return N == 1024 ? STile<1024>::COLS : 16; }
 int stile_box(int N) { return N < 256 ? N : 256; }
 int stile_ctas_per_sm(int N) {
     switch (N) {
