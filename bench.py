@@ -411,8 +411,10 @@ def run_usp(args, world, rank, local):
     if world == 1 and not args.no_cpu:
         v, dt, thr, desc = cpu_oracle_sample()
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
+    # separate transposes (NCCL all-to-all / device copies) add their staging
+    # reads and writes; the fused (peer-store) transposes add nothing to HBM
     iter_bpv = (ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D)) + \
-        ((16 if real else 32) if mode in ("slabs", "virtual") else 0)
+        ((16 if real else 32) if "all_to_all" in prof else 0)
     it_bytes = iter_bpv * nloc
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
                    "slabs": f"{world} z-slabs, NCCL all-to-all transposes",

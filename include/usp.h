@@ -114,7 +114,12 @@ typedef struct {
  * FFT passes are slab-local; the z pass runs on y-slabs reached by an
  * all-to-all transpose (and back), and the residual norm is one all-gather
  * of P doubles summed in rank order, so every rank takes the same stop
- * decision.  With nccl_comm, the arrays passed to
+ * decision.  The transposes are fused into the stores of
+ * the y-forward and z passes (each row goes straight to the buffer of the
+ * rank that needs it: CUDA-IPC-mapped peer memory over NVLink, mapped at
+ * usp_plan_set_workspace, which is then collective), with a cross-rank
+ * barrier after each; if any rank cannot map its peers (or P > 8, or
+ * USP_FUSED=0) NCCL all-to-alls are used instead.  With nccl_comm, the arrays passed to
  * set_potential / set_source / get_field are the rank's slab
  * [nz/P][ny][nx] (usp_local_extent gives z0); every call is collective.
  * Requires P a power of two dividing ny and nz, ny and nz in [64, 1024].

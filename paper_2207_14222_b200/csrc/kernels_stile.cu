@@ -71,6 +71,8 @@ struct STile {
     static constexpr int MINB = MINB1 < 1 ? 1 : MINB1;
 };
 
+__device__ __forceinline__ int ilog2c(int n) { return 31 - __clz(n); }   // n a power of two
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -302,7 +304,31 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
 #pragma unroll
             for (int m = 1; m < G::N2; m += 2) v[m] = cscale(v[m], -1.f);
         }
-        if (MODE == S_FWD && p.send_layout) {
+        if (MODE == S_FWD && p.peer_mode == 1) {
+            // K_B with the forward transpose fused in: row y of plane (r, z_loc)
+            // is stored straight into block r of the receive buffer of rank
+            // q = y / ny_loc ([z][y_loc][x] there) -- over NVLink for q != r
+            const long long rr = o / p.nz_loc, zl = o - rr * p.nz_loc, r = p.rank0 + rr;
+            const long long nyl = 1LL << p.nyl_lg;
+            const long long off = r * p.bk + zl * nyl * p.ncols + col;
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) {
+                const int y = j + G::N1 * m;
+                p.peer[y >> p.nyl_lg][off + (long long)(y & (nyl - 1)) * stride] = v[m];
+            }
+        } else if (MODE == S_FWD_MUL_INV && p.peer_mode == 2) {
+            // K_C with the return transpose fused in: z-line value z of y block r
+            // goes to block r of the send buffer of the rank q = z / nz_loc that
+            // owns plane z ([z_loc][y_loc][x] there); K_D reads it through the
+            // 5-D map
+            const long long off = (p.rank0 + o) * p.bk + col;
+            const int zmask = p.nz_loc - 1, zlg = ilog2c(p.nz_loc);
+#pragma unroll
+            for (int m = 0; m < G::N2; ++m) {
+                const int z = j + G::N1 * m;
+                p.peer[z >> zlg][off + (long long)(z & zmask) * stride] = cconj(v[m]);
+            }
+        } else if (MODE == S_FWD && p.send_layout) {
             // K_B before the forward transpose: row y of plane o goes to block
             // (r, q = y / ny_loc) of the send layout [r][q][z_loc][y_loc][x]
             const long long r = o / p.nz_loc, zl = o - r * p.nz_loc;

@@ -125,10 +125,10 @@ Nccl &nccl() {
     } while (0)
 
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
-              KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_N };
+              KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_BARRIER, KC_N };
 const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
                               "solve1d", "potential", "farthest", "set_state", "xpass_setup",
-                              "all_to_all", "finish", "allgather"};
+                              "all_to_all", "finish", "allgather", "rank_barrier"};
 
 struct Timed {
     int cls;
@@ -161,6 +161,10 @@ struct usp_plan_s {
     size_t ws_bytes = 0;
     float2 *x = nullptr, *delta = nullptr, *B = nullptr, *work = nullptr;
     float2 *sendb = nullptr, *recvb = nullptr;   // P > 1
+    // transposes fused into the K_B / K_C stores (peer memory; USP_FUSED=0 -> NCCL all-to-all)
+    bool fused = false;
+    float2 *peer_recv[kMaxPeers] = {}, *peer_send[kMaxPeers] = {};
+    std::vector<void *> ipc_bases;   // peer allocations mapped with cudaIpcOpenMemHandle
     // plan-owned small device memory
     IterState *st = nullptr;
     double *partials = nullptr;
@@ -556,6 +560,109 @@ SParams sparams(usp_plan_s *p, float2 *data, float2 *dst, const float2 *tw, long
     return sp;
 }
 
+typedef CUresult (*AddrRangeFn)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+AddrRangeFn addr_range_fn() {
+    static AddrRangeFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *ptr = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<AddrRangeFn>(ptr);
+    }
+    return fn;
+}
+
+void close_peers(usp_plan_s *p) {
+    for (void *b : p->ipc_bases) cudaIpcCloseMemHandle(b);
+    p->ipc_bases.clear();
+    p->fused = false;
+}
+
+// Map every rank's send / receive buffer for the fused transposes (collective
+// in NCCL mode: CUDA IPC handles of the workspace allocations are
+// all-gathered; every rank takes the same decision, falling back to the NCCL
+// all-to-alls if any rank cannot map its peers).
+usp_status setup_peers(usp_plan_s *p) {
+    close_peers(p);
+    const char *fz = std::getenv("USP_FUSED");
+    const bool want = p->P > 1 && p->P <= kMaxPeers && !(fz && fz[0] == '0');
+    const long long bk = p->nzs * p->nyl * p->rp;
+    if (!want) return USP_OK;
+    if (p->virt) {   // rank q's region of the one-GPU buffers
+        for (int q = 0; q < p->P; ++q) {
+            p->peer_recv[q] = p->recvb + (long long)q * p->P * bk;
+            p->peer_send[q] = p->sendb + (long long)q * p->P * bk;
+        }
+        p->fused = true;
+        return USP_OK;
+    }
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        long long off_recv, off_send;
+        long long ok;
+    } mine{};
+    CUdeviceptr base = 0;
+    size_t sz = 0;
+    AddrRangeFn ar = addr_range_fn();
+    if (ar && ar(&base, &sz, (CUdeviceptr)p->ws) == CUDA_SUCCESS &&
+        cudaIpcGetMemHandle(&mine.h, (void *)base) == cudaSuccess) {
+        mine.off_recv = (long long)((char *)p->recvb - (char *)base);
+        mine.off_send = (long long)((char *)p->sendb - (char *)base);
+        mine.ok = 1;
+    }
+    cudaGetLastError();   // clear a failed IPC query
+    Rec *d = reinterpret_cast<Rec *>(p->coll + 16);   // scratch: 8 x 88 bytes fits the 192 doubles
+    CU(cudaMemcpyAsync(d, &mine, sizeof(Rec), cudaMemcpyHostToDevice, p->stream));
+    NC(nccl().AllGather(d, d + 1, sizeof(Rec), ncclChar, p->comm, p->stream));
+    std::vector<Rec> all(p->P);
+    CU(cudaMemcpyAsync(all.data(), d + 1, sizeof(Rec) * p->P, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    bool ok = true;
+    for (auto &r : all) ok = ok && r.ok;
+    double good = 1.0;
+    if (ok) {
+        for (int q = 0; q < p->P; ++q) {
+            if (q == p->rank) {
+                p->peer_recv[q] = p->recvb;
+                p->peer_send[q] = p->sendb;
+                continue;
+            }
+            void *pb = nullptr;
+            if (cudaIpcOpenMemHandle(&pb, all[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                cudaGetLastError();
+                good = 0.0;
+                break;
+            }
+            p->ipc_bases.push_back(pb);
+            p->peer_recv[q] = (float2 *)((char *)pb + all[q].off_recv);
+            p->peer_send[q] = (float2 *)((char *)pb + all[q].off_send);
+        }
+    } else {
+        good = 0.0;
+    }
+    // consensus: fused only if every rank mapped every peer
+    CU(cudaMemcpyAsync(p->coll + 2, &good, sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    NC(nccl().AllReduce(p->coll + 2, p->coll + 2, 1, ncclDouble, ncclMin, p->comm, p->stream));
+    CU(cudaMemcpyAsync(&good, p->coll + 2, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    if (good == 1.0) p->fused = true;
+    else close_peers(p);
+    return USP_OK;
+}
+
+// Cross-rank barrier on the plan stream (fused transposes: the peers' stores
+// into this rank's buffers are complete before the next kernel reads them).
+usp_status rank_barrier(usp_plan_s *p) {
+    if (!multi_rank(p)) return USP_OK;
+    Tick t(p, KC_BARRIER, false);
+    NC(nccl().AllReduce(p->coll + 3, p->coll + 3, 1, ncclDouble, ncclSum, p->comm, p->stream));
+    return USP_OK;
+}
+
 // The two transposes of the slab decomposition.  Block (r, q) of the send
 // layout holds slab r's rows for y block q; block (r, q) of the receive
 // layout holds y block r's planes of slab q.  forward: recv(r,q) <- send(q,r);
@@ -602,6 +709,27 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
     }
     // slab decomposition: K_B -> transpose -> K_C -> transpose -> K_D
     const long long pv = p->virt ? p->P : 1;   // y blocks held here
+    if (p->fused) {   // transposes fused into the K_B / K_C stores (peer memory)
+        const int rank0 = p->virt ? 0 : p->rank;
+        SParams yb = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, p->nzh, p->rp * p->ny, 1, check_state, 3);
+        yb.peer_mode = 1;
+        yb.rank0 = rank0;
+        yb.bk = p->nzs * p->nyl * p->rp;
+        for (int q = 0; q < p->P; ++q) yb.peer[q] = p->peer_recv[q];
+        SParams zm = sparams(p, p->recvb, p->recvb, p->tw[2], p->nyl * p->rp, p->nyl * p->rp, pv,
+                             p->nz * p->nyl * p->rp, 2, check_state, 2);
+        zm.y0 = p->virt ? 0 : (long long)p->rank * p->nyl;
+        zm.peer_mode = 2;
+        zm.rank0 = rank0;
+        zm.bk = yb.bk;
+        for (int q = 0; q < p->P; ++q) zm.peer[q] = p->peer_send[q];
+        SParams yd = sparams(p, p->sendb, p->work, p->tw[1], p->rp, p->rp, p->nzh, p->rp * p->ny, 1, check_state, 5);
+        if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0))) return s;
+        if ((s = rank_barrier(p))) return s;
+        if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, true, 0))) return s;
+        if ((s = rank_barrier(p))) return s;
+        return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_kd, true, 0);
+    }
     SParams yb = sparams(p, p->work, p->sendb, p->tw[1], p->rp, p->rp, p->nzh, p->rp * p->ny, 1, check_state, 3);
     yb.send_layout = 1;
     SParams zm = sparams(p, p->recvb, p->recvb, p->tw[2], p->nyl * p->rp, p->nyl * p->rp, pv,
@@ -933,7 +1061,7 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     build_maps(p);
     if (p->P > 1 && !(p->stile_y && p->stile_z))
         return fail(USP_ERR_CUDA, "could not encode the tensor maps of the slab decomposition");
-    return USP_OK;
+    return setup_peers(p);
 }
 
 usp_status usp_local_extent(usp_plan_t p, int64_t *z0, int64_t *nz_local) {
@@ -1208,6 +1336,7 @@ void usp_plan_destroy(usp_plan_t p) {
     if (!p) return;
     cudaStreamSynchronize(p->stream);
     drain_timing(p);
+    close_peers(p);
     for (auto e : p->ev_pool) cudaEventDestroy(e);
     cudaFree(p->st);
     cudaFree(p->partials);

@@ -71,6 +71,7 @@ struct XParams {
 };
 
 // ---------------------------------------------------------- strided pass --
+constexpr int kMaxPeers = 8;   // ranks of a fused (peer-memory) slab decomposition
 enum SMode : int { S_FWD = 0, S_INV = 1, S_FWD_MUL_INV = 2 };
 
 struct SParams {
@@ -96,6 +97,15 @@ struct SParams {
     long long y0;        // global y of this rank's y block (z pass multiplier)
     long long o0;        // first outer index (plane) of this launch (chunked schedule)
     int store_hint;      // 0: plain stores; 1: evict_last (K_D: K_A re-reads from L2); 2: evict_first
+    // transposes fused into the stores (slab decomposition, peer memory):
+    // 1 = K_B stores into the ranks' receive buffers, 2 = K_C stores into the
+    // ranks' send buffers; peer[q] = rank q's buffer (this GPU's own for q = rank,
+    // CUDA-IPC-mapped peer memory over NVLink for the others, or the virtual
+    // ranks' regions of one buffer)
+    int peer_mode;
+    int rank0;           // rank of this plan's first slab / y block (NCCL: the rank; virtual: 0)
+    long long bk;        // elements per transpose block (nz_loc * ny_loc * row pitch)
+    float2 *peer[kMaxPeers];
 };
 
 // ------------------------------------------------------------------ 1-D --

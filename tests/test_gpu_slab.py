@@ -38,12 +38,17 @@ def _run(p, n, virtual_ranks, tol=0.0):
     return plan.get_field().cpu().numpy(), nd, term, plan
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("name,shape,P,n", [("C3", (64, 64, 64), 2, 40), ("C3", (128, 64, 64), 4, 30),
                                             ("C5", (64, 128, 64), 8, 20), ("C4", (64, 64, 128), 2, 30),
-                                            ("C3", (256, 128, 64), 2, 10)])
-def test_virtual_slabs_bit_identical_to_one_slab(name, shape, P, n):
+                                            ("C3", (256, 128, 64), 2, 10), ("C3", (64, 64, 64), 16, 10)])
+def test_virtual_slabs_bit_identical_to_one_slab(name, shape, P, n, fused, monkeypatch):
+    """fused = transposes in the K_B / K_C stores (peer-memory path; P <= 8);
+    0 = separate transposes (device copies standing in for the NCCL
+    all-to-alls)."""
     from synth import make
 
+    monkeypatch.setenv("USP_FUSED", fused)
     p = make(name, shape)
     x1, n1, _, pl1 = _run(p, n, 0)
     xp, n_p, _, plp = _run(p, n, P)
