@@ -14,6 +14,8 @@ What it computes (PAPER.md = /root/reference/PAPER.md):
   max|V| = target_norm (L99, L167).
 * ``fixed_point``                  -- Algorithm 1 (L80-89), x-form, or the
   Delta-form recurrence (L613) for the R-17 cross-check.
+* ``bicgstab``                     -- BiCGSTAB on the preconditioned system
+  Gamma^-1 A x = Gamma^-1 s, Eq. 5 (L73-76) -- Table 1b's BiCGSTAB column.
 
 Pins: see tests/test_oracle_*.py.  Parity status per function is listed in
 DESIGN.md ("Oracle and its pins"); every function here is pinned.
@@ -58,6 +60,9 @@ def lib():
                                       + [ctypes.c_double, ctypes.c_double, ctypes.c_long, ctypes.c_int,
                                          dp, dp, lp, dp])
         L.orc_mec.argtypes = [dp, dp, ctypes.c_long, dp, dp, dp]
+        L.orc_bicgstab.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 4
+                                   + [ctypes.c_double, ctypes.c_long, dp, dp, lp, dp,
+                                      ctypes.POINTER(ctypes.c_int)])
         L.orc_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -202,6 +207,37 @@ def fixed_point(w, S, h: Sequence[float], D: float, sigma: complex, c: complex, 
     if rc < 0:
         raise ValueError(f"orc_fixed_point rc={rc}")
     return Result(x=x, n_done=int(nd.value), hist=hist[: nd.value].copy(), n0=float(n0.value), rc=rc)
+
+
+@dataclass
+class KrylovResult:
+    x: np.ndarray
+    n_done: int          # BiCGSTAB loop passes (two applications of M each)
+    half: bool           # stopped after the half step (||s|| < tol)
+    hist: np.ndarray     # [||s_0||, ||r_1||, ||s_1||, ...] / ||b||
+    nb: float            # ||b|| = ||B (L+1)^-1 s||
+    rc: int
+
+
+def bicgstab(w, S, h: Sequence[float], D: float, sigma: complex, c: complex, tol: float,
+             n_max: int) -> KrylovResult:
+    """BiCGSTAB on M x = b with M = B[1 - (L+1)^-1 B] (Eq. 5 with alpha = 1,
+    reading R-25), b = B (L+1)^-1 s, x_0 = 0 (see usp_oracle.c)."""
+    wc, Sc = _c128(w), _c128(S)
+    x = np.zeros_like(wc)
+    hist = np.zeros(2 * n_max, dtype=np.float64)
+    hh = np.ascontiguousarray(h, dtype=np.float64)
+    nd, nb, half = ctypes.c_long(0), ctypes.c_double(0.0), ctypes.c_int(0)
+    rc = lib().orc_bicgstab(_dp(wc.view(np.float64)), _dp(Sc.view(np.float64)), wc.ndim, _dims(wc.shape),
+                            _dp(hh), float(D), float(np.real(sigma)), float(np.imag(sigma)),
+                            float(np.real(c)), float(np.imag(c)), float(tol), int(n_max),
+                            _dp(x.view(np.float64)), _dp(hist), ctypes.byref(nd), ctypes.byref(nb),
+                            ctypes.byref(half))
+    if rc < 0:
+        raise ValueError(f"orc_bicgstab rc={rc}")
+    k = int(nd.value)
+    nh = 2 * k - 1 if half.value else 2 * k
+    return KrylovResult(x=x, n_done=k, half=bool(half.value), hist=hist[:nh].copy(), nb=float(nb.value), rc=rc)
 
 
 def solve_problem(p, target_norm: float = 0.95, form: str = "x", n_iter: Optional[int] = None,

@@ -31,6 +31,10 @@
  *                 (the Delta-form) for the R-17 cross-check.
  *   orc_mec       smallest enclosing circle ("smallest circle
  *                 problem"), Welzl's randomised incremental algorithm.
+ *   orc_bicgstab  BiCGSTAB [van der Vorst 1992, cited PAPER.md L384] on the
+ *                 preconditioned system Gamma^-1 A x = Gamma^-1 s with
+ *                 Gamma^-1 A = alpha B[1 - (L+1)^-1 B] (Eq. 5, PAPER.md
+ *                 L73-76); the "BiCGSTAB" column of Table 1b (L305-311).
  *
  * Error behaviour: every entry point returns 0 on success, a negative code on
  * bad arguments (-1 non-power-of-two extent, -2 bad ndim/size, -3 alloc).
@@ -288,6 +292,115 @@ int orc_fixed_point(const double *w, const double *S, int ndim, const long *dims
     }
 done:
     free(B); free(s); free(u); free(Dl);
+    return rc;
+}
+
+/* --------------------------------------------------------- BiCGSTAB -- */
+/*
+ * M u = B [u - (L+1)^-1 (B u)]: the preconditioned operator Gamma^-1 A of
+ * Eq. 5 with alpha = 1 (a Krylov method's iterates do not
+ * depend on a scalar factor of the system; reading R-25).
+ */
+static int apply_M(const cplx *B, const cplx *u, cplx *out, cplx *tmp, long n, int ndim, const long *dims,
+                   const double *h, double D, double sig_re, double sig_im, double c_re, double c_im) {
+    for (long i = 0; i < n; ++i) tmp[i] = B[i] * u[i];
+    int rc = orc_apply_Linv((double *)tmp, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+    if (rc) return rc;
+    for (long i = 0; i < n; ++i) out[i] = B[i] * (u[i] - tmp[i]);
+    return 0;
+}
+
+/* (a, b) = sum conj(a_i) b_i in a fixed sequential order */
+static cplx dotc(const cplx *a, const cplx *b, long n) {
+    cplx acc = 0.0;
+    for (long i = 0; i < n; ++i) acc += conj(a[i]) * b[i];
+    return acc;
+}
+
+/*
+ * BiCGSTAB (van der Vorst 1992; the unpreconditioned form of Saad,
+ * "Iterative Methods for Sparse Linear Systems", Alg. 7.7, complex with
+ * conjugated inner products) on M x = b, b = B (L+1)^-1 s (Gamma^-1 s with
+ * alpha = 1), x_0 = 0, shadow residual rhat = r_0 = b:
+ *     rho = (rhat, r); p = r
+ *     loop j = 0, 1, ...
+ *        v = M p;  a = rho / (rhat, v);  s = r - a v
+ *        if ||s|| / ||b|| < tol: x += a p; stop          (half step)
+ *        t = M s;  w = (t, s) / (t, t)
+ *        x += a p + w s;  r = s - w t
+ *        if ||r|| / ||b|| < tol: stop
+ *        rho' = (rhat, r);  beta = (rho'/rho)(a/w);  p = r + beta (p - w v)
+ * The residual is r = b - M x: the same quantity as Algorithm 1's Delta
+ * (reading R-4), so the stopping test is comparable.  n_done counts loop
+ * passes (each two applications of M); hist[2j] = ||s_j||/||b||,
+ * hist[2j+1] = ||r_{j+1}||/||b|| (hist needs 2 n_max entries).  tol <= 0
+ * runs exactly n_max passes.  Returns 0, 1 non-finite residual, 2 breakdown
+ * (rho, (rhat, v) or (t, t) exactly 0), negative on argument errors.
+ */
+int orc_bicgstab(const double *w, const double *S, int ndim, const long *dims, const double *h, double D,
+                 double sig_re, double sig_im, double c_re, double c_im, double tol, long n_max,
+                 double *x_out, double *hist, long *n_done, double *nb_out, int *half) {
+    if (ndim < 1 || ndim > 3 || n_max < 1) return -2;
+    long n = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (!is_pow2(dims[a])) return -1;
+        n *= dims[a];
+    }
+    size_t bytes = sizeof(cplx) * (size_t)n;
+    cplx *B = malloc(bytes), *sv = malloc(bytes), *r = malloc(bytes), *rh = malloc(bytes), *p = malloc(bytes);
+    cplx *v = malloc(bytes), *sr = malloc(bytes), *t = malloc(bytes), *tmp = malloc(bytes);
+    cplx *x = (cplx *)x_out;
+    int rc = 0;
+    *n_done = 0;
+    *half = 0;
+    if (!B || !sv || !r || !rh || !p || !v || !sr || !t || !tmp) { rc = -3; goto done; }
+    orc_setup(w, S, n, sig_re, sig_im, c_re, c_im, NULL, (double *)B, (double *)sv);
+    /* b = B (L+1)^-1 s; r_0 = b (x_0 = 0) */
+    memcpy(tmp, sv, bytes);
+    rc = orc_apply_Linv((double *)tmp, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+    if (rc) goto done;
+    for (long i = 0; i < n; ++i) { r[i] = B[i] * tmp[i]; rh[i] = r[i]; p[i] = r[i]; x[i] = 0.0; }
+    double nb = norm2(r, n);
+    if (nb_out) *nb_out = nb;
+    if (nb == 0.0) goto done;
+    cplx rho = dotc(rh, r, n);
+    for (long j = 0; j < n_max; ++j) {
+        if (rho == 0.0) { rc = 2; goto done; }
+        rc = apply_M(B, p, v, tmp, n, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+        if (rc) goto done;
+        cplx rv = dotc(rh, v, n);
+        if (rv == 0.0) { rc = 2; goto done; }
+        cplx a = rho / rv;
+        for (long i = 0; i < n; ++i) sr[i] = r[i] - a * v[i];
+        double rs = norm2(sr, n) / nb;
+        if (hist) hist[2 * j] = rs;
+        *n_done = j + 1;
+        if (!isfinite(rs)) { rc = 1; goto done; }
+        if (tol > 0.0 && rs < tol) {
+            for (long i = 0; i < n; ++i) x[i] += a * p[i];
+            *half = 1;
+            goto done;
+        }
+        rc = apply_M(B, sr, t, tmp, n, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+        if (rc) goto done;
+        cplx tt = dotc(t, t, n);
+        if (tt == 0.0) { rc = 2; goto done; }
+        cplx om = dotc(t, sr, n) / tt;
+        for (long i = 0; i < n; ++i) {
+            x[i] += a * p[i] + om * sr[i];
+            r[i] = sr[i] - om * t[i];
+        }
+        double rr = norm2(r, n) / nb;
+        if (hist) hist[2 * j + 1] = rr;
+        if (!isfinite(rr)) { rc = 1; goto done; }
+        if (tol > 0.0 && rr < tol) goto done;
+        cplx rho1 = dotc(rh, r, n);
+        cplx beta = (rho1 / rho) * (a / om);
+        for (long i = 0; i < n; ++i) p[i] = r[i] + beta * (p[i] - om * v[i]);
+        rho = rho1;
+    }
+done:
+    free(B); free(sv); free(r); free(rh); free(p); free(v); free(sr); free(t); free(tmp);
     return rc;
 }
 
