@@ -235,6 +235,37 @@ def run_reference(args, world, rank):
 
 
 # -------------------------------------------------------------------- GPU --
+def solver_comparison(dev, name="C3", tol=1e-6):
+    """Time to tolerance of the two solvers on one config (Table 1b analogue
+    on B200): the fixed-point iteration (Alg. 1, alpha = 0.75) and BiCGSTAB
+    on the same preconditioned system (NEXT-2), device-timed."""
+    import torch
+    from paper_2207_14222_b200 import Plan
+    from synth import make
+
+    p = make(name, None, device=str(dev))
+    med, src = p.medium.to(torch.complex64), p.source.to(torch.complex64)
+    stream = torch.cuda.Stream(device=dev)
+    out = {"config": name, "grid": list(p.shape), "tol": tol}
+    with torch.cuda.stream(stream):
+        plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev)
+        for solver in ("fixed_point", "bicgstab", "fixed_point", "bicgstab"):   # 2nd round timed
+            plan.set_potential(med, 0.95)
+            plan.set_source(src)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            if solver == "fixed_point":
+                n, term = plan.iterate(20000, p.alpha, tol)
+            else:
+                n, term = plan.bicgstab(5000, tol)
+            b.record(stream)
+            torch.cuda.synchronize()
+            out[solver] = {"count": n, "term": term, "ms": round(a.elapsed_time(b), 3),
+                           "count_unit": "iterations" if solver == "fixed_point" else "passes (2 x (L+1)^-1)"}
+        plan.close()
+    return out
+
+
 def slab_selfcheck(comm, world, rank, dev, n_iter=8, shape=(128, 128, 128)):
     """Constant V through the decomposed path: x^_k = x^*(1 - q^k) per
     Fourier mode (the closed form of tests/test_gpu_parity.py).  Returns the
@@ -407,6 +438,11 @@ def run_usp(args, world, rank, local):
 
     if rank != 0:
         return 0
+    solvers = None
+    if world == 1 and not args.no_solvers and name == "C5":
+        del plan
+        torch.cuda.empty_cache()
+        solvers = solver_comparison(dev)
     cpu = None
     if world == 1 and not args.no_cpu:
         v, dt, thr, desc = cpu_oracle_sample()
@@ -443,6 +479,7 @@ def run_usp(args, world, rank, local):
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "solvers_to_tol": solvers,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -461,6 +498,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
+    ap.add_argument("--no-solvers", action="store_true", help="skip the C3 fixed-point vs BiCGSTAB comparison")
     ap.add_argument("--virtual-ranks", type=int, default=0,
                     help="N=1: run the slab-decomposed path with this many virtual slabs (measurement)")
     args = ap.parse_args()

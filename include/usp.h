@@ -187,6 +187,26 @@ usp_status usp_residual_history(usp_plan_t plan, double *host, int64_t cap, int6
 /* Copy the current iterate x_k into `out` ([z][y][x], desc.dtype). */
 usp_status usp_get_field(usp_plan_t plan, void *out, usp_where where);
 
+/* BiCGSTAB on the preconditioned system (PAPER.md
+ * Eq. 5 L73-76 and Table 1b, van der Vorst 1992):
+ *     M x = b,   M = B [1 - (L+1)^-1 B]  (Gamma^-1 A with alpha = 1; the
+ *     iterates do not depend on alpha, R-25),  b = B (L+1)^-1 s,
+ * x_0 = 0, shadow residual rhat = r_0 = b.  A pass is two applications of M
+ * (the fixed-point path's FFT passes).  Stops when ||s||/||b|| < tol after
+ * the half step (then x += a p) or ||r||/||b|| < tol after the full step
+ * (r = b - M x, the fixed-point path's Delta, reading R-4); tol <= 0 runs
+ * exactly n_max passes.  n_done = passes; usp_residual / _history report
+ * ||r_k|| / ||b|| per pass.  Needs a Krylov workspace (5 complex64 fields:
+ * rhat, p, v, s, t; 40 bytes per voxel, caller-owned, 256-B aligned) and
+ * the state right after usp_set_source (not resumable).  2-D / 3-D
+ * complex64 plans on one GPU (incl. virtual slabs).
+ * Errors: USP_ERR_STATE, USP_ERR_ARG, USP_ERR_UNSUPPORTED, USP_ERR_NOMEM;
+ * term = USP_DIVERGED also on a BiCGSTAB breakdown (rho, (rhat, v) or (t, t)
+ * exactly 0). */
+usp_status usp_krylov_workspace_size(usp_plan_t plan, size_t *bytes);
+usp_status usp_krylov_set_workspace(usp_plan_t plan, void *dev, size_t bytes);
+usp_status usp_bicgstab(usp_plan_t plan, int64_t n_max, double tol, int64_t *n_done, usp_term *term);
+
 /* Kernel timing (CUDA events on the plan stream, per kernel class) for the
  * roofline report.  enable != 0 starts accumulating; usp_profile_read copies
  * up to cap entries of (name, total ms, launches) for the kernel classes. */

@@ -125,10 +125,12 @@ Nccl &nccl() {
     } while (0)
 
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
-              KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_BARRIER, KC_N };
+              KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_BARRIER, KC_XOP,
+              KC_KUPD, KC_N };
 const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
                               "solve1d", "potential", "farthest", "set_state", "xpass_setup",
-                              "all_to_all", "finish", "allgather", "rank_barrier"};
+                              "all_to_all", "finish", "allgather", "rank_barrier", "krylov_xop",
+                              "krylov_update"};
 
 struct Timed {
     int cls;
@@ -165,6 +167,9 @@ struct usp_plan_s {
     bool fused = false;
     float2 *peer_recv[kMaxPeers] = {}, *peer_send[kMaxPeers] = {};
     std::vector<void *> ipc_bases;   // peer allocations mapped with cudaIpcOpenMemHandle
+    // BiCGSTAB (caller-owned Krylov workspace: rhat, p, v, s, t)
+    float2 *k_rh = nullptr, *k_p = nullptr, *k_v = nullptr, *k_s = nullptr, *k_t = nullptr;
+    KState *ks = nullptr;
     // plan-owned small device memory
     IterState *st = nullptr;
     double *partials = nullptr;
@@ -983,7 +988,8 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         const int u = p->real ? xreal_lines_per_unit((int)p->nx) : 32 / (1 << (log2ll(p->nx) / 2));
         p->gridp_x = occ_grid(p, xl / u, 1);   // one CTA per SM, persistent over the warp units
     }
-    p->partials_cap = std::max(1, std::max(p->grid_x, p->gridp_x));
+    // reduction partials: <= 3 doubles per CTA of the largest reducing grid
+    p->partials_cap = 3 * std::max(std::max(p->grid_x, p->gridp_x), p->nsm * 8);
     p->far_cap = p->nsm * 8;
     std::vector<float2> twh[3];
     const long long ext[3] = {p->nx, p->ny, p->nz};
@@ -1002,6 +1008,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->far_d, sizeof(double) * p->far_cap));
     TRY(cudaMalloc(&p->far_i, sizeof(long long) * p->far_cap));
     TRY(cudaMalloc(&p->coll, sizeof(double) * (16 + 3 * 64)));
+    TRY(cudaMalloc(&p->ks, sizeof(KState)));
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
         const int n = (int)p->nx, m = n / 2;
@@ -1298,6 +1305,113 @@ usp_status usp_get_field(usp_plan_t p, void *out, usp_where where) {
     return USP_OK;
 }
 
+usp_status usp_krylov_workspace_size(usp_plan_t p, size_t *bytes) {
+    if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
+    *bytes = 5 * align256((size_t)p->nloc * sizeof(float2));
+    return USP_OK;
+}
+
+usp_status usp_krylov_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
+    if (!p || !dev) return fail(USP_ERR_ARG, "NULL argument");
+    if (((uintptr_t)dev) & 255) return fail(USP_ERR_ARG, "Krylov workspace must be 256-byte aligned");
+    size_t need = 0;
+    usp_krylov_workspace_size(p, &need);
+    if (bytes < need) return fail(USP_ERR_NOMEM, "Krylov workspace %zu bytes < required %zu", bytes, need);
+    const size_t f = align256((size_t)p->nloc * sizeof(float2));
+    char *b = (char *)dev;
+    p->k_rh = (float2 *)b;
+    p->k_p = (float2 *)(b + f);
+    p->k_v = (float2 *)(b + 2 * f);
+    p->k_s = (float2 *)(b + 3 * f);
+    p->k_t = (float2 *)(b + 4 * f);
+    return USP_OK;
+}
+
+usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, usp_term *term) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
+    if (!p->k_rh) return fail(USP_ERR_STATE, "usp_krylov_set_workspace must be called first");
+    if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
+    if (p->ndim < 2 || p->real || multi_rank(p) || !p->pipe_xk)
+        return fail(USP_ERR_UNSUPPORTED, "BiCGSTAB runs on 2-D / 3-D complex64 plans on one GPU");
+    usp_status s = sync_state(p);
+    if (s) return s;
+    if (p->st_host->k != 0)
+        return fail(USP_ERR_STATE, "BiCGSTAB starts from x_0 = 0: call usp_set_source again first");
+    const long long nvb = (long long)p->nloc * sizeof(float2);
+    // r = b = Delta_0 (the fixed-point setup left it in `delta`), rhat = r, p = v = 0
+    CU(cudaMemcpyAsync(p->k_rh, p->delta, nvb, cudaMemcpyDeviceToDevice, p->stream));
+    CU(cudaMemsetAsync(p->k_p, 0, nvb, p->stream));
+    CU(cudaMemsetAsync(p->k_v, 0, nvb, p->stream));
+    KState k0{};
+    const double nb = p->st_host->n0;
+    k0.rho = make_double2(nb * nb, 0.0);
+    k0.omega = make_double2(1.0, 0.0);
+    k0.nb = nb;
+    CU(cudaMemcpyAsync(p->ks, &k0, sizeof k0, cudaMemcpyHostToDevice, p->stream));
+    {
+        Tick t(p, KC_SETSTATE);
+        CU(launch_set_state(p->st, 1.0, tol, n_max, p->stream));
+    }
+    KParams kp{};
+    kp.work = p->work;
+    kp.x = p->x;
+    kp.r = p->delta;
+    kp.rh = p->k_rh;
+    kp.p = p->k_p;
+    kp.v = p->k_v;
+    kp.s = p->k_s;
+    kp.t = p->k_t;
+    kp.B = p->B;
+    kp.tw = p->tw[0];
+    kp.nlines = p->ny * p->nzh;
+    kp.nvox = p->nloc;
+    kp.st = p->st;
+    kp.ks = p->ks;
+    kp.partials = p->partials;
+    kp.hist = p->hist;
+    kp.hist_cap = p->hist_cap;
+    const int gx = p->gridp_x, gu = occ_grid(p, (p->nloc + 255) / 256, 8);
+    auto xop = [&](KMode m) -> usp_status {
+        Tick t(p, KC_XOP);
+        CU(launch_xop((int)p->nx, m, kp, gx, p->stream));
+        return USP_OK;
+    };
+    const long long batch = 8;
+    long long launched = 0;
+    while (launched < n_max) {
+        const long long nb_ = std::min(batch, n_max - launched);
+        for (long long i = 0; i < nb_; ++i) {
+            if ((s = xop(K_PFWD))) return s;
+            if ((s = chain_mid(p, 1))) return s;
+            if ((s = xop(K_VINV))) return s;
+            if ((s = xop(K_SFWD))) return s;
+            if ((s = chain_mid(p, 1))) return s;
+            if ((s = xop(K_TINV))) return s;
+            {
+                Tick t(p, KC_KUPD);
+                CU(launch_kupd(kp, gu, p->stream));
+            }
+        }
+        launched += nb_;
+        if (tol > 0.0) {
+            if ((s = sync_state(p))) return s;
+            const int stt = p->st_host->status;
+            if (stt == ST_DONE_CONV || stt == ST_DIVERGED) break;
+        }
+    }
+    if ((s = sync_state(p))) return s;
+    drain_timing(p);
+    const IterState &h = *p->st_host;
+    if (n_done) *n_done = h.k;
+    if (term) {
+        if (h.status == ST_DONE_CONV) *term = USP_CONVERGED;
+        else if (h.status == ST_DIVERGED) *term = USP_DIVERGED;
+        else *term = USP_MAX_ITER;
+    }
+    return USP_OK;
+}
+
 usp_status usp_profile_enable(usp_plan_t p, int enable) {
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     drain_timing(p);
@@ -1345,6 +1459,7 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->far_d);
     cudaFree(p->far_i);
     cudaFree(p->coll);
+    cudaFree(p->ks);
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
     cudaFree(p->twr);
     cudaFreeHost(p->st_host);

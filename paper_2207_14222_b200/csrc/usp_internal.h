@@ -70,6 +70,29 @@ struct XParams {
     int l2hint;          // chunked schedule: stream Delta/x/B evict_first, keep work evict_last
 };
 
+// ------------------------------------------------------- BiCGSTAB (NEXT-2) --
+enum KMode : int { K_PFWD = 0, K_VINV = 1, K_SFWD = 2, K_TINV = 3 };
+
+struct KState {          // BiCGSTAB scalars (fp64, device)
+    double2 rho, alpha, omega, beta;
+    double nb;           // ||b|| = ||B (L+1)^-1 s|| (= n0 of the fixed-point iteration)
+    double res_s;        // ||s|| / ||b|| of the current pass (half-step test)
+    int breakdown;       // rho, (rhat, v) or (t, t) became exactly 0
+};
+
+struct KParams {
+    float2 *work, *x, *r, *rh, *p, *v, *s, *t;
+    const float2 *B;
+    const float2 *tw;    // four-step twiddles for nx
+    long long nlines;    // ny * nz
+    long long nvox;
+    IterState *st;
+    KState *ks;
+    double *partials;    // >= 3 doubles per CTA
+    double *hist;
+    int hist_cap;
+};
+
 // ---------------------------------------------------------- strided pass --
 constexpr int kMaxPeers = 8;   // ranks of a fused (peer-memory) slab decomposition
 enum SMode : int { S_FWD = 0, S_INV = 1, S_FWD_MUL_INV = 2 };
@@ -144,6 +167,10 @@ struct FarParams {       // farthest medium value from a centre (smallest circle
     double *best_d2;     // per CTA
     long long *best_idx; // per CTA
 };
+
+// BiCGSTAB (kernels_krylov.cu)
+cudaError_t launch_xop(int N, KMode mode, const KParams &p, int grid, cudaStream_t s);
+cudaError_t launch_kupd(const KParams &p, int grid, cudaStream_t s);
 
 // real path (kernels_real.cu)
 cudaError_t launch_xpass_real(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);

@@ -130,6 +130,23 @@ class Plan:
                                      ctypes.byref(term)))
         return int(nd.value), _TERM[term.value]
 
+    def bicgstab(self, n_max: int, tol: float = 0.0) -> Tuple[int, str]:
+        """BiCGSTAB on the preconditioned system (usp_bicgstab); starts from
+        x_0 = 0 right after set_source.  Allocates the Krylov workspace (5
+        complex64 fields) on first use.  Returns (passes, termination)."""
+        import torch
+
+        if getattr(self, "kworkspace", None) is None:
+            nbytes = ctypes.c_size_t()
+            L.check(self.lib.usp_krylov_workspace_size(self.handle, ctypes.byref(nbytes)))
+            self.kworkspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+            L.check(self.lib.usp_krylov_set_workspace(self.handle, ctypes.c_void_p(self.kworkspace.data_ptr()),
+                                                      int(nbytes.value)))
+        nd = ctypes.c_int64()
+        term = ctypes.c_int()
+        L.check(self.lib.usp_bicgstab(self.handle, int(n_max), float(tol), ctypes.byref(nd), ctypes.byref(term)))
+        return int(nd.value), _TERM[term.value]
+
     def residual(self) -> Tuple[float, float, int]:
         r, a, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
         L.check(self.lib.usp_residual(self.handle, ctypes.byref(r), ctypes.byref(a), ctypes.byref(k)))

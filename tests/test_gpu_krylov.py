@@ -1,0 +1,135 @@
+"""GPU parity of BiCGSTAB on the preconditioned system (usp_bicgstab;
+SURVEY.md §8(f) NEXT-2, Eq. 5, Table 1b) against the oracle's
+orc_bicgstab on the same complex64-rounded inputs.
+
+BiCGSTAB's iterates are not forward-stable: on a hard problem (C2, erratic
+residual) the complex64 and complex128 runs drift apart after a few passes
+(measured 1.9e-2 after 20 passes at 128^2) while both converge to the same
+solution.  So the iterate-level bar (1e-4 after the same count) is applied
+where the recurrence is well conditioned (C3, all passes) and to the first
+passes of C2; on C2 the bar is the CONVERGED field (unique: A^-1 s) and a
+pass count within 5 % (measured 639 vs 619 passes to 1e-6 at 512^2).  On
+C3 the pass counts to 1e-4..1e-6 are identical (R-25)."""
+import math
+
+import numpy as np
+import pytest
+
+from gpu_helpers import TOL_FIELD, rel_l2, rounded_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA GPU required for -m gpu tests")
+
+
+def _gpu(p, n, tol, virtual_ranks=0):
+    import torch
+    from paper_2207_14222_b200 import Plan
+
+    med, src, dtype = rounded_inputs(p)
+    plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype, virtual_ranks=virtual_ranks)
+    plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
+    plan.set_source(torch.from_numpy(src).cuda())
+    nd, term = plan.bicgstab(n, tol)
+    return plan.get_field().cpu().numpy().astype(np.complex128), nd, term, plan
+
+
+def _orc(orc, p, n, tol):
+    med, src, _ = rounded_inputs(p)
+    med64 = med.astype(np.complex128)
+    sp = orc.canonical(p.kind, med64, 0.95, D=p.D)
+    return orc.bicgstab(orc.medium_to_w(p.kind, med64), src.astype(np.complex128), p.h, sp.D, sp.sigma, sp.c,
+                        tol, n)
+
+
+@pytest.mark.parametrize("name,shape,n", [("C3", (64, 64, 64), 20), ("C2", (128, 128), 3),
+                                          ("C2", (512, 512), 3), ("C5", (32, 64, 128), 12),
+                                          ("C3", (64, 32, 16), 20)])
+def test_bicgstab_fixed_passes_match_oracle(orc, name, shape, n):
+    from synth import make
+
+    p = make(name, shape)
+    x, nd, term, plan = _gpu(p, n, 0.0)
+    assert nd == n and term == "max_iter"
+    ref = _orc(orc, p, n, 0.0)
+    assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)
+    h = plan.history()[1:n + 1]                       # ||r_k|| / ||b||, k = 1..n
+    assert np.allclose(h, ref.hist[1::2][:n], rtol=2e-3, atol=1e-7)
+
+
+@pytest.mark.parametrize("name,shape,tol", [("C3", (64, 64, 64), 1e-5), ("C3", (64, 64, 64), 1e-6),
+                                            ("C2", (128, 128), 1e-6), ("C2", (512, 512), 1e-6)])
+def test_bicgstab_converges_like_oracle(orc, name, shape, tol):
+    from synth import make
+
+    p = make(name, shape)
+    x, nd, term, plan = _gpu(p, 3000, tol)
+    ref = _orc(orc, p, 3000, tol)
+    assert term == "converged" and ref.rc == 0
+    if name == "C3":
+        assert abs(nd - ref.n_done) <= 1, (nd, ref.n_done)
+    else:
+        assert abs(nd - ref.n_done) <= 0.05 * ref.n_done, (nd, ref.n_done)
+    assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)
+
+
+def test_bicgstab_virtual_slabs_bit_identical():
+    from synth import make
+
+    p = make("C3", (64, 64, 64))
+    x1, _, _, p1 = _gpu(p, 8, 0.0)
+    x2, _, _, p2 = _gpu(p, 8, 0.0, virtual_ranks=4)
+    assert np.array_equal(x1, x2) and np.array_equal(p1.history(), p2.history())
+
+
+@pytest.mark.parametrize("shape", [(32, 64), (16, 32, 64)])
+def test_bicgstab_single_mode_half_step(shape):
+    """Constant V + one Fourier mode: M p = lambda p, s = 0 after the first
+    half step; x = g s^/(1 - b g) (the oracle pin, on the GPU)."""
+    import torch
+    from paper_2207_14222_b200 import Plan
+
+    k0, nn = 2 * math.pi / 8, 1.0 + 0.05j
+    k2 = (k0 * nn) ** 2
+    sigma, c, D = -k2.real, -1j * abs(k2.imag) / 0.95, 1.0
+    grids = np.meshgrid(*[np.arange(s) for s in shape], indexing="ij")
+    m = [1 + a for a in range(len(shape))]
+    S = np.exp(1j * sum(2 * np.pi * mi * gi / s for mi, gi, s in zip(m, grids, shape))).astype(np.complex64)
+    plan = Plan(shape, sigma=sigma, c=c)
+    plan.set_potential(torch.full(shape, k2, dtype=torch.complex64, device="cuda"), -1.0)
+    plan.set_source(torch.from_numpy(S).cuda())
+    nd, term = plan.bicgstab(10, 1e-4)
+    assert nd == 1 and term == "converged"
+    b = 1.0 - (-complex(np.complex64(k2)) - sigma) / c
+    p2 = sum((2 * np.pi * mi / s) ** 2 for mi, s in zip(m, shape))
+    g = c / (D * p2 + sigma + c)
+    xstar = g * (S.astype(np.complex128) / c) / (1.0 - b * g)
+    x = plan.get_field().cpu().numpy().astype(np.complex128)
+    assert rel_l2(x, xstar) <= 1e-5
+
+
+def test_bicgstab_state_errors():
+    import torch
+    from paper_2207_14222_b200 import Plan, USPError
+    from synth import make
+
+    p = make("C3", (64, 64, 64))
+    med, src, _ = rounded_inputs(p)
+    plan = Plan(p.shape)
+    plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
+    plan.set_source(torch.from_numpy(src).cuda())
+    plan.iterate(2, 0.75, 0.0)
+    with pytest.raises(USPError, match="STATE"):
+        plan.bicgstab(5, 0.0)                     # not from x_0 = 0
+    with pytest.raises(USPError, match="UNSUPPORTED"):
+        q = make("C1")
+        pl = Plan(q.shape)
+        m1, s1, _ = rounded_inputs(q)
+        pl.set_potential(torch.from_numpy(m1).cuda(), 0.95)
+        pl.set_source(torch.from_numpy(s1).cuda())
+        pl.bicgstab(5, 0.0)                       # 1-D
