@@ -122,7 +122,7 @@ typedef struct {
  * USP_FUSED=0) NCCL all-to-alls are used instead.  With nccl_comm, the arrays passed to
  * set_potential / set_source / get_field are the rank's slab
  * [nz/P][ny][nx] (usp_local_extent gives z0); every call is collective.
- * Requires P a power of two dividing ny and nz, ny and nz in [64, 1024].
+ * Requires P a power of two dividing ny and nz, ny and nz in [64, 2048].
  *
  * Errors: USP_ERR_ARG (NULL, ndim, D <= 0), USP_ERR_UNSUPPORTED (extent,
  * decomposition), USP_ERR_NCCL, USP_ERR_CUDA. */

@@ -50,7 +50,10 @@ struct STile {
     // one group of 16 columns (y 5.0 vs 3.1 ms, z 7.4 vs 4.6 ms: 64-byte TMA
     // rows), so one group of 16 columns (128-byte rows) is used.
     static constexpr int GROUPS = 1;
-    static constexpr int COLS = (GROUPS == 2) ? 8 : 16;
+    // N = 2048 (N2 = 64 values per thread): 8 columns, so 256 threads keep
+    // their 64 complex values in registers (64-byte rows; used for the
+    // 2048-plane z pass of C5w and its slab decomposition)
+    static constexpr int COLS = (GROUPS == 2 || N == 2048) ? 8 : 16;
     static constexpr int NTG = COLS * G::N1;                    // threads per group
     static constexpr int NT = GROUPS * NTG;
     static constexpr int TILE = COLS * N;                       // float2 per stage
@@ -382,8 +385,8 @@ static cudaError_t stile_mode(SMode mode, const CUtensorMap &map, const SParams 
     return stile_t<N, S_FWD_MUL_INV>(map, p, grid, s);
 }
 
-bool stile_supported(long long n) { return n >= 64 && n <= 1024 && (n & (n - 1)) == 0; }
-int stile_cols(int N) { return N == 1024 ? STile<1024>::COLS : 16; }
+bool stile_supported(long long n) { return n >= 64 && n <= 2048 && (n & (n - 1)) == 0; }
+int stile_cols(int N) { return N == 2048 ? STile<2048>::COLS : (N == 1024 ? STile<1024>::COLS : 16); }
 int stile_box(int N) { return N < 256 ? N : 256; }
 int stile_ctas_per_sm(int N) {
     switch (N) {
@@ -392,6 +395,7 @@ int stile_ctas_per_sm(int N) {
     case 256: return STile<256>::MINB;
     case 512: return STile<512>::MINB;
     case 1024: return STile<1024>::MINB;
+    case 2048: return STile<2048>::MINB;
     default: return 1;
     }
 }
@@ -403,6 +407,7 @@ cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const SParam
     case 256: return stile_mode<256>(mode, map, p, grid, s);
     case 512: return stile_mode<512>(mode, map, p, grid, s);
     case 1024: return stile_mode<1024>(mode, map, p, grid, s);
+    case 2048: return stile_mode<2048>(mode, map, p, grid, s);
     default: return cudaErrorInvalidValue;
     }
 }

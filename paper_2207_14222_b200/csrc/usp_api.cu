@@ -924,7 +924,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (desc->n[2] % P || desc->n[1] % P)
             return fail(USP_ERR_UNSUPPORTED, "rank count %d must divide ny and nz", P);
         if (!stile_supported(desc->n[1]) || !stile_supported(desc->n[2]))
-            return fail(USP_ERR_UNSUPPORTED, "slab decomposition needs ny, nz in [64, 1024]");
+            return fail(USP_ERR_UNSUPPORTED, "slab decomposition needs ny, nz in [64, 2048]");
     }
     usp_plan_s *p = new usp_plan_s();
     p->d = *desc;

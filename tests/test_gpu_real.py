@@ -43,7 +43,7 @@ def _ws_bytes(plan):
 
 
 @pytest.mark.parametrize("shape,n", [((64, 64, 64), 150), ((128, 64, 256), 60), ((64, 256, 64), 40),
-                                     ((256, 64, 32), 40), ((64, 64, 1024), 20)])
+                                     ((256, 64, 32), 40), ((64, 64, 1024), 20), ((64, 64, 2048), 10)])
 def test_real_path_matches_oracle(orc, shape, n):
     from synth import make
 

@@ -41,7 +41,8 @@ def _run(p, n, virtual_ranks, tol=0.0):
 @pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("name,shape,P,n", [("C3", (64, 64, 64), 2, 40), ("C3", (128, 64, 64), 4, 30),
                                             ("C5", (64, 128, 64), 8, 20), ("C4", (64, 64, 128), 2, 30),
-                                            ("C3", (256, 128, 64), 2, 10), ("C3", (64, 64, 64), 16, 10)])
+                                            ("C3", (256, 128, 64), 2, 10), ("C3", (64, 64, 64), 16, 10),
+                                            ("C5", (2048, 64, 32), 8, 6)])
 def test_virtual_slabs_bit_identical_to_one_slab(name, shape, P, n, fused, monkeypatch):
     """fused = transposes in the K_B / K_C stores (peer-memory path; P <= 8);
     0 = separate transposes (device copies standing in for the NCCL
@@ -121,7 +122,7 @@ def test_slab_decomposition_rejects_bad_layouts():
     with pytest.raises(USPError, match="UNSUPPORTED"):
         Plan((64, 64, 64), virtual_ranks=3)                   # not a power of two
     with pytest.raises(USPError, match="UNSUPPORTED"):
-        Plan((32, 64, 64), virtual_ranks=2)                   # nz outside the TMA-tiled range
+        Plan((32, 64, 64), virtual_ranks=2)                   # nz outside the TMA-tiled range [64, 2048]
     with pytest.raises(USPError, match="UNSUPPORTED"):
         Plan((64, 64, 64), virtual_ranks=128)                 # P does not divide
 
