@@ -315,14 +315,21 @@ def run_usp(args, world, rank, local):
     name = args.config
     # multi-GPU: z-slabs over the ranks (strong scaling) unless the check fails
     comm, slab_check, mode = None, None, ("1 GPU" if world == 1 else "replicas")
+    transposes = None
     if world > 1 and not args.replicas:
         from paper_2207_14222_b200 import comm_init
 
         comm = comm_init()
-        slab_check = slab_selfcheck(comm, world, rank, dev)
-        if slab_check <= 1e-4:
-            mode = "slabs"
-        else:
+        # fused peer-store transposes first; if their closed-form check fails,
+        # the NCCL all-to-all transposes; if that fails too, replicas
+        for fused in ("1", "0"):
+            os.environ["USP_FUSED"] = fused
+            slab_check = slab_selfcheck(comm, world, rank, dev)
+            if slab_check <= 1e-4:
+                mode = "slabs"
+                transposes = "fused peer-memory stores" if fused == "1" else "NCCL all-to-all"
+                break
+        if mode != "slabs":
             comm.close()
             comm = None
     p = make(name, None if args.size is None else (args.size,) * 3, device=str(dev))
@@ -453,7 +460,7 @@ def run_usp(args, world, rank, local):
         ((16 if real else 32) if "all_to_all" in prof else 0)
     it_bytes = iter_bpv * nloc
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
-                   "slabs": f"{world} z-slabs, NCCL all-to-all transposes",
+                   "slabs": f"{world} z-slabs, transposes: {transposes} (self-check first)",
                    "virtual": f"1 GPU, {args.virtual_ranks} virtual z-slabs (device-copy transposes)"}[mode]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
