@@ -1,0 +1,253 @@
+// kernels_small.cu -- persistent 2-D solver for grids whose fields stay in L2
+// (BASELINE.json config C2, 512^2: 2 MiB per field; SURVEY.md §7 hard part 8
+// "latency-bound small configs ... use a persistent kernel").
+//
+// The 4-pass schedule launches 2 kernels per iteration; at 512^2 each is
+// ~10 us of mostly launch/ramp latency for ~2 us of work.  k_solve2d runs
+// the whole iteration loop of Algorithm 1 (Delta-form, reading R-17) inside
+// one cooperative launch (all CTAs co-resident) with two grid barriers per
+// iteration:
+//   Y phase  y forward FFT, x g(p)/N (Eq. 12), y inverse, 16/32-column tiles
+//   -- barrier --
+//   X phase  x inverse FFT -> update x, Delta (L613) -> residual partial ->
+//            u = B Delta -> x forward FFT
+//   -- barrier --  every CTA sums the CTA partials in the same fixed order,
+//            so all take the same stop decision (R-4, R-5) without a host
+//            round trip; CTA 0 publishes the state and the residual history.
+// The arithmetic per line is the same four-step FFT of fft_core.cuh as the
+// pass kernels (register loads from L2 instead of TMA stages: the data is
+// resident and the phases are short).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fft_core.cuh"
+#include "kcommon.cuh"
+#include "tma.cuh"
+#include "usp_internal.h"
+
+namespace usp {
+
+// Sense-reversing grid barrier over co-resident CTAs (cooperative launch).
+// A 4-second watchdog turns a scheduling failure into an error code.
+__device__ __forceinline__ bool grid_barrier(unsigned *count, volatile unsigned *gen, IterState *st) {
+    __syncthreads();
+    __shared__ int ok;
+    if (threadIdx.x == 0) {
+        ok = 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *count = 0u;
+            __threadfence();
+            atomicAdd((unsigned *)gen, 1u);
+        } else {
+            const uint64_t t0 = globaltimer_ns();
+            unsigned n = 0;
+            while (*gen == g) {
+                if ((++n & 255u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
+                    if (atomicCAS(&st->err, 0, 10) == 0) st->err_info = blockIdx.x;
+                    ok = 0;
+                    break;
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    return ok != 0;
+}
+
+template <int NX, int NY>
+struct S2 {
+    using GX = LineGeo<NX>;
+    using GY = LineGeo<NY>;
+    static constexpr int NT = 256;
+    // work is dealt per CTA: an x unit = LPC lines, a y unit = COLS columns.
+    // (Dealing 32/N1-line warp units over every warp of 148 CTAs measured
+    // slower at 512^2: 26 vs 22 us per iteration -- more CTAs at each grid
+    // barrier, 16-byte column accesses.)
+    static constexpr int LPC = NT / GX::N1;                  // x lines per CTA step
+    static constexpr int XS = LPC * LayRow<NX>::kFloat2PerLine;
+    static constexpr int COLS = NT / GY::N1;                 // y tile columns (16 or 32): all threads work
+    static constexpr int YPAD = (COLS == 16 || COLS == 32) ? 0 : 8;
+    static constexpr int YS = GY::N1 * (GY::N2 * COLS + YPAD);
+    static constexpr int BUF = XS > YS ? XS : YS;
+    static constexpr int SMEM = (BUF + NX + NY) * 8;
+};
+
+template <int NX, int NY>
+__global__ void __launch_bounds__(256, 1) k_solve2d(S2Params p) {
+    using T = S2<NX, NY>;
+    using GX = typename T::GX;
+    using GY = typename T::GY;
+    extern __shared__ __align__(16) float2 smem2[];
+    float2 *buf = smem2;
+    float2 *twx = buf + T::BUF;
+    float2 *twy = twx + NX;
+    __shared__ double sh_red[8];
+    __shared__ int s_status;
+    __shared__ long long s_k;
+    IterState *st = p.st;
+
+    for (int i = threadIdx.x; i < NX; i += blockDim.x) twx[i] = __ldg(&p.twx[i]);
+    for (int i = threadIdx.x; i < NY; i += blockDim.x) twy[i] = __ldg(&p.twy[i]);
+    __syncthreads();
+
+    const float alpha = (float)st->alpha;
+    const double tol = st->tol, n0 = st->n0;
+    const long long kmax = st->kmax;
+    long long k = st->k;
+    int status = st->status;
+    double r = st->r;
+    int parity = 0;
+    const int tid = threadIdx.x;
+
+    while (k < kmax && (status == ST_RUNNING || status == ST_STOP_PENDING)) {
+        const bool xonly = status == ST_STOP_PENDING;
+        if (!xonly) {
+            // ---------------------------------------------------- Y phase
+            {
+                const int c = tid % T::COLS, j = tid / T::COLS;
+                const LayCol<NY, T::COLS, T::YPAD, 0> lay{buf, c};
+                const int ntile = NX / T::COLS;
+                for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+                    const int col = tile * T::COLS + c;
+                    float2 v[GY::N2];
+#pragma unroll
+                    for (int m = 0; m < GY::N2; ++m) v[m] = __ldcg(&p.work[(long long)(j + GY::N1 * m) * NX + col]);
+                    const float px = p.mp.kx * freq_m(col, NX), pt2 = px * px;
+#pragma unroll 1
+                    for (int pass = 0; pass < 2; ++pass) {
+                        fft_line<NY, false, LayCol<NY, T::COLS, T::YPAD, 0>, true>(v, lay, j, twy);
+                        if (pass == 0) {
+#pragma unroll
+                            for (int m = 0; m < GY::N2; ++m) {
+                                const float pl = p.mp.ky * freq_m(j + GY::N1 * m, NY);
+                                v[m] = cconj(cmul(v[m], multiplier(p.mp, fmaf(pl, pl, pt2))));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int m = 0; m < GY::N2; ++m) p.work[(long long)(j + GY::N1 * m) * NX + col] = cconj(v[m]);
+                }
+            }
+            if (!grid_barrier(p.bar_count, p.bar_gen, st)) return;
+        }
+        // -------------------------------------------------------- X phase
+        double acc = 0.0;
+        {
+            const int lq = tid / GX::N1, j = tid % GX::N1;
+            const LayRow<NX> lay{buf + lq * LayRow<NX>::kFloat2PerLine};
+            const int ngroups = NY / T::LPC;
+            for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+                const long long base = (long long)(g * T::LPC + lq) * NX + j;
+                float2 v[GX::N2];
+                if (xonly) {
+#pragma unroll
+                    for (int m = 0; m < GX::N2; ++m) {
+                        const long long i = base + GX::N1 * m;
+                        const float2 d = p.delta[i], xx = p.x[i];
+                        p.x[i] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                    }
+                    continue;
+                }
+#pragma unroll
+                for (int m = 0; m < GX::N2; ++m) v[m] = cconj(__ldcg(&p.work[base + GX::N1 * m]));
+                fft_line<NX, false, LayRow<NX>, true>(v, lay, j, twx);   // inverse via conj
+                float lacc = 0.f;
+#pragma unroll
+                for (int m = 0; m < GX::N2; ++m) {
+                    const long long i = base + GX::N1 * m;
+                    const float2 y = cconj(v[m]), b = p.B[i], d = p.delta[i], xx = p.x[i];
+                    const float2 t = cmul(b, csub(y, d));
+                    const float2 dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
+                    p.x[i] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                    p.delta[i] = dn;
+                    lacc += cabs2(dn);
+                    v[m] = cmul(b, dn);
+                }
+                acc += (double)lacc;
+                fft_line<NX, false, LayRow<NX>, true>(v, lay, j, twx);   // forward
+#pragma unroll
+                for (int m = 0; m < GX::N2; ++m) p.work[base + GX::N1 * m] = v[m];
+            }
+        }
+        // residual: CTA partial -> barrier -> every CTA sums all partials in order
+        const double mine = block_sum_d<256>(acc, sh_red);
+        double *part = p.partials + parity * gridDim.x;
+        if (tid == 0) part[blockIdx.x] = mine;
+        if (!grid_barrier(p.bar_count, p.bar_gen, st)) return;
+        if (tid == 0) {
+            double total = 0.0;
+            for (unsigned b = 0; b < gridDim.x; ++b) total += __ldcg(&part[b]);
+            const long long k1 = k + 1;
+            int stt = status;
+            double rr = r;
+            if (xonly) {
+                stt = ST_DONE_CONV;
+            } else {
+                rr = sqrt(total) / n0;
+                if (!(rr <= 1e6)) stt = ST_DIVERGED;
+                else if (tol > 0.0 && rr < tol) stt = ST_STOP_PENDING;
+                if (blockIdx.x == 0) p.red.hist[k1 % p.red.hist_cap] = rr;
+            }
+            s_status = stt;
+            s_k = k1;
+            sh_red[0] = rr;
+        }
+        __syncthreads();
+        status = s_status;
+        k = s_k;
+        r = sh_red[0];
+        __syncthreads();
+        parity ^= 1;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        st->k = k;
+        st->r = r;
+        st->status = status;
+    }
+}
+
+// ========================================================= launchers ====
+template <int NX, int NY>
+static cudaError_t solve2d_t(const S2Params &p, int nsm, cudaStream_t s, int *grid_out) {
+    static int grid = 0;
+    if (!grid) {
+        cudaError_t e = cudaFuncSetAttribute(k_solve2d<NX, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             S2<NX, NY>::SMEM);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve2d<NX, NY>, 256, S2<NX, NY>::SMEM);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+        // enough CTAs for the larger phase, at most one wave of co-resident CTAs
+        const int work = (NY / S2<NX, NY>::LPC) > (NX / S2<NX, NY>::COLS) ? (NY / S2<NX, NY>::LPC)
+                                                                        : (NX / S2<NX, NY>::COLS);
+        grid = work < nsm * per_sm ? work : nsm * per_sm;
+    }
+    if (grid_out) *grid_out = grid;
+    S2Params pp = p;
+    void *args[] = {&pp};
+    return cudaLaunchCooperativeKernel((const void *)k_solve2d<NX, NY>, dim3(grid), dim3(256), args,
+                                       S2<NX, NY>::SMEM, s);
+}
+
+bool solve2d_supported(long long nx, long long ny) {
+    auto ok = [](long long n) { return n >= 64 && n <= 512 && (n & (n - 1)) == 0; };
+    return ok(nx) && ok(ny);
+}
+
+cudaError_t launch_solve2d(int nx, int ny, const S2Params &p, int nsm, cudaStream_t s) {
+#define S2_Y(X, Y) \
+    case Y: return solve2d_t<X, Y>(p, nsm, s, nullptr);
+#define S2_X(X)                                                                  \
+    case X:                                                                      \
+        switch (ny) { S2_Y(X, 64) S2_Y(X, 128) S2_Y(X, 256) S2_Y(X, 512) default: return cudaErrorInvalidValue; }
+    switch (nx) { S2_X(64) S2_X(128) S2_X(256) S2_X(512) default: return cudaErrorInvalidValue; }
+#undef S2_X
+#undef S2_Y
+}
+
+}  // namespace usp

@@ -126,11 +126,11 @@ Nccl &nccl() {
 
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
               KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_BARRIER, KC_XOP,
-              KC_KUPD, KC_N };
+              KC_KUPD, KC_SOLVE2D, KC_N };
 const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
                               "solve1d", "potential", "farthest", "set_state", "xpass_setup",
                               "all_to_all", "finish", "allgather", "rank_barrier", "krylov_xop",
-                              "krylov_update"};
+                              "krylov_update", "solve2d"};
 
 struct Timed {
     int cls;
@@ -170,6 +170,9 @@ struct usp_plan_s {
     // BiCGSTAB (caller-owned Krylov workspace: rhat, p, v, s, t)
     float2 *k_rh = nullptr, *k_p = nullptr, *k_v = nullptr, *k_s = nullptr, *k_t = nullptr;
     KState *ks = nullptr;
+    // persistent 2-D solve (kernels_small.cu; USP_SOLVE2D=0 disables)
+    bool solve2d = false;
+    unsigned *bar = nullptr;   // [0] count, [1] generation
     // plan-owned small device memory
     IterState *st = nullptr;
     double *partials = nullptr;
@@ -1009,6 +1012,12 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->far_i, sizeof(long long) * p->far_cap));
     TRY(cudaMalloc(&p->coll, sizeof(double) * (16 + 3 * 64)));
     TRY(cudaMalloc(&p->ks, sizeof(KState)));
+    TRY(cudaMalloc(&p->bar, sizeof(unsigned) * 2));
+    TRY(cudaMemset(p->bar, 0, sizeof(unsigned) * 2));
+    {
+        const char *s2 = std::getenv("USP_SOLVE2D");
+        p->solve2d = p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
+    }
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
         const int n = (int)p->nx, m = n / 2;
@@ -1220,6 +1229,22 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         op.red = Red{p->partials, p->hist, p->hist_cap, nullptr};
         Tick t(p, KC_SOLVE1D);
         CU(launch_solve1d((int)p->nx, O_ITER, op, p->stream));
+    } else if (p->solve2d) {   // one cooperative launch runs every iteration
+        S2Params sp{};
+        sp.work = p->work;
+        sp.delta = p->delta;
+        sp.x = p->x;
+        sp.B = p->B;
+        sp.twx = p->tw[0];
+        sp.twy = p->tw[1];
+        sp.mp = mul_params(p);
+        sp.st = p->st;
+        sp.red = Red{p->partials, p->hist, p->hist_cap, nullptr};
+        sp.partials = p->partials;
+        sp.bar_count = p->bar;
+        sp.bar_gen = p->bar + 1;
+        Tick t(p, KC_SOLVE2D);
+        CU(launch_solve2d((int)p->nx, (int)p->ny, sp, p->nsm, p->stream));
     } else {
         const XParams xp = x_params(p);
         const long long batch = 16;
@@ -1460,6 +1485,7 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->far_i);
     cudaFree(p->coll);
     cudaFree(p->ks);
+    cudaFree(p->bar);
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
     cudaFree(p->twr);
     cudaFreeHost(p->st_host);

@@ -144,6 +144,19 @@ struct OneParams {
     Red red;
 };
 
+// ------------------------------------------------- persistent 2-D solve --
+struct S2Params {
+    float2 *work, *delta, *x;
+    const float2 *B;
+    const float2 *twx, *twy;   // four-step twiddles for nx, ny
+    MulParams mp;
+    IterState *st;
+    Red red;                   // hist
+    double *partials;          // 2 x gridDim doubles (double-buffered per iteration)
+    unsigned *bar_count;       // grid barrier (zeroed at plan creation)
+    unsigned *bar_gen;
+};
+
 // --------------------------------------------------------------- setup --
 struct PotParams {
     const void *medium;  // staged medium (device)
@@ -167,6 +180,10 @@ struct FarParams {       // farthest medium value from a centre (smallest circle
     double *best_d2;     // per CTA
     long long *best_idx; // per CTA
 };
+
+// persistent 2-D solve (kernels_small.cu)
+bool solve2d_supported(long long nx, long long ny);
+cudaError_t launch_solve2d(int nx, int ny, const S2Params &p, int nsm, cudaStream_t s);
 
 // BiCGSTAB (kernels_krylov.cu)
 cudaError_t launch_xop(int N, KMode mode, const KParams &p, int grid, cudaStream_t s);
