@@ -14,6 +14,8 @@ What it computes (PAPER.md = /root/reference/PAPER.md):
   max|V| = target_norm (L99, L167).
 * ``fixed_point``                  -- Algorithm 1 (L80-89), x-form, or the
   Delta-form recurrence (L613) for the R-17 cross-check.
+* ``canonical_anti``, ``fixed_point_anti`` -- the antisymmetrised system of
+  Eq. 9-10 (L100-128) for problems that are not accretive.
 * ``bicgstab``                     -- BiCGSTAB on the preconditioned system
   Gamma^-1 A x = Gamma^-1 s, Eq. 5 (L73-76) -- Table 1b's BiCGSTAB column.
 
@@ -60,6 +62,8 @@ def lib():
                                       + [ctypes.c_double, ctypes.c_double, ctypes.c_long, ctypes.c_int,
                                          dp, dp, lp, dp])
         L.orc_mec.argtypes = [dp, dp, ctypes.c_long, dp, dp, dp]
+        L.orc_fixed_point_anti.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 3
+                                           + [ctypes.c_double, ctypes.c_double, ctypes.c_long, dp, dp, lp, dp])
         L.orc_bicgstab.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 4
                                    + [ctypes.c_double, ctypes.c_long, dp, dp, lp, dp,
                                       ctypes.POINTER(ctypes.c_int)])
@@ -206,6 +210,35 @@ def fixed_point(w, S, h: Sequence[float], D: float, sigma: complex, c: complex, 
                                _dp(x.view(np.float64)), _dp(hist), ctypes.byref(nd), ctypes.byref(n0))
     if rc < 0:
         raise ValueError(f"orc_fixed_point rc={rc}")
+    return Result(x=x, n_done=int(nd.value), hist=hist[: nd.value].copy(), n0=float(n0.value), rc=rc)
+
+
+def canonical_anti(kind: str, medium, target_norm: float = 0.95, D: float = 1.0) -> Split:
+    """Canonical form of the antisymmetrised system (Eq. 9-10, PAPER.md
+    L100-128): bias = smallest-circle centre of w (as the standard form),
+    REAL scale c = r / target_norm so that ||V|| = max|V_raw| / c = target_norm."""
+    w = medium_to_w(kind, medium)
+    centre, r = mec(w)
+    if r == 0.0:
+        raise ValueError("homogeneous medium: smallest circle has radius 0")
+    return Split(D=D, sigma=centre, c=complex(r / target_norm), bias=centre, radius=r)
+
+
+def fixed_point_anti(w, S, h: Sequence[float], D: float, sigma: complex, c: float, alpha: float, tol: float,
+                     n_max: int) -> Result:
+    """Algorithm 1 on the antisymmetrised system (usp_oracle.c); x has shape
+    (2, *S.shape): [x, x'] (x solves A_raw x = S; x' -> 0 for s' = 0)."""
+    wc, Sc = _c128(w), _c128(S)
+    x = np.zeros((2,) + wc.shape, dtype=np.complex128)
+    hist = np.zeros(n_max, dtype=np.float64)
+    hh = np.ascontiguousarray(h, dtype=np.float64)
+    nd, n0 = ctypes.c_long(0), ctypes.c_double(0.0)
+    rc = lib().orc_fixed_point_anti(_dp(wc.view(np.float64)), _dp(Sc.view(np.float64)), wc.ndim, _dims(wc.shape),
+                                    _dp(hh), float(D), float(np.real(sigma)), float(np.imag(sigma)),
+                                    float(np.real(c)), float(alpha), float(tol), int(n_max),
+                                    _dp(x.view(np.float64)), _dp(hist), ctypes.byref(nd), ctypes.byref(n0))
+    if rc < 0:
+        raise ValueError(f"orc_fixed_point_anti rc={rc}")
     return Result(x=x, n_done=int(nd.value), hist=hist[: nd.value].copy(), n0=float(n0.value), rc=rc)
 
 

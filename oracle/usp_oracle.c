@@ -31,6 +31,10 @@
  *                 (the Delta-form) for the R-17 cross-check.
  *   orc_mec       smallest enclosing circle ("smallest circle
  *                 problem"), Welzl's randomised incremental algorithm.
+ *   orc_fixed_point_anti  Algorithm 1 on the antisymmetrised system of Eq. 9-10
+ *                 (PAPER.md L100-128): E = [x, x'], A = c^-1 [[0, -A_raw*], [A_raw, 0]],
+ *                 real c, for problems whose numerical range is not confined
+ *                 to a half plane (e.g. gain media).
  *   orc_bicgstab  BiCGSTAB [van der Vorst 1992, cited PAPER.md L384] on the
  *                 preconditioned system Gamma^-1 A x = Gamma^-1 s with
  *                 Gamma^-1 A = alpha B[1 - (L+1)^-1 B] (Eq. 5, PAPER.md
@@ -292,6 +296,108 @@ int orc_fixed_point(const double *w, const double *S, int ndim, const long *dims
     }
 done:
     free(B); free(s); free(u); free(Dl);
+    return rc;
+}
+
+/* ------------------------------------------- antisymmetrised system -- */
+/*
+ * Eq. 9-10: with a REAL scale c,
+ *     A = c^-1 [[0, -A_raw^*], [A_raw, 0]],  L = c^-1 [[0, -L_raw^*], [L_raw, 0]],
+ *     V = A - L = c^-1 [[0, -V_raw^*], [V_raw, 0]],  E = [x; x'],  s = c^-1 [-s'; S],
+ * s' = 0 (no adjoint problem: x' -> 0).  A is skew-Hermitian, hence
+ * accretive, for ANY A_raw, and ||V|| = max|V_raw| / c.  With v = V_raw/c
+ * pointwise (V_raw = w - sigma, adjoint = conj):
+ *     B = 1 - V = [[1, conj(v)], [-v, 1]]
+ * and per Fourier mode, l(p) = D|p|^2 + sigma (Eq. 12's symbol), a = l/c,
+ *     (L + 1)^-1 = [[1, -conj(a)], [a, 1]]^-1 = [[1, conj(a)], [-a, 1]] / (1 + |a|^2).
+ * E is stored as two complex fields (x then x'); Algorithm 1 x-form
+ * literally, r_k = ||Delta_k|| / ||B (L+1)^-1 s|| over both components.
+ */
+static int apply_Linv_anti(cplx *u1, cplx *u2, int ndim, const long *dims, const double *h, double D,
+                           cplx sigma, double c) {
+    int rc = orc_fftn((double *)u1, ndim, dims, 0);
+    if (!rc) rc = orc_fftn((double *)u2, ndim, dims, 0);
+    if (rc) return rc;
+    long nx = dims[ndim - 1];
+    long ny = ndim >= 2 ? dims[ndim - 2] : 1;
+    long nz = ndim >= 3 ? dims[ndim - 3] : 1;
+    double hx = h[ndim - 1], hy = ndim >= 2 ? h[ndim - 2] : 1.0, hz = ndim >= 3 ? h[ndim - 3] : 1.0;
+#pragma omp parallel for schedule(static)
+    for (long l = 0; l < nz; ++l) {
+        double pz = ndim >= 3 ? freq(l, nz, hz) : 0.0;
+        for (long j = 0; j < ny; ++j) {
+            double py = ndim >= 2 ? freq(j, ny, hy) : 0.0;
+            for (long i = 0; i < nx; ++i) {
+                double px = freq(i, nx, hx);
+                long q = (l * ny + j) * nx + i;
+                cplx a = (D * (px * px + py * py + pz * pz) + sigma) / c;
+                double det = 1.0 + creal(a) * creal(a) + cimag(a) * cimag(a);
+                cplx v1 = u1[q], v2 = u2[q];
+                u1[q] = (v1 + conj(a) * v2) / det;
+                u2[q] = (v2 - a * v1) / det;
+            }
+        }
+    }
+    rc = orc_fftn((double *)u1, ndim, dims, 1);
+    if (!rc) rc = orc_fftn((double *)u2, ndim, dims, 1);
+    return rc;
+}
+
+int orc_fixed_point_anti(const double *w, const double *S, int ndim, const long *dims, const double *h,
+                         double D, double sig_re, double sig_im, double c, double alpha, double tol,
+                         long n_max, double *x_out, double *hist, long *n_done, double *n0_out) {
+    if (ndim < 1 || ndim > 3 || n_max < 1 || !(c > 0.0)) return -2;
+    long n = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (!is_pow2(dims[a])) return -1;
+        n *= dims[a];
+    }
+    size_t bytes = sizeof(cplx) * (size_t)n;
+    cplx sigma = sig_re + I * sig_im;
+    const cplx *wc = (const cplx *)w, *Sc = (const cplx *)S;
+    cplx *v = malloc(bytes), *u1 = malloc(bytes), *u2 = malloc(bytes), *d1 = malloc(bytes), *d2 = malloc(bytes);
+    cplx *x1 = (cplx *)x_out, *x2 = x1 + n;
+    int rc = 0;
+    *n_done = 0;
+    if (!v || !u1 || !u2 || !d1 || !d2) { rc = -3; goto done; }
+    for (long i = 0; i < n; ++i) v[i] = (wc[i] - sigma) / c;          /* V_raw / c */
+    /* n0 = ||B (L+1)^-1 s||, s = [0; S/c] */
+    for (long i = 0; i < n; ++i) { u1[i] = 0.0; u2[i] = Sc[i] / c; }
+    rc = apply_Linv_anti(u1, u2, ndim, dims, h, D, sigma, c);
+    if (rc) goto done;
+    for (long i = 0; i < n; ++i) { d1[i] = u1[i] + conj(v[i]) * u2[i]; d2[i] = -v[i] * u1[i] + u2[i]; }
+    double acc = 0.0;
+    for (long i = 0; i < n; ++i) acc += creal(d1[i]) * creal(d1[i]) + cimag(d1[i]) * cimag(d1[i]);
+    for (long i = 0; i < n; ++i) acc += creal(d2[i]) * creal(d2[i]) + cimag(d2[i]) * cimag(d2[i]);
+    double n0 = sqrt(acc);
+    if (n0_out) *n0_out = n0;
+    for (long i = 0; i < n; ++i) { x1[i] = 0.0; x2[i] = 0.0; }
+    if (n0 == 0.0) goto done;
+    for (long k = 0; k < n_max; ++k) {
+        /* u = B x + s */
+        for (long i = 0; i < n; ++i) {
+            u1[i] = x1[i] + conj(v[i]) * x2[i];
+            u2[i] = -v[i] * x1[i] + x2[i] + Sc[i] / c;
+        }
+        rc = apply_Linv_anti(u1, u2, ndim, dims, h, D, sigma, c);
+        if (rc) goto done;
+        /* Delta = B (y - x); x += alpha Delta */
+        acc = 0.0;
+        for (long i = 0; i < n; ++i) {
+            cplx e1 = u1[i] - x1[i], e2 = u2[i] - x2[i];
+            cplx g1 = e1 + conj(v[i]) * e2, g2 = -v[i] * e1 + e2;
+            x1[i] += alpha * g1;
+            x2[i] += alpha * g2;
+            acc += creal(g1) * creal(g1) + cimag(g1) * cimag(g1) + creal(g2) * creal(g2) + cimag(g2) * cimag(g2);
+        }
+        double r = sqrt(acc) / n0;
+        if (hist) hist[k] = r;
+        *n_done = k + 1;
+        if (!isfinite(r)) { rc = 1; goto done; }
+        if (tol > 0.0 && r < tol) break;
+    }
+done:
+    free(v); free(u1); free(u2); free(d1); free(d2);
     return rc;
 }
 
