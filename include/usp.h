@@ -105,6 +105,14 @@ typedef struct {
                             this many slabs on ONE GPU, the transposes as device copies
                             (a test mode: every kernel, layout and index of the multi-GPU
                             path, no second GPU needed); 0 or 1 = off                        */
+    int antisymmetric;   /* != 0: solve the antisymmetrised system of PAPER.md Eq. 9-10
+                            (L100-128), E = [x; x'], A = c^-1 [[0, -A_raw^*], [A_raw, 0]]
+                            with a REAL scale c, accretive for ANY A_raw (e.g. gain media,
+                            where set_potential of the standard form fails); x' -> 0.
+                            set_potential's canonical form: sigma = smallest-circle centre
+                            of w, c = r / target_norm; no accretivity test.  2-D / 3-D
+                            complex64, extents in [64, 1024], one GPU; 56 B per voxel of
+                            workspace.  get_field returns x.                                */
 } usp_plan_desc;
 
 /* Create a plan for the grid and problem described by *desc (copied).

@@ -30,7 +30,7 @@ class PlanDesc(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_int64 * 3), ("h", ctypes.c_double * 3),
                 ("medium", ctypes.c_int), ("dtype", ctypes.c_int), ("D", ctypes.c_double),
                 ("sigma", c128), ("c", c128), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
-                ("virtual_ranks", ctypes.c_int)]
+                ("virtual_ranks", ctypes.c_int), ("antisymmetric", ctypes.c_int)]
 
 
 class USPError(RuntimeError):

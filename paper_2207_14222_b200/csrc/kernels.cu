@@ -367,8 +367,9 @@ __global__ void __launch_bounds__(256) k_potential(PotParams p) {
         if (av >= 1.0) vmax = fmaxf(vmax, 1.0f);
         // Re(w/c)
         const double wcr = (wr * cr + wi * ci) * inv_c2, wci = (wi * cr - wr * ci) * inv_c2;
-        if (wcr < -1e-6 * sqrt(wcr * wcr + wci * wci)) ++nacc;
-        if (p.b_real) reinterpret_cast<float *>(p.B)[i] = (float)(1.0 - vr);
+        if (!p.store_v && wcr < -1e-6 * sqrt(wcr * wcr + wci * wci)) ++nacc;
+        if (p.store_v) p.B[i] = make_float2((float)vr, (float)vi);
+        else if (p.b_real) reinterpret_cast<float *>(p.B)[i] = (float)(1.0 - vr);
         else p.B[i] = make_float2((float)(1.0 - vr), (float)(-vi));
     }
     // CTA reduce then one atomic each

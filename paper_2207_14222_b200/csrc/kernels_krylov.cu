@@ -257,30 +257,55 @@ __global__ void __launch_bounds__(256) k_kupd(KParams p) {
     const float2 alpha = tof(ks.alpha), omega = tof(ks.omega);
     float la[3] = {0.f, 0.f, 0.f};
     double acc[3] = {0.0, 0.0, 0.0};
-    const long long n = p.nvox;
-    int cnt = 0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const float2 pp = p.p[i];
-        float2 xx = p.x[i];
-        xx = cadd(xx, cmul(alpha, pp));
-        if (half) {
-            p.x[i] = xx;
-            continue;
-        }
-        const float2 ss = p.s[i], tt = p.t[i];
-        xx = cadd(xx, cmul(omega, ss));
-        p.x[i] = xx;
-        const float2 rr = csub(ss, cmul(omega, tt));
-        p.r[i] = rr;
-        const float2 rh = p.rh[i];
-        la[0] += rh.x * rr.x + rh.y * rr.y;
-        la[1] += rh.x * rr.y - rh.y * rr.x;
-        la[2] += cabs2(rr);
-        if (++cnt == 64) {   // fp32 partials over short runs, fp64 beyond
+    // 128-bit accesses (two complex values) and 2 pairs per thread and step,
+    // so each thread keeps ~10 independent loads in flight (the kernel is
+    // HBM-bound; one complex per step left it latency-bound, ncu)
+    const long long n2 = p.nvox / 2;                // nvox is even (power-of-two extents)
+    const float4 *P = reinterpret_cast<const float4 *>(p.p), *Sv = reinterpret_cast<const float4 *>(p.s);
+    const float4 *Tv = reinterpret_cast<const float4 *>(p.t), *RH = reinterpret_cast<const float4 *>(p.rh);
+    float4 *X = reinterpret_cast<float4 *>(p.x), *R = reinterpret_cast<float4 *>(p.r);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < n2; i0 += 2 * stride) {
+        float4 pp[2], xx[2], ss[2], tt[2], rh[2];
+        bool ok[2];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) { acc[q] += (double)la[q]; la[q] = 0.f; }
-            cnt = 0;
+        for (int u = 0; u < 2; ++u) {
+            const long long i = i0 + u * stride;
+            ok[u] = i < n2;
+            if (ok[u]) {
+                pp[u] = P[i];
+                xx[u] = X[i];
+                if (!half) {
+                    ss[u] = Sv[i];
+                    tt[u] = Tv[i];
+                    rh[u] = RH[i];
+                }
+            }
         }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (!ok[u]) continue;
+            const long long i = i0 + u * stride;
+            float2 x0 = cadd(make_float2(xx[u].x, xx[u].y), cmul(alpha, make_float2(pp[u].x, pp[u].y)));
+            float2 x1 = cadd(make_float2(xx[u].z, xx[u].w), cmul(alpha, make_float2(pp[u].z, pp[u].w)));
+            if (half) {
+                X[i] = make_float4(x0.x, x0.y, x1.x, x1.y);
+                continue;
+            }
+            const float2 s0 = make_float2(ss[u].x, ss[u].y), s1 = make_float2(ss[u].z, ss[u].w);
+            x0 = cadd(x0, cmul(omega, s0));
+            x1 = cadd(x1, cmul(omega, s1));
+            X[i] = make_float4(x0.x, x0.y, x1.x, x1.y);
+            const float2 r0 = csub(s0, cmul(omega, make_float2(tt[u].x, tt[u].y)));
+            const float2 r1 = csub(s1, cmul(omega, make_float2(tt[u].z, tt[u].w)));
+            R[i] = make_float4(r0.x, r0.y, r1.x, r1.y);
+            const float2 h0 = make_float2(rh[u].x, rh[u].y), h1 = make_float2(rh[u].z, rh[u].w);
+            la[0] += h0.x * r0.x + h0.y * r0.y + h1.x * r1.x + h1.y * r1.y;
+            la[1] += h0.x * r0.y - h0.y * r0.x + h1.x * r1.y - h1.y * r1.x;
+            la[2] += cabs2(r0) + cabs2(r1);
+        }
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { acc[q] += (double)la[q]; la[q] = 0.f; }   // fp64 across steps
     }
 #pragma unroll
     for (int q = 0; q < 3; ++q) acc[q] += (double)la[q];

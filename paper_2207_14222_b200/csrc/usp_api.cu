@@ -170,6 +170,9 @@ struct usp_plan_s {
     // BiCGSTAB (caller-owned Krylov workspace: rhat, p, v, s, t)
     float2 *k_rh = nullptr, *k_p = nullptr, *k_v = nullptr, *k_s = nullptr, *k_t = nullptr;
     KState *ks = nullptr;
+    // antisymmetrised system (Eq. 9-10; desc.antisymmetric): two-component x,
+    // Delta, work (component-major) and v = (w - sigma)/c in place of B
+    bool anti = false;
     // persistent 2-D solve (kernels_small.cu; USP_SOLVE2D=0 disables)
     bool solve2d = false;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -700,6 +703,57 @@ usp_status exchange(usp_plan_s *p, bool forward) {
     return USP_OK;
 }
 
+// ---- antisymmetrised system (Eq. 9-10): component-major two-component chain
+AParams anti_params(usp_plan_s *p) {
+    AParams a{};
+    a.work = p->work;
+    a.delta = p->delta;
+    a.x = p->x;
+    a.v = p->B;
+    a.tw = p->tw[0];
+    a.nlines = p->ny * p->nz;
+    a.nvox = p->nloc;
+    a.inv_c = (float)(1.0 / p->c.re);
+    a.sigma = make_float2((float)p->sigma.re, (float)p->sigma.im);
+    a.inv_n = (float)(1.0 / (double)p->nvox);
+    a.mp = mul_params(p);
+    a.st = p->st;
+    a.red = Red{p->partials, p->hist, p->hist_cap, nullptr};
+    return a;
+}
+
+usp_status run_anti_x(usp_plan_s *p, XMode mode) {
+    Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
+    const int grid = occ_grid(p, (p->ny * p->nz + anti_lines_per_cta((int)p->nx) - 1) / anti_lines_per_cta((int)p->nx), 4);
+    CU(launch_anti_x((int)p->nx, mode, anti_params(p), grid, p->stream));
+    return USP_OK;
+}
+
+// forward FFT (y, z) of both components, the 2x2 symbol, inverse FFT (z, y)
+usp_status chain_anti(usp_plan_s *p, int check_state) {
+    usp_status s;
+    const long long plane = p->nx * p->ny;
+    if (p->ndim == 2) {
+        SParams yf = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, 2, plane, 1, check_state, 2);
+        if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, true, 0))) return s;
+        {
+            Tick t(p, KC_ZMUL);
+            CU(launch_anti_mul(anti_params(p), check_state, occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
+        }
+        return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, true, 0);
+    }
+    SParams yf = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, 2 * p->nz, plane, 1, check_state, 3);
+    SParams zf = sparams(p, p->work, p->work, p->tw[2], plane, plane, 2, p->nz * plane, 2, check_state, 2);
+    if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, true, 0))) return s;
+    if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD, zf, p->smap_z, true, 0))) return s;
+    {
+        Tick t(p, KC_ZMUL);
+        CU(launch_anti_mul(anti_params(p), check_state, occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
+    }
+    if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_INV, zf, p->smap_z, true, 0))) return s;
+    return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, true, 0);
+}
+
 // The middle of the chain: every FFT pass between the x forward and the x
 // inverse, with the (L+1)^-1 multiplier on the last axis (Eq. 12).
 usp_status chain_mid(usp_plan_s *p, int check_state) {
@@ -810,14 +864,15 @@ void build_maps(usp_plan_s *p) {
     if (!p->stile || p->ndim < 2 || !stile_supported(p->ny)) return;
     const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
     if (p->ndim == 2) {
-        const cuuint64_t dims[2] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny};
+        const cuuint64_t dims[2] = {(cuuint64_t)p->rp, (cuuint64_t)(p->ny * (p->anti ? 2 : 1))};
         const cuuint64_t str[1] = {(cuuint64_t)p->rp * 8};
         const cuuint32_t box[2] = {cy, by};
         p->stile_y = make_map(&p->smap_y, p->work, 2, dims, str, box);
         return;
     }
+    const long long comps = p->anti ? 2 : 1;   // antisymmetrised: both components as extra planes
     {   // y pass over the planes held here: {x, y, z}
-        const cuuint64_t dims[3] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny, (cuuint64_t)p->nzh};
+        const cuuint64_t dims[3] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny, (cuuint64_t)(p->nzh * comps)};
         const cuuint64_t str[2] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->rp * p->ny) * 8};
         const cuuint32_t box[3] = {cy, by, 1};
         p->stile_y = make_map(&p->smap_y, p->work, 3, dims, str, box);
@@ -825,7 +880,7 @@ void build_maps(usp_plan_s *p) {
     if (!stile_supported(p->nz)) return;
     const cuuint32_t cz = (cuuint32_t)stile_cols((int)p->nz), bz = (cuuint32_t)stile_box((int)p->nz);
     if (p->P == 1) {   // z pass: {x*y columns, z}
-        const cuuint64_t dims[2] = {(cuuint64_t)(p->rp * p->ny), (cuuint64_t)p->nz};
+        const cuuint64_t dims[2] = {(cuuint64_t)(p->rp * p->ny), (cuuint64_t)(p->nz * comps)};
         const cuuint64_t str[1] = {(cuuint64_t)(p->rp * p->ny) * 8};
         const cuuint32_t box[2] = {cz, bz};
         p->stile_z = make_map(&p->smap_z, p->work, 2, dims, str, box);
@@ -929,8 +984,16 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (!stile_supported(desc->n[1]) || !stile_supported(desc->n[2]))
             return fail(USP_ERR_UNSUPPORTED, "slab decomposition needs ny, nz in [64, 2048]");
     }
+    if (desc->antisymmetric) {
+        if (desc->ndim < 2 || desc->dtype != USP_C64 || P > 1)
+            return fail(USP_ERR_UNSUPPORTED, "the antisymmetrised system runs on 2-D / 3-D complex64 plans on one GPU");
+        for (int a = 0; a < desc->ndim; ++a)
+            if (desc->n[a] < 64 || desc->n[a] > 1024)
+                return fail(USP_ERR_UNSUPPORTED, "the antisymmetrised system needs extents in [64, 1024]");
+    }
     usp_plan_s *p = new usp_plan_s();
     p->d = *desc;
+    p->anti = desc->antisymmetric != 0;
     p->ndim = desc->ndim;
     p->nx = desc->n[0];
     p->ny = desc->ndim >= 2 ? desc->n[1] : 1;
@@ -947,7 +1010,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     p->nloc = p->nx * p->ny * p->nzh;
     {
         const char *rl = std::getenv("USP_REAL");
-        p->real = !(rl && rl[0] == '0') && desc->dtype == USP_R32 && desc->medium == USP_MEDIUM_W &&
+        p->real = !p->anti && !(rl && rl[0] == '0') && desc->dtype == USP_R32 && desc->medium == USP_MEDIUM_W &&
                   desc->ndim == 3 && xreal_supported(p->nx) && stile_supported(p->ny) && stile_supported(p->nz);
         p->rp = p->real ? xreal_row_pitch((int)p->nx) : p->nx;
     }
@@ -981,11 +1044,12 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (chk) p->chunk_g = std::atoll(chk);
         while (p->chunk_g > 0 && (p->nz % p->chunk_g)) p->chunk_g >>= 1;
         const char *stl = std::getenv("USP_STILE");
-        p->stile = (P > 1) || p->real || (p->pipe && !(stl && stl[0] == '0'));
+        p->stile = (P > 1) || p->real || p->anti || (p->pipe && !(stl && stl[0] == '0'));
+        const long long comps = p->anti ? 2 : 1;
         if (p->ndim >= 2 && stile_supported(p->ny))
-            p->grids_y = occ_grid(p, (p->rp / stile_cols((int)p->ny)) * p->nzh, stile_ctas_per_sm((int)p->ny));
+            p->grids_y = occ_grid(p, (p->rp / stile_cols((int)p->ny)) * p->nzh * comps, stile_ctas_per_sm((int)p->ny));
         if (p->ndim >= 3 && stile_supported(p->nz)) {
-            const long long zcols = (P > 1) ? p->nyl * p->rp * (virt ? P : 1) : p->rp * p->ny;
+            const long long zcols = (P > 1) ? p->nyl * p->rp * (virt ? P : 1) : p->rp * p->ny * comps;
             p->grids_z = occ_grid(p, zcols / stile_cols((int)p->nz), stile_ctas_per_sm((int)p->nz));
         }
         const int u = p->real ? xreal_lines_per_unit((int)p->nx) : 32 / (1 << (log2ll(p->nx) / 2));
@@ -1016,7 +1080,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMemset(p->bar, 0, sizeof(unsigned) * 2));
     {
         const char *s2 = std::getenv("USP_SOLVE2D");
-        p->solve2d = p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
+        p->solve2d = !p->anti && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
     }
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
@@ -1049,6 +1113,10 @@ usp_status usp_plan_workspace_size(usp_plan_t p, size_t *bytes) {
     if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
     const size_t f = align256((size_t)p->nloc * (p->real ? sizeof(float) : sizeof(float2)));
     const size_t w = align256((size_t)p->nzh * p->ny * p->rp * sizeof(float2));
+    if (p->anti) {   // x, Delta, work: two components each; v
+        *bytes = 7 * f;
+        return USP_OK;
+    }
     *bytes = 3 * f + w * (p->P > 1 ? 3 : 1);
     return USP_OK;
 }
@@ -1067,6 +1135,12 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     p->delta = (float2 *)(p->ws + f);
     p->B = (float2 *)(p->ws + 2 * f);
     p->work = (float2 *)(p->ws + 3 * f);
+    if (p->anti) {   // [x x'] [Delta Delta'] [work work'] [v]
+        p->x = (float2 *)(p->ws);
+        p->delta = (float2 *)(p->ws + 2 * f);
+        p->work = (float2 *)(p->ws + 4 * f);
+        p->B = (float2 *)(p->ws + 6 * f);
+    }
     if (p->P > 1) {
         p->sendb = (float2 *)(p->ws + 3 * f + w);
         p->recvb = (float2 *)(p->ws + 3 * f + 2 * w);
@@ -1111,7 +1185,11 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
             return fail(USP_ERR_ARG, "homogeneous medium: smallest circle has radius 0; give sigma and c explicitly");
         p->centre = {cen.x, cen.y};
         p->radius = r;
-        if (p->d.medium == USP_MEDIUM_K2) {   // sigma = -kbar^2, c = -i r / 0.95 (R-1)
+        if (p->anti) {                        // Eq. 9-10: REAL scale, ||V|| = r / c (L100-128)
+            p->sigma = {cen.x, cen.y};
+            if (p->d.medium == USP_MEDIUM_K2) p->sigma = {-cen.x, -cen.y};
+            p->c = {r / target_norm, 0.0};
+        } else if (p->d.medium == USP_MEDIUM_K2) {   // sigma = -kbar^2, c = -i r / 0.95 (R-1)
             p->sigma = {-cen.x, -cen.y};
             p->c = {0.0, -r / target_norm};
         } else {                              // diffusion: sigma = centre, c = r / 0.95 (R-15)
@@ -1125,7 +1203,9 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
         p->radius = 0.0;
     }
     if (p->c.re == 0.0 && p->c.im == 0.0) return fail(USP_ERR_ARG, "c must be non-zero");
-    if (p->d.D * p->c.re < 0.0)
+    if (p->anti && !(p->c.im == 0.0 && p->c.re > 0.0))
+        return fail(USP_ERR_ARG, "the antisymmetrised system needs a real scale c > 0 (Eq. 9-10)");
+    if (!p->anti && p->d.D * p->c.re < 0.0)
         return fail(USP_ERR_NOT_ACCRETIVE, "D Re(c) < 0: -D lap / c is not accretive (Eq. 1)");
     CU(cudaMemsetAsync(p->red_u, 0, sizeof(unsigned) * 4, p->stream));
     if (p->real && (p->sigma.im != 0.0 || p->c.im != 0.0))
@@ -1133,6 +1213,7 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
     PotParams pp{p->work, p->d.dtype == USP_R32, p->d.medium == USP_MEDIUM_K2, p->B, p->nloc,
                  p->sigma.re, p->sigma.im, p->c.re, p->c.im, p->red_u, p->red_u + 1, p->red_u + 2};
     pp.b_real = p->real;
+    pp.store_v = p->anti;
     {
         Tick t(p, KC_POTENTIAL);
         CU(launch_potential(pp, occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
@@ -1190,6 +1271,10 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         op.red = Red{p->partials, p->hist, p->hist_cap, nullptr};
         Tick t(p, KC_SOLVE1D);
         CU(launch_solve1d((int)p->nx, O_SETUP, op, p->stream));
+    } else if (p->anti) {
+        if ((s = run_anti_x(p, X_SRC_FWD))) return s;
+        if ((s = chain_anti(p, 0))) return s;
+        if ((s = run_anti_x(p, X_SRC_EPI))) return s;
     } else {
         XParams xp = x_params(p);
         s = run_xpass(p, X_SRC_FWD, xp);
@@ -1255,6 +1340,11 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         while (launched < total) {
             const long long nb = std::min(batch, total - launched);
             for (long long i = 0; i < nb; ++i) {
+                if (p->anti) {
+                    if ((s = chain_anti(p, 1))) return s;
+                    if ((s = run_anti_x(p, X_ITER))) return s;
+                    continue;
+                }
                 if (p->chunked) {
                     if ((s = chunked_iteration(p))) return s;
                     continue;
@@ -1357,7 +1447,7 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->k_rh) return fail(USP_ERR_STATE, "usp_krylov_set_workspace must be called first");
     if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
-    if (p->ndim < 2 || p->real || multi_rank(p) || !p->pipe_xk)
+    if (p->ndim < 2 || p->real || p->anti || multi_rank(p) || !p->pipe_xk)
         return fail(USP_ERR_UNSUPPORTED, "BiCGSTAB runs on 2-D / 3-D complex64 plans on one GPU");
     usp_status s = sync_state(p);
     if (s) return s;

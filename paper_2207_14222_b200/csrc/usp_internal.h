@@ -144,6 +144,21 @@ struct OneParams {
     Red red;
 };
 
+// ------------------------------------------- antisymmetrised system (NEXT-3) --
+struct AParams {
+    float2 *work, *delta, *x;  // two components each, component-major (component 2 at + nvox)
+    const float2 *v;           // v = (w - sigma)/c
+    const float2 *tw;          // four-step twiddles for nx
+    long long nlines;          // ny * nz
+    long long nvox;            // voxels per component
+    float inv_c;               // 1/c (c real)
+    float2 sigma;
+    float inv_n;               // 1 / N_vox (the inverse DFT's normalisation)
+    MulParams mp;
+    IterState *st;
+    Red red;
+};
+
 // ------------------------------------------------- persistent 2-D solve --
 struct S2Params {
     float2 *work, *delta, *x;
@@ -170,6 +185,7 @@ struct PotParams {
     unsigned int *n_nonaccretive;
     unsigned int *n_nonfinite;
     int b_real;          // store B as float32 (real path; V is real there)
+    int store_v;         // antisymmetrised system: store v = V instead of B, no accretivity test
 };
 
 struct FarParams {       // farthest medium value from a centre (smallest circle)
@@ -180,6 +196,11 @@ struct FarParams {       // farthest medium value from a centre (smallest circle
     double *best_d2;     // per CTA
     long long *best_idx; // per CTA
 };
+
+// antisymmetrised system (kernels_anti.cu)
+cudaError_t launch_anti_x(int N, XMode mode, const AParams &p, int grid, cudaStream_t s);
+cudaError_t launch_anti_mul(const AParams &p, int check_state, int grid, cudaStream_t s);
+int anti_lines_per_cta(int N);
 
 // persistent 2-D solve (kernels_small.cu)
 bool solve2d_supported(long long nx, long long ny);

@@ -57,11 +57,14 @@ class Plan:
     per rank; arrays are the rank's slab, ``local_shape``);
     ``virtual_ranks=P`` runs the same decomposition with P slabs on one GPU
     (transposes as device copies; arrays are the full grid).
+
+    ``antisymmetric=True`` solves the antisymmetrised system of Eq. 9-10
+    (accretive for any problem, e.g. gain media); ``get_field`` returns x.
     """
 
     def __init__(self, shape: Sequence[int], kind: str = "helmholtz", h: Optional[Sequence[float]] = None,
                  D: float = 1.0, sigma: complex = 0j, c: complex = 1 + 0j, dtype: str = "c64",
-                 stream=None, device=None, comm=None, virtual_ranks: int = 0):
+                 stream=None, device=None, comm=None, virtual_ranks: int = 0, antisymmetric: bool = False):
         import torch
 
         self.lib = L.load()
@@ -87,6 +90,7 @@ class Plan:
         d.stream = ctypes.c_void_p(self.stream.cuda_stream)
         d.nccl_comm = comm.handle if comm is not None else None
         d.virtual_ranks = int(virtual_ranks)
+        d.antisymmetric = int(bool(antisymmetric))
         self.comm = comm
         self.desc = d
         h_ = ctypes.c_void_p()
