@@ -16,6 +16,8 @@ What it computes (PAPER.md = /root/reference/PAPER.md):
   Delta-form recurrence (L613) for the R-17 cross-check.
 * ``canonical_anti``, ``fixed_point_anti`` -- the antisymmetrised system of
   Eq. 9-10 (L100-128) for problems that are not accretive.
+* ``gmres``                        -- restarted GMRES(m) on the same system
+  (Table 1b's GMRES5 / GMRES20 columns).
 * ``bicgstab``                     -- BiCGSTAB on the preconditioned system
   Gamma^-1 A x = Gamma^-1 s, Eq. 5 (L73-76) -- Table 1b's BiCGSTAB column.
 
@@ -64,6 +66,8 @@ def lib():
         L.orc_mec.argtypes = [dp, dp, ctypes.c_long, dp, dp, dp]
         L.orc_fixed_point_anti.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 3
                                            + [ctypes.c_double, ctypes.c_double, ctypes.c_long, dp, dp, lp, dp])
+        L.orc_gmres.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 4
+                                + [ctypes.c_int, ctypes.c_double, ctypes.c_long, dp, dp, lp, dp])
         L.orc_bicgstab.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 4
                                    + [ctypes.c_double, ctypes.c_long, dp, dp, lp, dp,
                                       ctypes.POINTER(ctypes.c_int)])
@@ -271,6 +275,25 @@ def bicgstab(w, S, h: Sequence[float], D: float, sigma: complex, c: complex, tol
     k = int(nd.value)
     nh = 2 * k - 1 if half.value else 2 * k
     return KrylovResult(x=x, n_done=k, half=bool(half.value), hist=hist[:nh].copy(), nb=float(nb.value), rc=rc)
+
+
+def gmres(w, S, h: Sequence[float], D: float, sigma: complex, c: complex, m: int, tol: float,
+          n_max: int) -> KrylovResult:
+    """Restarted GMRES(m) on M x = b (same system as bicgstab; reading R-28).
+    n_done counts Arnoldi steps; hist[k-1] = residual estimate after step k."""
+    wc, Sc = _c128(w), _c128(S)
+    x = np.zeros_like(wc)
+    hist = np.zeros(n_max, dtype=np.float64)
+    hh = np.ascontiguousarray(h, dtype=np.float64)
+    nd, nb = ctypes.c_long(0), ctypes.c_double(0.0)
+    rc = lib().orc_gmres(_dp(wc.view(np.float64)), _dp(Sc.view(np.float64)), wc.ndim, _dims(wc.shape), _dp(hh),
+                         float(D), float(np.real(sigma)), float(np.imag(sigma)), float(np.real(c)),
+                         float(np.imag(c)), int(m), float(tol), int(n_max), _dp(x.view(np.float64)), _dp(hist),
+                         ctypes.byref(nd), ctypes.byref(nb))
+    if rc < 0:
+        raise ValueError(f"orc_gmres rc={rc}")
+    k = int(nd.value)
+    return KrylovResult(x=x, n_done=k, half=False, hist=hist[:k].copy(), nb=float(nb.value), rc=rc)
 
 
 def solve_problem(p, target_norm: float = 0.95, form: str = "x", n_iter: Optional[int] = None,

@@ -35,6 +35,8 @@
  *                 (PAPER.md L100-128): E = [x, x'], A = c^-1 [[0, -A_raw*], [A_raw, 0]],
  *                 real c, for problems whose numerical range is not confined
  *                 to a half plane (e.g. gain media).
+ *   orc_gmres     restarted GMRES(m) (Saad & Schultz 1986; Table 1b's GMRES5 /
+ *                 GMRES20 columns) on the same system.
  *   orc_bicgstab  BiCGSTAB [van der Vorst 1992, cited PAPER.md L384] on the
  *                 preconditioned system Gamma^-1 A x = Gamma^-1 s with
  *                 Gamma^-1 A = alpha B[1 - (L+1)^-1 B] (Eq. 5, PAPER.md
@@ -507,6 +509,114 @@ int orc_bicgstab(const double *w, const double *S, int ndim, const long *dims, c
     }
 done:
     free(B); free(sv); free(r); free(rh); free(p); free(v); free(sr); free(t); free(tmp);
+    return rc;
+}
+
+/* --------------------------------------------------------- GMRES(m) -- */
+/*
+ * Restarted GMRES(m) on M x = b (M, b, x_0 = 0 as orc_bicgstab; reading
+ * R-28), the textbook algorithm (Saad, "Iterative Methods for Sparse Linear
+ * Systems", Alg. 6.9 with Givens rotations): each cycle builds an Arnoldi
+ * basis by modified Gram-Schmidt from r = b - M x, minimises ||beta e1 - H y||
+ * and updates x = x + V y.  After every Arnoldi step the residual estimate
+ * |g_{i+1}| / ||b|| is tested against tol (the exact residual in exact
+ * arithmetic); on success x is updated with the current y and the solve
+ * stops.  n_done counts Arnoldi steps (= applications of M besides the
+ * restart residuals); hist[k-1] = estimate after step k (n_max entries).
+ * tol <= 0 runs exactly n_max steps.  Returns 0, 1 non-finite, 2 breakdown
+ * other than a lucky one, negative on argument errors.
+ */
+int orc_gmres(const double *w, const double *S, int ndim, const long *dims, const double *h, double D,
+              double sig_re, double sig_im, double c_re, double c_im, int m, double tol, long n_max,
+              double *x_out, double *hist, long *n_done, double *nb_out) {
+    if (ndim < 1 || ndim > 3 || n_max < 1 || m < 1) return -2;
+    long n = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (!is_pow2(dims[a])) return -1;
+        n *= dims[a];
+    }
+    size_t bytes = sizeof(cplx) * (size_t)n;
+    cplx *B = malloc(bytes), *sv = malloc(bytes), *b = malloc(bytes), *r = malloc(bytes), *tmp = malloc(bytes);
+    cplx *V = malloc(bytes * (size_t)(m + 1));
+    cplx *H = calloc((size_t)(m + 1) * m, sizeof(cplx));       /* H[i*m + j], column j */
+    cplx *cs = malloc(sizeof(cplx) * m), *sn = malloc(sizeof(cplx) * m), *g = malloc(sizeof(cplx) * (m + 1));
+    cplx *y = malloc(sizeof(cplx) * m);
+    cplx *x = (cplx *)x_out;
+    int rc = 0;
+    *n_done = 0;
+    if (!B || !sv || !b || !r || !tmp || !V || !H || !cs || !sn || !g || !y) { rc = -3; goto done; }
+    orc_setup(w, S, n, sig_re, sig_im, c_re, c_im, NULL, (double *)B, (double *)sv);
+    memcpy(tmp, sv, bytes);
+    rc = orc_apply_Linv((double *)tmp, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+    if (rc) goto done;
+    for (long i = 0; i < n; ++i) { b[i] = B[i] * tmp[i]; x[i] = 0.0; }
+    double nb = norm2(b, n);
+    if (nb_out) *nb_out = nb;
+    if (nb == 0.0) goto done;
+    long steps = 0;
+    while (steps < n_max) {
+        /* r = b - M x (x = 0 on the first cycle: r = b) */
+        if (steps == 0) {
+            memcpy(r, b, bytes);
+        } else {
+            rc = apply_M(B, x, r, tmp, n, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+            if (rc) goto done;
+            for (long i = 0; i < n; ++i) r[i] = b[i] - r[i];
+        }
+        double beta = norm2(r, n);
+        if (beta == 0.0) goto done;
+        for (long i = 0; i < n; ++i) V[i] = r[i] / beta;
+        for (int i = 0; i <= m; ++i) g[i] = 0.0;
+        g[0] = beta;
+        int k = 0, stop = 0;
+        for (int j = 0; j < m && steps < n_max; ++j) {
+            cplx *vj = V + (size_t)j * n, *wv = V + (size_t)(j + 1) * n;
+            rc = apply_M(B, vj, wv, tmp, n, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
+            if (rc) goto done;
+            for (int i = 0; i <= j; ++i) {                       /* modified Gram-Schmidt */
+                cplx hij = dotc(V + (size_t)i * n, wv, n);
+                H[i * m + j] = hij;
+                for (long q = 0; q < n; ++q) wv[q] -= hij * V[(size_t)i * n + q];
+            }
+            double hn = norm2(wv, n);
+            H[(j + 1) * m + j] = hn;
+            if (hn != 0.0)
+                for (long q = 0; q < n; ++q) wv[q] /= hn;
+            for (int i = 0; i < j; ++i) {                        /* previous rotations */
+                cplx t = cs[i] * H[i * m + j] + sn[i] * H[(i + 1) * m + j];
+                H[(i + 1) * m + j] = -conj(sn[i]) * H[i * m + j] + conj(cs[i]) * H[(i + 1) * m + j];
+                H[i * m + j] = t;
+            }
+            /* new rotation zeroing H[j+1][j]: [c s; -conj(s) conj(c)] unitary */
+            cplx hjj = H[j * m + j];
+            double den = sqrt(creal(hjj) * creal(hjj) + cimag(hjj) * cimag(hjj) + hn * hn);
+            if (den == 0.0) { rc = 2; goto done; }
+            cs[j] = conj(hjj) / den;
+            sn[j] = hn / den;
+            H[j * m + j] = den;
+            H[(j + 1) * m + j] = 0.0;
+            g[j + 1] = -conj(sn[j]) * g[j];
+            g[j] = cs[j] * g[j];
+            ++steps;
+            k = j + 1;
+            double est = cabs(g[j + 1]) / nb;
+            if (hist) hist[steps - 1] = est;
+            *n_done = steps;
+            if (!isfinite(est)) { rc = 1; goto done; }
+            if ((tol > 0.0 && est < tol) || hn == 0.0) { stop = 1; break; }
+        }
+        /* y = R^-1 g (k x k upper triangular), x += V y */
+        for (int i = k - 1; i >= 0; --i) {
+            cplx acc = g[i];
+            for (int q = i + 1; q < k; ++q) acc -= H[i * m + q] * y[q];
+            y[i] = acc / H[i * m + i];
+        }
+        for (int i = 0; i < k; ++i)
+            for (long q = 0; q < n; ++q) x[q] += y[i] * V[(size_t)i * n + q];
+        if (stop) break;
+    }
+done:
+    free(B); free(sv); free(b); free(r); free(tmp); free(V); free(H); free(cs); free(sn); free(g); free(y);
     return rc;
 }
 

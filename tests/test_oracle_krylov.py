@@ -112,3 +112,39 @@ def test_fewer_operator_applications_than_fixed_point_on_C1(orc):
     assert kr.rc == 0 and kr.hist[-1] < 1e-6
     assert 2 * kr.n_done < fp.n_done
     assert np.linalg.norm(kr.x - fp.x) <= 1e-4 * np.linalg.norm(fp.x)
+
+
+# ------------------------------------------------------------- GMRES(m) --
+@pytest.mark.parametrize("shape,seed,m", [((64,), 1, 5), ((16, 16), 2, 20), ((8, 8, 8), 3, 5)])
+def test_gmres_cycles_equal_scipy_gmres(orc, shape, seed, m):
+    """After k full restart cycles, orc_gmres = scipy's GMRES(m) (an
+    independent implementation; the iterate of a cycle is unique: it
+    minimises the residual over the Krylov space) on the dense operator."""
+    from scipy.sparse.linalg import LinearOperator, gmres
+
+    k2, S = _problem(shape, seed)
+    sp, w, M, b = _dense_M_b(orc, shape, k2, S)
+    n = M.shape[0]
+    op = LinearOperator((n, n), matvec=lambda u: M @ u, dtype=complex)
+    for cycles in (1, 3):
+        ref, _ = gmres(op, b, rtol=0.0, atol=0.0, restart=m, maxiter=cycles)
+        res = orc.gmres(w, S, [1.0] * len(shape), sp.D, sp.sigma, sp.c, m, 0.0, cycles * m)
+        assert res.n_done == cycles * m and res.rc == 0
+        assert np.linalg.norm(res.x.ravel() - ref) <= 1e-9 * np.linalg.norm(ref), cycles
+        true_r = np.linalg.norm(b - M @ res.x.ravel()) / np.linalg.norm(b)
+        assert abs(true_r - res.hist[-1]) <= 1e-6 * true_r + 1e-13   # estimate = true residual
+
+
+@pytest.mark.parametrize("shape,seed,m", [((32,), 4, 5), ((16, 16), 6, 20), ((8, 8, 8), 7, 10)])
+def test_gmres_converged_equals_dense_LU(orc, shape, seed, m):
+    k2, S = _problem(shape, seed)
+    sp, w, M, b = _dense_M_b(orc, shape, k2, S)
+    res = orc.gmres(w, S, [1.0] * len(shape), sp.D, sp.sigma, sp.c, m, 1e-11, 20000)
+    assert res.rc == 0 and res.hist[-1] < 1e-11
+    A = dense_A(shape, w, sp.D, sp.c)
+    xref = np.linalg.solve(A, (S / sp.c).ravel())
+    assert np.linalg.norm(res.x.ravel() - xref) <= 1e-8 * np.linalg.norm(xref)
+    # GMRES minimises the residual: non-increasing within a cycle
+    for c0 in range(0, len(res.hist), m):
+        seg = res.hist[c0:c0 + m]
+        assert np.all(np.diff(seg) <= 1e-12 * seg[:-1])
