@@ -215,6 +215,21 @@ usp_status usp_krylov_workspace_size(usp_plan_t plan, size_t *bytes);
 usp_status usp_krylov_set_workspace(usp_plan_t plan, void *dev, size_t bytes);
 usp_status usp_bicgstab(usp_plan_t plan, int64_t n_max, double tol, int64_t *n_done, usp_term *term);
 
+/* Restarted GMRES(m) on the same system M x = b (
+ * Table 1b's GMRES5 / GMRES20 columns; Saad & Schultz
+ * 1986), reading R-28: x_0 = 0, restart every m Arnoldi steps,
+ * classical Gram-Schmidt applied twice (CGS2) by fused multi-dot / multi-axpy
+ * kernels over blocks of 8 basis vectors, Givens rotations and the small
+ * least-squares solve on the host in fp64.  Stops when the residual
+ * estimate |g_{j+1}| / ||b|| < tol (then x is updated) or after n_max
+ * Arnoldi steps; n_done = Arnoldi steps; the residual history is the estimate
+ * per step.  Workspace: b and the basis U_0..U_m (m + 2 complex64 fields,
+ * caller-owned, 256-B aligned); 2-D / 3-D complex64 on one GPU; starts right
+ * after usp_set_source.  Errors as usp_bicgstab. */
+usp_status usp_gmres_workspace_size(usp_plan_t plan, int m, size_t *bytes);
+usp_status usp_gmres_set_workspace(usp_plan_t plan, int m, void *dev, size_t bytes);
+usp_status usp_gmres(usp_plan_t plan, int64_t n_max, double tol, int64_t *n_done, usp_term *term);
+
 /* Kernel timing (CUDA events on the plan stream, per kernel class) for the
  * roofline report.  enable != 0 starts accumulating; usp_profile_read copies
  * up to cap entries of (name, total ms, launches) for the kernel classes. */

@@ -74,6 +74,10 @@ SIGNATURES = {
     "usp_krylov_set_workspace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "usp_bicgstab": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
                                     ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
+    "usp_gmres_workspace_size": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+    "usp_gmres_set_workspace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]),
+    "usp_gmres": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                 ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)]),
     "usp_last_error": (ctypes.c_char_p, []),
     "usp_version": (ctypes.c_char_p, []),
 }

@@ -99,12 +99,14 @@ struct XOp {
 // Stage slots per mode (each slot = one unit of one field):
 //   K_PFWD: r, p, v, B     K_VINV: work, p, B, rhat
 //   K_SFWD: r, v, B        K_TINV: work, s, B
+//   K_OFWD: p, B           K_OINV: work, p, B      (plain M p -> v, for GMRES)
 template <int N, int MODE>
 __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p) {
     using G = LineGeo<N>;
     using T = XOp<N>;
-    constexpr int NSLOT = (MODE == K_SFWD || MODE == K_TINV) ? 3 : 4;
-    constexpr bool INV = (MODE == K_VINV || MODE == K_TINV);
+    constexpr int NSLOT = (MODE == K_OFWD) ? 2 : ((MODE == K_SFWD || MODE == K_TINV || MODE == K_OINV) ? 3 : 4);
+    constexpr bool INV = (MODE == K_VINV || MODE == K_TINV || MODE == K_OINV);
+    constexpr bool PLAIN = (MODE == K_OFWD || MODE == K_OINV);   // GMRES: host-driven, no device state
     constexpr int NV = (MODE == K_TINV) ? 3 : (MODE == K_VINV ? 2 : (MODE == K_SFWD ? 1 : 0));
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stages = reinterpret_cast<float2 *>(smem_raw);
@@ -113,12 +115,12 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p) {
     uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N);
     uint64_t *empty = full + T::S;
 
-    {
+    if (!PLAIN) {
         const int status = p.st->status;
         if (p.st->k >= p.st->kmax || status != ST_RUNNING) return;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const KState ks = *p.ks;
+    const KState ks = PLAIN ? KState{} : *p.ks;
     const float2 beta = tof(ks.beta), omega = tof(ks.omega), alpha = tof(ks.alpha);
     double acc[NV > 0 ? NV : 1];
 #pragma unroll
@@ -141,6 +143,8 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p) {
     if (MODE == K_VINV) { src[0] = p.work; src[1] = p.p; src[2] = p.B; src[3] = p.rh; }
     if (MODE == K_SFWD) { src[0] = p.r; src[1] = p.v; src[2] = p.B; src[3] = nullptr; }
     if (MODE == K_TINV) { src[0] = p.work; src[1] = p.s; src[2] = p.B; src[3] = nullptr; }
+    if (MODE == K_OFWD) { src[0] = p.p; src[1] = p.B; src[2] = nullptr; src[3] = nullptr; }
+    if (MODE == K_OINV) { src[0] = p.work; src[1] = p.p; src[2] = p.B; src[3] = nullptr; }
 
     if (warp == T::XC) {
         if (lane == 0) {
@@ -179,7 +183,9 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p) {
                     const int e = sb + G::N1 * m;
                     const long long gi = gb + G::N1 * m;
                     float2 d;
-                    if (MODE == K_PFWD) {   // p = r + beta (p - omega v)
+                    if (MODE == K_OFWD) {   // plain: u = B p
+                        d = st[e];
+                    } else if (MODE == K_PFWD) {   // p = r + beta (p - omega v)
                         const float2 t = csub(st[T::UE + e], cmul(omega, st[2 * T::UE + e]));
                         d = cadd(st[e], cmul(beta, t));
                         p.p[gi] = d;
@@ -188,7 +194,7 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p) {
                         p.s[gi] = d;
                         la[0] += cabs2(d);
                     }
-                    v[m] = cmul(st[(MODE == K_PFWD ? 3 : 2) * T::UE + e], d);
+                    v[m] = cmul(st[(MODE == K_PFWD ? 3 : (MODE == K_OFWD ? 1 : 2)) * T::UE + e], d);
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -207,7 +213,9 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p) {
                     const long long gi = gb + G::N1 * m;
                     const float2 u = st[T::UE + e], b = st[2 * T::UE + e];
                     const float2 o = cmul(b, csub(u, cconj(v[m])));
-                    if (MODE == K_VINV) {                 // v; (rhat, v)
+                    if (MODE == K_OINV) {                 // plain: v = M p
+                        p.v[gi] = o;
+                    } else if (MODE == K_VINV) {          // v; (rhat, v)
                         p.v[gi] = o;
                         const float2 rh = st[3 * T::UE + e];
                         la[0] += rh.x * o.x + rh.y * o.y;
@@ -336,6 +344,57 @@ __global__ void __launch_bounds__(256) k_kupd(KParams p) {
     k->rho = rho1;
 }
 
+// GMRES(m) Gram-Schmidt blocks (NB <= 8 basis vectors per launch):
+//   GS_DOT:  partials of (U_j, z), j < NB (and ||z||^2 when want_norm)
+//   GS_AXPY: z <- scale (z - sum_j c_j U_j)  (and ||z||^2 of the result)
+// Per-thread fp32 over chunks of 64 elements, fp64 across chunks, fixed-order
+// CTA sums -> one row of partials per CTA (the host sums them in order).
+template <int NB, int MODE>
+__global__ void __launch_bounds__(256) k_gs(GSParams p) {
+    constexpr int K = (MODE == GS_DOT) ? 2 * NB + 1 : 1;
+    double acc[K];
+    float la[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) { acc[q] = 0.0; la[q] = 0.f; }
+    const long long n = p.n, stride = (long long)gridDim.x * blockDim.x;
+    int cnt = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
+        float2 z = p.z[i];
+        if (MODE == GS_DOT) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const float2 u = p.U[b][i];
+                la[2 * b] += u.x * z.x + u.y * z.y;
+                la[2 * b + 1] += u.x * z.y - u.y * z.x;
+            }
+            la[2 * NB] += cabs2(z);
+        } else {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) z = csub(z, cmul(p.c[b], p.U[b][i]));
+            z = cmul(p.scale, z);
+            p.z[i] = z;
+            la[0] += cabs2(z);
+        }
+        if (++cnt == 64) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) { acc[q] += (double)la[q]; la[q] = 0.f; }
+            cnt = 0;
+        }
+    }
+    __shared__ double sh[8][K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        double v = warp_sum_d(acc[q] + (double)la[q]);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5][q] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sh[w][threadIdx.x];
+        p.partials[(size_t)blockIdx.x * K + threadIdx.x] = s;
+    }
+}
+
 // ========================================================= launchers ====
 template <int N, int MODE>
 static cudaError_t xop_t(const KParams &p, int grid, cudaStream_t s) {
@@ -355,10 +414,28 @@ cudaError_t launch_xop(int N, KMode mode, const KParams &p, int grid, cudaStream
         if (mode == K_PFWD) return xop_t<n, K_PFWD>(p, grid, s);     \
         if (mode == K_VINV) return xop_t<n, K_VINV>(p, grid, s);     \
         if (mode == K_SFWD) return xop_t<n, K_SFWD>(p, grid, s);     \
+        if (mode == K_OFWD) return xop_t<n, K_OFWD>(p, grid, s);     \
+        if (mode == K_OINV) return xop_t<n, K_OINV>(p, grid, s);     \
         return xop_t<n, K_TINV>(p, grid, s);
     switch (N) { XO_CASE(16) XO_CASE(32) XO_CASE(64) XO_CASE(128) XO_CASE(256) XO_CASE(512) XO_CASE(1024)
                  XO_CASE(2048) default: return cudaErrorInvalidValue; }
 #undef XO_CASE
+}
+
+template <int MODE>
+static cudaError_t gs_mode(int nb, const GSParams &p, int grid, cudaStream_t s) {
+    switch (nb) {
+#define GS_CASE(b) \
+    case b: k_gs<b, MODE><<<grid, 256, 0, s>>>(p); break;
+        GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
+#undef GS_CASE
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gs(int mode, int nb, const GSParams &p, int grid, cudaStream_t s) {
+    return mode == GS_DOT ? gs_mode<GS_DOT>(nb, p, grid, s) : gs_mode<GS_AXPY>(nb, p, grid, s);
 }
 
 cudaError_t launch_kupd(const KParams &p, int grid, cudaStream_t s) {

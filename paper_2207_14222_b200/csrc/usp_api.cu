@@ -22,6 +22,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <complex>
 #include <cstdlib>
 #include <cmath>
 #include <cstdarg>
@@ -170,6 +171,12 @@ struct usp_plan_s {
     // BiCGSTAB (caller-owned Krylov workspace: rhat, p, v, s, t)
     float2 *k_rh = nullptr, *k_p = nullptr, *k_v = nullptr, *k_s = nullptr, *k_t = nullptr;
     KState *ks = nullptr;
+    // GMRES(m) (caller-owned workspace: b, U_0 .. U_m; plan-owned partials)
+    int gm_m = 0;
+    float2 *gm_b = nullptr;
+    std::vector<float2 *> gm_U;
+    double *gm_part = nullptr;
+    int gm_grid = 0;
     // antisymmetrised system (Eq. 9-10; desc.antisymmetric): two-component x,
     // Delta, work (component-major) and v = (w - sigma)/c in place of B
     bool anti = false;
@@ -1527,6 +1534,234 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
     return USP_OK;
 }
 
+usp_status usp_gmres_workspace_size(usp_plan_t p, int m, size_t *bytes) {
+    if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
+    if (m < 1 || m > 64) return fail(USP_ERR_ARG, "restart length m must be in [1, 64]");
+    *bytes = (size_t)(m + 2) * align256((size_t)p->nloc * sizeof(float2));
+    return USP_OK;
+}
+
+usp_status usp_gmres_set_workspace(usp_plan_t p, int m, void *dev, size_t bytes) {
+    if (!p || !dev) return fail(USP_ERR_ARG, "NULL argument");
+    if (((uintptr_t)dev) & 255) return fail(USP_ERR_ARG, "GMRES workspace must be 256-byte aligned");
+    size_t need = 0;
+    usp_status s = usp_gmres_workspace_size(p, m, &need);
+    if (s) return s;
+    if (bytes < need) return fail(USP_ERR_NOMEM, "GMRES workspace %zu bytes < required %zu", bytes, need);
+    const size_t f = align256((size_t)p->nloc * sizeof(float2));
+    p->gm_m = m;
+    p->gm_b = (float2 *)dev;
+    p->gm_U.assign(m + 1, nullptr);
+    for (int j = 0; j <= m; ++j) p->gm_U[j] = (float2 *)((char *)dev + (size_t)(j + 1) * f);
+    return USP_OK;
+}
+
+namespace {
+typedef std::complex<double> zd;
+
+// Gram-Schmidt over basis vectors U[0..nv) in blocks of 8: GS_DOT returns
+// d_j = (U_j, z) (+ ||z||^2 in *nrm); GS_AXPY applies z <- scale (z - sum c_j U_j)
+// and returns ||z||^2 of the result.  Partial rows summed on the host in CTA order.
+usp_status gs_dots(usp_plan_s *p, int nv, float2 *z, std::vector<zd> &d, double *nrm) {
+    d.assign(nv, zd(0.0, 0.0));
+    std::vector<double> h((size_t)p->gm_grid * 17);
+    for (int b0 = 0; b0 < nv; b0 += 8) {
+        const int nb = std::min(8, nv - b0);
+        GSParams g{};
+        for (int q = 0; q < nb; ++q) g.U[q] = p->gm_U[b0 + q];
+        g.z = z;
+        g.n = p->nloc;
+        g.partials = p->gm_part;
+        {
+            Tick t(p, KC_KUPD);
+            CU(launch_gs(GS_DOT, nb, g, p->gm_grid, p->stream));
+        }
+        const int K = 2 * nb + 1;
+        CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * K * p->gm_grid, cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        for (int q = 0; q < nb; ++q) {
+            double re = 0.0, im = 0.0;
+            for (int c = 0; c < p->gm_grid; ++c) {
+                re += h[(size_t)c * K + 2 * q];
+                im += h[(size_t)c * K + 2 * q + 1];
+            }
+            d[b0 + q] = zd(re, im);
+        }
+        if (nrm && b0 == 0) {
+            double s2 = 0.0;
+            for (int c = 0; c < p->gm_grid; ++c) s2 += h[(size_t)c * K + 2 * nb];
+            *nrm = s2;
+        }
+    }
+    return USP_OK;
+}
+
+usp_status gs_axpy(usp_plan_s *p, int nv, const std::vector<float2 *> &U, const std::vector<zd> &c, float2 *z,
+                   zd scale, double *nrm) {
+    std::vector<double> h(p->gm_grid);
+    double s2 = 0.0;
+    for (int b0 = 0; b0 < std::max(nv, 1); b0 += 8) {
+        const int nb = std::min(8, nv - b0);
+        GSParams g{};
+        for (int q = 0; q < nb; ++q) {
+            g.U[q] = U[b0 + q];
+            g.c[q] = make_float2((float)c[b0 + q].real(), (float)c[b0 + q].imag());
+        }
+        const bool last = b0 + 8 >= nv;
+        g.scale = last ? make_float2((float)scale.real(), (float)scale.imag()) : make_float2(1.f, 0.f);
+        g.z = z;
+        g.n = p->nloc;
+        g.partials = p->gm_part;
+        {
+            Tick t(p, KC_KUPD);
+            CU(launch_gs(GS_AXPY, nb, g, p->gm_grid, p->stream));
+        }
+        if (last && nrm) {
+            CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * p->gm_grid, cudaMemcpyDeviceToHost, p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            for (int q = 0; q < p->gm_grid; ++q) s2 += h[q];
+        }
+    }
+    if (nrm) *nrm = s2;
+    return USP_OK;
+}
+
+// z = M u (the operator of the fixed-point path: two x passes + the chain)
+usp_status apply_M_dev(usp_plan_s *p, float2 *u, float2 *z) {
+    KParams kp{};
+    kp.work = p->work;
+    kp.p = u;
+    kp.v = z;
+    kp.B = p->B;
+    kp.tw = p->tw[0];
+    kp.nlines = p->ny * p->nzh;
+    kp.st = p->st;
+    usp_status s;
+    {
+        Tick t(p, KC_XOP);
+        CU(launch_xop((int)p->nx, K_OFWD, kp, p->gridp_x, p->stream));
+    }
+    if ((s = chain_mid(p, 0))) return s;
+    Tick t(p, KC_XOP);
+    CU(launch_xop((int)p->nx, K_OINV, kp, p->gridp_x, p->stream));
+    return USP_OK;
+}
+}  // namespace
+
+usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, usp_term *term) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
+    if (!p->gm_b) return fail(USP_ERR_STATE, "usp_gmres_set_workspace must be called first");
+    if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
+    if (p->ndim < 2 || p->real || p->anti || multi_rank(p) || !p->pipe_xk)
+        return fail(USP_ERR_UNSUPPORTED, "GMRES runs on 2-D / 3-D complex64 plans on one GPU");
+    usp_status s = sync_state(p);
+    if (s) return s;
+    if (p->st_host->k != 0)
+        return fail(USP_ERR_STATE, "GMRES starts from x_0 = 0: call usp_set_source again first");
+    if (!p->gm_part) {
+        p->gm_grid = p->nsm * 4;
+        CU(cudaMalloc(&p->gm_part, sizeof(double) * 17 * p->gm_grid));
+    }
+    const int m = p->gm_m;
+    const long long nvb = (long long)p->nloc * sizeof(float2);
+    const double nb = p->st_host->n0;   // ||b||, b = Delta_0 = B (L+1)^-1 s
+    CU(cudaMemcpyAsync(p->gm_b, p->delta, nvb, cudaMemcpyDeviceToDevice, p->stream));
+    std::vector<double> hist;
+    long long steps = 0;
+    double est = nb > 0.0 ? 1.0 : 0.0;
+    int status = nb > 0.0 ? ST_RUNNING : ST_DONE_CONV;
+    std::vector<double> nu(m + 1);
+    std::vector<zd> H((size_t)(m + 1) * m), cs(m), sn(m), g(m + 1), y(m), d, d2;
+    bool first = true;
+    while (status == ST_RUNNING && steps < n_max) {
+        // r = b - M x  (x = 0 on the first cycle: r = b)
+        double b2 = 0.0;
+        if (first) {
+            CU(cudaMemcpyAsync(p->gm_U[0], p->gm_b, nvb, cudaMemcpyDeviceToDevice, p->stream));
+            b2 = nb * nb;
+        } else {
+            if ((s = apply_M_dev(p, p->x, p->gm_U[0]))) return s;
+            std::vector<float2 *> Ub{p->gm_b};
+            if ((s = gs_axpy(p, 1, Ub, std::vector<zd>{zd(1.0, 0.0)}, p->gm_U[0], zd(-1.0, 0.0), &b2))) return s;
+        }
+        first = false;
+        nu[0] = std::sqrt(b2);
+        const double beta = nu[0];
+        if (!(beta > 0.0)) { status = ST_DONE_CONV; break; }
+        std::fill(g.begin(), g.end(), zd(0.0, 0.0));
+        g[0] = beta;
+        int k = 0;
+        bool stop = false;
+        for (int j = 0; j < m && steps < n_max; ++j) {
+            // z = M U_j into U_{j+1}: the stored vectors are U_i = nu_i v_i
+            if ((s = apply_M_dev(p, p->gm_U[j], p->gm_U[j + 1]))) return s;
+            std::vector<zd> hcol(j + 2, zd(0.0, 0.0));
+            double z2 = 0.0;
+            for (int round = 0; round < 2; ++round) {   // classical Gram-Schmidt, twice (CGS2)
+                if ((s = gs_dots(p, j + 1, p->gm_U[j + 1], d, nullptr))) return s;
+                std::vector<zd> c(j + 1);
+                for (int i = 0; i <= j; ++i) {
+                    c[i] = d[i] / (nu[i] * nu[i]);
+                    hcol[i] += d[i] / (nu[i] * nu[j]);
+                }
+                std::vector<float2 *> Ub(p->gm_U.begin(), p->gm_U.begin() + j + 1);
+                if ((s = gs_axpy(p, j + 1, Ub, c, p->gm_U[j + 1], zd(1.0, 0.0), &z2))) return s;
+            }
+            nu[j + 1] = std::sqrt(z2);
+            hcol[j + 1] = nu[j + 1] / nu[j];
+            for (int i = 0; i < j; ++i) {   // previous rotations
+                const zd t = cs[i] * hcol[i] + sn[i] * hcol[i + 1];
+                hcol[i + 1] = -std::conj(sn[i]) * hcol[i] + std::conj(cs[i]) * hcol[i + 1];
+                hcol[i] = t;
+            }
+            const double den = std::sqrt(std::norm(hcol[j]) + std::norm(hcol[j + 1]));
+            if (!(den > 0.0)) { status = ST_DIVERGED; break; }
+            cs[j] = std::conj(hcol[j]) / den;
+            sn[j] = hcol[j + 1] / den;
+            hcol[j] = den;
+            hcol[j + 1] = 0.0;
+            for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = hcol[i];
+            g[j + 1] = -std::conj(sn[j]) * g[j];
+            g[j] = cs[j] * g[j];
+            ++steps;
+            k = j + 1;
+            est = std::abs(g[j + 1]) / nb;
+            hist.push_back(est);
+            if (!std::isfinite(est) || est > 1e6) { status = ST_DIVERGED; stop = true; break; }
+            if ((tol > 0.0 && est < tol) || nu[j + 1] == 0.0) { status = ST_DONE_CONV; stop = true; break; }
+        }
+        if (status == ST_DIVERGED && !stop) break;
+        // y = R^-1 g; x += sum y_i v_i = sum (y_i / nu_i) U_i
+        for (int i = k - 1; i >= 0; --i) {
+            zd acc = g[i];
+            for (int q = i + 1; q < k; ++q) acc -= H[(size_t)i * m + q] * y[q];
+            y[i] = acc / H[(size_t)i * m + i];
+        }
+        std::vector<zd> c(k);
+        for (int i = 0; i < k; ++i) c[i] = -y[i] / nu[i];
+        std::vector<float2 *> Ub(p->gm_U.begin(), p->gm_U.begin() + k);
+        if (k > 0 && (s = gs_axpy(p, k, Ub, c, p->x, zd(1.0, 0.0), nullptr))) return s;
+        if (stop) break;
+    }
+    // publish the state (k = Arnoldi steps, r = residual estimate, history)
+    IterState h = *p->st_host;
+    h.k = steps;
+    h.r = est;
+    h.status = status == ST_RUNNING ? ST_RUNNING : status;
+    CU(cudaMemcpyAsync(p->st, &h, sizeof h, cudaMemcpyHostToDevice, p->stream));
+    for (size_t i = 0; i < hist.size(); ++i) {
+        const long long kk = (long long)i + 1;
+        CU(cudaMemcpyAsync(p->hist + (kk % p->hist_cap), &hist[i], sizeof(double), cudaMemcpyHostToDevice,
+                           p->stream));
+    }
+    if ((s = sync_state(p))) return s;
+    drain_timing(p);
+    if (n_done) *n_done = steps;
+    if (term) *term = status == ST_DONE_CONV ? USP_CONVERGED : (status == ST_DIVERGED ? USP_DIVERGED : USP_MAX_ITER);
+    return USP_OK;
+}
+
 usp_status usp_profile_enable(usp_plan_t p, int enable) {
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     drain_timing(p);
@@ -1575,6 +1810,7 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->far_i);
     cudaFree(p->coll);
     cudaFree(p->ks);
+    cudaFree(p->gm_part);
     cudaFree(p->bar);
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
     cudaFree(p->twr);

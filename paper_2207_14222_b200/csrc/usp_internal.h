@@ -71,7 +71,18 @@ struct XParams {
 };
 
 // ------------------------------------------------------- BiCGSTAB (NEXT-2) --
-enum KMode : int { K_PFWD = 0, K_VINV = 1, K_SFWD = 2, K_TINV = 3 };
+enum KMode : int { K_PFWD = 0, K_VINV = 1, K_SFWD = 2, K_TINV = 3, K_OFWD = 4, K_OINV = 5 };
+
+// GMRES(m) Gram-Schmidt blocks (kernels_krylov.cu k_gs)
+enum GSMode : int { GS_DOT = 0, GS_AXPY = 1 };
+struct GSParams {
+    const float2 *U[8];  // basis block
+    float2 c[8];         // GS_AXPY coefficients
+    float2 scale;        // GS_AXPY: z <- scale (z - sum c_j U_j)
+    float2 *z;
+    long long n;
+    double *partials;    // per CTA: 2 NB + 1 (GS_DOT) or 1 (GS_AXPY) doubles
+};
 
 struct KState {          // BiCGSTAB scalars (fp64, device)
     double2 rho, alpha, omega, beta;
@@ -209,6 +220,7 @@ cudaError_t launch_solve2d(int nx, int ny, const S2Params &p, int nsm, cudaStrea
 // BiCGSTAB (kernels_krylov.cu)
 cudaError_t launch_xop(int N, KMode mode, const KParams &p, int grid, cudaStream_t s);
 cudaError_t launch_kupd(const KParams &p, int grid, cudaStream_t s);
+cudaError_t launch_gs(int mode, int nb, const GSParams &p, int grid, cudaStream_t s);
 
 // real path (kernels_real.cu)
 cudaError_t launch_xpass_real(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);

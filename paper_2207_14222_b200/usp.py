@@ -151,6 +151,25 @@ class Plan:
         L.check(self.lib.usp_bicgstab(self.handle, int(n_max), float(tol), ctypes.byref(nd), ctypes.byref(term)))
         return int(nd.value), _TERM[term.value]
 
+    def gmres(self, m: int, n_max: int, tol: float = 0.0) -> Tuple[int, str]:
+        """Restarted GMRES(m) on the preconditioned system (usp_gmres); starts
+        from x_0 = 0 right after set_source.  Allocates the GMRES workspace
+        (m + 2 complex64 fields) for this m on first use.  Returns (Arnoldi
+        steps, termination)."""
+        import torch
+
+        if getattr(self, "gworkspace_m", None) != m:
+            nbytes = ctypes.c_size_t()
+            L.check(self.lib.usp_gmres_workspace_size(self.handle, int(m), ctypes.byref(nbytes)))
+            self.gworkspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+            L.check(self.lib.usp_gmres_set_workspace(self.handle, int(m), ctypes.c_void_p(self.gworkspace.data_ptr()),
+                                                     int(nbytes.value)))
+            self.gworkspace_m = m
+        nd = ctypes.c_int64()
+        term = ctypes.c_int()
+        L.check(self.lib.usp_gmres(self.handle, int(n_max), float(tol), ctypes.byref(nd), ctypes.byref(term)))
+        return int(nd.value), _TERM[term.value]
+
     def residual(self) -> Tuple[float, float, int]:
         r, a, k = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
         L.check(self.lib.usp_residual(self.handle, ctypes.byref(r), ctypes.byref(a), ctypes.byref(k)))

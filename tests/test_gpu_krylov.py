@@ -133,3 +133,49 @@ def test_bicgstab_state_errors():
         pl.set_potential(torch.from_numpy(m1).cuda(), 0.95)
         pl.set_source(torch.from_numpy(s1).cuda())
         pl.bicgstab(5, 0.0)                       # 1-D
+
+
+# ------------------------------------------------------------- GMRES(m) --
+def _gpu_gmres(p, m, n, tol):
+    import torch
+    from paper_2207_14222_b200 import Plan
+
+    med, src, dtype = rounded_inputs(p)
+    plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype)
+    plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
+    plan.set_source(torch.from_numpy(src).cuda())
+    nd, term = plan.gmres(m, n, tol)
+    return plan.get_field().cpu().numpy().astype(np.complex128), nd, term, plan
+
+
+def _orc_gmres(orc, p, m, n, tol):
+    med, src, _ = rounded_inputs(p)
+    med64 = med.astype(np.complex128)
+    sp = orc.canonical(p.kind, med64, 0.95, D=p.D)
+    return orc.gmres(orc.medium_to_w(p.kind, med64), src.astype(np.complex128), p.h, sp.D, sp.sigma, sp.c,
+                     m, tol, n)
+
+
+@pytest.mark.parametrize("name,shape,m,n", [("C3", (64, 64, 64), 5, 20), ("C3", (64, 64, 64), 20, 40),
+                                            ("C2", (128, 128), 20, 60), ("C5", (32, 64, 128), 10, 25)])
+def test_gmres_fixed_steps_match_oracle(orc, name, shape, m, n):
+    from synth import make
+
+    p = make(name, shape)
+    x, nd, term, plan = _gpu_gmres(p, m, n, 0.0)
+    assert nd == n and term == "max_iter"
+    ref = _orc_gmres(orc, p, m, n, 0.0)
+    assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)
+    assert np.allclose(plan.history()[1:n + 1], ref.hist[:n], rtol=2e-3, atol=1e-7)
+
+
+@pytest.mark.parametrize("name,shape,m", [("C3", (64, 64, 64), 20), ("C2", (128, 128), 20)])
+def test_gmres_converges_like_oracle(orc, name, shape, m):
+    from synth import make
+
+    p = make(name, shape)
+    x, nd, term, plan = _gpu_gmres(p, m, 5000, 1e-5)
+    ref = _orc_gmres(orc, p, m, 5000, 1e-5)
+    assert term == "converged" and ref.rc == 0
+    assert abs(nd - ref.n_done) <= max(1, 0.03 * ref.n_done), (nd, ref.n_done)
+    assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)

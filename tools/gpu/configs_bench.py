@@ -23,8 +23,8 @@ for name in only:
     with torch.cuda.stream(stream):
         plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype="r32" if real else "c64", stream=stream, device=dev)
         res = {}
-        for solver in ("fixed_point", "fixed_point", "bicgstab", "bicgstab"):
-            if solver == "bicgstab" and (real or len(p.shape) == 1):
+        for solver in ("fixed_point", "fixed_point", "bicgstab", "bicgstab", "gmres20", "gmres20"):
+            if solver != "fixed_point" and (real or len(p.shape) == 1):
                 continue
             plan.set_potential(med, 0.95)
             plan.set_source(src)
@@ -33,8 +33,10 @@ for name in only:
             a.record(stream)
             if solver == "fixed_point":
                 n, term = plan.iterate(p.n_iter, p.alpha, p.tol)
-            else:
+            elif solver == "bicgstab":
                 n, term = plan.bicgstab(20000, p.tol if p.tol > 0 else 1e-6)
+            else:
+                n, term = plan.gmres(20, 40000, p.tol if p.tol > 0 else 1e-6)
             b.record(stream)
             torch.cuda.synchronize()
             ms = a.elapsed_time(b)
