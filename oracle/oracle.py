@@ -16,6 +16,8 @@ What it computes (PAPER.md = /root/reference/PAPER.md):
   Delta-form recurrence (L613) for the R-17 cross-check.
 * ``canonical_anti``, ``fixed_point_anti`` -- the antisymmetrised system of
   Eq. 9-10 (L100-128) for problems that are not accretive.
+* ``canonical_tdiff``, ``fixed_point_tdiff`` -- the first-order (u, F)
+  form of tensor-D steady diffusion, §3.2 Eqs. 16-18 (L199-227).
 * ``gmres``                        -- restarted GMRES(m) on the same system
   (Table 1b's GMRES5 / GMRES20 columns).
 * ``bicgstab``                     -- BiCGSTAB on the preconditioned system
@@ -66,6 +68,8 @@ def lib():
         L.orc_mec.argtypes = [dp, dp, ctypes.c_long, dp, dp, dp]
         L.orc_fixed_point_anti.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 3
                                            + [ctypes.c_double, ctypes.c_double, ctypes.c_long, dp, dp, lp, dp])
+        L.orc_fixed_point_tdiff.argtypes = ([dp, dp, dp, ctypes.c_int, lp, dp, ctypes.c_double, dp]
+                                            + [ctypes.c_double] * 5 + [ctypes.c_long, dp, dp, lp, dp])
         L.orc_gmres.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 4
                                 + [ctypes.c_int, ctypes.c_double, ctypes.c_long, dp, dp, lp, dp])
         L.orc_bicgstab.argtypes = ([dp, dp, ctypes.c_int, lp, dp, ctypes.c_double] + [ctypes.c_double] * 4
@@ -244,6 +248,76 @@ def fixed_point_anti(w, S, h: Sequence[float], D: float, sigma: complex, c: floa
     if rc < 0:
         raise ValueError(f"orc_fixed_point_anti rc={rc}")
     return Result(x=x, n_done=int(nd.value), hist=hist[: nd.value].copy(), n0=float(n0.value), rc=rc)
+
+
+@dataclass
+class TdiffSplit:
+    """Canonical form of the first-order tensor-diffusion system (reading R-29)."""
+
+    mubar: float
+    dbar: np.ndarray      # packed symmetric Dbar^-1 (2-D: xx, xy, yy; 3-D: xx, xy, xz, yy, yz, zz)
+    s_u: float
+    s_F: float
+    c: float
+
+
+def _sym_pack_index(d):
+    return [(0, 0), (0, 1), (1, 1)] if d == 2 else [(0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2)]
+
+
+def dinv_field(D):
+    """Per-voxel inverse of the symmetric tensor field D[..., d, d], packed."""
+    Dinv = np.linalg.inv(np.asarray(D, dtype=np.float64))
+    d = Dinv.shape[-1]
+    return np.stack([Dinv[..., i, j] for i, j in _sym_pack_index(d)], axis=-1)
+
+
+def canonical_tdiff(mu, D, target_norm: float = 0.95) -> TdiffSplit:
+    """§3.2 (L222-225): the centre of the smallest circle of every element of
+    V_raw goes into L (for real values: the mid-range) -> mubar, Dbar^-1;
+    the radii are equilibrated by S = diag(s_u, s_F, ..) with s_u = radius of
+    mu and s_F = the largest radius of the D^-1 elements (reading R-29 of the
+    paper's [duff2001] equilibration); finally c = max_r ||V(r)||_F-bound /
+    target_norm, using max(|mu - mubar|/s_u, ||D^-1 - Dbar^-1||_F / s_F)."""
+    mu = np.asarray(mu, dtype=np.float64)
+    dpk = dinv_field(D)
+    d = np.asarray(D).shape[-1]
+    mubar = 0.5 * (mu.max() + mu.min())
+    r_mu = 0.5 * (mu.max() - mu.min())
+    lo, hi = dpk.reshape(-1, dpk.shape[-1]).min(axis=0), dpk.reshape(-1, dpk.shape[-1]).max(axis=0)
+    dbar = 0.5 * (hi + lo)
+    r_d = 0.5 * (hi - lo)
+    s_u = r_mu if r_mu > 0 else 1.0
+    s_F = r_d.max() if r_d.max() > 0 else 1.0
+    diff = (dpk - dbar) / s_F
+    w = np.ones(dpk.shape[-1])
+    for k, (i, j) in enumerate(_sym_pack_index(d)):
+        w[k] = 1.0 if i == j else 2.0          # off-diagonal elements appear twice in ||.||_F
+    fro = np.sqrt(np.sum(w * diff ** 2, axis=-1))
+    vmax = max(np.abs(mu - mubar).max() / s_u, fro.max())
+    return TdiffSplit(mubar=float(mubar), dbar=dbar.astype(np.float64), s_u=float(s_u), s_F=float(s_F),
+                      c=float(vmax / target_norm))
+
+
+def fixed_point_tdiff(mu, D, S, h: Sequence[float], split: TdiffSplit, alpha: float, tol: float,
+                      n_max: int) -> Result:
+    """Algorithm 1 on the first-order (u, F) system of §3.2 (Eqs. 16-18).
+    Returns Result with x = E [(d+1), *shape] (E[0] = sqrt(s_u) u)."""
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    dpk = np.ascontiguousarray(dinv_field(D), dtype=np.float64)
+    Sr = np.ascontiguousarray(np.real(S), dtype=np.float64)
+    d = mu.ndim
+    E = np.zeros((d + 1,) + mu.shape, dtype=np.complex128)
+    hist = np.zeros(n_max, dtype=np.float64)
+    hh = np.ascontiguousarray(h, dtype=np.float64)
+    nd, n0 = ctypes.c_long(0), ctypes.c_double(0.0)
+    db = np.ascontiguousarray(split.dbar, dtype=np.float64)
+    rc = lib().orc_fixed_point_tdiff(_dp(mu), _dp(dpk), _dp(Sr), d, _dims(mu.shape), _dp(hh), split.mubar, _dp(db),
+                                     split.s_u, split.s_F, split.c, float(alpha), float(tol), int(n_max),
+                                     _dp(E.view(np.float64)), _dp(hist), ctypes.byref(nd), ctypes.byref(n0))
+    if rc < 0:
+        raise ValueError(f"orc_fixed_point_tdiff rc={rc}")
+    return Result(x=E, n_done=int(nd.value), hist=hist[: nd.value].copy(), n0=float(n0.value), rc=rc)
 
 
 @dataclass

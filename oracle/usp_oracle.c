@@ -35,6 +35,9 @@
  *                 (PAPER.md L100-128): E = [x, x'], A = c^-1 [[0, -A_raw*], [A_raw, 0]],
  *                 real c, for problems whose numerical range is not confined
  *                 to a half plane (e.g. gain media).
+ *   orc_fixed_point_tdiff  Algorithm 1 on the first-order (u, F) form of
+ *                 steady diffusion with a tensor D (§3.2 Eqs. 16-18,
+ *                 L199-227): d + 1 components, block-diagonal V.
  *   orc_gmres     restarted GMRES(m) (Saad & Schultz 1986; Table 1b's GMRES5 /
  *                 GMRES20 columns) on the same system.
  *   orc_bicgstab  BiCGSTAB [van der Vorst 1992, cited PAPER.md L384] on the
@@ -509,6 +512,171 @@ int orc_bicgstab(const double *w, const double *S, int ndim, const long *dims, c
     }
 done:
     free(B); free(sv); free(r); free(rh); free(p); free(v); free(sr); free(t); free(tmp);
+    return rc;
+}
+
+/* ------------------------------------------- tensor diffusion (u, F) -- */
+/*
+ * PAPER.md §3.2 (L199-227), steady state (d_t = 0): F = -D grad u splits
+ * div(D grad u) - mu u + S = 0 into
+ *     mu u + div F = S,      D^-1 F + grad u = 0                (Eqs. 16-17)
+ * i.e. A_raw [u; F] = [S; 0] with A_raw = [[mu, div], [grad, D^-1]], and
+ *     L = c^-1 S^-1/2 [[mubar, div], [grad, Dbar^-1]] S^-1/2,
+ *     V = c^-1 S^-1/2 [[mu - mubar, 0], [0, D^-1 - Dbar^-1]] S^-1/2,
+ *     E = S^1/2 [u; F],   s = c^-1 S^-1/2 [S; 0]                 (Eq. 18)
+ * with S = diag(s_u, s_F, .., s_F) (the canonical-form parameters mubar,
+ * Dbar^-1, s_u, s_F, c come from oracle.py canonical_tdiff, reading R-29).
+ * Per Fourier mode (grad -> i p, div -> i p^T):
+ *     L + 1 = [[a, i q^T], [i q, Dm]],  a = mubar/(c s_u) + 1,
+ *     q = p / (c sqrt(s_u s_F)),  Dm = Dbar^-1 / (c s_F) + I
+ * inverted by its Schur complement: w = Dm^-1 q, sig = a + q^T w,
+ *     out_u = (u - i w^T F) / sig
+ *     out_F = Dm^-1 F - i w out_u
+ * (Dm symmetric).  V per voxel: v_u = (mu - mubar)/(c s_u) and the d x d
+ * block Vf = (D^-1 - Dbar^-1)/(c s_F); B = 1 - V.  Fields are stored
+ * component-major: E[k][voxel], k = 0 (u), 1..d (F_x, F_y, F_z in axis
+ * order x, y, z).  Algorithm 1 x-form; r_k over all components.
+ *
+ * Inputs: mu[n], dinv[n][d(d+1)/2] (the symmetric D^-1 per voxel, packed
+ * row-major upper: 2-D xx, xy, yy; 3-D xx, xy, xz, yy, yz, zz), S[n] (real),
+ * mubar, dbar[d(d+1)/2] (Dbar^-1 packed), s_u, s_F, c.  Output E[(d+1) n]
+ * complex (the first component is sqrt(s_u) u).
+ */
+static void sym_unpack(const double *pk, int d, double M[3][3]) {
+    if (d == 2) {
+        M[0][0] = pk[0]; M[0][1] = M[1][0] = pk[1]; M[1][1] = pk[2];
+    } else {
+        M[0][0] = pk[0]; M[0][1] = M[1][0] = pk[1]; M[0][2] = M[2][0] = pk[2];
+        M[1][1] = pk[3]; M[1][2] = M[2][1] = pk[4]; M[2][2] = pk[5];
+    }
+}
+
+/* inverse of a symmetric d x d matrix by cofactors (d = 2, 3) */
+static void sym_inv(double M[3][3], int d, double R[3][3]) {
+    if (d == 2) {
+        double det = M[0][0] * M[1][1] - M[0][1] * M[1][0];
+        R[0][0] = M[1][1] / det; R[1][1] = M[0][0] / det;
+        R[0][1] = R[1][0] = -M[0][1] / det;
+        return;
+    }
+    double c00 = M[1][1] * M[2][2] - M[1][2] * M[2][1], c01 = M[1][2] * M[2][0] - M[1][0] * M[2][2];
+    double c02 = M[1][0] * M[2][1] - M[1][1] * M[2][0];
+    double det = M[0][0] * c00 + M[0][1] * c01 + M[0][2] * c02;
+    R[0][0] = c00 / det; R[1][0] = c01 / det; R[2][0] = c02 / det;
+    R[0][1] = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) / det;
+    R[1][1] = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) / det;
+    R[2][1] = (M[0][1] * M[2][0] - M[0][0] * M[2][1]) / det;
+    R[0][2] = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) / det;
+    R[1][2] = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) / det;
+    R[2][2] = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) / det;
+}
+
+static int apply_Linv_tdiff(cplx *E, long n, int ndim, const long *dims, const double *h, double a,
+                            double Dm_inv[3][3], double qs) {
+    int d = ndim;
+    for (int k = 0; k <= d; ++k) {
+        int rc = orc_fftn((double *)(E + (size_t)k * n), ndim, dims, 0);
+        if (rc) return rc;
+    }
+    long nx = dims[ndim - 1], ny = ndim >= 2 ? dims[ndim - 2] : 1, nz = ndim >= 3 ? dims[ndim - 3] : 1;
+    double hx = h[ndim - 1], hy = ndim >= 2 ? h[ndim - 2] : 1.0, hz = ndim >= 3 ? h[ndim - 3] : 1.0;
+#pragma omp parallel for schedule(static)
+    for (long l = 0; l < nz; ++l)
+        for (long j = 0; j < ny; ++j)
+            for (long i = 0; i < nx; ++i) {
+                long v = (l * ny + j) * nx + i;
+                double pv[3] = {freq(i, nx, hx), ndim >= 2 ? freq(j, ny, hy) : 0.0, ndim >= 3 ? freq(l, nz, hz) : 0.0};
+                double q[3], w[3] = {0, 0, 0}, sig = a;
+                for (int k = 0; k < d; ++k) q[k] = pv[k] * qs;
+                for (int k = 0; k < d; ++k)
+                    for (int m = 0; m < d; ++m) w[k] += Dm_inv[k][m] * q[m];
+                for (int k = 0; k < d; ++k) sig += q[k] * w[k];
+                cplx u = E[v], F[3], wF = 0.0;
+                for (int k = 0; k < d; ++k) { F[k] = E[(size_t)(k + 1) * n + v]; wF += w[k] * F[k]; }
+                cplx ou = (u - I * wF) / sig;
+                E[v] = ou;
+                for (int k = 0; k < d; ++k) {
+                    cplx acc = 0.0;
+                    for (int m = 0; m < d; ++m) acc += Dm_inv[k][m] * F[m];
+                    E[(size_t)(k + 1) * n + v] = acc - I * w[k] * ou;
+                }
+            }
+    for (int k = 0; k <= d; ++k) {
+        int rc = orc_fftn((double *)(E + (size_t)k * n), ndim, dims, 1);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+/* out = B in, B = 1 - V per voxel (block-diagonal) */
+static void apply_B_tdiff(const cplx *in, cplx *out, long n, int d, const double *vu, const double *vf) {
+    const int np = d * (d + 1) / 2;
+    for (long v = 0; v < n; ++v) {
+        double Vf[3][3];
+        sym_unpack(vf + (size_t)v * np, d, Vf);
+        out[v] = (1.0 - vu[v]) * in[v];
+        for (int k = 0; k < d; ++k) {
+            cplx acc = in[(size_t)(k + 1) * n + v];
+            for (int m = 0; m < d; ++m) acc -= Vf[k][m] * in[(size_t)(m + 1) * n + v];
+            out[(size_t)(k + 1) * n + v] = acc;
+        }
+    }
+}
+
+int orc_fixed_point_tdiff(const double *mu, const double *dinv, const double *S, int ndim, const long *dims,
+                          const double *h, double mubar, const double *dbar, double s_u, double s_F, double c,
+                          double alpha, double tol, long n_max, double *E_out, double *hist, long *n_done,
+                          double *n0_out) {
+    if (ndim < 2 || ndim > 3 || n_max < 1 || !(c > 0.0) || !(s_u > 0.0) || !(s_F > 0.0)) return -2;
+    long n = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (!is_pow2(dims[a])) return -1;
+        n *= dims[a];
+    }
+    const int d = ndim, nc = d + 1, np = d * (d + 1) / 2;
+    size_t bytes = sizeof(cplx) * (size_t)n * nc;
+    double *vu = malloc(sizeof(double) * n), *vf = malloc(sizeof(double) * n * np);
+    cplx *s = malloc(bytes), *u = malloc(bytes), *Dl = malloc(bytes), *E = (cplx *)E_out;
+    int rc = 0;
+    *n_done = 0;
+    if (!vu || !vf || !s || !u || !Dl) { rc = -3; goto done; }
+    for (long v = 0; v < n; ++v) {
+        vu[v] = (mu[v] - mubar) / (c * s_u);
+        for (int q = 0; q < np; ++q) vf[(size_t)v * np + q] = (dinv[(size_t)v * np + q] - dbar[q]) / (c * s_F);
+    }
+    double Db[3][3], Dm[3][3], Dm_inv[3][3];
+    sym_unpack(dbar, d, Db);
+    for (int k = 0; k < d; ++k)
+        for (int m = 0; m < d; ++m) Dm[k][m] = Db[k][m] / (c * s_F) + (k == m ? 1.0 : 0.0);
+    sym_inv(Dm, d, Dm_inv);
+    const double a = mubar / (c * s_u) + 1.0, qs = 1.0 / (c * sqrt(s_u * s_F));
+    for (size_t q = 0; q < (size_t)n * nc; ++q) s[q] = 0.0;
+    for (long v = 0; v < n; ++v) s[v] = S[v] / (c * sqrt(s_u));
+    /* n0 = ||B (L+1)^-1 s|| */
+    memcpy(u, s, bytes);
+    rc = apply_Linv_tdiff(u, n, ndim, dims, h, a, Dm_inv, qs);
+    if (rc) goto done;
+    apply_B_tdiff(u, Dl, n, d, vu, vf);
+    double n0 = norm2(Dl, n * nc);
+    if (n0_out) *n0_out = n0;
+    for (size_t q = 0; q < (size_t)n * nc; ++q) E[q] = 0.0;
+    if (n0 == 0.0) goto done;
+    for (long k = 0; k < n_max; ++k) {
+        apply_B_tdiff(E, u, n, d, vu, vf);                               /* u = B E + s */
+        for (size_t q = 0; q < (size_t)n * nc; ++q) u[q] += s[q];
+        rc = apply_Linv_tdiff(u, n, ndim, dims, h, a, Dm_inv, qs);
+        if (rc) goto done;
+        for (size_t q = 0; q < (size_t)n * nc; ++q) u[q] -= E[q];       /* Delta = B (y - E) */
+        apply_B_tdiff(u, Dl, n, d, vu, vf);
+        for (size_t q = 0; q < (size_t)n * nc; ++q) E[q] += alpha * Dl[q];
+        double r = norm2(Dl, n * nc) / n0;
+        if (hist) hist[k] = r;
+        *n_done = k + 1;
+        if (!isfinite(r)) { rc = 1; goto done; }
+        if (tol > 0.0 && r < tol) break;
+    }
+done:
+    free(vu); free(vf); free(s); free(u); free(Dl);
     return rc;
 }
 

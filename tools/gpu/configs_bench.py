@@ -36,7 +36,8 @@ for name in only:
             elif solver == "bicgstab":
                 n, term = plan.bicgstab(20000, p.tol if p.tol > 0 else 1e-6)
             else:
-                n, term = plan.gmres(20, 40000, p.tol if p.tol > 0 else 1e-6)
+                m = 20 if int(np.prod(p.shape)) <= 256 ** 3 else 5     # basis memory: (m + 2) fields
+                n, term = plan.gmres(m, 40000, p.tol if p.tol > 0 else 1e-6)
             b.record(stream)
             torch.cuda.synchronize()
             ms = a.elapsed_time(b)
