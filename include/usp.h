@@ -113,6 +113,12 @@ typedef struct {
                             of w, c = r / target_norm; no accretivity test.  2-D / 3-D
                             complex64, extents in [64, 1024], one GPU; 56 B per voxel of
                             workspace.  get_field returns x.                                */
+    int tensor_diffusion; /* != 0: steady diffusion with a TENSOR D(r) in the first-order
+                            (u, F) form of PAPER.md §3.2 Eqs. 16-18 (L199-227): d + 1 field
+                            components, block-diagonal V; the medium is set with
+                            usp_set_tensor_medium (mu_a and D); dtype must be USP_R32
+                            (real mu_a, D, S; get_field returns u); 2-D / 3-D, extents in
+                            [64, 1024], one GPU.                                             */
 } usp_plan_desc;
 
 /* Create a plan for the grid and problem described by *desc (copied).
@@ -162,6 +168,21 @@ usp_status usp_local_extent(usp_plan_t plan, int64_t *z0, int64_t *nz_local);
  * or D Re(c) < 0; USP_ERR_NONFINITE on NaN/Inf.  Invalidates the source. */
 usp_status usp_set_potential(usp_plan_t plan, const void *medium, usp_where where,
                              double target_norm);
+
+/* Medium of a tensor-diffusion plan (desc.tensor_diffusion; §3.2 Eqs. 16-18):
+ * mu[n] = mu_a(r) (float32) and D[n][d(d+1)/2] the symmetric positive
+ * definite diffusion tensor per voxel, packed (2-D: xx, xy, yy; 3-D: xx, xy,
+ * xz, yy, yz, zz; [z][y][x] voxel order).  Canonical form (R-29):
+ * mubar and Dbar^-1 = element-wise mid-ranges of mu and D^-1(r) (the centres
+ * of the smallest circles of real values, L222-223), S = diag(s_u, s_F..)
+ * with s_u, s_F the largest radii of the mu and D^-1 elements (the
+ * equilibration), c = max_r max(|v_u|, ||V_F||_F) / target_norm so that
+ * ||V|| <= target_norm.  usp_get_split reports sigma = mubar, c, centre =
+ * (s_u, s_F), radius = radius of mu, max_abs_V.  Errors: USP_ERR_STATE (not a
+ * tensor-diffusion plan), USP_ERR_NONFINITE (non-finite mu or a D that is not
+ * positive definite), USP_ERR_ARG. */
+usp_status usp_set_tensor_medium(usp_plan_t plan, const float *mu, const float *D, usp_where where,
+                                 double target_norm);
 
 /* Read back the split in use: sigma, c, smallest-circle centre and radius of
  * the medium values (0 if not auto-scaled), and max |V|. */

@@ -30,7 +30,8 @@ class PlanDesc(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int), ("n", ctypes.c_int64 * 3), ("h", ctypes.c_double * 3),
                 ("medium", ctypes.c_int), ("dtype", ctypes.c_int), ("D", ctypes.c_double),
                 ("sigma", c128), ("c", c128), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
-                ("virtual_ranks", ctypes.c_int), ("antisymmetric", ctypes.c_int)]
+                ("virtual_ranks", ctypes.c_int), ("antisymmetric", ctypes.c_int),
+                ("tensor_diffusion", ctypes.c_int)]
 
 
 class USPError(RuntimeError):
@@ -49,6 +50,8 @@ SIGNATURES = {
     "usp_plan_set_workspace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "usp_local_extent": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
     "usp_set_potential": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_double]),
+    "usp_set_tensor_medium": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                             ctypes.c_double]),
     "usp_get_split": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(c128), ctypes.POINTER(c128),
                                      ctypes.POINTER(c128), ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)]),

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libusp.so")
-SOURCES = ["kernels.cu", "kernels_pipe.cu", "kernels_stile.cu", "kernels_real.cu", "kernels_krylov.cu", "kernels_small.cu", "kernels_anti.cu", "usp_api.cu"]
+SOURCES = ["kernels.cu", "kernels_pipe.cu", "kernels_stile.cu", "kernels_real.cu", "kernels_krylov.cu", "kernels_small.cu", "kernels_anti.cu", "kernels_tdiff.cu", "usp_api.cu"]
 HEADERS = ["fft_core.cuh", "kcommon.cuh", "tma.cuh", "usp_internal.h", "tw64.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

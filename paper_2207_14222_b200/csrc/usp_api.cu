@@ -180,6 +180,12 @@ struct usp_plan_s {
     // antisymmetrised system (Eq. 9-10; desc.antisymmetric): two-component x,
     // Delta, work (component-major) and v = (w - sigma)/c in place of B
     bool anti = false;
+    // first-order tensor diffusion (§3.2 Eqs. 16-18; desc.tensor_diffusion): d + 1
+    // component fields x, Delta, work; V and D^-1 per voxel (float32)
+    bool tdiff = false;
+    int ncomp = 1;                 // components of the fields (1; 2 anti; d + 1 tdiff)
+    float *td_vu = nullptr, *td_vf = nullptr, *td_dinv = nullptr, *td_red = nullptr;
+    TDParams td{};
     // persistent 2-D solve (kernels_small.cu; USP_SOLVE2D=0 disables)
     bool solve2d = false;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -761,6 +767,64 @@ usp_status chain_anti(usp_plan_s *p, int check_state) {
     return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, true, 0);
 }
 
+// ---- first-order tensor diffusion (§3.2): (d + 1)-component chain
+TDParams td_params(usp_plan_s *p) {
+    TDParams t = p->td;
+    t.d = p->ndim;
+    t.n = p->nloc;
+    t.work = p->work;
+    t.delta = p->delta;
+    t.x = p->x;
+    t.vu = p->td_vu;
+    t.vf = p->td_vf;
+    t.dinv = p->td_dinv;
+    t.red = p->td_red;
+    t.inv_n = (float)(1.0 / (double)p->nvox);
+    t.mp = mul_params(p);
+    t.st = p->st;
+    t.red_d = Red{p->partials, p->hist, p->hist_cap, nullptr};
+    return t;
+}
+
+usp_status td_xfft(usp_plan_s *p, bool inv) {
+    Tick t(p, inv ? KC_XPASS : KC_XSETUP);
+    const long long lines = (long long)p->ncomp * p->ny * p->nz;
+    const int lpc = 128 / (1 << (log2ll(p->nx) / 2));
+    CU(launch_xfft((int)p->nx, inv, p->work, p->tw[0], lines, occ_grid(p, (lines + lpc - 1) / lpc, 8), p->stream));
+    return USP_OK;
+}
+
+usp_status chain_tdiff(usp_plan_s *p, int check_state) {
+    usp_status s;
+    const long long plane = p->nx * p->ny, nc = p->ncomp;
+    const int ge = occ_grid(p, (p->nloc + 255) / 256, 8);
+    if (p->ndim == 2) {
+        SParams yf = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, nc, plane, 1, check_state, 2);
+        if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, true, 0))) return s;
+        {
+            Tick t(p, KC_ZMUL);
+            CU(launch_tdiff_mul(td_params(p), check_state, ge, p->stream));
+        }
+        return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, true, 0);
+    }
+    SParams yf = sparams(p, p->work, p->work, p->tw[1], p->nx, p->nx, nc * p->nz, plane, 1, check_state, 3);
+    SParams zf = sparams(p, p->work, p->work, p->tw[2], plane, plane, nc, p->nz * plane, 2, check_state, 2);
+    if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, true, 0))) return s;
+    if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD, zf, p->smap_z, true, 0))) return s;
+    {
+        Tick t(p, KC_ZMUL);
+        CU(launch_tdiff_mul(td_params(p), check_state, ge, p->stream));
+    }
+    if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_INV, zf, p->smap_z, true, 0))) return s;
+    return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, true, 0);
+}
+
+usp_status td_upd(usp_plan_s *p, XMode mode) {
+    Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
+    CU(launch_tdiff_upd(mode, td_params(p), occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
+    return USP_OK;
+}
+
 // The middle of the chain: every FFT pass between the x forward and the x
 // inverse, with the (L+1)^-1 multiplier on the last axis (Eq. 12).
 usp_status chain_mid(usp_plan_s *p, int check_state) {
@@ -871,13 +935,13 @@ void build_maps(usp_plan_s *p) {
     if (!p->stile || p->ndim < 2 || !stile_supported(p->ny)) return;
     const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
     if (p->ndim == 2) {
-        const cuuint64_t dims[2] = {(cuuint64_t)p->rp, (cuuint64_t)(p->ny * (p->anti ? 2 : 1))};
+        const cuuint64_t dims[2] = {(cuuint64_t)p->rp, (cuuint64_t)(p->ny * p->ncomp)};
         const cuuint64_t str[1] = {(cuuint64_t)p->rp * 8};
         const cuuint32_t box[2] = {cy, by};
         p->stile_y = make_map(&p->smap_y, p->work, 2, dims, str, box);
         return;
     }
-    const long long comps = p->anti ? 2 : 1;   // antisymmetrised: both components as extra planes
+    const long long comps = p->ncomp;   // multi-component fields: the components as extra planes
     {   // y pass over the planes held here: {x, y, z}
         const cuuint64_t dims[3] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny, (cuuint64_t)(p->nzh * comps)};
         const cuuint64_t str[2] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->rp * p->ny) * 8};
@@ -991,6 +1055,13 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (!stile_supported(desc->n[1]) || !stile_supported(desc->n[2]))
             return fail(USP_ERR_UNSUPPORTED, "slab decomposition needs ny, nz in [64, 2048]");
     }
+    if (desc->tensor_diffusion) {
+        if (desc->ndim < 2 || desc->dtype != USP_R32 || P > 1 || desc->antisymmetric)
+            return fail(USP_ERR_UNSUPPORTED, "tensor diffusion runs on 2-D / 3-D float32 plans on one GPU");
+        for (int a = 0; a < desc->ndim; ++a)
+            if (desc->n[a] < 64 || desc->n[a] > 1024)
+                return fail(USP_ERR_UNSUPPORTED, "tensor diffusion needs extents in [64, 1024]");
+    }
     if (desc->antisymmetric) {
         if (desc->ndim < 2 || desc->dtype != USP_C64 || P > 1)
             return fail(USP_ERR_UNSUPPORTED, "the antisymmetrised system runs on 2-D / 3-D complex64 plans on one GPU");
@@ -1001,6 +1072,8 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     usp_plan_s *p = new usp_plan_s();
     p->d = *desc;
     p->anti = desc->antisymmetric != 0;
+    p->tdiff = desc->tensor_diffusion != 0;
+    p->ncomp = p->anti ? 2 : (p->tdiff ? desc->ndim + 1 : 1);
     p->ndim = desc->ndim;
     p->nx = desc->n[0];
     p->ny = desc->ndim >= 2 ? desc->n[1] : 1;
@@ -1017,7 +1090,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     p->nloc = p->nx * p->ny * p->nzh;
     {
         const char *rl = std::getenv("USP_REAL");
-        p->real = !p->anti && !(rl && rl[0] == '0') && desc->dtype == USP_R32 && desc->medium == USP_MEDIUM_W &&
+        p->real = !p->anti && !p->tdiff && !(rl && rl[0] == '0') && desc->dtype == USP_R32 && desc->medium == USP_MEDIUM_W &&
                   desc->ndim == 3 && xreal_supported(p->nx) && stile_supported(p->ny) && stile_supported(p->nz);
         p->rp = p->real ? xreal_row_pitch((int)p->nx) : p->nx;
     }
@@ -1051,8 +1124,8 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (chk) p->chunk_g = std::atoll(chk);
         while (p->chunk_g > 0 && (p->nz % p->chunk_g)) p->chunk_g >>= 1;
         const char *stl = std::getenv("USP_STILE");
-        p->stile = (P > 1) || p->real || p->anti || (p->pipe && !(stl && stl[0] == '0'));
-        const long long comps = p->anti ? 2 : 1;
+        p->stile = (P > 1) || p->real || p->anti || p->tdiff || (p->pipe && !(stl && stl[0] == '0'));
+        const long long comps = p->ncomp;
         if (p->ndim >= 2 && stile_supported(p->ny))
             p->grids_y = occ_grid(p, (p->rp / stile_cols((int)p->ny)) * p->nzh * comps, stile_ctas_per_sm((int)p->ny));
         if (p->ndim >= 3 && stile_supported(p->nz)) {
@@ -1087,7 +1160,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMemset(p->bar, 0, sizeof(unsigned) * 2));
     {
         const char *s2 = std::getenv("USP_SOLVE2D");
-        p->solve2d = !p->anti && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
+        p->solve2d = !p->anti && !p->tdiff && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
     }
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
@@ -1124,6 +1197,11 @@ usp_status usp_plan_workspace_size(usp_plan_t p, size_t *bytes) {
         *bytes = 7 * f;
         return USP_OK;
     }
+    if (p->tdiff) {  // x, Delta, work: d + 1 components each; v_u, V_F, D^-1 (float32)
+        const int np = p->ndim * (p->ndim + 1) / 2;
+        *bytes = 3 * (size_t)p->ncomp * f + align256((size_t)p->nloc * 4) * (1 + 2 * np);
+        return USP_OK;
+    }
     *bytes = 3 * f + w * (p->P > 1 ? 3 : 1);
     return USP_OK;
 }
@@ -1147,6 +1225,17 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
         p->delta = (float2 *)(p->ws + 2 * f);
         p->work = (float2 *)(p->ws + 4 * f);
         p->B = (float2 *)(p->ws + 6 * f);
+    }
+    if (p->tdiff) {  // [x]*(d+1) [Delta]*(d+1) [work]*(d+1) [v_u] [V_F]*np [D^-1]*np
+        const int nc = p->ncomp, np = p->ndim * (p->ndim + 1) / 2;
+        const size_t fr = align256((size_t)p->nloc * 4);
+        p->x = (float2 *)(p->ws);
+        p->delta = (float2 *)(p->ws + nc * f);
+        p->work = (float2 *)(p->ws + 2 * nc * f);
+        p->B = nullptr;
+        p->td_vu = (float *)(p->ws + 3 * nc * f);
+        p->td_vf = (float *)(p->ws + 3 * nc * f + fr);
+        p->td_dinv = (float *)(p->ws + 3 * nc * f + fr + np * fr);
     }
     if (p->P > 1) {
         p->sendb = (float2 *)(p->ws + 3 * f + w);
@@ -1175,6 +1264,7 @@ usp_status usp_local_extent(usp_plan_t p, int64_t *z0, int64_t *nz_local) {
 
 usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, double target_norm) {
     if (!p || !medium) return fail(USP_ERR_ARG, "NULL argument");
+    if (p->tdiff) return fail(USP_ERR_STATE, "tensor-diffusion plans take usp_set_tensor_medium");
     if (!p->ws) return fail(USP_ERR_STATE, "workspace not set");
     if (where != USP_HOST && where != USP_DEVICE) return fail(USP_ERR_ARG, "bad where");
     // stage the medium in the chain buffer (the source resets it later)
@@ -1244,6 +1334,103 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
     return USP_OK;
 }
 
+usp_status usp_set_tensor_medium(usp_plan_t p, const float *mu, const float *D, usp_where where, double target_norm) {
+    if (!p || !mu || !D) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p->tdiff) return fail(USP_ERR_STATE, "the plan was not created with desc.tensor_diffusion");
+    if (!p->ws) return fail(USP_ERR_STATE, "workspace not set");
+    if (!(target_norm > 0.0 && target_norm < 1.0)) return fail(USP_ERR_ARG, "target_norm must be in (0, 1)");
+    const int d = p->ndim, np = d * (d + 1) / 2;
+    const size_t nb = (size_t)p->nloc * 4;
+    usp_status s;
+    p->have_source = p->have_potential = false;
+    // stage: mu into v_u, D (packed) into V_F (both rewritten by the second pass)
+    if ((s = stage(p, p->td_vu, mu, nb, where))) return s;
+    if ((s = stage(p, p->td_vf, D, nb * np, where))) return s;
+    const int grid = occ_grid(p, (p->nloc + 255) / 256, 4);
+    if (!p->td_red) CU(cudaMalloc(&p->td_red, sizeof(float) * 16 * p->nsm * 4));
+    TDParams t = td_params(p);
+    t.mu = p->td_vu;
+    t.Dpk = p->td_vf;
+    t.red = p->td_red;
+    CU(launch_tdiff_pot(t, 0, grid, p->stream));
+    std::vector<float> red((size_t)16 * grid);
+    CU(cudaMemcpyAsync(red.data(), p->td_red, sizeof(float) * red.size(), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    double lo[7], hi[7], bad = 0.0;
+    for (int q = 0; q < 7; ++q) { lo[q] = 3e38; hi[q] = -3e38; }
+    for (int c = 0; c < grid; ++c) {
+        for (int q = 0; q <= np; ++q) {
+            lo[q] = std::min(lo[q], (double)red[(size_t)c * 16 + q]);
+            hi[q] = std::max(hi[q], (double)red[(size_t)c * 16 + 7 + q]);
+        }
+        bad += red[(size_t)c * 16 + 15];
+    }
+    if (bad > 0) return fail(USP_ERR_NONFINITE, "%g voxels with non-finite mu or a D that is not positive definite", bad);
+    // canonical form (reading R-29): mid-ranges into L, radii equilibrated by S
+    const double mubar = 0.5 * (hi[0] + lo[0]), r_mu = 0.5 * (hi[0] - lo[0]);
+    double dbar[6] = {0, 0, 0, 0, 0, 0}, r_d = 0.0;
+    for (int q = 0; q < np; ++q) {
+        dbar[q] = 0.5 * (hi[q + 1] + lo[q + 1]);
+        r_d = std::max(r_d, 0.5 * (hi[q + 1] - lo[q + 1]));
+    }
+    const double s_u = r_mu > 0 ? r_mu : 1.0, s_F = r_d > 0 ? r_d : 1.0;
+    t.mubar = (float)mubar;
+    for (int q = 0; q < np; ++q) t.dbar[q] = (float)dbar[q];
+    double c = 1.0;
+    for (int pass = 0; pass < 2; ++pass) {   // pass 0: max |V| at c = 1; pass 1: V with c
+        t.inv_cu = (float)(1.0 / (c * s_u));
+        t.inv_cf = (float)(1.0 / (c * s_F));
+        CU(launch_tdiff_pot(t, pass == 0 ? 1 : 2, grid, p->stream));
+        CU(cudaMemcpyAsync(red.data(), p->td_red, sizeof(float) * red.size(), cudaMemcpyDeviceToHost, p->stream));
+        CU(cudaStreamSynchronize(p->stream));
+        double vmax = 0.0;
+        for (int q = 0; q < grid; ++q) vmax = std::max(vmax, (double)red[(size_t)q * 16 + 14]);
+        if (pass == 0) {
+            if (!(vmax > 0.0)) return fail(USP_ERR_ARG, "homogeneous medium: give a heterogeneous mu or D");
+            c = vmax / target_norm;
+        } else {
+            p->vmax = vmax;
+        }
+    }
+    // (L + 1)^-1 symbol: a, q scale, (Dbar^-1 / (c s_F) + I)^-1
+    double Dm[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    const int idx2[3][2] = {{0, 0}, {0, 1}, {1, 1}};
+    const int idx3[6][2] = {{0, 0}, {0, 1}, {0, 2}, {1, 1}, {1, 2}, {2, 2}};
+    for (int q = 0; q < np; ++q) {
+        const int i = d == 2 ? idx2[q][0] : idx3[q][0], j = d == 2 ? idx2[q][1] : idx3[q][1];
+        Dm[i][j] = Dm[j][i] = dbar[q] / (c * s_F);
+    }
+    for (int k = 0; k < d; ++k) Dm[k][k] += 1.0;
+    double R[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    if (d == 2) {
+        const double det = Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0];
+        R[0][0] = Dm[1][1] / det; R[1][1] = Dm[0][0] / det; R[0][1] = R[1][0] = -Dm[0][1] / det;
+    } else {
+        const double c00 = Dm[1][1] * Dm[2][2] - Dm[1][2] * Dm[2][1], c01 = Dm[1][2] * Dm[2][0] - Dm[1][0] * Dm[2][2];
+        const double c02 = Dm[1][0] * Dm[2][1] - Dm[1][1] * Dm[2][0];
+        const double det = Dm[0][0] * c00 + Dm[0][1] * c01 + Dm[0][2] * c02;
+        R[0][0] = c00 / det; R[1][0] = c01 / det; R[2][0] = c02 / det;
+        R[0][1] = (Dm[0][2] * Dm[2][1] - Dm[0][1] * Dm[2][2]) / det;
+        R[1][1] = (Dm[0][0] * Dm[2][2] - Dm[0][2] * Dm[2][0]) / det;
+        R[2][1] = (Dm[0][1] * Dm[2][0] - Dm[0][0] * Dm[2][1]) / det;
+        R[0][2] = (Dm[0][1] * Dm[1][2] - Dm[0][2] * Dm[1][1]) / det;
+        R[1][2] = (Dm[0][2] * Dm[1][0] - Dm[0][0] * Dm[1][2]) / det;
+        R[2][2] = (Dm[0][0] * Dm[1][1] - Dm[0][1] * Dm[1][0]) / det;
+    }
+    for (int k = 0; k < 3; ++k)
+        for (int m = 0; m < 3; ++m) t.dm_inv[k * 3 + m] = (float)R[k][m];
+    t.a = (float)(mubar / (c * s_u) + 1.0);
+    t.qs = (float)(1.0 / (c * std::sqrt(s_u * s_F)));
+    t.s_scale = (float)(1.0 / (c * std::sqrt(s_u)));
+    p->td = t;
+    p->sigma = {mubar, 0.0};
+    p->c = {c, 0.0};
+    p->centre = {s_u, s_F};   // reported by usp_get_split: (s_u, s_F) of the equilibration S
+    p->radius = r_mu;
+    p->have_potential = true;
+    return USP_OK;
+}
+
 usp_status usp_get_split(usp_plan_t p, usp_c128 *sigma, usp_c128 *c, usp_c128 *centre, double *radius,
                          double *max_abs_V) {
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
@@ -1278,6 +1465,13 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         op.red = Red{p->partials, p->hist, p->hist_cap, nullptr};
         Tick t(p, KC_SOLVE1D);
         CU(launch_solve1d((int)p->nx, O_SETUP, op, p->stream));
+    } else if (p->tdiff) {
+        p->td.Sraw = (const float *)p->x;   // the staged raw source (float32)
+        if ((s = td_upd(p, X_SRC_FWD))) return s;
+        if ((s = td_xfft(p, false))) return s;
+        if ((s = chain_tdiff(p, 0))) return s;
+        if ((s = td_xfft(p, true))) return s;
+        if ((s = td_upd(p, X_SRC_EPI))) return s;
     } else if (p->anti) {
         if ((s = run_anti_x(p, X_SRC_FWD))) return s;
         if ((s = chain_anti(p, 0))) return s;
@@ -1347,6 +1541,13 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         while (launched < total) {
             const long long nb = std::min(batch, total - launched);
             for (long long i = 0; i < nb; ++i) {
+                if (p->tdiff) {
+                    if ((s = td_xfft(p, false))) return s;
+                    if ((s = chain_tdiff(p, 1))) return s;
+                    if ((s = td_xfft(p, true))) return s;
+                    if ((s = td_upd(p, X_ITER))) return s;
+                    continue;
+                }
                 if (p->anti) {
                     if ((s = chain_anti(p, 1))) return s;
                     if ((s = run_anti_x(p, X_ITER))) return s;
@@ -1414,7 +1615,17 @@ usp_status usp_get_field(usp_plan_t p, void *out, usp_where where) {
     if (!p || !out) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
     const cudaMemcpyKind kind = where == USP_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    if (p->d.dtype == USP_C64) {
+    if (p->tdiff) {   // u = E_0 / sqrt(s_u), float32
+        float *dst = (float *)out;
+        float *tmp = nullptr;
+        if (where == USP_HOST) {
+            tmp = (float *)(p->work);   // scratch (overwritten by the next chain)
+            dst = tmp;
+        }
+        CU(launch_tdiff_out(p->x, dst, (float)(1.0 / std::sqrt(p->centre.re)), p->nloc,
+                            occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
+        if (where == USP_HOST) CU(cudaMemcpyAsync(out, tmp, (size_t)p->nloc * 4, cudaMemcpyDeviceToHost, p->stream));
+    } else if (p->d.dtype == USP_C64) {
         CU(cudaMemcpyAsync(out, p->x, (size_t)p->nloc * sizeof(float2), kind, p->stream));
     } else if (p->real) {
         CU(cudaMemcpyAsync(out, p->x, (size_t)p->nloc * sizeof(float), kind, p->stream));
@@ -1454,7 +1665,7 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->k_rh) return fail(USP_ERR_STATE, "usp_krylov_set_workspace must be called first");
     if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
-    if (p->ndim < 2 || p->real || p->anti || multi_rank(p) || !p->pipe_xk)
+    if (p->ndim < 2 || p->real || p->anti || p->tdiff || multi_rank(p) || !p->pipe_xk)
         return fail(USP_ERR_UNSUPPORTED, "BiCGSTAB runs on 2-D / 3-D complex64 plans on one GPU");
     usp_status s = sync_state(p);
     if (s) return s;
@@ -1653,7 +1864,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->gm_b) return fail(USP_ERR_STATE, "usp_gmres_set_workspace must be called first");
     if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
-    if (p->ndim < 2 || p->real || p->anti || multi_rank(p) || !p->pipe_xk)
+    if (p->ndim < 2 || p->real || p->anti || p->tdiff || multi_rank(p) || !p->pipe_xk)
         return fail(USP_ERR_UNSUPPORTED, "GMRES runs on 2-D / 3-D complex64 plans on one GPU");
     usp_status s = sync_state(p);
     if (s) return s;
@@ -1811,6 +2022,7 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->coll);
     cudaFree(p->ks);
     cudaFree(p->gm_part);
+    cudaFree(p->td_red);
     cudaFree(p->bar);
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
     cudaFree(p->twr);

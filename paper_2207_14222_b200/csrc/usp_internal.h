@@ -170,6 +170,26 @@ struct AParams {
     Red red;
 };
 
+// ------------------------------------------- tensor diffusion (NEXT-3) --
+struct TDParams {
+    int d;                       // 2 or 3 (components d + 1: u, F_x, F_y[, F_z])
+    long long n;                 // voxels
+    float2 *work, *delta, *x;    // (d + 1) components each, component-major
+    const float *mu, *Dpk;       // setup inputs: mu_a, D packed symmetric (xx, xy, [xz,] yy[, yz, zz])
+    float *dinv;                 // per-voxel D^-1 packed
+    float *vu, *vf;              // V per voxel: u block, flux block (packed)
+    float mubar, inv_cu, inv_cf; // 1/(c s_u), 1/(c s_F)
+    float dbar[6];               // Dbar^-1 packed
+    float a, qs, inv_n;          // symbol: a = mubar/(c s_u) + 1, q = p qs, 1/N_vox
+    float dm_inv[9];             // (Dbar^-1/(c s_F) + I)^-1, row-major 3x3
+    const float *Sraw;           // staged raw source
+    float s_scale;               // 1/(c sqrt(s_u))
+    float *red;                  // setup reductions: 16 floats per CTA
+    MulParams mp;
+    IterState *st;
+    Red red_d;
+};
+
 // ------------------------------------------------- persistent 2-D solve --
 struct S2Params {
     float2 *work, *delta, *x;
@@ -212,6 +232,13 @@ struct FarParams {       // farthest medium value from a centre (smallest circle
 cudaError_t launch_anti_x(int N, XMode mode, const AParams &p, int grid, cudaStream_t s);
 cudaError_t launch_anti_mul(const AParams &p, int check_state, int grid, cudaStream_t s);
 int anti_lines_per_cta(int N);
+
+// tensor diffusion (kernels_tdiff.cu)
+cudaError_t launch_xfft(int N, bool inv, float2 *data, const float2 *tw, long long nlines, int grid, cudaStream_t s);
+cudaError_t launch_tdiff_pot(const TDParams &p, int mode, int grid, cudaStream_t s);
+cudaError_t launch_tdiff_mul(const TDParams &p, int check_state, int grid, cudaStream_t s);
+cudaError_t launch_tdiff_upd(XMode mode, const TDParams &p, int grid, cudaStream_t s);
+cudaError_t launch_tdiff_out(const float2 *E0, float *out, float scale, long long n, int grid, cudaStream_t s);
 
 // persistent 2-D solve (kernels_small.cu)
 bool solve2d_supported(long long nx, long long ny);

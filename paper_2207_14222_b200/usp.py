@@ -64,7 +64,8 @@ class Plan:
 
     def __init__(self, shape: Sequence[int], kind: str = "helmholtz", h: Optional[Sequence[float]] = None,
                  D: float = 1.0, sigma: complex = 0j, c: complex = 1 + 0j, dtype: str = "c64",
-                 stream=None, device=None, comm=None, virtual_ranks: int = 0, antisymmetric: bool = False):
+                 stream=None, device=None, comm=None, virtual_ranks: int = 0, antisymmetric: bool = False,
+                 tensor_diffusion: bool = False):
         import torch
 
         self.lib = L.load()
@@ -91,6 +92,10 @@ class Plan:
         d.nccl_comm = comm.handle if comm is not None else None
         d.virtual_ranks = int(virtual_ranks)
         d.antisymmetric = int(bool(antisymmetric))
+        d.tensor_diffusion = int(bool(tensor_diffusion))
+        if tensor_diffusion:
+            d.dtype = L.R32
+            self.dtype = "r32"
         self.comm = comm
         self.desc = d
         h_ = ctypes.c_void_p()
@@ -111,6 +116,25 @@ class Plan:
         ptr, where, keep = _ptr_where(medium, self.dtype)
         L.check(self.lib.usp_set_potential(self.handle, ptr, where, float(target_norm)))
         del keep
+        return self.split
+
+    def set_tensor_medium(self, mu, D, target_norm: float = 0.95):
+        """Tensor-diffusion plans (§3.2): mu_a [shape] and D [shape + (d, d)]
+        (symmetric positive definite), packed for usp_set_tensor_medium."""
+        import torch
+
+        d = self.ndim
+        idx = [(0, 0), (0, 1), (1, 1)] if d == 2 else [(0, 0), (0, 1), (0, 2), (1, 1), (1, 2), (2, 2)]
+        if isinstance(D, torch.Tensor):
+            pk = torch.stack([D[..., i, j] for i, j in idx], dim=-1).to(torch.float32).contiguous()
+        else:
+            pk = np.ascontiguousarray(np.stack([np.asarray(D)[..., i, j] for i, j in idx], axis=-1), dtype=np.float32)
+        mptr, where, k1 = _ptr_where(mu, "r32")
+        dptr, where2, k2 = _ptr_where(pk, "r32")
+        if where != where2:
+            raise ValueError("mu and D must both be host or both device arrays")
+        L.check(self.lib.usp_set_tensor_medium(self.handle, mptr, dptr, where, float(target_norm)))
+        del k1, k2
         return self.split
 
     @property
