@@ -245,8 +245,10 @@ usp_status usp_bicgstab(usp_plan_t plan, int64_t n_max, double tol, int64_t *n_d
  * estimate |g_{j+1}| / ||b|| < tol (then x is updated) or after n_max
  * Arnoldi steps; n_done = Arnoldi steps; the residual history is the estimate
  * per step.  Workspace: b and the basis U_0..U_m (m + 2 complex64 fields,
- * caller-owned, 256-B aligned); 2-D / 3-D complex64 on one GPU; starts right
- * after usp_set_source.  Errors as usp_bicgstab. */
+ * caller-owned, 256-B aligned); 2-D / 3-D complex64, also slab-decomposed
+ * (the inner products are all-gathered and summed in rank order, so every
+ * rank takes the same decisions); starts right after usp_set_source.
+ * Errors as usp_bicgstab. */
 usp_status usp_gmres_workspace_size(usp_plan_t plan, int m, size_t *bytes);
 usp_status usp_gmres_set_workspace(usp_plan_t plan, int m, void *dev, size_t bytes);
 usp_status usp_gmres(usp_plan_t plan, int64_t n_max, double tol, int64_t *n_done, usp_term *term);

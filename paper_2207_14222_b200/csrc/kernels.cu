@@ -503,10 +503,6 @@ cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStre
 #undef X_CASE
 }
 
-cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_t s) {
-    (void)p; (void)nvox; (void)grid; (void)s;
-    return cudaSuccess;   // x-only update is folded into k_xpass<X_ITER>
-}
 
 template <int N, int MODE, int COLS>
 static cudaError_t strided_t(const SParams &p, int grid, cudaStream_t s) {

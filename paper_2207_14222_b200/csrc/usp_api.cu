@@ -200,7 +200,8 @@ struct usp_plan_s {
     double *far_d = nullptr;
     long long *far_i = nullptr;
     int far_cap = 0;
-    double *coll = nullptr;         // collective scratch: [0] local x-pass total, [8..] gathers
+    double *coll = nullptr;         // collective scratch: [0] local x-pass total, [1] chunk sum, [8..15]
+                                    // all-gathered totals, [16..] IPC records, [64..] / [128..] host gathers
     IterState *st_host = nullptr;   // pinned mirror
     // split
     usp_c128 sigma{}, c{}, centre{};
@@ -352,7 +353,8 @@ usp_status gather_host(usp_plan_s *p, const double *mine, int n, std::vector<dou
         std::copy(mine, mine + n, out.begin());
         return USP_OK;
     }
-    double *snd = p->coll + 8, *rcv = p->coll + 16;
+    if (n > 64 || (size_t)p->P * n > 1920) return fail(USP_ERR_ARG, "gather of %d doubles x %d ranks too large", n, p->P);
+    double *snd = p->coll + 64, *rcv = p->coll + 128;
     CU(cudaMemcpyAsync(snd, mine, sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
     NC(nccl().AllGather(snd, rcv, (size_t)n, ncclDouble, p->comm, p->stream));
     CU(cudaMemcpyAsync(out.data(), rcv, sizeof(double) * n * p->P, cudaMemcpyDeviceToHost, p->stream));
@@ -1154,7 +1156,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->red_u, sizeof(unsigned) * 4));
     TRY(cudaMalloc(&p->far_d, sizeof(double) * p->far_cap));
     TRY(cudaMalloc(&p->far_i, sizeof(long long) * p->far_cap));
-    TRY(cudaMalloc(&p->coll, sizeof(double) * (16 + 3 * 64)));
+    TRY(cudaMalloc(&p->coll, sizeof(double) * 2048));
     TRY(cudaMalloc(&p->ks, sizeof(KState)));
     TRY(cudaMalloc(&p->bar, sizeof(unsigned) * 2));
     TRY(cudaMemset(p->bar, 0, sizeof(unsigned) * 2));
@@ -1790,19 +1792,20 @@ usp_status gs_dots(usp_plan_s *p, int nv, float2 *z, std::vector<zd> &d, double 
         const int K = 2 * nb + 1;
         CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * K * p->gm_grid, cudaMemcpyDeviceToHost, p->stream));
         CU(cudaStreamSynchronize(p->stream));
-        for (int q = 0; q < nb; ++q) {
-            double re = 0.0, im = 0.0;
-            for (int c = 0; c < p->gm_grid; ++c) {
-                re += h[(size_t)c * K + 2 * q];
-                im += h[(size_t)c * K + 2 * q + 1];
-            }
-            d[b0 + q] = zd(re, im);
+        std::vector<double> loc(K, 0.0);
+        for (int q = 0; q < K; ++q)
+            for (int c = 0; c < p->gm_grid; ++c) loc[q] += h[(size_t)c * K + q];
+        // slab-decomposed: every rank's local sums, added in rank order
+        std::vector<double> all;
+        usp_status s = gather_host(p, loc.data(), K, all);
+        if (s) return s;
+        for (int q = 0; q < K; ++q) {
+            double t = 0.0;
+            for (int r = 0; r < (multi_rank(p) ? p->P : 1); ++r) t += all[(size_t)r * K + q];
+            loc[q] = t;
         }
-        if (nrm && b0 == 0) {
-            double s2 = 0.0;
-            for (int c = 0; c < p->gm_grid; ++c) s2 += h[(size_t)c * K + 2 * nb];
-            *nrm = s2;
-        }
+        for (int q = 0; q < nb; ++q) d[b0 + q] = zd(loc[2 * q], loc[2 * q + 1]);
+        if (nrm && b0 == 0) *nrm = loc[2 * nb];
     }
     return USP_OK;
 }
@@ -1831,6 +1834,11 @@ usp_status gs_axpy(usp_plan_s *p, int nv, const std::vector<float2 *> &U, const 
             CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * p->gm_grid, cudaMemcpyDeviceToHost, p->stream));
             CU(cudaStreamSynchronize(p->stream));
             for (int q = 0; q < p->gm_grid; ++q) s2 += h[q];
+            std::vector<double> all;   // slab-decomposed: ranks' norms in rank order
+            usp_status st = gather_host(p, &s2, 1, all);
+            if (st) return st;
+            s2 = 0.0;
+            for (int r = 0; r < (multi_rank(p) ? p->P : 1); ++r) s2 += all[r];
         }
     }
     if (nrm) *nrm = s2;
@@ -1864,8 +1872,8 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->gm_b) return fail(USP_ERR_STATE, "usp_gmres_set_workspace must be called first");
     if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
-    if (p->ndim < 2 || p->real || p->anti || p->tdiff || multi_rank(p) || !p->pipe_xk)
-        return fail(USP_ERR_UNSUPPORTED, "GMRES runs on 2-D / 3-D complex64 plans on one GPU");
+    if (p->ndim < 2 || p->real || p->anti || p->tdiff || !p->pipe_xk)
+        return fail(USP_ERR_UNSUPPORTED, "GMRES runs on 2-D / 3-D complex64 plans");
     usp_status s = sync_state(p);
     if (s) return s;
     if (p->st_host->k != 0)

@@ -259,7 +259,6 @@ int xreal_lines_per_unit(int N);
 cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);
 cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s, int cols = 0);
 cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s);
-cudaError_t launch_xonly(const XParams &p, long long nvox, int grid, cudaStream_t s);
 cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s);

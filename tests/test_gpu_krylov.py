@@ -179,3 +179,22 @@ def test_gmres_converges_like_oracle(orc, name, shape, m):
     assert term == "converged" and ref.rc == 0
     assert abs(nd - ref.n_done) <= max(1, 0.03 * ref.n_done), (nd, ref.n_done)
     assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)
+
+
+def test_gmres_virtual_slabs_bit_identical():
+    """GMRES through the slab-decomposed operator (virtual ranks, fused
+    transposes) = one slab, bit for bit."""
+    import torch
+    from paper_2207_14222_b200 import Plan
+    from synth import make
+
+    p = make("C3", (64, 64, 64))
+    med, src, _ = rounded_inputs(p)
+    out = []
+    for vr in (0, 4):
+        plan = Plan(p.shape, virtual_ranks=vr)
+        plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
+        plan.set_source(torch.from_numpy(src).cuda())
+        plan.gmres(10, 25, 0.0)
+        out.append((plan.get_field().cpu().numpy(), plan.history()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
