@@ -29,6 +29,7 @@ DESIGN.md ("Oracle and its pins"); every function here is pinned.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 from dataclasses import dataclass
@@ -171,15 +172,41 @@ def medium_to_w(kind: str, medium) -> np.ndarray:
     return -m if kind == "helmholtz" else m
 
 
-def canonical(kind: str, medium, target_norm: float = 0.95, D: float = 1.0) -> Split:
+def real_bias_circle(points) -> Tuple[float, float]:
+    """Smallest circle CENTRED ON THE REAL AXIS enclosing the points: the
+    real bias of the earlier convergent-Born-series work the paper compares
+    against (Table 1b's "R bias" rows).  f(t) = max_i
+    |z_i - t| is convex in t; golden-section search to machine precision."""
+    z = _c128(points).ravel()
+    f = lambda t: float(np.max(np.abs(z - t)))
+    lo, hi = float(z.real.min()), float(z.real.max())
+    g = (math.sqrt(5.0) - 1.0) / 2.0
+    a, b = lo, hi
+    for _ in range(200):
+        c1, c2 = b - g * (b - a), a + g * (b - a)
+        if f(c1) <= f(c2):
+            b = c2
+        else:
+            a = c1
+    t = 0.5 * (a + b)
+    return t, f(t)
+
+
+def canonical(kind: str, medium, target_norm: float = 0.95, D: float = 1.0, real_bias: bool = False) -> Split:
     """Canonical form of §2.2 / §3.1.
 
     Helmholtz: kbar^2 = centre of the smallest circle enclosing the k^2 values,
     c_paper = -(1/(0.95 i)) r = i r / 0.95 (L167); in the unified form
     sigma = -kbar^2, c = -c_paper.  Diffusion (§3.2 scalar, reading R-15):
     mu0 = centre (mid-range) of mu_a, c = r / 0.95 (real, so A stays accretive).
+    real_bias: the centre is restricted to the real axis (the prior real-bias
+    choice the paper improves on, L174, L396).
     """
-    centre, r = mec(_c128(medium))
+    if real_bias:
+        t, r = real_bias_circle(_c128(medium))
+        centre = complex(t)
+    else:
+        centre, r = mec(_c128(medium))
     if r == 0.0:
         raise ValueError("homogeneous medium: smallest circle has radius 0; pass sigma, c explicitly")
     if kind == "helmholtz":
