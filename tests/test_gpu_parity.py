@@ -243,3 +243,38 @@ def test_full_size_C5_plane_waves():
     ref = field(coefs)
     err = float(torch.linalg.vector_norm(x - ref) / torch.linalg.vector_norm(ref))
     assert err <= 2e-5, err
+
+
+def test_full_size_C5_linear_in_source():
+    """BASELINE.json C5 at its full size (1024^3, the heterogeneous GRF medium,
+    the bench's launch configuration), where the oracle cannot run: with
+    x_0 = 0 and a fixed count, Alg. 1 is a fixed linear map of the
+    source, so x_k(s1 + 2 s2) = x_k(s1) + 2 x_k(s2) voxel by voxel (up to fp32
+    rounding), and the residual is monotone (Cor. 1)."""
+    import torch
+    from paper_2207_14222_b200 import Plan
+    from synth import make
+
+    p = make("C5", device="cuda")
+    shape, K = p.shape, 5
+    med = p.medium.to(torch.complex64)
+    s1 = p.source.to(torch.complex64)
+    del p
+    s2 = torch.zeros_like(s1)
+    s2[300, 700, 123] = 1.0 - 0.5j
+    s2[900, 64, 1000] = 0.25
+    plan = Plan(shape)
+    plan.set_potential(med, 0.95)
+    del med
+    xs = []
+    for s in (s1, s2, s1 + 2 * s2):
+        plan.set_source(s)
+        nd, term = plan.iterate(K, 0.75, 0.0)
+        assert nd == K and term == "max_iter"
+        h = plan.history()[: K + 1]
+        assert np.all(np.diff(h) <= 1e-5 * h[:-1]), h
+        xs.append(plan.get_field())
+    x1, x2, x12 = xs
+    err = float(torch.linalg.vector_norm(x12 - x1 - 2 * x2) / torch.linalg.vector_norm(x12))
+    assert err <= 1e-5, err
+    assert float(torch.linalg.vector_norm(x2)) > 0.1 * float(torch.linalg.vector_norm(x1))
