@@ -169,6 +169,49 @@ __device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *x
     }
 }
 
+// USP_ST128: 0 = 64-bit stores everywhere, 1 = paired 128-bit stores
+// everywhere, 2 (default) = paired stores in the inverse y pass (K_D) only.
+// Measured at 1024^3 (tools/gpu/kab.py, medians of 5): K_D 3.30 -> 2.77 ms with
+// paired stores, while K_B (2.67 -> 2.82) and K_C (4.45 -> 4.51) are faster
+// with 64-bit stores.
+#ifndef USP_ST128
+#define USP_ST128 2
+#endif
+// Store register slots m in [M0, M1) (rows j + N1 m of column c) of a tile.
+// Paired stores: adjacent-column lane pairs swap one value per slot pair with
+// a shuffle so each lane writes two columns of one row with one 128-bit store
+// (half the store instructions).  base = &dst[row 0][column c].
+template <int N, int MODE, int M0, int M1>
+__device__ __forceinline__ void store_slots(const float2 (&v)[LineGeo<N>::N2], float2 *base, long long stride,
+                                            int j, int c) {
+    using G = LineGeo<N>;
+    auto val = [&](int m) { return (MODE == S_FWD) ? v[m] : cconj(v[m]); };
+    constexpr bool paired = USP_ST128 == 1 || (USP_ST128 == 2 && MODE == S_INV);
+    if constexpr (paired && STile<N>::COLS == 16 && ((M1 - M0) % 2) == 0) {
+        const bool odd = c & 1;
+        float2 *b = base - (odd ? 1 : 0) + (long long)(j + (odd ? G::N1 : 0)) * stride;
+        const long long step = 2LL * G::N1 * stride;
+#pragma unroll
+        for (int m = M0; m < M1; m += 2) {
+            const float2 a0 = val(m), a1 = val(m + 1);
+            const float2 send = odd ? a0 : a1, keep = odd ? a1 : a0;
+            const float2 recv = make_float2(__shfl_xor_sync(0xffffffffu, send.x, 1),
+                                            __shfl_xor_sync(0xffffffffu, send.y, 1));
+            const float4 o4 = odd ? make_float4(recv.x, recv.y, keep.x, keep.y)
+                                  : make_float4(keep.x, keep.y, recv.x, recv.y);
+            *reinterpret_cast<float4 *>(b + (long long)((m - M0) / 2) * step + (long long)M0 * G::N1 * stride) = o4;
+        }
+    } else {
+        float2 *sb = base + (long long)(j + G::N1 * M0) * stride;
+        const long long step = (long long)G::N1 * stride;
+#pragma unroll
+        for (int m = M0; m < M1; ++m) {
+            sb[0] = val(m);
+            sb += step;
+        }
+    }
+}
+
 template <int N, int MODE>
 __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     k_stile(const __grid_constant__ CUtensorMap tmap, SParams p) {
@@ -228,6 +271,11 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     // outputs (see header).  The bit is uniform per warp (a warp holds the
     // rows 32/COLS consecutive j), so the flips are a non-divergent branch.
     const bool flip = T::FLIP && ((j >> (ilog2(G::N1) - 1)) & 1);
+    // stashed tile rows [N - SROWS, N) = register slots m >= SM0 (see SParams::tma_store)
+    constexpr int SROWS = T::HALFX ? N / 2 : N;
+    constexpr int SM0 = T::HALFX ? G::N2 / 2 : 0;
+    static_assert(!T::HALFX || T::XB >= (N / 2) * T::COLS, "stash needs half a tile");
+    const bool TST = T::COLS == 16 && SROWS >= T::BOXN && p.tma_store;
 
     for (int i = 0; i < nloc; ++i) {
         if (!mbar_wait(full, i & 1)) {
@@ -245,6 +293,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
             for (int m = 1; m < G::N2; m += 2) v[m] = cscale(v[m], -1.f);
         }
         fence_proxy_async_smem();
+        // the previous tile's stashed half must have left the exchange buffer
+        // before anyone writes it again (first exchange of this tile)
+        if (TST && tl == 0) bulk_wait_read0();
         gsync<N>(bar);                   // stage consumed: prefetch the next tile
         if (tl == 0 && i + 1 < nloc) issue(i + 1);
 
@@ -343,6 +394,26 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 const int y = j + G::N1 * m;
                 sb[(y >> p.nyl_lg) * bk + (long long)(y & (nyl - 1)) * stride] = v[m];
             }
+        } else if (TST) {
+            // rows < N - SROWS straight from registers; rows >= N - SROWS into
+            // the (free) exchange buffer as a dense [row][COLS] block, written
+            // back by tensor-map stores while the next tile computes
+            store_slots<N, MODE, 0, SM0>(v, p.dst + (o * p.ostride + col), stride, j, c);
+#pragma unroll
+            for (int m = SM0; m < G::N2; ++m)
+                xb[(j + G::N1 * m - (N - SROWS)) * T::COLS + c] = (MODE == S_FWD) ? v[m] : cconj(v[m]);
+            fence_proxy_async_smem();
+            gsync<N>(bar);
+            if (tl == 0) {
+                const int c0 = (int)(col - c);
+#pragma unroll
+                for (int bx = 0; bx < SROWS / T::BOXN; ++bx) {
+                    const int r0 = N - SROWS + bx * T::BOXN;
+                    if (p.map_rank == 3) tma_store_3d(&tmap, c0, r0, (int)o, xb + (r0 - (N - SROWS)) * T::COLS);
+                    else tma_store_2d(&tmap, c0, (int)o * N + r0, xb + (r0 - (N - SROWS)) * T::COLS);
+                }
+                bulk_commit();
+            }
         } else {
             float2 *sb = p.dst + (o * p.ostride + col) + (long long)j * stride;
             const long long step = (long long)G::N1 * stride;
@@ -354,14 +425,11 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                     sb += step;
                 }
             } else {
-#pragma unroll
-                for (int m = 0; m < G::N2; ++m) {
-                    sb[0] = (MODE == S_FWD) ? v[m] : cconj(v[m]);
-                    sb += step;
-                }
+                store_slots<N, MODE, 0, G::N2>(v, p.dst + (o * p.ostride + col), stride, j, c);
             }
         }
     }
+    if (TST && tl == 0) bulk_wait0();   // the exchange buffer outlives the last bulk store
 }
 
 // ========================================================= launchers ====

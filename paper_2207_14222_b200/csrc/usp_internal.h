@@ -131,6 +131,9 @@ struct SParams {
     long long y0;        // global y of this rank's y block (z pass multiplier)
     long long o0;        // first outer index (plane) of this launch (chunked schedule)
     int store_hint;      // 0: plain stores; 1: evict_last (K_D: K_A re-reads from L2); 2: evict_first
+    int tma_store;       // k_stile: store the upper half of each tile (rows >= N/2; all rows for
+                         // N <= 256) through the exchange buffer with tensor-map stores on the
+                         // load map (in-place passes whose map describes dst only)
     // transposes fused into the stores (slab decomposition, peer memory):
     // 1 = K_B stores into the ranks' receive buffers, 2 = K_C stores into the
     // ranks' send buffers; peer[q] = rank q's buffer (this GPU's own for q = rank,
