@@ -89,7 +89,11 @@ __device__ __forceinline__ void finish_xpass(bool src_epi, bool xonly, double to
     const double r = sqrt(total) / st->n0;
     st->r = r;
     red.hist[k1 % red.hist_cap] = r;
+#ifdef USP_DIAG_NODIV   // diagnostics builds only: keep iterating through overflow (timing ablations)
+    if (false) st->status = ST_DIVERGED;
+#else
     if (!(r <= 1e6)) st->status = ST_DIVERGED;            // NaN, Inf or r > 1e6
+#endif
     else if (st->tol > 0.0 && r < st->tol) st->status = ST_STOP_PENDING;
 }
 

@@ -174,6 +174,13 @@ __device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *x
 // Measured at 1024^3 (tools/gpu/kab.py, medians of 5): K_D 3.30 -> 2.77 ms with
 // paired stores, while K_B (2.67 -> 2.82) and K_C (4.45 -> 4.51) are faster
 // with 64-bit stores.
+// diagnostics only (timing ablations of K_C; results wrong when changed)
+#ifndef USP_DIAG_PASSES
+#define USP_DIAG_PASSES 2
+#endif
+#ifndef USP_DIAG_NOMUL
+#define USP_DIAG_NOMUL 0
+#endif
 #ifndef USP_ST128
 #define USP_ST128 2
 #endif
@@ -319,9 +326,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 base = fmaf(p.mp.D, pt2, p.mp.sc.x);
             }
 #pragma unroll 1
-            for (int pass = 0; pass < 2; ++pass) {
+            for (int pass = 0; pass < USP_DIAG_PASSES; ++pass) {
                 stile_fft<N>(v, xb, sm_tw, c, j, bar);
-                if (pass == 0) {
+                if (pass == 0 && !USP_DIAG_NOMUL) {
                     // (L+1)^-1 symbol (Eq. 12) at the signed frequency of k = j + N1 m:
                     //   g = cn (dr - i di) / (dr^2 + di^2),  dr = D |p|^2 + Re(sigma + c),
                     //   di = Im(sigma + c);  then conj so the second forward DFT inverts.
