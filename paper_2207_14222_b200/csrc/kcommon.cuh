@@ -4,10 +4,35 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "fft_core.cuh"
 #include "usp_internal.h"
 
 namespace usp {
+
+// Launch with programmatic stream serialization (PDL, see tma.cuh
+// pdl_trigger/pdl_wait) unless USP_PDL=0: the next kernel's launch overlaps
+// the tail of this one instead of following its completion.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t s,
+                              const Args &...args) {
+    static const int use = [] {
+        const char *e = std::getenv("USP_PDL");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = use;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 // ------------------------------------------------------------ helpers --
 __device__ __forceinline__ double warp_sum_d(double v) {

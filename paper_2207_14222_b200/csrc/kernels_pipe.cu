@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    pdl_trigger();
+    pdl_wait();
     bool xonly = false;
     float alpha = 0.f;
     if (MODE == X_ITER) {
@@ -242,8 +244,7 @@ static cudaError_t xpipe_t(const XParams &p, int grid, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_xpass_pipe<N, MODE><<<grid, XPipe<N>::NT, XPipe<N>::SMEM, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(k_xpass_pipe<N, MODE>, grid, XPipe<N>::NT, XPipe<N>::SMEM, s, p);
 }
 
 cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s) {

@@ -232,6 +232,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     float2 *sm_tw = reinterpret_cast<float2 *>(smem_raw) + T::GROUPS * T::GSM;
     uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N) + g;
     const int bar = 1 + g;
+    pdl_trigger();
+    if (tid == 0) prefetch_tmap(&tmap);
+    pdl_wait();
     if (p.check_state) {
         const bool running = p.st->status == ST_RUNNING && p.st->k < p.st->kmax;
         if (p.check_state == 3 && blockIdx.x == 0 && threadIdx.x == 0) p.st->full_iter = running;
@@ -449,8 +452,7 @@ static cudaError_t stile_t(const CUtensorMap &map, const SParams &p, int grid, c
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_stile<N, MODE><<<grid, STile<N>::NT, STile<N>::SMEM, s>>>(map, p);
-    return cudaGetLastError();
+    return launch_pdl(k_stile<N, MODE>, grid, STile<N>::NT, STile<N>::SMEM, s, map, p);
 }
 
 template <int N>

@@ -149,6 +149,15 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 // every committed bulk store has completed (writes performed)
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// Programmatic dependent launch (the iteration kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a CTA lets the next
+// kernel in the stream be scheduled as soon as it starts (all our grids are
+// one persistent wave), and waits for the previous kernel's completion and
+// memory flush before touching anything it wrote.  Both are no-ops for a
+// normal launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
