@@ -18,6 +18,7 @@
 // pass kernels (register loads from L2 instead of TMA stages: the data is
 // resident and the phases are short).
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <math.h>
 #include <stdint.h>
 
@@ -58,11 +59,11 @@ __device__ __forceinline__ bool grid_barrier(unsigned *count, volatile unsigned 
     return ok != 0;
 }
 
-template <int NX, int NY>
+template <int NX, int NY, int NT_ = 256>
 struct S2 {
     using GX = LineGeo<NX>;
     using GY = LineGeo<NY>;
-    static constexpr int NT = 256;
+    static constexpr int NT = NT_;
     // work is dealt per CTA: an x unit = LPC lines, a y unit = COLS columns.
     // (Dealing 32/N1-line warp units over every warp of 148 CTAs measured
     // slower at 512^2: 26 vs 22 us per iteration -- more CTAs at each grid
@@ -70,21 +71,28 @@ struct S2 {
     static constexpr int LPC = NT / GX::N1;                  // x lines per CTA step
     static constexpr int XS = LPC * LayRow<NX>::kFloat2PerLine;
     static constexpr int COLS = NT / GY::N1;                 // y tile columns (16 or 32): all threads work
-    static constexpr int YPAD = (COLS == 16 || COLS == 32) ? 0 : 8;
+    // writer rows of the y exchange: pitch = 8 or 4 (mod 16) float2 keeps the
+    // 16 lanes of a 64-bit phase on distinct banks for 8 / 4 columns
+    static constexpr int YPAD = (COLS == 16 || COLS == 32) ? 0 : (COLS == 8 ? 8 : 4);
     static constexpr int YS = GY::N1 * (GY::N2 * COLS + YPAD);
     static constexpr int BUF = XS > YS ? XS : YS;
-    static constexpr int SMEM = (BUF + NX + NY) * 8;
+    // X phase: B, Delta, x of the CTA's lines prefetched into shared memory
+    // (cp.async) before the inverse FFT, so the update does not wait on L2
+    static constexpr int PFE = LPC * NX;                      // float2 per field
+    static constexpr bool PF = (BUF + NX + NY + 3 * PFE) * 8 <= 200 * 1024;
+    static constexpr int SMEM = (BUF + NX + NY + (PF ? 3 * PFE : 0)) * 8;
 };
 
-template <int NX, int NY>
-__global__ void __launch_bounds__(256, 1) k_solve2d(S2Params p) {
-    using T = S2<NX, NY>;
+template <int NX, int NY, int NT>
+__global__ void __launch_bounds__(NT, 1) k_solve2d(S2Params p) {
+    using T = S2<NX, NY, NT>;
     using GX = typename T::GX;
     using GY = typename T::GY;
     extern __shared__ __align__(16) float2 smem2[];
     float2 *buf = smem2;
     float2 *twx = buf + T::BUF;
     float2 *twy = twx + NX;
+    float2 *pf = twy + NY;   // PF: [B | Delta | x][lq][line element]
     __shared__ double sh_red[8];
     __shared__ int s_status;
     __shared__ long long s_k;
@@ -152,14 +160,36 @@ __global__ void __launch_bounds__(256, 1) k_solve2d(S2Params p) {
                     }
                     continue;
                 }
+                const int eb = lq * NX + j;   // this thread's elements in the PF block: eb + N1 m
+                if constexpr (T::PF) {
+#pragma unroll
+                    for (int m = 0; m < GX::N2; ++m) {
+                        const long long i = base + GX::N1 * m;
+                        cp_async8(pf + eb + GX::N1 * m, p.B + i);
+                        cp_async8(pf + T::PFE + eb + GX::N1 * m, p.delta + i);
+                        cp_async8(pf + 2 * T::PFE + eb + GX::N1 * m, p.x + i);
+                    }
+                    cp_async_commit();
+                }
 #pragma unroll
                 for (int m = 0; m < GX::N2; ++m) v[m] = cconj(__ldcg(&p.work[base + GX::N1 * m]));
                 fft_line<NX, false, LayRow<NX>, true>(v, lay, j, twx);   // inverse via conj
+                if constexpr (T::PF) cp_async_wait0();
                 float lacc = 0.f;
 #pragma unroll
                 for (int m = 0; m < GX::N2; ++m) {
                     const long long i = base + GX::N1 * m;
-                    const float2 y = cconj(v[m]), b = p.B[i], d = p.delta[i], xx = p.x[i];
+                    float2 b, d, xx;
+                    if constexpr (T::PF) {
+                        b = pf[eb + GX::N1 * m];
+                        d = pf[T::PFE + eb + GX::N1 * m];
+                        xx = pf[2 * T::PFE + eb + GX::N1 * m];
+                    } else {
+                        b = p.B[i];
+                        d = p.delta[i];
+                        xx = p.x[i];
+                    }
+                    const float2 y = cconj(v[m]);
                     const float2 t = cmul(b, csub(y, d));
                     const float2 dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
                     p.x[i] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
@@ -174,13 +204,18 @@ __global__ void __launch_bounds__(256, 1) k_solve2d(S2Params p) {
             }
         }
         // residual: CTA partial -> barrier -> every CTA sums all partials in order
-        const double mine = block_sum_d<256>(acc, sh_red);
+        const double mine = block_sum_d<NT>(acc, sh_red);
         double *part = p.partials + parity * gridDim.x;
         if (tid == 0) part[blockIdx.x] = mine;
         if (!grid_barrier(p.bar_count, p.bar_gen, st)) return;
-        if (tid == 0) {
+        if (tid < 32) {
+            // warp 0 sums the CTA partials: lane l takes partials l, l+32, ...
+            // (loads in flight together), then a fixed shuffle tree -- the
+            // same order in every CTA, so every CTA takes the same decision
             double total = 0.0;
-            for (unsigned b = 0; b < gridDim.x; ++b) total += __ldcg(&part[b]);
+            for (unsigned b = tid; b < gridDim.x; b += 32) total += __ldcg(&part[b]);
+            total = warp_sum_d(total);
+            if (tid == 0) {
             const long long k1 = k + 1;
             int stt = status;
             double rr = r;
@@ -195,6 +230,7 @@ __global__ void __launch_bounds__(256, 1) k_solve2d(S2Params p) {
             s_status = stt;
             s_k = k1;
             sh_red[0] = rr;
+            }
         }
         __syncthreads();
         status = s_status;
@@ -211,27 +247,42 @@ __global__ void __launch_bounds__(256, 1) k_solve2d(S2Params p) {
 }
 
 // ========================================================= launchers ====
-template <int NX, int NY>
+template <int NX, int NY, int NT>
 static cudaError_t solve2d_t(const S2Params &p, int nsm, cudaStream_t s, int *grid_out) {
+    using T = S2<NX, NY, NT>;
     static int grid = 0;
     if (!grid) {
-        cudaError_t e = cudaFuncSetAttribute(k_solve2d<NX, NY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             S2<NX, NY>::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_solve2d<NX, NY, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             T::SMEM);
         if (e != cudaSuccess) return e;
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve2d<NX, NY>, 256, S2<NX, NY>::SMEM);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve2d<NX, NY, NT>, NT, T::SMEM);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
         // enough CTAs for the larger phase, at most one wave of co-resident CTAs
-        const int work = (NY / S2<NX, NY>::LPC) > (NX / S2<NX, NY>::COLS) ? (NY / S2<NX, NY>::LPC)
-                                                                        : (NX / S2<NX, NY>::COLS);
+        const int work = (NY / T::LPC) > (NX / T::COLS) ? (NY / T::LPC) : (NX / T::COLS);
         grid = work < nsm * per_sm ? work : nsm * per_sm;
     }
     if (grid_out) *grid_out = grid;
     S2Params pp = p;
     void *args[] = {&pp};
-    return cudaLaunchCooperativeKernel((const void *)k_solve2d<NX, NY>, dim3(grid), dim3(256), args,
-                                       S2<NX, NY>::SMEM, s);
+    return cudaLaunchCooperativeKernel((const void *)k_solve2d<NX, NY, NT>, dim3(grid), dim3(NT), args, T::SMEM,
+                                       s);
+}
+
+// CTA size (USP_S2NT = 64 / 128 / 256).  Default 128: twice the CTAs of the
+// 256-thread version, and the X phase's B, Delta, x fit the shared-memory
+// prefetch.  C2 (512^2, 1680 iterations to 1e-6): 256 threads 35.9 ms, 128
+// threads 25.5 ms (15.2 us per iteration), 64 threads 25.6 ms.
+template <int NX, int NY>
+static cudaError_t solve2d_nt(const S2Params &p, int nsm, cudaStream_t s) {
+    static const int nt = [] {
+        const char *e = std::getenv("USP_S2NT");
+        return e ? std::atoi(e) : 128;
+    }();
+    if (nt == 64) return solve2d_t<NX, NY, 64>(p, nsm, s, nullptr);
+    if (nt == 128) return solve2d_t<NX, NY, 128>(p, nsm, s, nullptr);
+    return solve2d_t<NX, NY, 256>(p, nsm, s, nullptr);
 }
 
 bool solve2d_supported(long long nx, long long ny) {
@@ -241,7 +292,7 @@ bool solve2d_supported(long long nx, long long ny) {
 
 cudaError_t launch_solve2d(int nx, int ny, const S2Params &p, int nsm, cudaStream_t s) {
 #define S2_Y(X, Y) \
-    case Y: return solve2d_t<X, Y>(p, nsm, s, nullptr);
+    case Y: return solve2d_nt<X, Y>(p, nsm, s);
 #define S2_X(X)                                                                  \
     case X:                                                                      \
         switch (ny) { S2_Y(X, 64) S2_Y(X, 128) S2_Y(X, 256) S2_Y(X, 512) default: return cudaErrorInvalidValue; }
