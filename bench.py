@@ -50,6 +50,11 @@ KERNEL_BYTES = {
     "y_fwd_mul_inv": 16,
 }
 ITER_BYTES_3D = 104         # 56 + 3 * 16 (SURVEY.md §8 geometry table)
+# x-form plans (reading R-30): Algorithm 1 literally; the x pass
+# reads work, s, x, B and writes x, work (its end-of-call probe moves the
+# same bytes: writes Delta instead of x)
+XFORM_XPASS_BYTES = 48
+ITER_BYTES_3D_XFORM = 96
 # Chunked schedule (1 GPU, 3-D): per z-chunk K_D -> K_A -> K_B
 # with the chunk's work array L2-resident in between, so HBM sees only
 KERNEL_BYTES_CHUNKED = {
@@ -409,12 +414,21 @@ def run_usp(args, world, rank, local):
     n_it_total = n_iter * args.steps
     chunks = max(1, prof.get("xpass", (0, n_it_total))[1] // n_it_total)
     schedule = "chunked" if chunks > 1 else "4-pass"
-    kbytes = KERNEL_BYTES_REAL if real else (KERNEL_BYTES_CHUNKED if chunks > 1 else KERNEL_BYTES)
+    kbytes = dict(KERNEL_BYTES_REAL if real else (KERNEL_BYTES_CHUNKED if chunks > 1 else KERNEL_BYTES))
+    # which algebraic form ran: every timed step starts from set_source (x-form
+    # on x-form plans) and ends still in the x-form unless r fell below r_switch
+    xform_plan, xform_now, r_switch = plan.iteration_form()
+    xform_all = xform_plan and xform_now
+    if xform_all:
+        kbytes["xpass"] = XFORM_XPASS_BYTES
+    form_desc = ("x-form (Algorithm 1 literally) throughout" if xform_all else
+                 ("x-form, then Delta-form below r_switch" if xform_plan else "Delta-form"))
     dname = "xpass" if "xpass" in prof else max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
     dms, dcount = prof[dname]
     d_ms_per_iter = dms / n_it_total
     dbytes = kbytes[dname] * nloc                   # per iteration (= per launch x chunks)
-    achieved = dbytes / (d_ms_per_iter / 1e3) / 1e9
+    # every launch of the kernel (x-form plans: + one probe pass per step) over its total time
+    achieved = kbytes[dname] * nloc * dcount / (dms / 1e3) / 1e9
     traffic = ncu_traffic(name).get(dname) if args.size is None and mode != "virtual" else None
     # iteration time: device time of the iterate() calls / iterations
     iter_ms = sum(a.elapsed_time(b) for a, b in it_events) / n_it_total
@@ -459,7 +473,8 @@ def run_usp(args, world, rank, local):
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
     # separate transposes (NCCL all-to-all / device copies) add their staging
     # reads and writes; the fused (peer-store) transposes add nothing to HBM
-    iter_bpv = (ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D)) + \
+    iter_bpv = (ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else
+                                              (ITER_BYTES_3D_XFORM if xform_all else ITER_BYTES_3D))) + \
         ((16 if real else 32) if "all_to_all" in prof else 0)
     it_bytes = iter_bpv * nloc
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
@@ -473,13 +488,14 @@ def run_usp(args, world, rank, local):
         "config": {"workload": f"{name} 3-D {'diffusion' if real else 'Helmholtz'} {shape[2]}x{shape[1]}x{shape[0]} "
                                f"{'float32 (half-spectrum path)' if real else 'complex64'}, "
                                f"{n_iter} iterations of Alg. 1 per step (setup + iterations), alpha=0.75",
-                   "grid": list(shape), "iterations_per_step": n_iter,
+                   "grid": list(shape), "iterations_per_step": n_iter, "iteration_form": form_desc,
                    "parallelism": parallelism, "slab_check_rel_l2": slab_check,
                    "l2": "inputs (8 GiB fields) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                      "algorithmic_bytes_per_iteration": dbytes, "ms_per_iteration": d_ms_per_iter,
-                     "launches_per_iteration": dcount // n_it_total, "schedule": schedule},
+                     "launches_per_iteration": dcount // n_it_total, "launches_per_step": dcount / args.steps,
+                     "schedule": schedule},
         "iteration_roofline": {"bytes_per_voxel": iter_bpv, "iter_ms": iter_ms,
                                "achieved_gbs": it_bytes / (iter_ms / 1e3) / 1e9,
                                "frac": it_bytes / (iter_ms / 1e3) / 1e9 / hbm},

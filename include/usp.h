@@ -263,6 +263,16 @@ usp_status usp_profile_read(usp_plan_t plan, int cap, char (*names)[32], double 
 /* Number of kernel launches the library issued since plan creation. */
 usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
 
+/* Algebraic form of the iteration (reading R-30).  xform = 1: the
+ * plan runs Algorithm 1 literally (x-form: 8 fewer HBM bytes per
+ * voxel and iteration; s = S/c kept in the workspace) while the last
+ * residual is >= r_switch (default 1e-2, env USP_XSWITCH; USP_XFORM=0 at
+ * plan creation disables), then the Delta-form recurrence (exact
+ * down to fp32 rounding near convergence).  form: 0 = Delta-form now,
+ * 1 = x-form now.  Every usp_iterate call leaves r_k and Delta_k of the
+ * current x_k in the state, whichever form ran.  Errors: USP_ERR_ARG. */
+usp_status usp_iteration_form(usp_plan_t plan, int *xform, int *form, double *r_switch);
+
 /* NCCL communicator for the slab decomposition (one process per GPU).
  * Rank 0 calls usp_comm_unique_id and broadcasts the 128 bytes (e.g. with
  * torch.distributed); every rank then calls usp_comm_init with the same id,

@@ -92,34 +92,60 @@ __device__ __forceinline__ float2 multiplier(const MulParams &mp, float p2) {
 
 __device__ __forceinline__ float freq_m(int k, int n) { return (float)(k < (n >> 1) ? k : k - n); }
 
+// The x pass's action for this launch (read by every CTA before the last
+// CTA's finish changes the state): the x-form state turns into the
+// Delta-form once the last residual is below r_sw (reading R-30).
+__device__ __forceinline__ int xform_act(const IterState *st) {
+    const int f = st->form;
+    if (f == FORM_X) return (st->r < st->r_sw) ? ACT_TO_DELTA : ACT_X;
+    return f == FORM_PROBE ? ACT_PROBE : ACT_DELTA;
+}
+
+// Does an iteration launch run?  (RUNNING below kmax, or the end-of-call probe.)
+__device__ __forceinline__ bool iter_running(const IterState *st) {
+    return (st->status == ST_RUNNING && st->k < st->kmax) || (st->form == FORM_PROBE && st->status == ST_RUNNING);
+}
+
 // Thread 0 of the last CTA of an x pass: publish n0 (source setup) or
-// r_{k+1} and the stop decision (iteration), see kernels.cu header.
+// the residual and the stop decision (iteration), see kernels.cu header.
+//   ACT_DELTA     Delta-form: x_{k+1} done, r_{k+1} of Delta_{k+1}; below tol
+//                 -> STOP_PENDING (the next pass applies x += alpha Delta_{k+1})
+//   ACT_X         x-form: x_{k+1} done, r_k of the Delta_k it used; below tol
+//                 -> converged (reading R-5)
+//   ACT_PROBE / ACT_TO_DELTA: Delta_k stored, x not updated, r_k; k unchanged;
+//                 below tol -> STOP_PENDING, as the Delta-form
 __device__ __forceinline__ void finish_xpass(bool src_epi, bool xonly, double total, IterState *st,
-                                             const Red &red) {
+                                             const Red &red, int act = ACT_DELTA) {
     if (src_epi) {
         const double n0 = sqrt(total);
         st->n0 = n0;
         st->r = (n0 > 0.0) ? 1.0 : 0.0;
         st->k = 0;
         st->status = (n0 > 0.0) ? ST_RUNNING : ST_DONE_CONV;
+        st->form = st->xform ? FORM_X : FORM_DELTA;
         red.hist[0] = st->r;
         return;
     }
-    const long long k1 = st->k + 1;
-    st->k = k1;
+    const long long k = st->k;
     if (xonly) {                       // the final update x_{k+1} = x_k + alpha Delta_k
+        st->k = k + 1;
         st->status = ST_DONE_CONV;
         return;
     }
     const double r = sqrt(total) / st->n0;
     st->r = r;
-    red.hist[k1 % red.hist_cap] = r;
+    long long hi = k;                  // index of the Delta whose norm this is
+    if (act == ACT_DELTA || act == ACT_X) st->k = k + 1;
+    if (act == ACT_DELTA) hi = k + 1;
+    if (act == ACT_TO_DELTA) st->form = FORM_DELTA;
+    if (act == ACT_PROBE) st->form = FORM_X;
+    red.hist[hi % red.hist_cap] = r;
 #ifdef USP_DIAG_NODIV   // diagnostics builds only: keep iterating through overflow (timing ablations)
     if (false) st->status = ST_DIVERGED;
 #else
     if (!(r <= 1e6)) st->status = ST_DIVERGED;            // NaN, Inf or r > 1e6
 #endif
-    else if (st->tol > 0.0 && r < st->tol) st->status = ST_STOP_PENDING;
+    else if (st->tol > 0.0 && r < st->tol) st->status = (act == ACT_X) ? ST_DONE_CONV : ST_STOP_PENDING;
 }
 
 }  // namespace usp

@@ -175,10 +175,7 @@ __global__ void __launch_bounds__(SGeo<N, COLS>::NT, SGeo<N, COLS>::MINB) k_stri
     float2 *sm_tw = smem + G::N1 * SG::PITCH;
     const int tid = threadIdx.x;
     const int c = tid % COLS, j = tid / COLS;
-    if (p.check_state) {
-        const int status = p.st->status;
-        if (status != ST_RUNNING || p.st->k >= p.st->kmax) return;
-    }
+    if (p.check_state && !iter_running(p.st)) return;
     load_twiddles<N>(sm_tw, p.tw);
     __syncthreads();
     const LayCol<N, COLS, SG::PAD, 0> lay{smem, c};
@@ -455,15 +452,20 @@ __global__ void __launch_bounds__(256) k_farthest(FarParams p) {
 // and takes the same stop decision (reading R-4).
 __global__ void k_finish(IterState *st, const double *sums, int P, int src_epi, Red red) {
     bool xonly = false;
+    int act = ACT_DELTA;
     if (!src_epi) {
         const int status = st->status;
-        if (st->k >= st->kmax || (status != ST_RUNNING && status != ST_STOP_PENDING)) return;
+        const bool probe = st->form == FORM_PROBE && status == ST_RUNNING;
+        if (!probe && (st->k >= st->kmax || (status != ST_RUNNING && status != ST_STOP_PENDING))) return;
         xonly = (status == ST_STOP_PENDING);
+        act = xform_act(st);   // unchanged since the x pass read it (it did not finish)
     }
     double total = 0.0;
     for (int q = 0; q < P; ++q) total += sums[q];
-    finish_xpass(src_epi != 0, xonly, total, st, red);
+    finish_xpass(src_epi != 0, xonly, total, st, red, act);
 }
+
+__global__ void k_set_form(IterState *st, int form) { st->form = form; }
 
 __global__ void k_set_state(IterState *st, double alpha, double tol, long long kmax) {
     st->alpha = alpha;
@@ -564,6 +566,11 @@ cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s) {
 
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s) {
     k_finish<<<1, 1, 0, s>>>(st, sums, P, src_epi, red);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_form(IterState *st, int form, cudaStream_t s) {
+    k_set_form<<<1, 1, 0, s>>>(st, form);
     return cudaGetLastError();
 }
 

@@ -67,13 +67,23 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
     pdl_wait();
     bool xonly = false;
     float alpha = 0.f;
+    int act = ACT_DELTA;   // X_ITER: Delta-form, x-form, probe or x-form -> Delta-form (kcommon.cuh)
     if (MODE == X_ITER) {
         const int status = p.st->status;
         const long long k = p.st->k, kmax = p.st->kmax;
-        if (k >= kmax || (status != ST_RUNNING && status != ST_STOP_PENDING)) return;
+        const bool probe = p.st->form == FORM_PROBE && status == ST_RUNNING;
+        if (!probe && (k >= kmax || (status != ST_RUNNING && status != ST_STOP_PENDING))) return;
         xonly = (status == ST_STOP_PENDING);
         alpha = (float)p.st->alpha;
+        act = xform_act(p.st);
     }
+    const bool dform = act == ACT_DELTA;
+    const float c1 = dform ? alpha : 1.f;                       // Delta_new = d0 + c1 t
+    const float e1 = (act == ACT_X || act == ACT_PROBE) ? 1.f : 0.f;   // u = B w + e1 s
+    const bool store_x = act == ACT_DELTA || act == ACT_X, store_d = act != ACT_X;
+    const bool u_from_d = act == ACT_DELTA || act == ACT_TO_DELTA;
+    // stage slot 1: Delta (Delta-form) or s (x-form passes; source setup of x-form plans)
+    const float2 *slot1 = (MODE == X_ITER && act != ACT_DELTA) || (MODE == X_SRC_EPI && p.s) ? p.s : p.delta;
     double acc = 0.0;
     const long long nvox = p.nlines * (long long)N;
 
@@ -116,8 +126,9 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                         const char *src = reinterpret_cast<const char *>(p.x) + off * (p.src_real ? 4 : 8);
                         bulk_g2s(st, src, sb, &full[s]);
                     } else if (MODE == X_SRC_EPI) {
-                        mbar_arrive_expect_tx(&full[s], 2 * ub);
+                        mbar_arrive_expect_tx(&full[s], (p.s ? 3 : 2) * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
+                        if (p.s) bulk_g2s(st + 1 * T::UE, slot1 + off, ub, &full[s]);
                         bulk_g2s(st + 3 * T::UE, p.B + off, ub, &full[s]);
                     } else if (p.l2hint) {
                         mbar_arrive_expect_tx(&full[s], 4 * ub);
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                     } else {
                         mbar_arrive_expect_tx(&full[s], 4 * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
-                        bulk_g2s(st + 1 * T::UE, p.delta + off, ub, &full[s]);
+                        bulk_g2s(st + 1 * T::UE, slot1 + off, ub, &full[s]);
                         bulk_g2s(st + 2 * T::UE, p.x + off, ub, &full[s]);
                         bulk_g2s(st + 3 * T::UE, p.B + off, ub, &full[s]);
                     }
@@ -138,7 +149,8 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
         } else {
             // ------------------------------------------------ consumer warps
             const int lq = lane / G::N1, j = lane % G::N1;
-            const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+            // (the chunked schedule's L2 hints apply to the loads only: hinted
+            // stores cost a uniform-register move per store in this body)
             const LayRow<N> lay{xbufs + warp * T::XBUF + lq * LayRow<N>::kFloat2PerLine};
             for (int i = warp; i < nloc; i += T::XC) {
                 const int s = i % T::S;
@@ -157,6 +169,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                         const float2 sv = p.src_real ? make_float2(reinterpret_cast<const float *>(st)[e], 0.f)
                                                      : st[e];
                         v[m] = cmul(sv, p.inv_c);               // s = S / c
+                        if (p.s) p.s[gb + G::N1 * m] = v[m];   // x-form plans keep s
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -182,19 +195,32 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                             if (MODE == X_SRC_EPI) {
                                 dn = cmul(b, y);                    // Delta_0 = B (L+1)^-1 s
                                 p.x[gi] = make_float2(0.f, 0.f);    // x_0 = 0 (L83)
-                            } else {
-                                const float2 d = st[1 * T::UE + e];
-                                const float2 xx = st[2 * T::UE + e];
-                                const float2 t = cmul(b, csub(y, d));
-                                dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
-                                const float2 xn = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
-                                if (p.l2hint) st_hint(&p.x[gi], xn, pol_first);
-                                else p.x[gi] = xn;
+                                p.delta[gi] = dn;
+                                lacc += cabs2(dn);
+                                // next chain: u = B Delta (x-form plans: u_0 = s)
+                                v[m] = p.s ? st[1 * T::UE + e] : cmul(b, dn);
+                                continue;
                             }
-                            if (MODE != X_SRC_EPI && p.l2hint) st_hint(&p.delta[gi], dn, pol_first);
-                            else p.delta[gi] = dn;
+                            // One body for every action (uniform selects, no duplicated code):
+                            //   Delta-form: t = B (y - Delta_k), Delta_{k+1} = Delta_k + alpha t,
+                            //                        x_{k+1} = x_k + alpha Delta_k, u = B Delta_{k+1}
+                            //   x-form (Alg. 1 lines 3-4): Delta_k = B (y - x_k),
+                            //                        x_{k+1} = x_k + alpha Delta_k, u = B x_{k+1} + s
+                            //   probe: Delta_k = B (y - x_k) stored, x kept, u = B x_k + s
+                            //   x-form -> Delta-form: Delta_k stored, x kept, u = B Delta_k
+                            const float2 a1 = st[1 * T::UE + e];    // Delta_k or s
+                            const float2 xx = st[2 * T::UE + e];
+                            const float2 t = cmul(b, csub(y, dform ? a1 : xx));
+                            const float2 d0 = dform ? a1 : make_float2(0.f, 0.f);
+                            dn = make_float2(fmaf(c1, t.x, d0.x), fmaf(c1, t.y, d0.y));
+                            const float2 xi = dform ? a1 : t;
+                            const float2 xn = make_float2(fmaf(alpha, xi.x, xx.x), fmaf(alpha, xi.y, xx.y));
+                            if (store_x) p.x[gi] = xn;
+                            if (store_d) p.delta[gi] = dn;
                             lacc += cabs2(dn);
-                            v[m] = cmul(b, dn);                     // next chain: u = B Delta
+                            const float2 w = u_from_d ? dn : (act == ACT_X ? xn : xx);
+                            const float2 bw = cmul(b, w);
+                            v[m] = make_float2(fmaf(e1, a1.x, bw.x), fmaf(e1, a1.y, bw.y));
                         }
                         acc += (double)lacc;
                         fence_proxy_async_smem();
@@ -202,13 +228,8 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                         if (lane == 0) mbar_arrive(&empty[s]);
                     }
                 }
-                if (p.l2hint) {
 #pragma unroll
-                    for (int m = 0; m < G::N2; ++m) st_hint(&p.work[gb + G::N1 * m], v[m], pol_last);
-                } else {
-#pragma unroll
-                    for (int m = 0; m < G::N2; ++m) p.work[gb + G::N1 * m] = v[m];
-                }
+                for (int m = 0; m < G::N2; ++m) p.work[gb + G::N1 * m] = v[m];
             }
         }
     }
@@ -229,7 +250,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
         *p.red.local_sum = total;
         return;
     }
-    finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red);
+    finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red, act);
 }
 
 // ========================================================= launchers ====

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     if (tid == 0) prefetch_tmap(&tmap);
     pdl_wait();
     if (p.check_state) {
-        const bool running = p.st->status == ST_RUNNING && p.st->k < p.st->kmax;
+        const bool running = iter_running(p.st);
         if (p.check_state == 3 && blockIdx.x == 0 && threadIdx.x == 0) p.st->full_iter = running;
         if (!((p.check_state == 2) ? (p.st->full_iter != 0) : running)) return;
     }

@@ -188,6 +188,11 @@ struct usp_plan_s {
     TDParams td{};
     // persistent 2-D solve (kernels_small.cu; USP_SOLVE2D=0 disables)
     bool solve2d = false;
+    // x-form passes while r >= r_sw (reading R-30; USP_XFORM=0 disables,
+    // USP_XSWITCH sets r_sw): s = S / c kept in its own field
+    bool xform_cap = false, xform = false;
+    double r_sw = 1e-2;
+    float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
     // plan-owned small device memory
     IterState *st = nullptr;
@@ -525,6 +530,7 @@ XParams x_params(usp_plan_s *p) {
     xp.inv_c = make_float2((float)(p->c.re / m), (float)(-p->c.im / m));
     xp.st = p->st;
     xp.red = red_params(p);
+    xp.s = p->xform ? p->s : nullptr;
     return xp;
 }
 
@@ -1172,6 +1178,11 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     {
         const char *s2 = std::getenv("USP_SOLVE2D");
         p->solve2d = !p->anti && !p->tdiff && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
+        const char *xf = std::getenv("USP_XFORM");
+        p->xform_cap = !p->real && !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && p->pipe_xk &&
+                       !(xf && xf[0] == '0');
+        const char *xs = std::getenv("USP_XSWITCH");
+        if (xs) p->r_sw = std::atof(xs);
     }
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
@@ -1213,7 +1224,7 @@ usp_status usp_plan_workspace_size(usp_plan_t p, size_t *bytes) {
         *bytes = 3 * (size_t)p->ncomp * f + align256((size_t)p->nloc * 4) * (1 + 2 * np);
         return USP_OK;
     }
-    *bytes = 3 * f + w * (p->P > 1 ? 3 : 1);
+    *bytes = 3 * f + w * (p->P > 1 ? 3 : 1) + (p->xform_cap ? f : 0);   // + s for the x-form
     return USP_OK;
 }
 
@@ -1252,6 +1263,7 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
         p->sendb = (float2 *)(p->ws + 3 * f + w);
         p->recvb = (float2 *)(p->ws + 3 * f + 2 * w);
     }
+    p->s = p->xform_cap ? (float2 *)(p->ws + 3 * f + w * (p->P > 1 ? 3 : 1)) : nullptr;
     if (p->real)   // the spectrum rows' padding columns are never written by the x pass: keep them 0
         CU(cudaMemsetAsync(p->work, 0, w * (p->P > 1 ? 3 : 1), p->stream));
     p->have_potential = p->have_source = false;
@@ -1461,6 +1473,10 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
     IterState s0{};
     s0.status = ST_NO_SOURCE;
     s0.alpha = 0.75;
+    p->xform = p->xform_cap && !p->chunked;
+    s0.xform = p->xform ? 1 : 0;
+    s0.r_sw = p->r_sw;
+    s0.form = FORM_DELTA;   // the source setup's finish sets FORM_X on x-form plans
     CU(cudaMemcpyAsync(p->st, &s0, sizeof s0, cudaMemcpyHostToDevice, p->stream));
     if (p->ndim == 1) {
         OneParams op{};
@@ -1547,8 +1563,10 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         const long long batch = 16;
         long long launched = 0;
         // with tol > 0 the device stops itself (every kernel checks the state);
-        // the host looks once per batch
-        const long long total = n_max;
+        // the host looks once per batch.  x-form plans: one spare launch for
+        // the pass that turns the x-form into the Delta-form (it does not
+        // count as an iteration); spare launches skip themselves.
+        const long long total = n_max + (p->xform ? 1 : 0);
         while (launched < total) {
             const long long nb = std::min(batch, total - launched);
             for (long long i = 0; i < nb; ++i) {
@@ -1579,6 +1597,21 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
                 if (s) return s;
                 const int stt = p->st_host->status;
                 if (stt == ST_DONE_CONV || stt == ST_DIVERGED) break;
+            }
+        }
+        if (p->xform) {
+            // still in the x-form at the end of the call: one probe pass computes
+            // Delta_k of the current x_k (x unchanged), so the state carries
+            // r_k and Delta_k as after a Delta-form iteration (reading R-30)
+            s = sync_state(p);
+            if (s) return s;
+            if (p->st_host->form == FORM_X && p->st_host->status == ST_RUNNING) {
+                {
+                    Tick t(p, KC_SETSTATE);
+                    CU(launch_set_form(p->st, FORM_PROBE, p->stream));
+                }
+                if ((s = chain_mid(p, 1))) return s;
+                if ((s = run_xpass(p, X_ITER, xp))) return s;
             }
         }
     }
@@ -2021,6 +2054,16 @@ usp_status usp_profile_read(usp_plan_t p, int cap, char (*names)[32], double *ms
 usp_status usp_launch_count(usp_plan_t p, int64_t *launches) {
     if (!p || !launches) return fail(USP_ERR_ARG, "NULL argument");
     *launches = p->launches;
+    return USP_OK;
+}
+
+usp_status usp_iteration_form(usp_plan_t p, int *xform, int *form, double *r_switch) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    usp_status s = sync_state(p);
+    if (s) return s;
+    if (xform) *xform = (p->xform_cap && !p->chunked) ? 1 : 0;
+    if (form) *form = (p->st_host->form == FORM_DELTA) ? 0 : 1;
+    if (r_switch) *r_switch = p->r_sw;
     return USP_OK;
 }
 

@@ -29,7 +29,20 @@ struct IterState {
     int err;               // pipeline watchdog: non-zero = a kernel gave up waiting (see tma.cuh)
     int err_info;
     int full_iter;         // chunked schedule: the running iteration does the full chain (snapshot by K_C)
+    // Algebraic form of the x pass (reading R-30): FORM_DELTA = Delta-form
+    // recurrence; FORM_X = Algorithm 1 literally (needs s,
+    // 8 fewer bytes per voxel); FORM_PROBE = one pass that computes Delta_k
+    // of the x-form state without updating x (end of an iterate call).  An
+    // x-form pass whose previous residual is below r_sw converts the state
+    // to the Delta-form instead (see xform_act).
+    int form;
+    int xform;             // the plan runs the x-form while r >= r_sw (set at set_source)
+    double r_sw;
 };
+
+enum : int { FORM_DELTA = 0, FORM_X = 1, FORM_PROBE = 2 };
+// what an x-pass launch does, decided from the state every CTA reads at its start
+enum : int { ACT_DELTA = 0, ACT_X = 1, ACT_PROBE = 2, ACT_TO_DELTA = 3 };
 
 struct Red {             // reduction scratch (device)
     double *partials;    // one per CTA of the reducing kernel
@@ -68,6 +81,7 @@ struct XParams {
     IterState *st;
     Red red;
     int l2hint;          // chunked schedule: stream Delta/x/B evict_first, keep work evict_last
+    float2 *s;           // x-form plans: s = S / c (else nullptr)
 };
 
 // ------------------------------------------------------- BiCGSTAB (NEXT-2) --
@@ -266,6 +280,7 @@ cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s);
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
+cudaError_t launch_set_form(IterState *st, int form, cudaStream_t s);
 
 // TMA-pipelined variants (kernels_pipe.cu)
 cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);

@@ -235,6 +235,12 @@ class Plan:
         L.check(self.lib.usp_launch_count(self.handle, ctypes.byref(n)))
         return int(n.value)
 
+    def iteration_form(self):
+        """(x-form plan?, currently in the x-form?, r_switch) -- usp_iteration_form."""
+        xf, fm, rs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
+        L.check(self.lib.usp_iteration_form(self.handle, ctypes.byref(xf), ctypes.byref(fm), ctypes.byref(rs)))
+        return bool(xf.value), bool(fm.value), float(rs.value)
+
     def close(self):
         if getattr(self, "handle", None):
             self.lib.usp_plan_destroy(self.handle)
