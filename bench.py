@@ -427,8 +427,9 @@ def run_usp(args, world, rank, local):
     dms, dcount = prof[dname]
     d_ms_per_iter = dms / n_it_total
     dbytes = kbytes[dname] * nloc                   # per iteration (= per launch x chunks)
-    # every launch of the kernel (x-form plans: + one probe pass per step) over its total time
-    achieved = kbytes[dname] * nloc * dcount / (dms / 1e3) / 1e9
+    # algorithmic bytes of the iterations over the kernel's total time (x-form
+    # plans add one launch per iterate call that skips itself: time only)
+    achieved = dbytes / (d_ms_per_iter / 1e3) / 1e9
     traffic = ncu_traffic(name).get(dname) if args.size is None and mode != "virtual" else None
     # iteration time: device time of the iterate() calls / iterations
     iter_ms = sum(a.elapsed_time(b) for a, b in it_events) / n_it_total

@@ -205,8 +205,10 @@ usp_status usp_set_source(usp_plan_t plan, const void *src, usp_where where);
 usp_status usp_iterate(usp_plan_t plan, int64_t n_max, double alpha, double tol,
                        int64_t *n_done, usp_term *term);
 
-/* Current residual: rel = ||Delta_k|| / n0 of the last Delta the iteration
- * used, abs_norm = n0 * rel, k = iterations since set_source. */
+/* Current residual: rel = ||Delta_k|| / n0 of the current x_k (after a
+ * converged stop: of the last Delta the iteration used), abs_norm = n0 * rel,
+ * k = iterations since set_source.  x-form plans may run one probe pass
+ * (usp_iteration_form): collective with slab decomposition. */
 usp_status usp_residual(usp_plan_t plan, double *rel, double *abs_norm, int64_t *k);
 
 /* Copy r_0 .. r_{n-1} (fp64) into host[0..cap); *n = number available
@@ -269,8 +271,10 @@ usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
  * residual is >= r_switch (default 1e-2, env USP_XSWITCH; USP_XFORM=0 at
  * plan creation disables), then the Delta-form recurrence (exact
  * down to fp32 rounding near convergence).  form: 0 = Delta-form now,
- * 1 = x-form now.  Every usp_iterate call leaves r_k and Delta_k of the
- * current x_k in the state, whichever form ran.  Errors: USP_ERR_ARG. */
+ * 1 = x-form now.  After x-form iterations, r_k and Delta_k of the current
+ * x_k are computed on demand by usp_residual / usp_residual_history (one
+ * probe pass: x unchanged); those two calls are therefore collective over
+ * the ranks of a slab-decomposed plan.  Errors: USP_ERR_ARG. */
 usp_status usp_iteration_form(usp_plan_t plan, int *xform, int *form, double *r_switch);
 
 /* NCCL communicator for the slab decomposition (one process per GPU).

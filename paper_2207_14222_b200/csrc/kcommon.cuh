@@ -112,8 +112,10 @@ __device__ __forceinline__ bool iter_running(const IterState *st) {
 //                 -> STOP_PENDING (the next pass applies x += alpha Delta_{k+1})
 //   ACT_X         x-form: x_{k+1} done, r_k of the Delta_k it used; below tol
 //                 -> converged (reading R-5)
-//   ACT_PROBE / ACT_TO_DELTA: Delta_k stored, x not updated, r_k; k unchanged;
-//                 below tol -> STOP_PENDING, as the Delta-form
+//   ACT_TO_DELTA  Delta_k stored, x not updated, r_k; k unchanged; below tol
+//                 -> STOP_PENDING, as the Delta-form
+//   ACT_PROBE     as ACT_TO_DELTA but the state stays in the x-form and the
+//                 status is left alone (an on-demand query of r_k)
 __device__ __forceinline__ void finish_xpass(bool src_epi, bool xonly, double total, IterState *st,
                                              const Red &red, int act = ACT_DELTA) {
     if (src_epi) {
@@ -145,7 +147,9 @@ __device__ __forceinline__ void finish_xpass(bool src_epi, bool xonly, double to
 #else
     if (!(r <= 1e6)) st->status = ST_DIVERGED;            // NaN, Inf or r > 1e6
 #endif
-    else if (st->tol > 0.0 && r < st->tol) st->status = (act == ACT_X) ? ST_DONE_CONV : ST_STOP_PENDING;
+    // (a probe only reports r_k: the x-form pass that follows decides the stop)
+    else if (st->tol > 0.0 && r < st->tol && act != ACT_PROBE)
+        st->status = (act == ACT_X) ? ST_DONE_CONV : ST_STOP_PENDING;
 }
 
 }  // namespace usp

@@ -473,6 +473,9 @@ __global__ void k_set_state(IterState *st, double alpha, double tol, long long k
     st->kmax = kmax;
     st->counter = 0u;
     const bool below = tol > 0.0 && st->r < tol;
+    // x-form state (reading R-30): st->r may be r_{k-1}; the next x-form pass
+    // computes r_k and stops itself after its update (the same count)
+    if (st->form == FORM_X) return;
     if (st->status == ST_RUNNING && below) st->status = ST_STOP_PENDING;
     if (st->status == ST_STOP_PENDING && !below) st->status = ST_RUNNING;
 }

@@ -190,7 +190,7 @@ struct usp_plan_s {
     bool solve2d = false;
     // x-form passes while r >= r_sw (reading R-30; USP_XFORM=0 disables,
     // USP_XSWITCH sets r_sw): s = S / c kept in its own field
-    bool xform_cap = false, xform = false;
+    bool xform_cap = false, xform = false, probe_needed = false;
     double r_sw = 1e-2;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -936,6 +936,15 @@ usp_status chunked_iteration(usp_plan_s *p) {
     return USP_OK;
 }
 
+usp_status chain_mid(usp_plan_s *p, int check_state);
+usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp);
+
+// x-form state after iterations (reading R-30): one probe pass computes
+// Delta_k = B(y_k - x_k) of the current x_k (x and the x-form chain input
+// unchanged), so r_k, Delta_k and the history r_0..r_k are as after a
+// Delta-form iteration.  Runs only when a query needs them.
+usp_status probe_xform(usp_plan_s *p);
+
 usp_status sync_state(usp_plan_s *p) {
     CU(cudaMemcpyAsync(p->st_host, p->st, sizeof(IterState), cudaMemcpyDeviceToHost, p->stream));
     CU(cudaStreamSynchronize(p->stream));
@@ -1474,6 +1483,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
     s0.status = ST_NO_SOURCE;
     s0.alpha = 0.75;
     p->xform = p->xform_cap && !p->chunked;
+    p->probe_needed = false;
     s0.xform = p->xform ? 1 : 0;
     s0.r_sw = p->r_sw;
     s0.form = FORM_DELTA;   // the source setup's finish sets FORM_X on x-form plans
@@ -1518,6 +1528,26 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
     p->have_source = true;
     return USP_OK;
 }
+
+}  // extern "C"
+
+namespace {
+usp_status probe_xform(usp_plan_s *p) {
+    if (!p->probe_needed) return USP_OK;
+    p->probe_needed = false;
+    usp_status s = sync_state(p);
+    if (s) return s;
+    if (p->st_host->form != FORM_X || p->st_host->status != ST_RUNNING || p->st_host->k == 0) return USP_OK;
+    {
+        Tick t(p, KC_SETSTATE);
+        CU(launch_set_form(p->st, FORM_PROBE, p->stream));
+    }
+    if ((s = chain_mid(p, 1))) return s;
+    return run_xpass(p, X_ITER, x_params(p));
+}
+}  // namespace
+
+extern "C" {
 
 usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, int64_t *n_done, usp_term *term) {
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
@@ -1599,21 +1629,9 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
                 if (stt == ST_DONE_CONV || stt == ST_DIVERGED) break;
             }
         }
-        if (p->xform) {
-            // still in the x-form at the end of the call: one probe pass computes
-            // Delta_k of the current x_k (x unchanged), so the state carries
-            // r_k and Delta_k as after a Delta-form iteration (reading R-30)
-            s = sync_state(p);
-            if (s) return s;
-            if (p->st_host->form == FORM_X && p->st_host->status == ST_RUNNING) {
-                {
-                    Tick t(p, KC_SETSTATE);
-                    CU(launch_set_form(p->st, FORM_PROBE, p->stream));
-                }
-                if ((s = chain_mid(p, 1))) return s;
-                if ((s = run_xpass(p, X_ITER, xp))) return s;
-            }
-        }
+        // still in the x-form: r_k / Delta_k of the current x_k are computed on
+        // demand (usp_residual*, probe_xform) -- a resumed call continues in the x-form
+        p->probe_needed = p->xform;
     }
     s = sync_state(p);
     if (s) return s;
@@ -1631,7 +1649,9 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
 usp_status usp_residual(usp_plan_t p, double *rel, double *abs_norm, int64_t *k) {
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
-    usp_status s = sync_state(p);
+    usp_status s = probe_xform(p);
+    if (s) return s;
+    s = sync_state(p);
     if (s) return s;
     if (rel) *rel = p->st_host->r;
     if (abs_norm) *abs_norm = p->st_host->r * p->st_host->n0;
@@ -1642,7 +1662,9 @@ usp_status usp_residual(usp_plan_t p, double *rel, double *abs_norm, int64_t *k)
 usp_status usp_residual_history(usp_plan_t p, double *host, int64_t cap, int64_t *n) {
     if (!p || !n) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
-    usp_status s = sync_state(p);
+    usp_status s = probe_xform(p);
+    if (s) return s;
+    s = sync_state(p);
     if (s) return s;
     const long long avail = std::min<long long>(p->st_host->k + 1, p->hist_cap);
     *n = avail;
