@@ -1839,6 +1839,14 @@ typedef std::complex<double> zd;
 // Gram-Schmidt over basis vectors U[0..nv) in blocks of 8: GS_DOT returns
 // d_j = (U_j, z) (+ ||z||^2 in *nrm); GS_AXPY applies z <- scale (z - sum c_j U_j)
 // and returns ||z||^2 of the result.  Partial rows summed on the host in CTA order.
+bool gm_always_cgs2() {   // USP_GMRES_CGS2=1: always two passes (the previous behaviour)
+    static const bool v = [] {
+        const char *e = std::getenv("USP_GMRES_CGS2");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 usp_status gs_dots(usp_plan_s *p, int nv, float2 *z, std::vector<zd> &d, double *nrm) {
     d.assign(nv, zd(0.0, 0.0));
     std::vector<double> h((size_t)p->gm_grid * 17);
@@ -1981,8 +1989,12 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
             if ((s = apply_M_dev(p, p->gm_U[j], p->gm_U[j + 1]))) return s;
             std::vector<zd> hcol(j + 2, zd(0.0, 0.0));
             double z2 = 0.0;
-            for (int round = 0; round < 2; ++round) {   // classical Gram-Schmidt, twice (CGS2)
-                if ((s = gs_dots(p, j + 1, p->gm_U[j + 1], d, nullptr))) return s;
+            // classical Gram-Schmidt with selective re-orthogonalisation (DGKS,
+            // eta = 1/sqrt(2)): a second pass only when the first cancelled
+            // more than half of ||w||^2 ("twice is enough")
+            for (int round = 0; round < 2; ++round) {
+                double w2 = 0.0;
+                if ((s = gs_dots(p, j + 1, p->gm_U[j + 1], d, round == 0 ? &w2 : nullptr))) return s;
                 std::vector<zd> c(j + 1);
                 for (int i = 0; i <= j; ++i) {
                     c[i] = d[i] / (nu[i] * nu[i]);
@@ -1990,6 +2002,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
                 }
                 std::vector<float2 *> Ub(p->gm_U.begin(), p->gm_U.begin() + j + 1);
                 if ((s = gs_axpy(p, j + 1, Ub, c, p->gm_U[j + 1], zd(1.0, 0.0), &z2))) return s;
+                if (round == 0 && z2 >= 0.5 * w2 && !gm_always_cgs2()) break;
             }
             nu[j + 1] = std::sqrt(z2);
             hcol[j + 1] = nu[j + 1] / nu[j];
