@@ -480,7 +480,9 @@ def run_usp(args, world, rank, local):
     it_bytes = iter_bpv * nloc
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
                    "slabs": f"{world} z-slabs, transposes: {transposes} (self-check first)",
-                   "virtual": f"1 GPU, {args.virtual_ranks} virtual z-slabs (device-copy transposes)"}[mode]
+                   "virtual": f"1 GPU, {args.virtual_ranks} virtual z-slabs ("
+                              + ("separate transposes" if os.environ.get("USP_FUSED") == "0" else
+                                 "transposes fused into the K_B / K_C stores") + ")"}[mode]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
