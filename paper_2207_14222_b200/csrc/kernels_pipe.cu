@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                     } else if (p.l2hint) {
                         mbar_arrive_expect_tx(&full[s], 4 * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
-                        bulk_g2s_hint(st + 1 * T::UE, p.delta + off, ub, &full[s], pol_first);
+                        bulk_g2s_hint(st + 1 * T::UE, slot1 + off, ub, &full[s], pol_first);
                         bulk_g2s_hint(st + 2 * T::UE, p.x + off, ub, &full[s], pol_first);
                         bulk_g2s_hint(st + 3 * T::UE, p.B + off, ub, &full[s], pol_first);
                     } else {
