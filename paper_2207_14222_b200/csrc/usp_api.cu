@@ -191,6 +191,7 @@ struct usp_plan_s {
     // x-form passes while r >= r_sw (reading R-30; USP_XFORM=0 disables,
     // USP_XSWITCH sets r_sw): s = S / c kept in its own field
     bool xform_cap = false, xform = false, probe_needed = false;
+    bool force_finish = false;   // USP_FORCE_FINISH=1 (test hook, see rank_finish)
     double r_sw = 1e-2;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -510,9 +511,14 @@ MulParams mul_params(const usp_plan_s *p) {
     return mp;
 }
 
+// The x pass's residual goes through the all-gather + k_finish path: with
+// P > 1 ranks, or (test hook USP_FORCE_FINISH=1) on a one-rank communicator,
+// so the rank-ordered finish is exercised on one GPU.
+bool rank_finish(const usp_plan_s *p) { return multi_rank(p) || (p->comm && p->force_finish); }
+
 Red red_params(usp_plan_s *p) {
     Red r{p->partials, p->hist, p->hist_cap, nullptr};
-    if (multi_rank(p)) r.local_sum = p->coll;
+    if (rank_finish(p)) r.local_sum = p->coll;
     return r;
 }
 
@@ -543,7 +549,7 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
         else if (p->pipe_xk) CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream));
         else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
     }
-    if (mode != X_SRC_FWD && multi_rank(p)) {
+    if (mode != X_SRC_FWD && rank_finish(p)) {
         {
             Tick t(p, KC_ALLGATHER, false);
             NC(nccl().AllGather(p->coll, p->coll + 8, 1, ncclDouble, p->comm, p->stream));
@@ -1192,6 +1198,8 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
                        !(xf && xf[0] == '0');
         const char *xs = std::getenv("USP_XSWITCH");
         if (xs) p->r_sw = std::atof(xs);
+        const char *ff = std::getenv("USP_FORCE_FINISH");
+        p->force_finish = ff && ff[0] == '1';
     }
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps

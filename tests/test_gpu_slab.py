@@ -161,6 +161,48 @@ def test_nccl_communicator_single_rank():
             dist.destroy_process_group()
 
 
+def test_rank_finish_path_with_xform_switch(monkeypatch):
+    """The rank-ordered finish (x pass total -> NCCL all-gather -> k_finish)
+    that P > 1 ranks use, forced on a one-rank communicator: the x-form
+    passes, the switch to the Delta-form, the pending stop and the probe of a
+    residual query give the single-GPU result bit for bit (reading R-30)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+    from paper_2207_14222_b200 import Plan, comm_init
+    from synth import make
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29733")
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        p = make("C3", (64, 64, 64))
+        med, src, _ = rounded_inputs(p)
+        x1, n1, t1, pl1 = _run(p, 2000, 0, tol=1e-6)
+        comm = comm_init()
+        monkeypatch.setenv("USP_FORCE_FINISH", "1")
+        plan = Plan(p.shape, comm=comm)
+        plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
+        plan.set_source(torch.from_numpy(src).cuda())
+        n, term = plan.iterate(7, p.alpha, 0.0)
+        r7 = plan.residual()                       # probe pass through k_finish
+        n2, term = plan.iterate(2000, p.alpha, 1e-6)
+        x = plan.get_field().cpu().numpy()
+        assert plan.launch_count() > 0 and term == t1 == "converged"
+        assert n + n2 == n1
+        assert np.array_equal(x, x1)
+        assert np.array_equal(plan.history(), pl1.history())
+        assert r7[2] == 7 and r7[0] == pl1.history()[7]
+        plan.close()
+        comm.close()
+    finally:
+        if own:
+            dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("G", [4, 16])
 def test_chunked_schedule_matches_four_pass(G, monkeypatch):
     """The experimental chunked schedule (USP_CHUNK=G: K_C, then K_D/K_A/K_B
