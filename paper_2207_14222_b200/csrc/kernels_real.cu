@@ -76,13 +76,23 @@ __global__ void __launch_bounds__(XReal<N>::NT, 1) k_xpass_real(XParams p) {
 
     bool xonly = false;
     float alpha = 0.f;
+    int act = ACT_DELTA;   // X_ITER: Delta-form, x-form, probe or x-form -> Delta-form (kcommon.cuh, R-30)
     if (MODE == X_ITER) {
         const int status = p.st->status;
         const long long k = p.st->k, kmax = p.st->kmax;
-        if (k >= kmax || (status != ST_RUNNING && status != ST_STOP_PENDING)) return;
+        const bool probe = p.st->form == FORM_PROBE && status == ST_RUNNING;
+        if (!probe && (k >= kmax || (status != ST_RUNNING && status != ST_STOP_PENDING))) return;
         xonly = (status == ST_STOP_PENDING);
         alpha = (float)p.st->alpha;
+        act = xform_act(p.st);
     }
+    const bool dform = act == ACT_DELTA;
+    const float c1 = dform ? alpha : 1.f;
+    const float e1 = (act == ACT_X || act == ACT_PROBE) ? 1.f : 0.f;
+    const bool store_x = act == ACT_DELTA || act == ACT_X, store_d = act != ACT_X;
+    const bool u_from_d = act == ACT_DELTA || act == ACT_TO_DELTA;
+    // stage slot D0: Delta (Delta-form) or s (x-form passes; source setup of x-form plans)
+    const float2 *slot_d = (MODE == X_ITER && act != ACT_DELTA) || (MODE == X_SRC_EPI && p.s) ? p.s : p.delta;
     double acc = 0.0;
     const long long nvox = p.nlines * (long long)N;
 
@@ -121,13 +131,14 @@ __global__ void __launch_bounds__(XReal<N>::NT, 1) k_xpass_real(XParams p) {
                         mbar_arrive_expect_tx(&full[s], fb);
                         bulk_g2s(st + T::D0, p.x + offf, fb, &full[s]);
                     } else if (MODE == X_SRC_EPI) {
-                        mbar_arrive_expect_tx(&full[s], wb + fb);
+                        mbar_arrive_expect_tx(&full[s], wb + (p.s ? 2 : 1) * fb);
                         bulk_g2s(st + T::W0, p.work + offw, wb, &full[s]);
+                        if (p.s) bulk_g2s(st + T::D0, slot_d + offf, fb, &full[s]);
                         bulk_g2s(st + T::B0, p.B + offf, fb, &full[s]);
                     } else {
                         mbar_arrive_expect_tx(&full[s], wb + 3 * fb);
                         bulk_g2s(st + T::W0, p.work + offw, wb, &full[s]);
-                        bulk_g2s(st + T::D0, p.delta + offf, fb, &full[s]);
+                        bulk_g2s(st + T::D0, slot_d + offf, fb, &full[s]);
                         bulk_g2s(st + T::X0, p.x + offf, fb, &full[s]);
                         bulk_g2s(st + T::B0, p.B + offf, fb, &full[s]);
                     }
@@ -155,7 +166,10 @@ __global__ void __launch_bounds__(XReal<N>::NT, 1) k_xpass_real(XParams p) {
                 float2 v[G::N2];
                 if (MODE == X_SRC_FWD) {
 #pragma unroll
-                    for (int m = 0; m < G::N2; ++m) v[m] = cscale(st[T::D0 + fbase + G::N1 * m], cr);   // s = S/c
+                    for (int m = 0; m < G::N2; ++m) {
+                        v[m] = cscale(st[T::D0 + fbase + G::N1 * m], cr);   // s = S/c
+                        if (p.s) p.s[gf + G::N1 * m] = v[m];                // x-form plans keep s
+                    }
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
@@ -185,15 +199,28 @@ __global__ void __launch_bounds__(XReal<N>::NT, 1) k_xpass_real(XParams p) {
                             if (MODE == X_SRC_EPI) {
                                 dn = make_float2(b.x * y.x, b.y * y.y);          // Delta_0 = B (L+1)^-1 s
                                 p.x[gi] = make_float2(0.f, 0.f);                 // x_0 = 0 (L83)
-                            } else {
-                                const float2 d = st[T::D0 + e], xx = st[T::X0 + e];
-                                // Delta_{k+1} = Delta_k + alpha B (y - Delta_k); x_{k+1} = x_k + alpha Delta_k
-                                dn = make_float2(fmaf(alpha * b.x, y.x - d.x, d.x), fmaf(alpha * b.y, y.y - d.y, d.y));
-                                p.x[gi] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                                p.delta[gi] = dn;
+                                lacc = fmaf(dn.x, dn.x, fmaf(dn.y, dn.y, lacc));
+                                // u = B Delta (x-form plans: u_0 = s)
+                                v[m] = p.s ? st[T::D0 + e] : make_float2(b.x * dn.x, b.y * dn.y);
+                                continue;
                             }
-                            p.delta[gi] = dn;
+                            // every action in one body (see kernels_pipe.cu; real, elementwise):
+                            // Delta-form  dn = d + alpha B (y - d), x += alpha d, u = B dn
+                            // x-form      dn = B (y - x), x += alpha dn, u = B x + s
+                            // probe       dn = B (y - x) stored, u = B x + s;  to-Delta: u = B dn
+                            const float2 a1 = st[T::D0 + e], xx = st[T::X0 + e];
+                            const float2 z = dform ? a1 : xx;
+                            const float2 t = make_float2(b.x * (y.x - z.x), b.y * (y.y - z.y));
+                            const float2 d0 = dform ? a1 : make_float2(0.f, 0.f);
+                            dn = make_float2(fmaf(c1, t.x, d0.x), fmaf(c1, t.y, d0.y));
+                            const float2 xi = dform ? a1 : t;
+                            const float2 xn = make_float2(fmaf(alpha, xi.x, xx.x), fmaf(alpha, xi.y, xx.y));
+                            if (store_x) p.x[gi] = xn;
+                            if (store_d) p.delta[gi] = dn;
                             lacc = fmaf(dn.x, dn.x, fmaf(dn.y, dn.y, lacc));
-                            v[m] = make_float2(b.x * dn.x, b.y * dn.y);           // u = B Delta
+                            const float2 w = u_from_d ? dn : (act == ACT_X ? xn : xx);
+                            v[m] = make_float2(fmaf(e1, a1.x, b.x * w.x), fmaf(e1, a1.y, b.y * w.y));
                         }
                         acc += (double)lacc;
                         fence_proxy_async_smem();
@@ -232,7 +259,7 @@ __global__ void __launch_bounds__(XReal<N>::NT, 1) k_xpass_real(XParams p) {
         *p.red.local_sum = total;
         return;
     }
-    finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red);
+    finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red, act);
 }
 
 // ========================================================= launchers ====

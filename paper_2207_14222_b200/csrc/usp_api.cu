@@ -1194,7 +1194,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         const char *s2 = std::getenv("USP_SOLVE2D");
         p->solve2d = !p->anti && !p->tdiff && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
         const char *xf = std::getenv("USP_XFORM");
-        p->xform_cap = !p->real && !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && p->pipe_xk &&
+        p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && (p->pipe_xk || p->real) &&
                        !(xf && xf[0] == '0');
         const char *xs = std::getenv("USP_XSWITCH");
         if (xs) p->r_sw = std::atof(xs);

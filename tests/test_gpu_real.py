@@ -50,9 +50,9 @@ def test_real_path_matches_oracle(orc, shape, n):
     p = make("C4", shape)
     x, nd, term, plan = _run(p, n)
     assert nd == n and term == "max_iter" and x.dtype == np.float32
-    # the real path's workspace: 3 float32 fields + the half spectrum
+    # the real path's workspace: 3 float32 fields (+ s for the x-form, R-30) + the half spectrum
     nz, ny, nx = shape
-    assert _ws_bytes(plan) < 3 * 4 * nz * ny * nx + 8 * nz * ny * (nx // 2 + 16) + 4096
+    assert _ws_bytes(plan) < 4 * 4 * nz * ny * nx + 8 * nz * ny * (nx // 2 + 16) + 4096
     res, _ = run_oracle(orc, p, n_iter=n)
     assert np.abs(res.x.imag).max() <= 1e-12 * np.abs(res.x).max()
     err = rel_l2(x.astype(np.complex128), res.x)
@@ -64,9 +64,9 @@ def test_real_path_equals_complex_path(monkeypatch):
     from synth import make
 
     p = make("C4", (64, 128, 64))
+    monkeypatch.setenv("USP_XFORM", "0")   # the same (Delta-form) arithmetic on both paths
     xr, _, _, pr = _run(p, 50)
     monkeypatch.setenv("USP_REAL", "0")
-    monkeypatch.setenv("USP_XFORM", "0")   # the same (Delta-form) arithmetic on both paths
     xc, _, _, pc = _run(p, 50)
     assert _ws_bytes(pr) < 0.7 * _ws_bytes(pc)
     assert rel_l2(xr.astype(np.float64), xc.astype(np.float64)) <= 2e-6

@@ -111,3 +111,21 @@ def test_xform_sweep_bytes_lower(monkeypatch):
     pd = _plan(p, monkeypatch, False)
     fx, fd = px.workspace.numel(), pd.workspace.numel()
     assert fx == fd + 8 * 32 * 32 * 32 or fx == fd + 256 * ((8 * 32 ** 3 + 255) // 256)
+
+
+@pytest.mark.parametrize("shape,n", [((64, 64, 64), 30), ((32, 64, 128), 20)])
+def test_xform_real_path_equals_delta_form(monkeypatch, shape, n):
+    """The real (half-spectrum) path's x-form against its Delta-form."""
+    from synth import make
+
+    p = make("C4", shape)
+    px = _plan(p, monkeypatch, True)
+    pd = _plan(p, monkeypatch, False)
+    assert px.iteration_form()[0] and not pd.iteration_form()[0]
+    xx, _, _, _ = run_gpu(p, n_iter=n, tol=0.0, plan=px)
+    xd, _, _, _ = run_gpu(p, n_iter=n, tol=0.0, plan=pd)
+    assert rel_l2(xx, xd) <= 1e-5
+    assert np.allclose(px.history(), pd.history(), rtol=1e-3, atol=0.0)
+    xt, nt, tt, _ = run_gpu(p, n_iter=2000, tol=1e-6, plan=px)
+    xu, nu, tu, _ = run_gpu(p, n_iter=2000, tol=1e-6, plan=pd)
+    assert tt == tu == "converged" and abs(nt - nu) <= TOL_COUNT and rel_l2(xt, xu) <= 1e-4
