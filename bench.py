@@ -55,6 +55,8 @@ ITER_BYTES_3D = 104         # 56 + 3 * 16 (SURVEY.md §8 geometry table)
 # same bytes: writes Delta instead of x)
 XFORM_XPASS_BYTES = 48
 ITER_BYTES_3D_XFORM = 96
+XFORM_XPASS_BYTES_REAL = 24     # real path: Delta (4 B) neither read nor written, s (4 B) read
+ITER_BYTES_REAL_XFORM = 48
 # Chunked schedule (1 GPU, 3-D): per z-chunk K_D -> K_A -> K_B
 # with the chunk's work array L2-resident in between, so HBM sees only
 KERNEL_BYTES_CHUNKED = {
@@ -419,14 +421,24 @@ def run_usp(args, world, rank, local):
     # on x-form plans) and ends still in the x-form unless r fell below r_switch
     xform_plan, xform_now, r_switch = plan.iteration_form()
     xform_all = xform_plan and xform_now
+    n_x = 0                                         # x-form iterations per step
     if xform_all:
-        kbytes["xpass"] = XFORM_XPASS_BYTES
+        n_x = n_iter
+    elif xform_plan:
+        # iteration k runs the x-form while r_{k-1} >= r_switch (R-30)
+        h = plan.history()
+        below = [k for k, r in enumerate(h[:n_iter]) if r < r_switch]
+        n_x = min(n_iter, below[0] + 1) if below else n_iter
+    fx = n_x / n_iter
+    xb = XFORM_XPASS_BYTES_REAL if real else XFORM_XPASS_BYTES
+    kbytes["xpass"] = fx * xb + (1 - fx) * kbytes["xpass"]
     form_desc = ("x-form (Algorithm 1 literally) throughout" if xform_all else
-                 ("x-form, then Delta-form below r_switch" if xform_plan else "Delta-form"))
+                 (f"x-form for {n_x} of {n_iter} iterations, then Delta-form below r_switch = {r_switch:g}"
+                  if xform_plan else "Delta-form"))
     dname = "xpass" if "xpass" in prof else max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
     dms, dcount = prof[dname]
     d_ms_per_iter = dms / n_it_total
-    dbytes = kbytes[dname] * nloc                   # per iteration (= per launch x chunks)
+    dbytes = int(kbytes[dname] * nloc)              # per iteration (= per launch x chunks)
     # algorithmic bytes of the iterations over the kernel's total time (x-form
     # plans add one launch per iterate call that skips itself: time only)
     achieved = dbytes / (d_ms_per_iter / 1e3) / 1e9
@@ -474,8 +486,9 @@ def run_usp(args, world, rank, local):
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
     # separate transposes (NCCL all-to-all / device copies) add their staging
     # reads and writes; the fused (peer-store) transposes add nothing to HBM
-    iter_bpv = (ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else
-                                              (ITER_BYTES_3D_XFORM if xform_all else ITER_BYTES_3D))) + \
+    base_bpv = ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D)
+    xform_bpv = ITER_BYTES_REAL_XFORM if real else ITER_BYTES_3D_XFORM
+    iter_bpv = fx * xform_bpv + (1 - fx) * base_bpv + \
         ((16 if real else 32) if "all_to_all" in prof else 0)
     it_bytes = iter_bpv * nloc
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
