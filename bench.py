@@ -57,6 +57,10 @@ XFORM_XPASS_BYTES = 48
 ITER_BYTES_3D_XFORM = 96
 XFORM_XPASS_BYTES_REAL = 24     # real path: Delta (4 B) neither read nor written, s (4 B) read
 ITER_BYTES_REAL_XFORM = 48
+# sparse source (reading R-31: the source on <= 64 x-lines): the x-form pass
+# does not read s at all -- reads work, x, B, writes x, work
+XFORM_XPASS_BYTES_SPARSE = 40
+ITER_BYTES_3D_XFORM_SPARSE = 88
 # Chunked schedule (1 GPU, 3-D): per z-chunk K_D -> K_A -> K_B
 # with the chunk's work array L2-resident in between, so HBM sees only
 KERNEL_BYTES_CHUNKED = {
@@ -430,9 +434,11 @@ def run_usp(args, world, rank, local):
         below = [k for k, r in enumerate(h[:n_iter]) if r < r_switch]
         n_x = min(n_iter, below[0] + 1) if below else n_iter
     fx = n_x / n_iter
-    xb = XFORM_XPASS_BYTES_REAL if real else XFORM_XPASS_BYTES
+    sparse_lines = plan.source_lines()
+    xb = XFORM_XPASS_BYTES_REAL if real else (XFORM_XPASS_BYTES_SPARSE if sparse_lines else XFORM_XPASS_BYTES)
     kbytes["xpass"] = fx * xb + (1 - fx) * kbytes["xpass"]
-    form_desc = ("x-form (Algorithm 1 literally) throughout" if xform_all else
+    form_desc = ("x-form (Algorithm 1 literally) throughout" +
+                 (f", source on {sparse_lines} x-line(s) (s not streamed)" if sparse_lines else "") if xform_all else
                  (f"x-form for {n_x} of {n_iter} iterations, then Delta-form below r_switch = {r_switch:g}"
                   if xform_plan else "Delta-form"))
     dname = "xpass" if "xpass" in prof else max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
@@ -487,7 +493,7 @@ def run_usp(args, world, rank, local):
     # separate transposes (NCCL all-to-all / device copies) add their staging
     # reads and writes; the fused (peer-store) transposes add nothing to HBM
     base_bpv = ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D)
-    xform_bpv = ITER_BYTES_REAL_XFORM if real else ITER_BYTES_3D_XFORM
+    xform_bpv = ITER_BYTES_REAL_XFORM if real else (ITER_BYTES_3D_XFORM_SPARSE if sparse_lines else ITER_BYTES_3D_XFORM)
     iter_bpv = fx * xform_bpv + (1 - fx) * base_bpv + \
         ((16 if real else 32) if "all_to_all" in prof else 0)
     it_bytes = iter_bpv * nloc

@@ -271,11 +271,14 @@ usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
  * residual is >= r_switch (default 1e-2, env USP_XSWITCH; USP_XFORM=0 at
  * plan creation disables), then the Delta-form recurrence (exact
  * down to fp32 rounding near convergence).  form: 0 = Delta-form now,
- * 1 = x-form now.  After x-form iterations, r_k and Delta_k of the current
+ * 1 = x-form now.  source_lines > 0: the source lives on that many x-lines
+ * (<= 64) and the x-form passes never read s (reading R-31: the x-transformed
+ * source lines are added after each x pass); 0: s is read densely.  After
+ * x-form iterations, r_k and Delta_k of the current
  * x_k are computed on demand by usp_residual / usp_residual_history (one
  * probe pass: x unchanged); those two calls are therefore collective over
  * the ranks of a slab-decomposed plan.  Errors: USP_ERR_ARG. */
-usp_status usp_iteration_form(usp_plan_t plan, int *xform, int *form, double *r_switch);
+usp_status usp_iteration_form(usp_plan_t plan, int *xform, int *form, double *r_switch, int *source_lines);
 
 /* NCCL communicator for the slab decomposition (one process per GPU).
  * Rank 0 calls usp_comm_unique_id and broadcasts the 128 bytes (e.g. with

@@ -141,6 +141,7 @@ __device__ __forceinline__ void finish_xpass(bool src_epi, bool xonly, double to
     if (act == ACT_DELTA) hi = k + 1;
     if (act == ACT_TO_DELTA) st->form = FORM_DELTA;
     if (act == ACT_PROBE) st->form = FORM_X;
+    st->add_s = (act == ACT_X || act == ACT_PROBE) ? 1 : 0;   // sparse source: k_sadd adds s
     red.hist[hi % red.hist_cap] = r;
 #ifdef USP_DIAG_NODIV   // diagnostics builds only: keep iterating through overflow (timing ablations)
     if (false) st->status = ST_DIVERGED;

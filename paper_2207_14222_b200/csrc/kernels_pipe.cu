@@ -82,8 +82,12 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
     const float e1 = (act == ACT_X || act == ACT_PROBE) ? 1.f : 0.f;   // u = B w + e1 s
     const bool store_x = act == ACT_DELTA || act == ACT_X, store_d = act != ACT_X;
     const bool u_from_d = act == ACT_DELTA || act == ACT_TO_DELTA;
-    // stage slot 1: Delta (Delta-form) or s (x-form passes; source setup of x-form plans)
+    // stage slot 1: Delta (Delta-form) or s (x-form passes; source setup of x-form plans).
+    // Sparse source (R-31): the x-form passes form u = B x without s (k_sadd
+    // adds the transformed source lines), so slot 1 is not loaded at all.
     const float2 *slot1 = (MODE == X_ITER && act != ACT_DELTA) || (MODE == X_SRC_EPI && p.s) ? p.s : p.delta;
+    const bool need1 = !(MODE == X_ITER && p.s_sparse && act != ACT_DELTA);
+    const float e1s = need1 ? e1 : 0.f;
     double acc = 0.0;
     const long long nvox = p.nlines * (long long)N;
 
@@ -137,9 +141,9 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                         bulk_g2s_hint(st + 2 * T::UE, p.x + off, ub, &full[s], pol_first);
                         bulk_g2s_hint(st + 3 * T::UE, p.B + off, ub, &full[s], pol_first);
                     } else {
-                        mbar_arrive_expect_tx(&full[s], 4 * ub);
+                        mbar_arrive_expect_tx(&full[s], (need1 ? 4 : 3) * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
-                        bulk_g2s(st + 1 * T::UE, slot1 + off, ub, &full[s]);
+                        if (need1) bulk_g2s(st + 1 * T::UE, slot1 + off, ub, &full[s]);
                         bulk_g2s(st + 2 * T::UE, p.x + off, ub, &full[s]);
                         bulk_g2s(st + 3 * T::UE, p.B + off, ub, &full[s]);
                     }
@@ -170,6 +174,14 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                                                      : st[e];
                         v[m] = cmul(sv, p.inv_c);               // s = S / c
                         if (p.s) p.s[gb + G::N1 * m] = v[m];   // x-form plans keep s
+                    }
+                    if (p.s_flag) {   // does this x-line carry any source? (R-31)
+                        bool nz = false;
+#pragma unroll
+                        for (int m = 0; m < G::N2; ++m) nz |= (v[m].x != 0.f) || (v[m].y != 0.f);
+                        const unsigned bal = __ballot_sync(0xffffffffu, nz);
+                        const unsigned lmask = (G::N1 >= 32) ? 0xffffffffu : (((1u << G::N1) - 1u) << (lq * G::N1));
+                        if (j == 0) p.s_flag[(blockIdx.x + (long long)i * gridDim.x) * T::U + lq] = (bal & lmask) != 0u;
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -208,7 +220,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                             //                        x_{k+1} = x_k + alpha Delta_k, u = B x_{k+1} + s
                             //   probe: Delta_k = B (y - x_k) stored, x kept, u = B x_k + s
                             //   x-form -> Delta-form: Delta_k stored, x kept, u = B Delta_k
-                            const float2 a1 = st[1 * T::UE + e];    // Delta_k or s
+                            const float2 a1 = need1 ? st[1 * T::UE + e] : make_float2(0.f, 0.f);   // Delta_k or s
                             const float2 xx = st[2 * T::UE + e];
                             const float2 t = cmul(b, csub(y, dform ? a1 : xx));
                             const float2 d0 = dform ? a1 : make_float2(0.f, 0.f);
@@ -220,7 +232,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                             lacc += cabs2(dn);
                             const float2 w = u_from_d ? dn : (act == ACT_X ? xn : xx);
                             const float2 bw = cmul(b, w);
-                            v[m] = make_float2(fmaf(e1, a1.x, bw.x), fmaf(e1, a1.y, bw.y));
+                            v[m] = make_float2(fmaf(e1s, a1.x, bw.x), fmaf(e1s, a1.y, bw.y));
                         }
                         acc += (double)lacc;
                         fence_proxy_async_smem();
@@ -251,6 +263,75 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
         return;
     }
     finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red, act);
+}
+
+// ================================================ sparse source (R-31) ==
+// Source lines: count the flagged x-lines, gather their x-transformed source
+// (work after the x-form setup holds FFT_x(s)) into a compact buffer, and
+// after each x-form pass add them to the forward x-transform of B x
+// (FFT_x(B x + s) = FFT_x(B x) + FFT_x(s): the x pass then never reads s).
+__global__ void k_sparse_count(const unsigned char *flag, long long nlines, unsigned *count) {
+    unsigned c = 0;
+    for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < nlines;
+         l += (long long)gridDim.x * blockDim.x)
+        c += flag[l] ? 1u : 0u;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+__global__ void k_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, int n, int *list,
+                                float2 *comp, unsigned *count) {
+    for (long long l = blockIdx.x; l < nlines; l += gridDim.x) {
+        if (!flag[l]) continue;   // uniform per CTA
+        __shared__ unsigned idx;
+        if (threadIdx.x == 0) {
+            idx = atomicAdd(count, 1u);
+            list[idx] = (int)l;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) comp[(long long)idx * n + i] = work[l * n + i];
+        __syncthreads();
+    }
+}
+
+__global__ void k_sparse_add(SAddParams p) {
+    pdl_wait();
+    if (!p.st->add_s) return;
+    for (int q = blockIdx.x; q < p.count; q += gridDim.x) {
+        float2 *w = p.work + (long long)p.list[q] * p.n;
+        const float2 *c = p.comp + (long long)q * p.n;
+        for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
+            const float2 a = w[i], b = c[i];
+            w[i] = make_float2(a.x + b.x, a.y + b.y);
+        }
+    }
+}
+
+__global__ void k_sparse_clear(IterState *st) { st->add_s = 0; }
+
+cudaError_t launch_sparse_count(const unsigned char *flag, long long nlines, unsigned *count, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    k_sparse_count<<<296, 256, 0, s>>>(flag, nlines, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, int n, int *list,
+                                 float2 *comp, unsigned *count, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    k_sparse_gather<<<592, 256, 0, s>>>(flag, nlines, work, n, list, comp, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s) {
+    const int grid = p.count < 148 ? p.count : 148;
+    if (grid > 0) {
+        cudaError_t e = launch_pdl(k_sparse_add, grid, 256, 0, s, p);
+        if (e != cudaSuccess) return e;
+    }
+    k_sparse_clear<<<1, 1, 0, s>>>(p.st);
+    return cudaGetLastError();
 }
 
 // ========================================================= launchers ====

@@ -127,11 +127,11 @@ Nccl &nccl() {
 
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
               KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_BARRIER, KC_XOP,
-              KC_KUPD, KC_SOLVE2D, KC_N };
+              KC_KUPD, KC_SOLVE2D, KC_SADD, KC_N };
 const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
                               "solve1d", "potential", "farthest", "set_state", "xpass_setup",
                               "all_to_all", "finish", "allgather", "rank_barrier", "krylov_xop",
-                              "krylov_update", "solve2d"};
+                              "krylov_update", "solve2d", "sparse_source_add"};
 
 struct Timed {
     int cls;
@@ -192,6 +192,12 @@ struct usp_plan_s {
     // USP_XSWITCH sets r_sw): s = S / c kept in its own field
     bool xform_cap = false, xform = false, probe_needed = false;
     bool force_finish = false;   // USP_FORCE_FINISH=1 (test hook, see rank_finish)
+    // sparse source (R-31; USP_SPARSE_S=0 disables): <= kSparseMaxLines x-lines carry
+    // the source; their x-transforms live in the s field (list, then lines)
+    unsigned char *s_flag = nullptr;
+    unsigned *s_ctr = nullptr;
+    bool s_sparse = false;
+    int s_count = 0;
     double r_sw = 1e-2;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -537,6 +543,7 @@ XParams x_params(usp_plan_s *p) {
     xp.st = p->st;
     xp.red = red_params(p);
     xp.s = p->xform ? p->s : nullptr;
+    xp.s_sparse = p->s_sparse ? 1 : 0;
     return xp;
 }
 
@@ -557,6 +564,24 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
         Tick t(p, KC_FINISH);
         CU(launch_finish(p->st, p->coll + 8, p->P, mode == X_SRC_EPI, red_params(p), p->stream));
     }
+    return USP_OK;
+}
+
+constexpr int kSparseMaxLines = 64;
+
+// sparse source: after an x pass of the iteration, add the x-transformed
+// source lines if that pass formed u = B x (k_sparse_add checks st->add_s)
+usp_status sparse_add(usp_plan_s *p) {
+    if (!p->s_sparse) return USP_OK;
+    SAddParams sa{};
+    sa.work = p->work;
+    sa.list = reinterpret_cast<const int *>(p->s);
+    sa.comp = p->s + 256;   // list: kSparseMaxLines ints in the first 2 KiB
+    sa.count = p->s_count;
+    sa.n = (int)p->nx;
+    sa.st = p->st;
+    Tick t(p, KC_SADD);
+    CU(launch_sparse_add(sa, p->stream));
     return USP_OK;
 }
 
@@ -1522,14 +1547,40 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         if ((s = chain_anti(p, 0))) return s;
         if ((s = run_anti_x(p, X_SRC_EPI))) return s;
     } else {
+        p->s_sparse = false;
         XParams xp = x_params(p);
+        const char *sps = std::getenv("USP_SPARSE_S");
+        const bool try_sparse = p->xform && !p->real && !(sps && sps[0] == '0');
+        if (try_sparse) {
+            if (!p->s_flag) CU(cudaMalloc(&p->s_flag, (size_t)p->ny * p->nzh));
+            if (!p->s_ctr) CU(cudaMalloc(&p->s_ctr, sizeof(unsigned)));
+            xp.s_flag = p->s_flag;
+        }
         s = run_xpass(p, X_SRC_FWD, xp);
         if (s) return s;
+        xp.s_flag = nullptr;
         s = chain_mid(p, 0);
         if (s) return s;
         s = run_xpass(p, X_SRC_EPI, xp);
         if (s) return s;
         if (p->chunked && (s = chunk_kb_all(p))) return s;   // establish the chunked invariant
+        if (try_sparse) {
+            // reading R-31: few source lines -> keep FFT_x(s) of those lines only
+            // (work holds FFT_x(u_0) = FFT_x(s) after the x-form setup)
+            const long long nlines = p->ny * p->nzh;
+            unsigned cnt = 0;
+            CU(launch_sparse_count(p->s_flag, nlines, p->s_ctr, p->stream));
+            CU(cudaMemcpyAsync(&cnt, p->s_ctr, sizeof cnt, cudaMemcpyDeviceToHost, p->stream));
+            CU(cudaStreamSynchronize(p->stream));
+            // the list (2 KiB) and the lines must fit in the s field
+            const long long cap = std::min<long long>(kSparseMaxLines, ((long long)p->nloc - 256) / p->nx);
+            if (cnt > 0 && (long long)cnt <= cap) {
+                CU(launch_sparse_gather(p->s_flag, nlines, p->work, (int)p->nx, reinterpret_cast<int *>(p->s),
+                                        p->s + 256, p->s_ctr, p->stream));
+                p->s_sparse = true;
+                p->s_count = (int)cnt;
+            }
+        }
     }
     s = sync_state(p);
     if (s) return s;
@@ -1551,7 +1602,8 @@ usp_status probe_xform(usp_plan_s *p) {
         CU(launch_set_form(p->st, FORM_PROBE, p->stream));
     }
     if ((s = chain_mid(p, 1))) return s;
-    return run_xpass(p, X_ITER, x_params(p));
+    if ((s = run_xpass(p, X_ITER, x_params(p)))) return s;
+    return sparse_add(p);
 }
 }  // namespace
 
@@ -1628,6 +1680,7 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
                 if (s) return s;
                 s = run_xpass(p, X_ITER, xp);
                 if (s) return s;
+                if ((s = sparse_add(p))) return s;
             }
             launched += nb;
             if (tol > 0.0) {
@@ -2100,10 +2153,11 @@ usp_status usp_launch_count(usp_plan_t p, int64_t *launches) {
     return USP_OK;
 }
 
-usp_status usp_iteration_form(usp_plan_t p, int *xform, int *form, double *r_switch) {
+usp_status usp_iteration_form(usp_plan_t p, int *xform, int *form, double *r_switch, int *source_lines) {
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     usp_status s = sync_state(p);
     if (s) return s;
+    if (source_lines) *source_lines = p->s_sparse ? p->s_count : 0;
     if (xform) *xform = (p->xform_cap && !p->chunked) ? 1 : 0;
     if (form) *form = (p->st_host->form == FORM_DELTA) ? 0 : 1;
     if (r_switch) *r_switch = p->r_sw;
@@ -2120,6 +2174,8 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->partials);
     cudaFree(p->hist);
     cudaFree(p->red_u);
+    if (p->s_flag) cudaFree(p->s_flag);
+    if (p->s_ctr) cudaFree(p->s_ctr);
     cudaFree(p->far_d);
     cudaFree(p->far_i);
     cudaFree(p->coll);

@@ -38,6 +38,7 @@ struct IterState {
     int form;
     int xform;             // the plan runs the x-form while r >= r_sw (set at set_source)
     double r_sw;
+    int add_s;             // sparse source: the last x pass formed u = B x (+ s still to add)
 };
 
 enum : int { FORM_DELTA = 0, FORM_X = 1, FORM_PROBE = 2 };
@@ -82,6 +83,20 @@ struct XParams {
     Red red;
     int l2hint;          // chunked schedule: stream Delta/x/B evict_first, keep work evict_last
     float2 *s;           // x-form plans: s = S / c (else nullptr)
+    // sparse source (R-31): the x pass forms u = B x and k_sadd adds the
+    // x-transformed source lines afterwards; X_SRC_FWD flags the source lines
+    unsigned char *s_flag;   // per x-line: s != 0 (written by X_SRC_FWD when non-null)
+    int s_sparse;            // X_ITER: do not read s (its x-transform is added by k_sadd)
+};
+
+// sparse source lines (R-31): line l = list[i] of the local grid gets comp[i*N .. +N) added
+struct SAddParams {
+    float2 *work;
+    const float2 *comp;
+    const int *list;
+    int count;
+    int n;               // line length (row pitch of work)
+    IterState *st;
 };
 
 // ------------------------------------------------------- BiCGSTAB (NEXT-2) --
@@ -281,6 +296,10 @@ cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s);
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
 cudaError_t launch_set_form(IterState *st, int form, cudaStream_t s);
+cudaError_t launch_sparse_count(const unsigned char *flag, long long nlines, unsigned *count, cudaStream_t s);
+cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, int n, int *list,
+                                 float2 *comp, unsigned *count, cudaStream_t s);
+cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s);
 
 // TMA-pipelined variants (kernels_pipe.cu)
 cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);

@@ -237,9 +237,18 @@ class Plan:
 
     def iteration_form(self):
         """(x-form plan?, currently in the x-form?, r_switch) -- usp_iteration_form."""
-        xf, fm, rs = ctypes.c_int(), ctypes.c_int(), ctypes.c_double()
-        L.check(self.lib.usp_iteration_form(self.handle, ctypes.byref(xf), ctypes.byref(fm), ctypes.byref(rs)))
+        xf, fm, rs, sl = ctypes.c_int(), ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
+        L.check(self.lib.usp_iteration_form(self.handle, ctypes.byref(xf), ctypes.byref(fm), ctypes.byref(rs),
+                                            ctypes.byref(sl)))
         return bool(xf.value), bool(fm.value), float(rs.value)
+
+    def source_lines(self) -> int:
+        """Number of x-lines carrying the source when the x-form skips the
+        dense s field (reading R-31), else 0."""
+        xf, fm, rs, sl = ctypes.c_int(), ctypes.c_int(), ctypes.c_double(), ctypes.c_int()
+        L.check(self.lib.usp_iteration_form(self.handle, ctypes.byref(xf), ctypes.byref(fm), ctypes.byref(rs),
+                                            ctypes.byref(sl)))
+        return int(sl.value)
 
     def close(self):
         if getattr(self, "handle", None):

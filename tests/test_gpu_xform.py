@@ -129,3 +129,35 @@ def test_xform_real_path_equals_delta_form(monkeypatch, shape, n):
     xt, nt, tt, _ = run_gpu(p, n_iter=2000, tol=1e-6, plan=px)
     xu, nu, tu, _ = run_gpu(p, n_iter=2000, tol=1e-6, plan=pd)
     assert tt == tu == "converged" and abs(nt - nu) <= TOL_COUNT and rel_l2(xt, xu) <= 1e-4
+
+
+def test_sparse_source_xform(monkeypatch):
+    """Reading R-31: a point source lives on one x-line; the x-form passes then
+    never read s (its x-transform is added after each x pass).  Same iterate
+    as the dense-s x-form and the Delta-form; a dense source keeps dense s."""
+    from synth import make
+
+    p = make("C5", (32, 32, 64))
+    pa = _plan(p, monkeypatch, True)
+    xa, na, _, _ = run_gpu(p, n_iter=30, tol=0.0, plan=pa)
+    assert pa.source_lines() == 1
+    monkeypatch.setenv("USP_SPARSE_S", "0")
+    pb = _plan(p, monkeypatch, True)
+    xb, nb, _, _ = run_gpu(p, n_iter=30, tol=0.0, plan=pb)
+    assert pb.source_lines() == 0
+    pd = _plan(p, monkeypatch, False)
+    xd, _, _, _ = run_gpu(p, n_iter=30, tol=0.0, plan=pd)
+    assert rel_l2(xa, xb) <= 1e-6 and rel_l2(xa, xd) <= 1e-5
+    assert np.allclose(pa.history(), pd.history(), rtol=1e-4, atol=0.0)
+    # to tolerance (x-form with the added source lines, switch, Delta-form)
+    xt, nt, tt, _ = run_gpu(p, n_iter=3000, tol=1e-6, plan=pa)
+    xu, nu, tu, _ = run_gpu(p, n_iter=3000, tol=1e-6, plan=pd)
+    assert tt == tu == "converged" and abs(nt - nu) <= TOL_COUNT and rel_l2(xt, xu) <= 1e-4
+    # a source on many lines stays dense
+    monkeypatch.delenv("USP_SPARSE_S")
+    rng = np.random.default_rng(5)
+    med, src, _ = rounded_inputs(p)
+    src = (rng.standard_normal(src.shape) + 1j * rng.standard_normal(src.shape)).astype(np.complex64)
+    pc = _plan(p, monkeypatch, True)
+    run_gpu(p, n_iter=3, tol=0.0, plan=pc, med=med, src=src, dtype="c64")
+    assert pc.source_lines() == 0
