@@ -29,15 +29,21 @@ namespace usp {
 constexpr int kSmemBudget = 232448 - 2048;   // max dynamic smem per CTA on sm_100 minus slack
 
 // ============================================================ x pass ====
-template <int N>
+// LEAN (reading R-31): the x-form passes of a sparse-source plan need only
+// work, x, B -> 3-slot stages, and the smem saved buys a sixth consumer warp.
+// (A Delta-form pass landing on a LEAN launch reads Delta from global memory.)
+template <int N, bool LEAN = false>
 struct XPipe {
     using G = LineGeo<N>;
     static constexpr int U = 32 / G::N1;                    // lines per warp unit
     static constexpr int UE = 32 * G::N2;                   // elements per unit (= U * N)
-    static constexpr int XC = (N >= 2048) ? 2 : 5;          // consumer warps
+    static constexpr int XC = (N >= 2048) ? 2 : (LEAN ? 6 : 5);   // consumer warps
     static constexpr int NT = 32 * (XC + 1);
     static constexpr int XBUF = U * LayRow<N>::kFloat2PerLine;   // float2 per consumer warp
-    static constexpr int STAGE = 4 * UE;                    // float2 per stage (4 slots)
+    static constexpr int NSLOT = LEAN ? 3 : 4;
+    static constexpr int STAGE = NSLOT * UE;                // float2 per stage
+    // slot offsets (float2): work, Delta-or-s (not LEAN), x, B
+    static constexpr int SD = UE, SX = (LEAN ? 1 : 2) * UE, SB = (LEAN ? 2 : 3) * UE;
     // Bulk copies complete out of order, so a stage may only be reused by the
     // warp that consumed it: S = XC * SPW and unit i -> stage i % S, warp
     // i % XC.  A consumer at unit i has itself finished unit i - S, so the
@@ -49,10 +55,10 @@ struct XPipe {
     static constexpr int SMEM = (S * STAGE + XC * XBUF + N) * 8 + 2 * S * 8;   // stages, exchange, twiddles, barriers
 };
 
-template <int N, int MODE>
-__global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
+template <int N, int MODE, bool LEAN>
+__global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p) {
     using G = LineGeo<N>;
-    using T = XPipe<N>;
+    using T = XPipe<N, LEAN>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float2 *stages = reinterpret_cast<float2 *>(smem_raw);
     float2 *xbufs = stages + T::S * T::STAGE;
@@ -87,6 +93,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
     // adds the transformed source lines), so slot 1 is not loaded at all.
     const float2 *slot1 = (MODE == X_ITER && act != ACT_DELTA) || (MODE == X_SRC_EPI && p.s) ? p.s : p.delta;
     const bool need1 = !(MODE == X_ITER && p.s_sparse && act != ACT_DELTA);
+    const bool stage1 = need1 && !LEAN;   // slot 1 streamed through the stage
     const float e1s = need1 ? e1 : 0.f;
     double acc = 0.0;
     const long long nvox = p.nlines * (long long)N;
@@ -132,20 +139,20 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                     } else if (MODE == X_SRC_EPI) {
                         mbar_arrive_expect_tx(&full[s], (p.s ? 3 : 2) * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
-                        if (p.s) bulk_g2s(st + 1 * T::UE, slot1 + off, ub, &full[s]);
-                        bulk_g2s(st + 3 * T::UE, p.B + off, ub, &full[s]);
+                        if (p.s) bulk_g2s(st + T::SD, slot1 + off, ub, &full[s]);
+                        bulk_g2s(st + T::SB, p.B + off, ub, &full[s]);
                     } else if (p.l2hint) {
                         mbar_arrive_expect_tx(&full[s], 4 * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
-                        bulk_g2s_hint(st + 1 * T::UE, slot1 + off, ub, &full[s], pol_first);
-                        bulk_g2s_hint(st + 2 * T::UE, p.x + off, ub, &full[s], pol_first);
-                        bulk_g2s_hint(st + 3 * T::UE, p.B + off, ub, &full[s], pol_first);
+                        bulk_g2s_hint(st + T::SD, slot1 + off, ub, &full[s], pol_first);
+                        bulk_g2s_hint(st + T::SX, p.x + off, ub, &full[s], pol_first);
+                        bulk_g2s_hint(st + T::SB, p.B + off, ub, &full[s], pol_first);
                     } else {
-                        mbar_arrive_expect_tx(&full[s], (need1 ? 4 : 3) * ub);
+                        mbar_arrive_expect_tx(&full[s], (stage1 ? 4 : 3) * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
-                        if (need1) bulk_g2s(st + 1 * T::UE, slot1 + off, ub, &full[s]);
-                        bulk_g2s(st + 2 * T::UE, p.x + off, ub, &full[s]);
-                        bulk_g2s(st + 3 * T::UE, p.B + off, ub, &full[s]);
+                        if (stage1) bulk_g2s(st + T::SD, slot1 + off, ub, &full[s]);
+                        bulk_g2s(st + T::SX, p.x + off, ub, &full[s]);
+                        bulk_g2s(st + T::SB, p.B + off, ub, &full[s]);
                     }
                 }
             }
@@ -202,7 +209,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                             const int e = sbase + G::N1 * m;
                             const long long gi = gb + G::N1 * m;
                             const float2 y = cconj(v[m]);           // (L+1)^-1 u, chain complete
-                            const float2 b = st[3 * T::UE + e];
+                            const float2 b = st[T::SB + e];
                             float2 dn;
                             if (MODE == X_SRC_EPI) {
                                 dn = cmul(b, y);                    // Delta_0 = B (L+1)^-1 s
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                                 p.delta[gi] = dn;
                                 lacc += cabs2(dn);
                                 // next chain: u = B Delta (x-form plans: u_0 = s)
-                                v[m] = p.s ? st[1 * T::UE + e] : cmul(b, dn);
+                                v[m] = p.s ? st[T::SD + e] : cmul(b, dn);
                                 continue;
                             }
                             // One body for every action (uniform selects, no duplicated code):
@@ -220,8 +227,9 @@ __global__ void __launch_bounds__(XPipe<N>::NT, 1) k_xpass_pipe(XParams p) {
                             //                        x_{k+1} = x_k + alpha Delta_k, u = B x_{k+1} + s
                             //   probe: Delta_k = B (y - x_k) stored, x kept, u = B x_k + s
                             //   x-form -> Delta-form: Delta_k stored, x kept, u = B Delta_k
-                            const float2 a1 = need1 ? st[1 * T::UE + e] : make_float2(0.f, 0.f);   // Delta_k or s
-                            const float2 xx = st[2 * T::UE + e];
+                            // Delta_k or s (LEAN: a Delta-form pass reads Delta from global memory)
+                            const float2 a1 = !need1 ? make_float2(0.f, 0.f) : (LEAN ? slot1[gi] : st[T::SD + e]);
+                            const float2 xx = st[T::SX + e];
                             const float2 t = cmul(b, csub(y, dform ? a1 : xx));
                             const float2 d0 = dform ? a1 : make_float2(0.f, 0.f);
                             dn = make_float2(fmaf(c1, t.x, d0.x), fmaf(c1, t.y, d0.y));
@@ -337,24 +345,28 @@ cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s) {
 // ========================================================= launchers ====
 #define USP_PIPE_X_N(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
 
-template <int N, int MODE>
+template <int N, int MODE, bool LEAN>
 static cudaError_t xpipe_t(const XParams &p, int grid, cudaStream_t s) {
+    using T = XPipe<N, LEAN>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_xpass_pipe<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             XPipe<N>::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_xpass_pipe<N, MODE, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             T::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_pdl(k_xpass_pipe<N, MODE>, grid, XPipe<N>::NT, XPipe<N>::SMEM, s, p);
+    return launch_pdl(k_xpass_pipe<N, MODE, LEAN>, grid, T::NT, T::SMEM, s, p);
 }
 
-cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s) {
-#define XP_CASE(n)                                                           \
-    case n:                                                                  \
-        if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD>(p, grid, s);     \
-        if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI>(p, grid, s);     \
-        return xpipe_t<n, X_ITER>(p, grid, s);
+// lean: X_ITER of a sparse-source plan expected in the x-form (3-slot stages,
+// one more consumer warp; N <= 1024)
+cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean) {
+#define XP_CASE(n)                                                                    \
+    case n:                                                                           \
+        if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD, false>(p, grid, s);       \
+        if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI, false>(p, grid, s);       \
+        if (lean && n <= 1024) return xpipe_t<n, X_ITER, true>(p, grid, s);           \
+        return xpipe_t<n, X_ITER, false>(p, grid, s);
     switch (N) { USP_PIPE_X_N(XP_CASE) default: return cudaErrorInvalidValue; }
 #undef XP_CASE
 }

@@ -198,6 +198,9 @@ struct usp_plan_s {
     unsigned *s_ctr = nullptr;
     bool s_sparse = false;
     int s_count = 0;
+    // sparse x-form passes use the 3-slot x pass (USP_LEAN=0 disables); the
+    // host's view of the form, refreshed at batch boundaries
+    bool lean_ok = true, lean_hint = false;
     double r_sw = 1e-2;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -553,7 +556,9 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
     {
         Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
         if (p->real) CU(launch_xpass_real((int)p->nx, mode, xp, p->gridp_x, p->stream));
-        else if (p->pipe_xk) CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream));
+        else if (p->pipe_xk)
+            CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream,
+                                 mode == X_ITER && p->s_sparse && p->lean_hint && p->lean_ok));
         else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
     }
     if (mode != X_SRC_FWD && rank_finish(p)) {
@@ -1225,6 +1230,8 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         if (xs) p->r_sw = std::atof(xs);
         const char *ff = std::getenv("USP_FORCE_FINISH");
         p->force_finish = ff && ff[0] == '1';
+        const char *ln = std::getenv("USP_LEAN");
+        p->lean_ok = !(ln && ln[0] == '0');
     }
     TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
@@ -1548,6 +1555,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         if ((s = run_anti_x(p, X_SRC_EPI))) return s;
     } else {
         p->s_sparse = false;
+        p->lean_hint = false;
         XParams xp = x_params(p);
         const char *sps = std::getenv("USP_SPARSE_S");
         const bool try_sparse = p->xform && !p->real && !(sps && sps[0] == '0');
@@ -1579,6 +1587,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
                                         p->s + 256, p->s_ctr, p->stream));
                 p->s_sparse = true;
                 p->s_count = (int)cnt;
+                p->lean_hint = true;
             }
         }
     }
@@ -1597,6 +1606,7 @@ usp_status probe_xform(usp_plan_s *p) {
     usp_status s = sync_state(p);
     if (s) return s;
     if (p->st_host->form != FORM_X || p->st_host->status != ST_RUNNING || p->st_host->k == 0) return USP_OK;
+    p->lean_hint = true;
     {
         Tick t(p, KC_SETSTATE);
         CU(launch_set_form(p->st, FORM_PROBE, p->stream));
@@ -1615,6 +1625,7 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
     if (n_max < 0 || !(alpha > 0.0)) return fail(USP_ERR_ARG, "need n_max >= 0 and alpha > 0");
     usp_status s = sync_state(p);
     if (s) return s;
+    p->lean_hint = p->st_host->form != FORM_DELTA;
     const long long k0 = p->st_host->k;
     const long long kmax = k0 + n_max;
     {
@@ -1659,6 +1670,11 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         const long long total = n_max + (p->xform ? 1 : 0);
         while (launched < total) {
             const long long nb = std::min(batch, total - launched);
+            if (p->s_sparse && launched > 0) {   // the x-form may have switched to the Delta-form
+                s = sync_state(p);
+                if (s) return s;
+                p->lean_hint = p->st_host->form != FORM_DELTA;
+            }
             for (long long i = 0; i < nb; ++i) {
                 if (p->tdiff) {
                     if ((s = td_xfft(p, false))) return s;
