@@ -577,7 +577,8 @@ constexpr int kSparseMaxLines = 64;
 // sparse source: after an x pass of the iteration, add the x-transformed
 // source lines if that pass formed u = B x (k_sparse_add checks st->add_s)
 usp_status sparse_add(usp_plan_s *p) {
-    if (!p->s_sparse) return USP_OK;
+    // (once the host has seen the Delta-form, no x-form pass can follow in this call)
+    if (!p->s_sparse || !p->lean_hint) return USP_OK;
     SAddParams sa{};
     sa.work = p->work;
     sa.list = reinterpret_cast<const int *>(p->s);
