@@ -204,6 +204,20 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
                     fft_line<N, false, LayRow<N>, true>(v, lay, j, sm_tw);
                     if (pass == 0) {
                         float lacc = 0.f;
+                        if (LEAN && MODE == X_ITER && act == ACT_X && !need1) {
+                            // the lean pass's common case, without the selects of the
+                            // general body: Delta_k = B (y - x_k), x_{k+1}, u = B x_{k+1}
+#pragma unroll
+                            for (int m = 0; m < G::N2; ++m) {
+                                const int e = sbase + G::N1 * m;
+                                const float2 y = cconj(v[m]), b = st[T::SB + e], xx = st[T::SX + e];
+                                const float2 dk = cmul(b, csub(y, xx));
+                                const float2 xn = make_float2(fmaf(alpha, dk.x, xx.x), fmaf(alpha, dk.y, xx.y));
+                                p.x[gb + G::N1 * m] = xn;
+                                lacc += cabs2(dk);
+                                v[m] = cmul(b, xn);
+                            }
+                        } else
 #pragma unroll
                         for (int m = 0; m < G::N2; ++m) {
                             const int e = sbase + G::N1 * m;
