@@ -55,7 +55,12 @@ struct XPipe {
     static constexpr int SMEM = (S * STAGE + XC * XBUF + N) * 8 + 2 * S * 8;   // stages, exchange, twiddles, barriers
 };
 
-template <int N, int MODE, bool LEAN>
+// DSPEC: the Delta-form update has its own loop body (launched when the host
+// expects the Delta-form).  Extra bodies that a launch does not execute still
+// cost: the dense x-form measured 8.3 ms with the general body alone and
+// 10.3 ms next to a Delta-form body, the Delta-form 13.4 vs 9.7 ms the other
+// way round -- so each expected form gets its own instantiation.
+template <int N, int MODE, bool LEAN, bool DSPEC>
 __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p) {
     using G = LineGeo<N>;
     using T = XPipe<N, LEAN>;
@@ -217,6 +222,21 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
                                 lacc += cabs2(dk);
                                 v[m] = cmul(b, xn);
                             }
+                        } else if (DSPEC && !LEAN && MODE == X_ITER && act == ACT_DELTA && !p.l2hint) {
+                            // the Delta-form's dedicated body
+#pragma unroll
+                            for (int m = 0; m < G::N2; ++m) {
+                                const int e = sbase + G::N1 * m;
+                                const long long gi = gb + G::N1 * m;
+                                const float2 y = cconj(v[m]), b = st[T::SB + e];
+                                const float2 d = st[T::SD + e], xx = st[T::SX + e];
+                                const float2 t = cmul(b, csub(y, d));
+                                const float2 dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
+                                p.x[gi] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
+                                p.delta[gi] = dn;
+                                lacc += cabs2(dn);
+                                v[m] = cmul(b, dn);
+                            }
                         } else
 #pragma unroll
                         for (int m = 0; m < G::N2; ++m) {
@@ -359,28 +379,31 @@ cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s) {
 // ========================================================= launchers ====
 #define USP_PIPE_X_N(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
 
-template <int N, int MODE, bool LEAN>
+template <int N, int MODE, bool LEAN, bool DSPEC>
 static cudaError_t xpipe_t(const XParams &p, int grid, cudaStream_t s) {
     using T = XPipe<N, LEAN>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_xpass_pipe<N, MODE, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             T::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k_xpass_pipe<N, MODE, LEAN, DSPEC>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_pdl(k_xpass_pipe<N, MODE, LEAN>, grid, T::NT, T::SMEM, s, p);
+    return launch_pdl(k_xpass_pipe<N, MODE, LEAN, DSPEC>, grid, T::NT, T::SMEM, s, p);
 }
 
-// lean: X_ITER of a sparse-source plan expected in the x-form (3-slot stages,
-// one more consumer warp; N <= 1024)
-cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean) {
+// X_ITER variants by the form the host expects: lean (sparse-source x-form:
+// 3-slot stages, one more consumer warp; N <= 1024), x-form (general body),
+// Delta-form (dedicated body)
+cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean,
+                              bool expect_x) {
 #define XP_CASE(n)                                                                    \
     case n:                                                                           \
-        if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD, false>(p, grid, s);       \
-        if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI, false>(p, grid, s);       \
-        if (lean && n <= 1024) return xpipe_t<n, X_ITER, true>(p, grid, s);           \
-        return xpipe_t<n, X_ITER, false>(p, grid, s);
+        if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD, false, false>(p, grid, s); \
+        if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI, false, false>(p, grid, s); \
+        if (lean && n <= 1024) return xpipe_t<n, X_ITER, true, false>(p, grid, s);    \
+        if (expect_x) return xpipe_t<n, X_ITER, false, false>(p, grid, s);            \
+        return xpipe_t<n, X_ITER, false, true>(p, grid, s);
     switch (N) { USP_PIPE_X_N(XP_CASE) default: return cudaErrorInvalidValue; }
 #undef XP_CASE
 }

@@ -558,7 +558,8 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
         if (p->real) CU(launch_xpass_real((int)p->nx, mode, xp, p->gridp_x, p->stream));
         else if (p->pipe_xk)
             CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream,
-                                 mode == X_ITER && p->s_sparse && p->lean_hint && p->lean_ok));
+                                 mode == X_ITER && p->s_sparse && p->lean_hint && p->lean_ok,
+                                 p->xform && p->lean_hint));
         else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
     }
     if (mode != X_SRC_FWD && rank_finish(p)) {
@@ -1671,7 +1672,7 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
         const long long total = n_max + (p->xform ? 1 : 0);
         while (launched < total) {
             const long long nb = std::min(batch, total - launched);
-            if (p->s_sparse && launched > 0) {   // the x-form may have switched to the Delta-form
+            if (p->xform && launched > 0) {   // the x-form may have switched to the Delta-form
                 s = sync_state(p);
                 if (s) return s;
                 p->lean_hint = p->st_host->form != FORM_DELTA;

@@ -302,7 +302,8 @@ cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, co
 cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s);
 
 // TMA-pipelined variants (kernels_pipe.cu)
-cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean = false);
+cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean = false,
+                              bool expect_x = false);
 cudaError_t launch_strided_pipe(int N, SMode mode, int rank, const CUtensorMap &map, const SParams &p, int grid,
                                 cudaStream_t s);
 bool strided_pipe_supported(long long n);
