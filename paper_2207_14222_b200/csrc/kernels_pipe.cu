@@ -60,7 +60,7 @@ struct XPipe {
 // cost: the dense x-form measured 8.3 ms with the general body alone and
 // 10.3 ms next to a Delta-form body, the Delta-form 13.4 vs 9.7 ms the other
 // way round -- so each expected form gets its own instantiation.
-template <int N, int MODE, bool LEAN, bool DSPEC>
+template <int N, int MODE, bool LEAN, bool DSPEC, bool XSPEC = false>
 __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p) {
     using G = LineGeo<N>;
     using T = XPipe<N, LEAN>;
@@ -222,6 +222,20 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
                                 lacc += cabs2(dk);
                                 v[m] = cmul(b, xn);
                             }
+                        } else if (XSPEC && !LEAN && MODE == X_ITER && act == ACT_X && need1 && !p.l2hint) {
+                            // the dense-source x-form's dedicated body: u = B x_{k+1} + s
+#pragma unroll
+                            for (int m = 0; m < G::N2; ++m) {
+                                const int e = sbase + G::N1 * m;
+                                const float2 y = cconj(v[m]), b = st[T::SB + e];
+                                const float2 sv = st[T::SD + e], xx = st[T::SX + e];
+                                const float2 dk = cmul(b, csub(y, xx));
+                                const float2 xn = make_float2(fmaf(alpha, dk.x, xx.x), fmaf(alpha, dk.y, xx.y));
+                                p.x[gb + G::N1 * m] = xn;
+                                lacc += cabs2(dk);
+                                const float2 bx = cmul(b, xn);
+                                v[m] = make_float2(bx.x + sv.x, bx.y + sv.y);
+                            }
                         } else if (DSPEC && !LEAN && MODE == X_ITER && act == ACT_DELTA && !p.l2hint) {
                             // the Delta-form's dedicated body
 #pragma unroll
@@ -379,18 +393,23 @@ cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s) {
 // ========================================================= launchers ====
 #define USP_PIPE_X_N(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
 
-template <int N, int MODE, bool LEAN, bool DSPEC>
+template <int N, int MODE, bool LEAN, bool DSPEC, bool XSPEC = false>
 static cudaError_t xpipe_t(const XParams &p, int grid, cudaStream_t s) {
     using T = XPipe<N, LEAN>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_xpass_pipe<N, MODE, LEAN, DSPEC>,
+        cudaError_t e = cudaFuncSetAttribute(k_xpass_pipe<N, MODE, LEAN, DSPEC, XSPEC>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_pdl(k_xpass_pipe<N, MODE, LEAN, DSPEC>, grid, T::NT, T::SMEM, s, p);
+    return launch_pdl(k_xpass_pipe<N, MODE, LEAN, DSPEC, XSPEC>, grid, T::NT, T::SMEM, s, p);
 }
+
+#ifndef USP_XSPEC
+#define USP_XSPEC 1
+#endif
+constexpr bool XSPEC_ON = USP_XSPEC != 0;
 
 // X_ITER variants by the form the host expects: lean (sparse-source x-form:
 // 3-slot stages, one more consumer warp; N <= 1024), x-form (general body),
@@ -402,7 +421,7 @@ cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cud
         if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD, false, false>(p, grid, s); \
         if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI, false, false>(p, grid, s); \
         if (lean && n <= 1024) return xpipe_t<n, X_ITER, true, false>(p, grid, s);    \
-        if (expect_x) return xpipe_t<n, X_ITER, false, false>(p, grid, s);            \
+        if (expect_x) return xpipe_t<n, X_ITER, false, false, XSPEC_ON>(p, grid, s);  \
         return xpipe_t<n, X_ITER, false, true>(p, grid, s);
     switch (N) { USP_PIPE_X_N(XP_CASE) default: return cudaErrorInvalidValue; }
 #undef XP_CASE
