@@ -85,7 +85,7 @@ typedef enum {
     USP_R32 = 1  /* real float32 arrays (imaginary part 0); the field returned is real    */
 } usp_dtype;
 
-typedef enum { USP_DEVICE = 0, USP_HOST = 1 } usp_where;
+typedef enum { USP_DEVICE = 0, USP_HOST = 1, USP_STAGED = 2 /* see usp_stage_inputs */ } usp_where;
 
 typedef struct { double re, im; } usp_c128;
 
@@ -214,6 +214,23 @@ usp_status usp_residual(usp_plan_t plan, double *rel, double *abs_norm, int64_t 
 /* Copy r_0 .. r_{n-1} (fp64) into host[0..cap); *n = number available
  * (ring of the most recent 65536 iterations). */
 usp_status usp_residual_history(usp_plan_t plan, double *host, int64_t cap, int64_t *n);
+
+/* Asynchronous input staging (pipelining a sequence of problems).
+ * usp_staging_size: bytes of the caller-owned staging workspace (room for one
+ * medium and one source of this plan, 256-byte aligned); usp_plan_set_staging
+ * hands it over (it must outlive the plan).  usp_stage_inputs copies a medium
+ * and a source from host memory (pinned for full speed; layouts and dtypes as
+ * usp_set_potential / usp_set_source) into it on an internal copy stream and
+ * returns at once, so the copies overlap whatever the plan stream is running
+ * (e.g. the iterations of the previous problem).  The next usp_set_potential
+ * and usp_set_source called with where = USP_STAGED (pointer argument
+ * ignored, may be NULL) make the plan stream wait for those copies and use
+ * them; the staging area is reused only after that set_source has consumed
+ * it.  Not for tensor-diffusion plans.  Errors: USP_ERR_STATE (no staging
+ * workspace / nothing staged), USP_ERR_ARG, USP_ERR_CUDA. */
+usp_status usp_staging_size(usp_plan_t plan, size_t *bytes);
+usp_status usp_plan_set_staging(usp_plan_t plan, void *dev, size_t bytes);
+usp_status usp_stage_inputs(usp_plan_t plan, const void *medium_host, const void *source_host);
 
 /* Copy the current iterate x_k into `out` ([z][y][x], desc.dtype). */
 usp_status usp_get_field(usp_plan_t plan, void *out, usp_where where);

@@ -19,7 +19,7 @@ STATUS_NAMES = {0: "USP_OK", 1: "USP_ERR_ARG", 2: "USP_ERR_STATE", 3: "USP_ERR_N
 TERM_NAMES = {0: "converged", 1: "max_iter", 2: "diverged"}
 MEDIUM_K2, MEDIUM_W = 0, 1
 C64, R32 = 0, 1
-DEVICE, HOST = 0, 1
+DEVICE, HOST, STAGED = 0, 1, 2
 
 
 class c128(ctypes.Structure):
@@ -63,6 +63,9 @@ SIGNATURES = {
     "usp_residual_history": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
                                             ctypes.POINTER(ctypes.c_int64)]),
     "usp_get_field": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+    "usp_staging_size": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
+    "usp_plan_set_staging": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
+    "usp_stage_inputs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "usp_profile_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "usp_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),

@@ -201,6 +201,13 @@ struct usp_plan_s {
     // sparse x-form passes use the 3-slot x pass (USP_LEAN=0 disables); the
     // host's view of the form, refreshed at batch boundaries
     bool lean_ok = true, lean_hint = false;
+    // asynchronous input staging (usp_stage_inputs): caller-owned area, copy
+    // stream, "copies done" and "staging area consumed" events
+    char *stg = nullptr;
+    size_t stg_bytes = 0;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_staged = nullptr, ev_consumed = nullptr;
+    bool staged = false, consumed_recorded = false;
     double r_sw = 1e-2;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -1337,13 +1344,26 @@ usp_status usp_local_extent(usp_plan_t p, int64_t *z0, int64_t *nz_local) {
 }
 
 usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, double target_norm) {
-    if (!p || !medium) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    bool from_stage = false;
+    if (where == USP_STAGED) {   // the medium staged by usp_stage_inputs
+        if (!p->staged) return fail(USP_ERR_STATE, "nothing staged (usp_stage_inputs)");
+        CU(cudaStreamWaitEvent(p->stream, p->ev_staged, 0));
+        medium = p->stg;
+        where = USP_DEVICE;
+        from_stage = true;
+    }
+    if (!medium) return fail(USP_ERR_ARG, "NULL argument");
     if (p->tdiff) return fail(USP_ERR_STATE, "tensor-diffusion plans take usp_set_tensor_medium");
     if (!p->ws) return fail(USP_ERR_STATE, "workspace not set");
     if (where != USP_HOST && where != USP_DEVICE) return fail(USP_ERR_ARG, "bad where");
     // stage the medium in the chain buffer (the source resets it later)
     usp_status s = stage(p, p->work, medium, (size_t)p->nloc * elem_bytes(p), where);
     if (s) return s;
+    if (from_stage) {   // (set_source records it again after the source copy)
+        CU(cudaEventRecord(p->ev_consumed, p->stream));
+        p->consumed_recorded = true;
+    }
     p->have_source = false;
     p->have_potential = false;
     if (target_norm > 0.0) {
@@ -1517,10 +1537,23 @@ usp_status usp_get_split(usp_plan_t p, usp_c128 *sigma, usp_c128 *c, usp_c128 *c
 }
 
 usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
-    if (!p || !src) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    const bool from_stage = where == USP_STAGED;
+    if (from_stage) {   // the source staged by usp_stage_inputs
+        if (!p->staged) return fail(USP_ERR_STATE, "nothing staged (usp_stage_inputs)");
+        CU(cudaStreamWaitEvent(p->stream, p->ev_staged, 0));
+        src = p->stg + align256((size_t)p->nloc * elem_bytes(p));
+        where = USP_DEVICE;
+    }
+    if (!src) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->have_potential) return fail(USP_ERR_STATE, "set_potential must succeed first");
     usp_status s = stage(p, p->x, src, (size_t)p->nloc * elem_bytes(p), where);
     if (s) return s;
+    if (from_stage) {   // the staging area may be refilled once this copy has run
+        CU(cudaEventRecord(p->ev_consumed, p->stream));
+        p->consumed_recorded = true;
+        p->staged = false;
+    }
     IterState s0{};
     s0.status = ST_NO_SOURCE;
     s0.alpha = 0.75;
@@ -1753,6 +1786,43 @@ usp_status usp_residual_history(usp_plan_t p, double *host, int64_t cap, int64_t
         const long long first = p->st_host->k + 1 - avail;
         for (long long i = 0; i < std::min<long long>(cap, avail); ++i) host[i] = all[(first + i) % p->hist_cap];
     }
+    return USP_OK;
+}
+
+usp_status usp_staging_size(usp_plan_t p, size_t *bytes) {
+    if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
+    *bytes = 2 * align256((size_t)p->nloc * elem_bytes(p));
+    return USP_OK;
+}
+
+usp_status usp_plan_set_staging(usp_plan_t p, void *dev, size_t bytes) {
+    if (!p || !dev) return fail(USP_ERR_ARG, "NULL argument");
+    if (((uintptr_t)dev) & 255) return fail(USP_ERR_ARG, "staging area must be 256-byte aligned");
+    size_t need = 0;
+    usp_staging_size(p, &need);
+    if (bytes < need) return fail(USP_ERR_NOMEM, "staging area %zu bytes < required %zu", bytes, need);
+    if (p->tdiff) return fail(USP_ERR_UNSUPPORTED, "tensor-diffusion plans do not stage inputs");
+    if (!p->cstream) {
+        CU(cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&p->ev_staged, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&p->ev_consumed, cudaEventDisableTiming));
+    }
+    CU(cudaStreamSynchronize(p->cstream));
+    p->stg = (char *)dev;
+    p->stg_bytes = bytes;
+    p->staged = false;
+    return USP_OK;
+}
+
+usp_status usp_stage_inputs(usp_plan_t p, const void *medium, const void *source) {
+    if (!p || !medium || !source) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p->stg) return fail(USP_ERR_STATE, "usp_plan_set_staging must be called first");
+    const size_t nb = (size_t)p->nloc * elem_bytes(p);
+    if (p->consumed_recorded) CU(cudaStreamWaitEvent(p->cstream, p->ev_consumed, 0));
+    CU(cudaMemcpyAsync(p->stg, medium, nb, cudaMemcpyHostToDevice, p->cstream));
+    CU(cudaMemcpyAsync(p->stg + align256(nb), source, nb, cudaMemcpyHostToDevice, p->cstream));
+    CU(cudaEventRecord(p->ev_staged, p->cstream));
+    p->staged = true;
     return USP_OK;
 }
 
@@ -2191,6 +2261,12 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->st);
     cudaFree(p->partials);
     cudaFree(p->hist);
+    if (p->cstream) {
+        cudaStreamSynchronize(p->cstream);
+        cudaStreamDestroy(p->cstream);
+        cudaEventDestroy(p->ev_staged);
+        cudaEventDestroy(p->ev_consumed);
+    }
     cudaFree(p->red_u);
     if (p->s_flag) cudaFree(p->s_flag);
     if (p->s_ctr) cudaFree(p->s_ctr);

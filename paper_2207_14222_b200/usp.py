@@ -112,7 +112,31 @@ class Plan:
         self.local_shape = ((int(nzl.value),) + self.shape[1:]) if self.ndim == 3 else self.shape
 
     # -- setup ---------------------------------------------------------------
+    def stage_inputs(self, medium, source):
+        """usp_stage_inputs: start copying the NEXT problem's medium and source
+        (host arrays, ideally pinned) into the staging area on the plan's copy
+        stream; returns at once.  Then call set_potential("staged") and
+        set_source("staged").  The host buffers must stay untouched until
+        set_source("staged") has returned."""
+        if getattr(self, "staging", None) is None:
+            import torch
+
+            nbytes = ctypes.c_size_t()
+            L.check(self.lib.usp_staging_size(self.handle, ctypes.byref(nbytes)))
+            self.staging = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+            L.check(self.lib.usp_plan_set_staging(self.handle, ctypes.c_void_p(self.staging.data_ptr()),
+                                                  int(nbytes.value)))
+        pm, wm, km = _ptr_where(medium, self.dtype)
+        ps, ws, ks = _ptr_where(source, self.dtype)
+        if wm != L.HOST or ws != L.HOST:
+            raise ValueError("stage_inputs takes host buffers")
+        self._staged_keep = (km, ks)   # the copies read them asynchronously
+        L.check(self.lib.usp_stage_inputs(self.handle, pm, ps))
+
     def set_potential(self, medium, target_norm: float = 0.95):
+        if isinstance(medium, str) and medium == "staged":
+            L.check(self.lib.usp_set_potential(self.handle, None, L.STAGED, float(target_norm)))
+            return self.split
         ptr, where, keep = _ptr_where(medium, self.dtype)
         L.check(self.lib.usp_set_potential(self.handle, ptr, where, float(target_norm)))
         del keep
@@ -146,6 +170,9 @@ class Plan:
         return Split(complex(s.re, s.im), complex(c.re, c.im), complex(ce.re, ce.im), r.value, v.value)
 
     def set_source(self, src):
+        if isinstance(src, str) and src == "staged":
+            L.check(self.lib.usp_set_source(self.handle, None, L.STAGED))
+            return
         ptr, where, keep = _ptr_where(src, self.dtype)
         L.check(self.lib.usp_set_source(self.handle, ptr, where))
         del keep
