@@ -198,9 +198,12 @@ struct usp_plan_s {
     unsigned *s_ctr = nullptr;
     bool s_sparse = false;
     int s_count = 0;
-    // sparse x-form passes use the 3-slot x pass (USP_LEAN=0 disables); the
-    // host's view of the form, refreshed at batch boundaries
-    bool lean_ok = true, lean_hint = false;
+    // expect_x: the host's view of the device-side form (x-form or not),
+    // refreshed at call start and batch boundaries; it picks the x-pass
+    // instance (lean 3-slot pass for sparse-source x-form passes unless
+    // USP_LEAN=0, general body, Delta-form body) and whether the sparse
+    // source lines are added after a pass
+    bool lean_ok = true, expect_x = false;
     // asynchronous input staging (usp_stage_inputs): caller-owned area, copy
     // stream, "copies done" and "staging area consumed" events
     char *stg = nullptr;
@@ -565,8 +568,8 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
         if (p->real) CU(launch_xpass_real((int)p->nx, mode, xp, p->gridp_x, p->stream));
         else if (p->pipe_xk)
             CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream,
-                                 mode == X_ITER && p->s_sparse && p->lean_hint && p->lean_ok,
-                                 p->xform && p->lean_hint));
+                                 mode == X_ITER && p->s_sparse && p->expect_x && p->lean_ok,
+                                 p->xform && p->expect_x));
         else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
     }
     if (mode != X_SRC_FWD && rank_finish(p)) {
@@ -586,7 +589,7 @@ constexpr int kSparseMaxLines = 64;
 // source lines if that pass formed u = B x (k_sparse_add checks st->add_s)
 usp_status sparse_add(usp_plan_s *p) {
     // (once the host has seen the Delta-form, no x-form pass can follow in this call)
-    if (!p->s_sparse || !p->lean_hint) return USP_OK;
+    if (!p->s_sparse || !p->expect_x) return USP_OK;
     SAddParams sa{};
     sa.work = p->work;
     sa.list = reinterpret_cast<const int *>(p->s);
@@ -1590,7 +1593,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         if ((s = run_anti_x(p, X_SRC_EPI))) return s;
     } else {
         p->s_sparse = false;
-        p->lean_hint = false;
+        p->expect_x = false;
         XParams xp = x_params(p);
         const char *sps = std::getenv("USP_SPARSE_S");
         const bool try_sparse = p->xform && !p->real && !(sps && sps[0] == '0');
@@ -1622,7 +1625,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
                                         p->s + 256, p->s_ctr, p->stream));
                 p->s_sparse = true;
                 p->s_count = (int)cnt;
-                p->lean_hint = true;
+                p->expect_x = true;
             }
         }
     }
@@ -1641,7 +1644,7 @@ usp_status probe_xform(usp_plan_s *p) {
     usp_status s = sync_state(p);
     if (s) return s;
     if (p->st_host->form != FORM_X || p->st_host->status != ST_RUNNING || p->st_host->k == 0) return USP_OK;
-    p->lean_hint = true;
+    p->expect_x = true;
     {
         Tick t(p, KC_SETSTATE);
         CU(launch_set_form(p->st, FORM_PROBE, p->stream));
@@ -1660,7 +1663,7 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
     if (n_max < 0 || !(alpha > 0.0)) return fail(USP_ERR_ARG, "need n_max >= 0 and alpha > 0");
     usp_status s = sync_state(p);
     if (s) return s;
-    p->lean_hint = p->st_host->form != FORM_DELTA;
+    p->expect_x = p->st_host->form != FORM_DELTA;
     const long long k0 = p->st_host->k;
     const long long kmax = k0 + n_max;
     {
@@ -1708,7 +1711,7 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
             if (p->xform && launched > 0) {   // the x-form may have switched to the Delta-form
                 s = sync_state(p);
                 if (s) return s;
-                p->lean_hint = p->st_host->form != FORM_DELTA;
+                p->expect_x = p->st_host->form != FORM_DELTA;
             }
             for (long long i = 0; i < nb; ++i) {
                 if (p->tdiff) {
