@@ -2001,24 +2001,30 @@ bool gm_always_cgs2() {   // USP_GMRES_CGS2=1: always two passes (the previous b
 
 usp_status gs_dots(usp_plan_s *p, int nv, float2 *z, std::vector<zd> &d, double *nrm) {
     d.assign(nv, zd(0.0, 0.0));
-    std::vector<double> h((size_t)p->gm_grid * 17);
-    for (int b0 = 0; b0 < nv; b0 += 8) {
-        const int nb = std::min(8, nv - b0);
+    // every block of 8 basis vectors writes its own partials region; one
+    // read-back and one host sync for the whole round
+    const int nblk = (nv + 7) / 8;
+    const size_t region = (size_t)17 * p->gm_grid;
+    for (int bi = 0; bi < nblk; ++bi) {
+        const int b0 = 8 * bi, nb = std::min(8, nv - b0);
         GSParams g{};
         for (int q = 0; q < nb; ++q) g.U[q] = p->gm_U[b0 + q];
         g.z = z;
         g.n = p->nloc;
-        g.partials = p->gm_part;
-        {
-            Tick t(p, KC_KUPD);
-            CU(launch_gs(GS_DOT, nb, g, p->gm_grid, p->stream));
-        }
+        g.partials = p->gm_part + bi * region;
+        Tick t(p, KC_KUPD);
+        CU(launch_gs(GS_DOT, nb, g, p->gm_grid, p->stream));
+    }
+    std::vector<double> h(region * nblk);
+    CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * region * nblk, cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int bi = 0; bi < nblk; ++bi) {
+        const int b0 = 8 * bi, nb = std::min(8, nv - b0);
         const int K = 2 * nb + 1;
-        CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * K * p->gm_grid, cudaMemcpyDeviceToHost, p->stream));
-        CU(cudaStreamSynchronize(p->stream));
+        const double *hb = h.data() + bi * region;
         std::vector<double> loc(K, 0.0);
         for (int q = 0; q < K; ++q)
-            for (int c = 0; c < p->gm_grid; ++c) loc[q] += h[(size_t)c * K + q];
+            for (int c = 0; c < p->gm_grid; ++c) loc[q] += hb[(size_t)c * K + q];
         // slab-decomposed: every rank's local sums, added in rank order
         std::vector<double> all;
         usp_status s = gather_host(p, loc.data(), K, all);
@@ -2104,7 +2110,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
         return fail(USP_ERR_STATE, "GMRES starts from x_0 = 0: call usp_set_source again first");
     if (!p->gm_part) {
         p->gm_grid = p->nsm * 4;
-        CU(cudaMalloc(&p->gm_part, sizeof(double) * 17 * p->gm_grid));
+        CU(cudaMalloc(&p->gm_part, sizeof(double) * 17 * p->gm_grid * 9));   // (m + 1 <= 65 vectors) / 8 blocks
     }
     const int m = p->gm_m;
     const long long nvb = (long long)p->nloc * sizeof(float2);
