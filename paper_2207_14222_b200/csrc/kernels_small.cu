@@ -31,11 +31,50 @@ namespace usp {
 
 // Sense-reversing grid barrier over co-resident CTAs (cooperative launch).
 // A 4-second watchdog turns a scheduling failure into an error code.
+#ifndef USP_S2_SCOPED_BARRIER
+#define USP_S2_SCOPED_BARRIER 1
+#endif
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acqrel_gpu(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// Sense-reversing grid barrier over co-resident CTAs (cooperative launch).
+// Scoped acquire/release at gpu scope instead of full fences: the CTA
+// barrier orders the CTA's writes before thread 0's release (cumulativity).
+// A 4-second watchdog turns a scheduling failure into an error code.
 __device__ __forceinline__ bool grid_barrier(unsigned *count, volatile unsigned *gen, IterState *st) {
     __syncthreads();
     __shared__ int ok;
     if (threadIdx.x == 0) {
         ok = 1;
+#if USP_S2_SCOPED_BARRIER
+        unsigned *genp = const_cast<unsigned *>(gen);
+        const unsigned g = ld_acquire_gpu(genp);
+        if (atom_add_acqrel_gpu(count, 1u) == gridDim.x - 1) {
+            *count = 0u;   // ordered before the release below
+            st_release_gpu(genp, g + 1u);
+        } else {
+            const uint64_t t0 = globaltimer_ns();
+            unsigned n = 0;
+            while (ld_acquire_gpu(genp) == g) {
+                if ((++n & 255u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
+                    if (atomicCAS(&st->err, 0, 10) == 0) st->err_info = blockIdx.x;
+                    ok = 0;
+                    break;
+                }
+            }
+        }
+#else
         const unsigned g = *gen;
         __threadfence();
         if (atomicAdd(count, 1u) == gridDim.x - 1) {
@@ -54,6 +93,7 @@ __device__ __forceinline__ bool grid_barrier(unsigned *count, volatile unsigned 
             }
         }
         __threadfence();
+#endif
     }
     __syncthreads();
     return ok != 0;
