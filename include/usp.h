@@ -232,6 +232,16 @@ usp_status usp_staging_size(usp_plan_t plan, size_t *bytes);
 usp_status usp_plan_set_staging(usp_plan_t plan, void *dev, size_t bytes);
 usp_status usp_stage_inputs(usp_plan_t plan, const void *medium_host, const void *source_host);
 
+/* Asynchronous result read-back (same staging workspace, which also holds
+ * one field for this): usp_get_field_async snapshots x_k into the staging
+ * area on the plan stream and copies it to host memory `out` on a second
+ * copy stream, returning at once -- the copy overlaps what the plan stream
+ * does next (the next problem).  usp_wait_field blocks until that copy has
+ * landed; `out` must not be read before.  Errors: USP_ERR_STATE (no staging
+ * workspace / no source), USP_ERR_ARG, USP_ERR_CUDA. */
+usp_status usp_get_field_async(usp_plan_t plan, void *out_host);
+usp_status usp_wait_field(usp_plan_t plan);
+
 /* Copy the current iterate x_k into `out` ([z][y][x], desc.dtype). */
 usp_status usp_get_field(usp_plan_t plan, void *out, usp_where where);
 

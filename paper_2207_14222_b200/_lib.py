@@ -66,6 +66,8 @@ SIGNATURES = {
     "usp_staging_size": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
     "usp_plan_set_staging": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "usp_stage_inputs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "usp_get_field_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "usp_wait_field": (ctypes.c_int, [ctypes.c_void_p]),
     "usp_profile_enable": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "usp_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),

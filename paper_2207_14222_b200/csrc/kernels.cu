@@ -467,6 +467,21 @@ __global__ void k_finish(IterState *st, const double *sums, int P, int src_epi, 
 
 __global__ void k_set_form(IterState *st, int form) { st->form = form; }
 
+// Byte copy by the SMs (16-byte vectors when both ends allow): device-to-device
+// and device-to-mapped-host copies that must not queue behind bulk transfers
+// on the copy engines (asynchronous staging / read-back, usp_stage_inputs).
+__global__ void k_copy_bytes(char *dst, const char *src, size_t n) {
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        const size_t n16 = n / 16;
+        for (size_t i = tid; i < n16; i += nt)
+            reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+        for (size_t i = n16 * 16 + tid; i < n; i += nt) dst[i] = src[i];
+    } else {
+        for (size_t i = tid; i < n; i += nt) dst[i] = src[i];
+    }
+}
+
 __global__ void k_set_state(IterState *st, double alpha, double tol, long long kmax) {
     st->alpha = alpha;
     st->tol = tol;
@@ -569,6 +584,14 @@ cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s) {
 
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s) {
     k_finish<<<1, 1, 0, s>>>(st, sums, P, src_epi, red);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy_bytes(void *dst, const void *src, size_t n, int grid, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const size_t need = (n + 16 * 256 - 1) / (16 * 256);
+    const int g = (int)(need < (size_t)grid ? (need ? need : 1) : grid);
+    k_copy_bytes<<<g, 256, 0, s>>>(static_cast<char *>(dst), static_cast<const char *>(src), n);
     return cudaGetLastError();
 }
 

@@ -140,6 +140,8 @@ struct Timed {
 
 }  // namespace
 
+constexpr size_t kHostMapBytes = 64 * 1024;   // mapped pinned scratch for small read-backs
+
 struct usp_plan_s {
     usp_plan_desc d{};
     int ndim = 0;
@@ -204,13 +206,16 @@ struct usp_plan_s {
     // USP_LEAN=0, general body, Delta-form body) and whether the sparse
     // source lines are added after a pass
     bool lean_ok = true, expect_x = false;
+    // mapped pinned scratch for small read-backs (see readback) and the
+    // device view of st_host
+    void *hmap = nullptr, *hmap_dev = nullptr, *st_host_dev = nullptr;
     // asynchronous input staging (usp_stage_inputs): caller-owned area, copy
     // stream, "copies done" and "staging area consumed" events
     char *stg = nullptr;
     size_t stg_bytes = 0;
-    cudaStream_t cstream = nullptr;
-    cudaEvent_t ev_staged = nullptr, ev_consumed = nullptr;
-    bool staged = false, consumed_recorded = false;
+    cudaStream_t cstream = nullptr, dstream = nullptr;   // H2D staging, D2H results
+    cudaEvent_t ev_staged = nullptr, ev_consumed = nullptr, ev_snap = nullptr, ev_out = nullptr;
+    bool staged = false, consumed_recorded = false, out_pending = false;
     double r_sw = 1e-2;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -438,16 +443,27 @@ void mec_small(const std::vector<P2> &pts, P2 &c, double &r) {
     }
 }
 
+// Small device -> host read-backs through mapped pinned memory, copied by
+// an SM kernel on the plan stream: they never wait behind bulk transfers on
+// the copy engines (usp_stage_inputs / usp_get_field_async).
+usp_status readback(usp_plan_s *p, void *host, const void *dev, size_t bytes) {
+    if (bytes > kHostMapBytes) return fail(USP_ERR_ARG, "read-back of %zu bytes exceeds the mapped scratch", bytes);
+    CU(launch_copy_bytes(p->hmap_dev, dev, bytes, 4, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    std::memcpy(host, p->hmap, bytes);
+    return USP_OK;
+}
+
 usp_status read_point(usp_plan_s *p, const void *medium_dev, long long idx, P2 &out) {
     if (p->d.dtype == USP_R32) {
         float v = 0.f;
-        CU(cudaMemcpyAsync(&v, (const float *)medium_dev + idx, sizeof(float), cudaMemcpyDeviceToHost, p->stream));
-        CU(cudaStreamSynchronize(p->stream));
+        usp_status s = readback(p, &v, (const float *)medium_dev + idx, sizeof(float));
+        if (s) return s;
         out = {v, 0.0};
     } else {
         float2 v{};
-        CU(cudaMemcpyAsync(&v, (const float2 *)medium_dev + idx, sizeof(float2), cudaMemcpyDeviceToHost, p->stream));
-        CU(cudaStreamSynchronize(p->stream));
+        usp_status s = readback(p, &v, (const float2 *)medium_dev + idx, sizeof(float2));
+        if (s) return s;
         out = {v.x, v.y};
     }
     return USP_OK;
@@ -482,9 +498,8 @@ usp_status device_mec(usp_plan_s *p, const void *medium_dev, P2 &centre, double 
             Tick t(p, KC_FARTHEST);
             CU(launch_farthest(fp, grid, p->stream));
         }
-        CU(cudaMemcpyAsync(bd.data(), p->far_d, sizeof(double) * grid, cudaMemcpyDeviceToHost, p->stream));
-        CU(cudaMemcpyAsync(bi.data(), p->far_i, sizeof(long long) * grid, cudaMemcpyDeviceToHost, p->stream));
-        CU(cudaStreamSynchronize(p->stream));
+        if ((s = readback(p, bd.data(), p->far_d, sizeof(double) * grid))) return s;
+        if ((s = readback(p, bi.data(), p->far_i, sizeof(long long) * grid))) return s;
         int b = 0;
         for (int i = 1; i < grid; ++i)
             if (bd[i] > bd[b] || (bd[i] == bd[b] && bi[i] < bi[b])) b = i;
@@ -506,8 +521,8 @@ usp_status device_mec(usp_plan_s *p, const void *medium_dev, P2 &centre, double 
 }
 
 usp_status stage(usp_plan_s *p, void *dst, const void *src, size_t bytes, usp_where where) {
-    CU(cudaMemcpyAsync(dst, src, bytes, where == USP_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                       p->stream));
+    if (where == USP_HOST) CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
+    else CU(launch_copy_bytes(dst, src, bytes, 4 * p->nsm, p->stream));   // SMs, not a copy engine
     return USP_OK;
 }
 
@@ -994,7 +1009,8 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp);
 usp_status probe_xform(usp_plan_s *p);
 
 usp_status sync_state(usp_plan_s *p) {
-    CU(cudaMemcpyAsync(p->st_host, p->st, sizeof(IterState), cudaMemcpyDeviceToHost, p->stream));
+    // (st_host is mapped pinned memory: an SM copy, see readback)
+    CU(launch_copy_bytes(p->st_host_dev, p->st, sizeof(IterState), 1, p->stream));
     CU(cudaStreamSynchronize(p->stream));
     if (p->st_host->err)
         return fail(USP_ERR_CUDA, "pipeline watchdog: a kernel gave up waiting (code %d, unit %d)",
@@ -1245,7 +1261,10 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         const char *ln = std::getenv("USP_LEAN");
         p->lean_ok = !(ln && ln[0] == '0');
     }
-    TRY(cudaMallocHost(&p->st_host, sizeof(IterState)));
+    TRY(cudaHostAlloc(&p->st_host, sizeof(IterState), cudaHostAllocMapped));
+    TRY(cudaHostGetDevicePointer(&p->st_host_dev, p->st_host, 0));
+    TRY(cudaHostAlloc(&p->hmap, kHostMapBytes, cudaHostAllocMapped));
+    TRY(cudaHostGetDevicePointer(&p->hmap_dev, p->hmap, 0));
     if (p->real) {   // M-point four-step table for x, plus W_nx^k for the split/merge steps
         const int n = (int)p->nx, m = n / 2;
         std::vector<float2> tr(m);
@@ -1417,8 +1436,7 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
         NC(nccl().AllReduce(p->red_u + 1, p->red_u + 1, 2, ncclUint32, ncclSum, p->comm, p->stream));
     }
     unsigned red[4];
-    CU(cudaMemcpyAsync(red, p->red_u, sizeof red, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if ((s = readback(p, red, p->red_u, sizeof red))) return s;
     float vmax;
     std::memcpy(&vmax, &red[0], sizeof vmax);
     p->vmax = vmax;
@@ -1616,8 +1634,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
             const long long nlines = p->ny * p->nzh;
             unsigned cnt = 0;
             CU(launch_sparse_count(p->s_flag, nlines, p->s_ctr, p->stream));
-            CU(cudaMemcpyAsync(&cnt, p->s_ctr, sizeof cnt, cudaMemcpyDeviceToHost, p->stream));
-            CU(cudaStreamSynchronize(p->stream));
+            if ((s = readback(p, &cnt, p->s_ctr, sizeof cnt))) return s;
             // the list (2 KiB) and the lines must fit in the s field
             const long long cap = std::min<long long>(kSparseMaxLines, ((long long)p->nloc - 256) / p->nx);
             if (cnt > 0 && (long long)cnt <= cap) {
@@ -1794,7 +1811,7 @@ usp_status usp_residual_history(usp_plan_t p, double *host, int64_t cap, int64_t
 
 usp_status usp_staging_size(usp_plan_t p, size_t *bytes) {
     if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
-    *bytes = 2 * align256((size_t)p->nloc * elem_bytes(p));
+    *bytes = 3 * align256((size_t)p->nloc * elem_bytes(p));   // medium, source, result
     return USP_OK;
 }
 
@@ -1807,10 +1824,15 @@ usp_status usp_plan_set_staging(usp_plan_t p, void *dev, size_t bytes) {
     if (p->tdiff) return fail(USP_ERR_UNSUPPORTED, "tensor-diffusion plans do not stage inputs");
     if (!p->cstream) {
         CU(cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&p->dstream, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&p->ev_staged, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&p->ev_consumed, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&p->ev_snap, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
     }
     CU(cudaStreamSynchronize(p->cstream));
+    CU(cudaStreamSynchronize(p->dstream));
+    p->out_pending = false;
     p->stg = (char *)dev;
     p->stg_bytes = bytes;
     p->staged = false;
@@ -1826,6 +1848,31 @@ usp_status usp_stage_inputs(usp_plan_t p, const void *medium, const void *source
     CU(cudaMemcpyAsync(p->stg + align256(nb), source, nb, cudaMemcpyHostToDevice, p->cstream));
     CU(cudaEventRecord(p->ev_staged, p->cstream));
     p->staged = true;
+    return USP_OK;
+}
+
+usp_status usp_get_field_async(usp_plan_t p, void *out) {
+    if (!p || !out) return fail(USP_ERR_ARG, "NULL argument");
+    if (!p->stg) return fail(USP_ERR_STATE, "usp_plan_set_staging must be called first");
+    if (!p->have_source) return fail(USP_ERR_STATE, "no source");
+    if (p->tdiff || (p->d.dtype != USP_C64 && !p->real))
+        return fail(USP_ERR_UNSUPPORTED, "asynchronous read-back of this field layout");
+    const size_t nb = (size_t)p->nloc * elem_bytes(p);
+    char *res = p->stg + 2 * align256(nb);
+    // the previous read-back must have left the result slot
+    if (p->out_pending) CU(cudaStreamWaitEvent(p->stream, p->ev_out, 0));
+    CU(launch_copy_bytes(res, p->x, nb, 4 * p->nsm, p->stream));   // SMs, not a copy engine
+    CU(cudaEventRecord(p->ev_snap, p->stream));
+    CU(cudaStreamWaitEvent(p->dstream, p->ev_snap, 0));
+    CU(cudaMemcpyAsync(out, res, nb, cudaMemcpyDeviceToHost, p->dstream));
+    CU(cudaEventRecord(p->ev_out, p->dstream));
+    p->out_pending = true;
+    return USP_OK;
+}
+
+usp_status usp_wait_field(usp_plan_t p) {
+    if (!p) return fail(USP_ERR_ARG, "NULL plan");
+    if (p->out_pending) CU(cudaEventSynchronize(p->ev_out));
     return USP_OK;
 }
 
@@ -2272,9 +2319,13 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->hist);
     if (p->cstream) {
         cudaStreamSynchronize(p->cstream);
+        cudaStreamSynchronize(p->dstream);
         cudaStreamDestroy(p->cstream);
+        cudaStreamDestroy(p->dstream);
         cudaEventDestroy(p->ev_staged);
         cudaEventDestroy(p->ev_consumed);
+        cudaEventDestroy(p->ev_snap);
+        cudaEventDestroy(p->ev_out);
     }
     cudaFree(p->red_u);
     if (p->s_flag) cudaFree(p->s_flag);
@@ -2289,6 +2340,7 @@ void usp_plan_destroy(usp_plan_t p) {
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
     cudaFree(p->twr);
     cudaFreeHost(p->st_host);
+    if (p->hmap) cudaFreeHost(p->hmap);
     delete p;
 }
 

@@ -296,6 +296,7 @@ cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s);
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
 cudaError_t launch_set_form(IterState *st, int form, cudaStream_t s);
+cudaError_t launch_copy_bytes(void *dst, const void *src, size_t n, int grid, cudaStream_t s);
 cudaError_t launch_sparse_count(const unsigned char *flag, long long nlines, unsigned *count, cudaStream_t s);
 cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, int n, int *list,
                                  float2 *comp, unsigned *count, cudaStream_t s);

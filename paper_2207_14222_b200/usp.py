@@ -118,6 +118,15 @@ class Plan:
         stream; returns at once.  Then call set_potential("staged") and
         set_source("staged").  The host buffers must stay untouched until
         set_source("staged") has returned."""
+        self._ensure_staging()
+        pm, wm, km = _ptr_where(medium, self.dtype)
+        ps, ws, ks = _ptr_where(source, self.dtype)
+        if wm != L.HOST or ws != L.HOST:
+            raise ValueError("stage_inputs takes host buffers")
+        self._staged_keep = (km, ks)   # the copies read them asynchronously
+        L.check(self.lib.usp_stage_inputs(self.handle, pm, ps))
+
+    def _ensure_staging(self):
         if getattr(self, "staging", None) is None:
             import torch
 
@@ -126,12 +135,20 @@ class Plan:
             self.staging = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
             L.check(self.lib.usp_plan_set_staging(self.handle, ctypes.c_void_p(self.staging.data_ptr()),
                                                   int(nbytes.value)))
-        pm, wm, km = _ptr_where(medium, self.dtype)
-        ps, ws, ks = _ptr_where(source, self.dtype)
-        if wm != L.HOST or ws != L.HOST:
-            raise ValueError("stage_inputs takes host buffers")
-        self._staged_keep = (km, ks)   # the copies read them asynchronously
-        L.check(self.lib.usp_stage_inputs(self.handle, pm, ps))
+
+    def get_field_async(self, out):
+        """usp_get_field_async: start copying x_k into the host array `out`
+        (pinned for full speed) on the plan's read-back stream; call
+        wait_field() before reading `out`."""
+        self._ensure_staging()
+        ptr, where, keep = _ptr_where(out, self.dtype)
+        if where != L.HOST:
+            raise ValueError("get_field_async writes host memory")
+        self._out_keep = keep
+        L.check(self.lib.usp_get_field_async(self.handle, ptr))
+
+    def wait_field(self):
+        L.check(self.lib.usp_wait_field(self.handle))
 
     def set_potential(self, medium, target_norm: float = 0.95):
         if isinstance(medium, str) and medium == "staged":

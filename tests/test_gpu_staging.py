@@ -39,3 +39,16 @@ def test_staged_inputs_pipeline():
     assert np.array_equal(x1, ref1) and np.array_equal(x2, ref2)
     with pytest.raises(USPError):
         plan.set_source("staged")                    # consumed
+    # asynchronous read-back: the field lands after wait_field, even when the
+    # plan stream moves on to the next problem right away
+    out = torch.empty(plan.local_shape, dtype=torch.complex64).pin_memory()
+    plan.get_field_async(out)
+    plan.stage_inputs(hm, hs1)
+    plan.set_potential("staged")
+    plan.set_source("staged")
+    plan.iterate(25, p.alpha, 0.0)
+    plan.wait_field()
+    assert np.array_equal(out.numpy().astype(np.complex128), ref2)
+    plan.get_field_async(out)
+    plan.wait_field()
+    assert np.array_equal(out.numpy().astype(np.complex128), ref1)
