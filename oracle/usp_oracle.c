@@ -119,7 +119,12 @@ int orc_fft1d(double *data, long n, int inverse) {
 
 /* n-D DFT of a C-ordered array (dims[ndim-1] contiguous): a 1-D DFT along
  * each axis in turn.  Lines are independent, so they are spread over OpenMP
- * threads; each thread gathers a line into its own scratch buffer. */
+ * threads.  Each thread copies a group of up to ORC_GROUP lines that are
+ * adjacent in memory (neighbouring columns of a strided axis) into its own
+ * scratch buffer, transforms each line on its own with fft1d_with_table, and
+ * copies them back: the per-line arithmetic is the plain DFT above, the
+ * grouping only makes the strided copies use whole cache lines. */
+#define ORC_GROUP 8
 int orc_fftn(double *data, int ndim, const long *dims, int inverse) {
     if (ndim < 1 || ndim > 3) return -2;
     long total = 1;
@@ -134,26 +139,29 @@ int orc_fftn(double *data, int ndim, const long *dims, int inverse) {
         long stride = 1;
         for (int b = a + 1; b < ndim; ++b) stride *= dims[b];
         long outer = total / (n * stride);
-        long nlines = outer * stride;
+        long grp = stride < ORC_GROUP ? stride : ORC_GROUP;   /* stride, ORC_GROUP: powers of 2 */
+        long ngroups = outer * (stride / grp);
         cplx *tw = make_twiddles(n);
         if (!tw) return -3;
         int err = 0;
 #pragma omp parallel
         {
-            cplx *line = (cplx *)malloc(sizeof(cplx) * (size_t)n);
-            if (!line) {
+            cplx *lines = (cplx *)malloc(sizeof(cplx) * (size_t)(n * grp));
+            if (!lines) {
 #pragma omp atomic write
                 err = 1;
             } else {
 #pragma omp for schedule(static)
-                for (long l = 0; l < nlines; ++l) {
-                    long o = l / stride, i = l % stride;
-                    cplx *base = x + o * n * stride + i;
-                    for (long t = 0; t < n; ++t) line[t] = base[t * stride];
-                    fft1d_with_table(line, n, tw, inverse);
-                    for (long t = 0; t < n; ++t) base[t * stride] = line[t];
+                for (long gi = 0; gi < ngroups; ++gi) {
+                    long o = gi / (stride / grp), i0 = (gi % (stride / grp)) * grp;
+                    cplx *base = x + o * n * stride + i0;
+                    for (long t = 0; t < n; ++t)
+                        for (long b = 0; b < grp; ++b) lines[b * n + t] = base[t * stride + b];
+                    for (long b = 0; b < grp; ++b) fft1d_with_table(lines + b * n, n, tw, inverse);
+                    for (long t = 0; t < n; ++t)
+                        for (long b = 0; b < grp; ++b) base[t * stride + b] = lines[b * n + t];
                 }
-                free(line);
+                free(lines);
             }
         }
         free(tw);
@@ -214,6 +222,7 @@ int orc_setup(const double *w, const double *S, long n, double sig_re, double si
               double c_re, double c_im, double *V_out, double *B_out, double *s_out) {
     cplx sigma = sig_re + I * sig_im, c = c_re + I * c_im;
     const cplx *wc = (const cplx *)w, *Sc = (const cplx *)S;
+#pragma omp parallel for schedule(static)
     for (long i = 0; i < n; ++i) {
         cplx V = (wc[i] - sigma) / c;
         if (V_out) ((cplx *)V_out)[i] = V;
@@ -269,22 +278,28 @@ int orc_fixed_point(const double *w, const double *S, int ndim, const long *dims
     memcpy(u, s, bytes);
     int rc = orc_apply_Linv((double *)u, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
     if (rc) goto done;
+#pragma omp parallel for schedule(static)
     for (long i = 0; i < n; ++i) Dl[i] = B[i] * u[i];
     double n0 = norm2(Dl, n);
     if (n0_out) *n0_out = n0;
+#pragma omp parallel for schedule(static)
     for (long i = 0; i < n; ++i) x[i] = 0.0;
     *n_done = 0;
     if (n0 == 0.0) goto done;   /* zero source: x = 0 is exact */
 
     for (long k = 0; k < n_max; ++k) {
         if (form == 0) {
+#pragma omp parallel for schedule(static)
             for (long i = 0; i < n; ++i) u[i] = B[i] * x[i] + s[i];
             rc = orc_apply_Linv((double *)u, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
             if (rc) goto done;
+#pragma omp parallel for schedule(static)
             for (long i = 0; i < n; ++i) Dl[i] = B[i] * (u[i] - x[i]);
+#pragma omp parallel for schedule(static)
             for (long i = 0; i < n; ++i) x[i] = x[i] + alpha * Dl[i];
         } else {
             /* Dl holds Delta_k here */
+#pragma omp parallel for schedule(static)
             for (long i = 0; i < n; ++i) x[i] = x[i] + alpha * Dl[i];
         }
         double r = norm2(Dl, n) / n0;
@@ -293,9 +308,11 @@ int orc_fixed_point(const double *w, const double *S, int ndim, const long *dims
         if (!isfinite(r)) { rc = 1; goto done; }
         if (tol > 0.0 && r < tol) break;
         if (form == 1 && k + 1 < n_max) {
+#pragma omp parallel for schedule(static)
             for (long i = 0; i < n; ++i) u[i] = B[i] * Dl[i];
             rc = orc_apply_Linv((double *)u, ndim, dims, h, D, sig_re, sig_im, c_re, c_im);
             if (rc) goto done;
+#pragma omp parallel for schedule(static)
             for (long i = 0; i < n; ++i) Dl[i] = Dl[i] + alpha * B[i] * (u[i] - Dl[i]);
         }
     }

@@ -47,7 +47,8 @@ def _homog(shape, k0=2 * math.pi / 8, n=1.0 + 0.05j):
 
 SHAPES = [(16,), (64,), (256,), (1024,), (2048,), (16, 16), (32, 512), (512, 64), (1024, 16), (16, 2048),
           (2048, 16), (16, 32, 64), (64, 16, 128), (32, 256, 16), (16, 16, 1024), (128, 128, 128),
-          (2048, 16, 16), (16, 2048, 16), (16, 16, 2048), (32, 64, 32), (64, 32, 64)]
+          (2048, 16, 16), (16, 2048, 16), (16, 16, 2048), (32, 64, 32), (64, 32, 64), (512, 512, 64),
+          (512, 64, 512)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
