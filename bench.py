@@ -61,15 +61,6 @@ ITER_BYTES_REAL_XFORM = 48
 # does not read s at all -- reads work, x, B, writes x, work
 XFORM_XPASS_BYTES_SPARSE = 40
 ITER_BYTES_3D_XFORM_SPARSE = 88
-# Chunked schedule (1 GPU, 3-D): per z-chunk K_D -> K_A -> K_B
-# with the chunk's work array L2-resident in between, so HBM sees only
-KERNEL_BYTES_CHUNKED = {
-    "xpass": 40,            # read Delta, x, B; write Delta, x (work read/written in L2)
-    "y_fwd": 8,             # write work (read from L2)
-    "z_fwd_mul_inv": 16,
-    "y_inv": 8,             # read work (written to L2)
-}
-ITER_BYTES_CHUNKED = 72
 # Real path (C4 diffusion, float32 fields, half spectra; SURVEY.md §8 geometry
 # table): x pass reads x, Delta, B (4 B each) + half spectrum (4) and writes
 # x, Delta (4 each) + half spectrum (4); each strided pass moves the half
@@ -280,7 +271,7 @@ def solver_comparison(dev, name="C3", tol=1e-6):
     return out
 
 
-def slab_selfcheck(comm, world, rank, dev, n_iter=8, shape=(128, 128, 128)):
+def slab_selfcheck(comm, world, rank, dev, separate, n_iter=8, shape=(128, 128, 128)):
     """Constant V through the decomposed path: x^_k = x^*(1 - q^k) per
     Fourier mode (the closed form of tests/test_gpu_parity.py).  Returns the
     relative L2 error (all ranks)."""
@@ -294,7 +285,7 @@ def slab_selfcheck(comm, world, rank, dev, n_iter=8, shape=(128, 128, 128)):
     S = np.zeros(shape, dtype=np.complex64)
     S[tuple(s // 3 for s in shape)] = 1.0
     S[tuple(s // 5 for s in shape)] = 0.5 - 0.25j
-    plan = Plan(shape, sigma=sigma, c=c, comm=comm, device=dev)
+    plan = Plan(shape, sigma=sigma, c=c, comm=comm, device=dev, separate_transposes=separate)
     z0, nzl = plan.z0, plan.local_shape[0]
     plan.set_potential(torch.full(plan.local_shape, k2, dtype=torch.complex64, device=dev), -1.0)
     plan.set_source(torch.from_numpy(np.ascontiguousarray(S[z0:z0 + nzl])).to(dev))
@@ -330,18 +321,19 @@ def run_usp(args, world, rank, local):
     # multi-GPU: z-slabs over the ranks (strong scaling) unless the check fails
     comm, slab_check, mode = None, None, ("1 GPU" if world == 1 else "replicas")
     transposes = None
+    separate = args.separate_transposes
     if world > 1 and not args.replicas:
         from paper_2207_14222_b200 import comm_init
 
         comm = comm_init()
         # fused peer-store transposes first; if their closed-form check fails,
         # the NCCL all-to-all transposes; if that fails too, replicas
-        for fused in ("1", "0"):
-            os.environ["USP_FUSED"] = fused
-            slab_check = slab_selfcheck(comm, world, rank, dev)
+        for sep in ((True,) if separate else (False, True)):
+            slab_check = slab_selfcheck(comm, world, rank, dev, sep)
             if slab_check <= 1e-4:
                 mode = "slabs"
-                transposes = "fused peer-memory stores" if fused == "1" else "NCCL all-to-all"
+                separate = sep
+                transposes = "NCCL all-to-all" if sep else "fused peer-memory stores"
                 break
         if mode != "slabs":
             comm.close()
@@ -357,7 +349,8 @@ def run_usp(args, world, rank, local):
     esz = 4 if real else 8
     with torch.cuda.stream(stream):
         plan = Plan(shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev, comm=comm,
-                    dtype="r32" if real else "c64", virtual_ranks=args.virtual_ranks if mode == "virtual" else 0)
+                    dtype="r32" if real else "c64", virtual_ranks=args.virtual_ranks if mode == "virtual" else 0,
+                    separate_transposes=separate)
     z0, nzl = plan.z0, plan.local_shape[0]
     if real:
         med = p.medium[z0:z0 + nzl].real.to(fdt).contiguous()
@@ -414,13 +407,11 @@ def run_usp(args, world, rank, local):
     value = units * n_iter * args.steps / (ms_max / 1e3)
 
     # dominant kernel roofline: its algorithmic HBM bytes per iteration over
-    # its device time per iteration (x-pass launches are iterations only; the
-    # chunked schedule launches it once per z-chunk)
+    # its device time per iteration
     hbm, peak_kind = peaks()
     n_it_total = n_iter * args.steps
-    chunks = max(1, prof.get("xpass", (0, n_it_total))[1] // n_it_total)
-    schedule = "chunked" if chunks > 1 else "4-pass"
-    kbytes = dict(KERNEL_BYTES_REAL if real else (KERNEL_BYTES_CHUNKED if chunks > 1 else KERNEL_BYTES))
+    schedule = "4-pass"
+    kbytes = dict(KERNEL_BYTES_REAL if real else KERNEL_BYTES)
     # which algebraic form ran: every timed step starts from set_source (x-form
     # on x-form plans) and ends still in the x-form unless r fell below r_switch
     xform_plan, xform_now, r_switch = plan.iteration_form()
@@ -444,7 +435,7 @@ def run_usp(args, world, rank, local):
     dname = "xpass" if "xpass" in prof else max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
     dms, dcount = prof[dname]
     d_ms_per_iter = dms / n_it_total
-    dbytes = int(kbytes[dname] * nloc)              # per iteration (= per launch x chunks)
+    dbytes = int(kbytes[dname] * nloc)              # per iteration (= per launch)
     # algorithmic bytes of the iterations over the kernel's total time (x-form
     # plans add one launch per iterate call that skips itself: time only)
     achieved = dbytes / (d_ms_per_iter / 1e3) / 1e9
@@ -529,7 +520,7 @@ def run_usp(args, world, rank, local):
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
     # separate transposes (NCCL all-to-all / device copies) add their staging
     # reads and writes; the fused (peer-store) transposes add nothing to HBM
-    base_bpv = ITER_BYTES_REAL if real else (ITER_BYTES_CHUNKED if chunks > 1 else ITER_BYTES_3D)
+    base_bpv = ITER_BYTES_REAL if real else ITER_BYTES_3D
     xform_bpv = ITER_BYTES_REAL_XFORM if real else (ITER_BYTES_3D_XFORM_SPARSE if sparse_lines else ITER_BYTES_3D_XFORM)
     iter_bpv = fx * xform_bpv + (1 - fx) * base_bpv + \
         ((16 if real else 32) if "all_to_all" in prof else 0)
@@ -537,7 +528,7 @@ def run_usp(args, world, rank, local):
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
                    "slabs": f"{world} z-slabs, transposes: {transposes} (self-check first)",
                    "virtual": f"1 GPU, {args.virtual_ranks} virtual z-slabs ("
-                              + ("separate transposes" if os.environ.get("USP_FUSED") == "0" else
+                              + ("separate transposes" if separate else
                                  "transposes fused into the K_B / K_C stores") + ")"}[mode]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -584,6 +575,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
     ap.add_argument("--no-solvers", action="store_true", help="skip the C3 fixed-point vs BiCGSTAB comparison")
+    ap.add_argument("--separate-transposes", action="store_true",
+                    help="slab decomposition: NCCL all-to-all transposes instead of the fused peer stores")
     ap.add_argument("--virtual-ranks", type=int, default=0,
                     help="N=1: run the slab-decomposed path with this many virtual slabs (measurement)")
     args = ap.parse_args()

@@ -12,8 +12,10 @@
  *
  * with B = 1 - V (L73), (L+1)^-1 applied as a Fourier multiplier (Eq. 12,
  * L168-172) by hand-written sm_100a FFT kernels (no cuFFT), in complex64.
- * Internally the mathematically identical Delta-recurrence of L613 is used
- * (reading R-17):  Delta_{k+1} = Delta_k + alpha B[(L+1)^-1(B Delta_k) - Delta_k].
+ * The plan runs this literal form while r_k >= r_switch and then the
+ * mathematically identical Delta-recurrence of L613 (readings R-17,
+ * R-30), which keeps fp32 accurate near convergence:
+ *     Delta_{k+1} = Delta_k + alpha B[(L+1)^-1(B Delta_k) - Delta_k].
  *
  * Problem form (reading R-1, §2.2):
  *     A_raw = -D lap + w(r),   L_raw = -D lap + sigma,   V_raw = w - sigma,
@@ -52,7 +54,7 @@ extern "C" {
 #endif
 
 #define USP_VERSION_MAJOR 0
-#define USP_VERSION_MINOR 2
+#define USP_VERSION_MINOR 3
 
 typedef struct usp_plan_s *usp_plan_t;
 
@@ -119,7 +121,35 @@ typedef struct {
                             usp_set_tensor_medium (mu_a and D); dtype must be USP_R32
                             (real mu_a, D, S; get_field returns u); 2-D / 3-D, extents in
                             [64, 1024], one GPU.                                             */
+    /* Options.  Zero (a zero-initialised desc) selects the default behaviour
+     * everywhere; no environment variable changes what a plan computes.      */
+    int delta_form;       /* != 0: run the Delta-form recurrence of PAPER.md L613 from the
+                             first iteration.  0: Algorithm 1 literally (x-form, L85-86,
+                             8 fewer HBM bytes per voxel; s = S/c kept in the workspace)
+                             while r_k >= r_switch, then the Delta-form (R-30).
+                             The two are the same iteration in exact arithmetic.        */
+    double r_switch;      /* x-form -> Delta-form threshold on r_k (0: 1e-2)                */
+    int dense_source;     /* != 0: the x-form passes always read s densely.  0: when the
+                             source lives on <= 64 x-lines, their x-transforms are added
+                             after each x pass instead (R-31, exact up to fp32
+                             rounding order).                                            */
+    int separate_transposes; /* slab decomposition: != 0 selects NCCL all-to-all transposes
+                             (device copies in virtual mode); 0: transposes fused into the
+                             K_B / K_C stores over peer memory when every rank maps its
+                             peers (else the all-to-alls, decided collectively).       */
+    int complex_path;     /* != 0: float32 diffusion data on the complex64 path (widened on
+                             the device); 0: the half-spectrum real path where supported
+                             (3-D, medium USP_MEDIUM_W, R-26).                 */
+    int launch_per_pass;  /* != 0: 2-D grids up to 512^2 launch one kernel per pass and
+                             iteration; 0: one persistent cooperative launch per iterate
+                             call (kernels_small.cu).                                    */
+    int test_hooks;       /* bit 0 (USP_HOOK_RANK_FINISH): on a one-rank communicator, reduce
+                             the residual through the rank-ordered all-gather + k_finish
+                             path of P > 1 plans (a test of that path on one GPU).  0 in
+                             production.                                                  */
 } usp_plan_desc;
+
+#define USP_HOOK_RANK_FINISH 1
 
 /* Create a plan for the grid and problem described by *desc (copied).
  *
@@ -133,7 +163,7 @@ typedef struct {
  * rank that needs it: CUDA-IPC-mapped peer memory over NVLink, mapped at
  * usp_plan_set_workspace, which is then collective), with a cross-rank
  * barrier after each; if any rank cannot map its peers (or P > 8, or
- * USP_FUSED=0) NCCL all-to-alls are used instead.  With nccl_comm, the arrays passed to
+ * desc.separate_transposes) NCCL all-to-alls are used instead.  With nccl_comm, the arrays passed to
  * set_potential / set_source / get_field are the rank's slab
  * [nz/P][ny][nx] (usp_local_extent gives z0); every call is collective.
  * Requires P a power of two dividing ny and nz, ny and nz in [64, 2048].
@@ -216,29 +246,42 @@ usp_status usp_residual(usp_plan_t plan, double *rel, double *abs_norm, int64_t 
 usp_status usp_residual_history(usp_plan_t plan, double *host, int64_t cap, int64_t *n);
 
 /* Asynchronous input staging (pipelining a sequence of problems).
- * usp_staging_size: bytes of the caller-owned staging workspace (room for one
- * medium and one source of this plan, 256-byte aligned); usp_plan_set_staging
- * hands it over (it must outlive the plan).  usp_stage_inputs copies a medium
- * and a source from host memory (pinned for full speed; layouts and dtypes as
- * usp_set_potential / usp_set_source) into it on an internal copy stream and
- * returns at once, so the copies overlap whatever the plan stream is running
- * (e.g. the iterations of the previous problem).  The next usp_set_potential
- * and usp_set_source called with where = USP_STAGED (pointer argument
- * ignored, may be NULL) make the plan stream wait for those copies and use
- * them; the staging area is reused only after that set_source has consumed
- * it.  Not for tensor-diffusion plans.  Errors: USP_ERR_STATE (no staging
- * workspace / nothing staged), USP_ERR_ARG, USP_ERR_CUDA. */
-usp_status usp_staging_size(usp_plan_t plan, size_t *bytes);
+ * usp_staging_size: bytes of the caller-owned staging workspace: one medium
+ * and one source of this plan (with_readback = 0), or those plus one field
+ * for usp_get_field_async (with_readback != 0); each slot 256-byte aligned.
+ * usp_plan_set_staging hands it over (it must outlive the plan; a staging
+ * area of the smaller size supports usp_stage_inputs only).
+ * usp_stage_inputs copies a medium and a source from host memory (pinned for
+ * full speed; layouts and dtypes as usp_set_potential / usp_set_source) into
+ * it on an internal copy stream and returns at once, so the copies overlap
+ * whatever the plan stream is running (e.g. the iterations of the previous
+ * problem).  The next usp_set_potential and usp_set_source called with
+ * where = USP_STAGED (pointer argument ignored, may be NULL) make the plan
+ * stream wait for those copies and use them.  Each slot is refilled only
+ * after the plan stream has consumed it, and usp_stage_inputs refuses
+ * (USP_ERR_STATE) while a staged medium has been taken by set_potential but
+ * its source not yet by set_source, so a medium is never paired with the
+ * next problem's source.  The host buffers must stay untouched until the
+ * set_source(USP_STAGED) that consumes them has returned.  Not for
+ * tensor-diffusion plans.  Errors: USP_ERR_STATE (no staging workspace /
+ * nothing staged / source of the previous medium not consumed), USP_ERR_ARG,
+ * USP_ERR_NOMEM (area too small), USP_ERR_UNSUPPORTED (tensor diffusion),
+ * USP_ERR_CUDA. */
+usp_status usp_staging_size(usp_plan_t plan, int with_readback, size_t *bytes);
 usp_status usp_plan_set_staging(usp_plan_t plan, void *dev, size_t bytes);
 usp_status usp_stage_inputs(usp_plan_t plan, const void *medium_host, const void *source_host);
 
-/* Asynchronous result read-back (same staging workspace, which also holds
- * one field for this): usp_get_field_async snapshots x_k into the staging
- * area on the plan stream and copies it to host memory `out` on a second
- * copy stream, returning at once -- the copy overlaps what the plan stream
- * does next (the next problem).  usp_wait_field blocks until that copy has
- * landed; `out` must not be read before.  Errors: USP_ERR_STATE (no staging
- * workspace / no source), USP_ERR_ARG, USP_ERR_CUDA. */
+/* Asynchronous result read-back (the staging workspace's third slot, see
+ * usp_staging_size with with_readback != 0): usp_get_field_async snapshots
+ * x_k into that slot on the plan stream and copies it to host memory `out`
+ * (nz_local * ny * nx elements of desc.dtype) on a second copy stream,
+ * returning at once -- the copy overlaps what the plan stream does next (the
+ * next problem).  usp_wait_field blocks until that copy has landed; `out`
+ * must not be read, and must stay allocated, before.  Errors: USP_ERR_STATE
+ * (no staging workspace / no source), USP_ERR_NOMEM (staging area sized
+ * without the read-back slot), USP_ERR_UNSUPPORTED (tensor-diffusion plans;
+ * float32 fields on the complex path, desc.complex_path), USP_ERR_ARG,
+ * USP_ERR_CUDA. */
 usp_status usp_get_field_async(usp_plan_t plan, void *out_host);
 usp_status usp_wait_field(usp_plan_t plan);
 
@@ -295,12 +338,13 @@ usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
 /* Algebraic form of the iteration (reading R-30).  xform = 1: the
  * plan runs Algorithm 1 literally (x-form: 8 fewer HBM bytes per
  * voxel and iteration; s = S/c kept in the workspace) while the last
- * residual is >= r_switch (default 1e-2, env USP_XSWITCH; USP_XFORM=0 at
- * plan creation disables), then the Delta-form recurrence (exact
+ * residual is >= r_switch (desc.r_switch, default 1e-2; desc.delta_form
+ * disables), then the Delta-form recurrence (exact
  * down to fp32 rounding near convergence).  form: 0 = Delta-form now,
  * 1 = x-form now.  source_lines > 0: the source lives on that many x-lines
  * (<= 64) and the x-form passes never read s (reading R-31: the x-transformed
- * source lines are added after each x pass); 0: s is read densely.  After
+ * source lines are added after each x pass); 0: s is read densely
+ * (desc.dense_source, or a source on more lines).  After
  * x-form iterations, r_k and Delta_k of the current
  * x_k are computed on demand by usp_residual / usp_residual_history (one
  * probe pass: x unchanged); those two calls are therefore collective over

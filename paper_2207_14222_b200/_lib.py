@@ -31,7 +31,12 @@ class PlanDesc(ctypes.Structure):
                 ("medium", ctypes.c_int), ("dtype", ctypes.c_int), ("D", ctypes.c_double),
                 ("sigma", c128), ("c", c128), ("stream", ctypes.c_void_p), ("nccl_comm", ctypes.c_void_p),
                 ("virtual_ranks", ctypes.c_int), ("antisymmetric", ctypes.c_int),
-                ("tensor_diffusion", ctypes.c_int)]
+                ("tensor_diffusion", ctypes.c_int), ("delta_form", ctypes.c_int), ("r_switch", ctypes.c_double),
+                ("dense_source", ctypes.c_int), ("separate_transposes", ctypes.c_int),
+                ("complex_path", ctypes.c_int), ("launch_per_pass", ctypes.c_int), ("test_hooks", ctypes.c_int)]
+
+
+HOOK_RANK_FINISH = 1
 
 
 class USPError(RuntimeError):
@@ -63,7 +68,7 @@ SIGNATURES = {
     "usp_residual_history": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int64,
                                             ctypes.POINTER(ctypes.c_int64)]),
     "usp_get_field": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
-    "usp_staging_size": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
+    "usp_staging_size": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
     "usp_plan_set_staging": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
     "usp_stage_inputs": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "usp_get_field_async": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),

@@ -4,7 +4,6 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include <cstdlib>
 
 #include "fft_core.cuh"
 #include "usp_internal.h"
@@ -12,15 +11,11 @@
 namespace usp {
 
 // Launch with programmatic stream serialization (PDL, see tma.cuh
-// pdl_trigger/pdl_wait) unless USP_PDL=0: the next kernel's launch overlaps
-// the tail of this one instead of following its completion.
+// pdl_trigger/pdl_wait): the next kernel's launch overlaps the tail of this
+// one instead of following its completion.
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, int smem, cudaStream_t s,
                               const Args &...args) {
-    static const int use = [] {
-        const char *e = std::getenv("USP_PDL");
-        return (e && e[0] == '0') ? 0 : 1;
-    }();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
@@ -30,7 +25,7 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int block, int s
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = use;
+    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -143,11 +138,7 @@ __device__ __forceinline__ void finish_xpass(bool src_epi, bool xonly, double to
     if (act == ACT_PROBE) st->form = FORM_X;
     st->add_s = (act == ACT_X || act == ACT_PROBE) ? 1 : 0;   // sparse source: k_sadd adds s
     red.hist[hi % red.hist_cap] = r;
-#ifdef USP_DIAG_NODIV   // diagnostics builds only: keep iterating through overflow (timing ablations)
-    if (false) st->status = ST_DIVERGED;
-#else
     if (!(r <= 1e6)) st->status = ST_DIVERGED;            // NaN, Inf or r > 1e6
-#endif
     // (a probe only reports r_k: the x-form pass that follows decides the stop)
     else if (st->tol > 0.0 && r < st->tol && act != ACT_PROBE)
         st->status = (act == ACT_X) ? ST_DONE_CONV : ST_STOP_PENDING;

@@ -1,153 +1,39 @@
-// kernels.cu -- sm_100a kernels of the universal-split-preconditioner hot path.
+// kernels.cu -- sm_100a kernels of the universal-split-preconditioner hot path
+// that are not pass pipelines: the register-staged strided pass for short
+// lines (N = 16, 32), the on-chip 1-D solve, the setup kernels (potential,
+// farthest point of the smallest-circle search), the rank-ordered residual
+// finish, and small state / copy kernels.
 //
-// One iteration of Algorithm 1 in the Delta-form of L613
-// (reading R-17) is a chain of FFT passes over the field:
+// One iteration of Algorithm 1 is a chain of FFT passes:
 //
-//   3-D:  K_B  y forward            (strided, k_strided<S_FWD>)
-//         K_C  z forward, x g(p), z inverse  (k_strided<S_FWD_MUL_INV>)  Eq. 12
-//         K_D  y inverse            (k_strided<S_INV>)
-//         K_A  x inverse -> epilogue -> prologue -> x forward  (k_xpass<X_ITER>)
-//   2-D:  K_Y  y forward, x g, y inverse; K_A as above.
-//   1-D:  one CTA runs the whole solve (k_solve1d).
+//   3-D:  K_B  y forward                               (k_stile<S_FWD>, kernels_stile.cu)
+//         K_C  z forward, x g(p), z inverse  (Eq. 12)  (k_stile<S_FWD_MUL_INV>)
+//         K_D  y inverse                               (k_stile<S_INV>)
+//         K_A  x inverse -> update -> prologue -> x forward   (k_xpass_pipe, kernels_pipe.cu)
+//   2-D:  one persistent cooperative kernel (kernels_small.cu), or K_Y (y forward,
+//         x g, y inverse) and K_A per pass
+//   1-D:  one CTA runs the whole solve (k_solve1d, here).
 //
-// K_A's epilogue is the update of Algorithm 1 lines 3-4 in Delta-form:
-//     y = (L+1)^-1 (B Delta_k)            (the chain that just completed)
-//     x_{k+1}     = x_k + alpha Delta_k                       (line 4)
-//     Delta_{k+1} = Delta_k + alpha B (y - Delta_k)           (L613)
-//     r_{k+1}     = ||Delta_{k+1}|| / n0                      (line 5, reading R-4)
-// and its prologue starts the next chain: u = B Delta_{k+1}, forward x-FFT.
+// K_A's update is Algorithm 1 lines 3-4 (x-form while r_k >= r_switch) or the
+// Delta-form of L613 (readings R-17, R-30):
+//     y = (L+1)^-1 u                      (the chain that just completed)
+//     x-form:  Delta_k = B (y - x_k),  x_{k+1} = x_k + alpha Delta_k,  u = B x_{k+1} + s
+//     Delta-form: x_{k+1} = x_k + alpha Delta_k,
+//              Delta_{k+1} = Delta_k + alpha B (y - Delta_k),  u = B Delta_{k+1}
+//     r = ||Delta|| / n0                  (line 5, reading R-4)
 // The residual is reduced per CTA (fp32 per line -> fp64), and the last CTA
 // to finish sums the CTA partials in a fixed order (deterministic) and
 // updates the device-side IterState (stop flag, counter, history).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <string.h>
 
 #include "fft_core.cuh"
 #include "kcommon.cuh"
 #include "usp_internal.h"
 
 namespace usp {
-
-// ================================================================ x pass ==
-template <int N>
-struct XGeo {
-    using G = LineGeo<N>;
-    static constexpr int NT = 256;
-    static constexpr int LPC = NT / G::N1;   // lines per CTA
-    static constexpr int SMEM = LPC * LayRow<N>::kFloat2PerLine * (int)sizeof(float2);
-};
-
-template <int N, int MODE>
-__global__ void __launch_bounds__(256) k_xpass(XParams p) {
-    using G = LineGeo<N>;
-    using XG = XGeo<N>;
-    extern __shared__ float2 smem[];
-    __shared__ double sh_red[XG::NT / 32];
-    const int tid = threadIdx.x;
-    const int lq = tid / G::N1, j = tid % G::N1;
-    const LayRow<N> lay{smem + lq * LayRow<N>::kFloat2PerLine};
-
-    bool xonly = false;
-    float alpha = 0.f;
-    if (MODE == X_ITER) {
-        const int status = p.st->status;
-        const long long k = p.st->k, kmax = p.st->kmax;
-        if (k >= kmax || (status != ST_RUNNING && status != ST_STOP_PENDING)) return;
-        xonly = (status == ST_STOP_PENDING);
-        alpha = (float)p.st->alpha;
-    }
-
-    double acc = 0.0;
-    const long long ngroups = (p.nlines + XG::LPC - 1) / XG::LPC;
-    for (long long g = blockIdx.x; g < ngroups; g += gridDim.x) {
-        const long long line = g * XG::LPC + lq;
-        const bool valid = line < p.nlines;
-        const long long base = line * (long long)N + j;
-        float2 v[G::N2];
-
-        if (MODE == X_ITER && xonly) {   // final x update after convergence (reading R-5)
-            if (valid) {
-#pragma unroll
-                for (int m = 0; m < G::N2; ++m) {
-                    const long long i = base + (long long)G::N1 * m;
-                    const float2 d = p.delta[i];
-                    float2 xx = p.x[i];
-                    xx.x = fmaf(alpha, d.x, xx.x);
-                    xx.y = fmaf(alpha, d.y, xx.y);
-                    p.x[i] = xx;
-                }
-            }
-            continue;
-        }
-
-        if (MODE == X_SRC_FWD) {
-            // s = S / c, staged raw source in the x buffer
-#pragma unroll
-            for (int m = 0; m < G::N2; ++m) {
-                const long long i = base + (long long)G::N1 * m;
-                float2 sv = make_float2(0.f, 0.f);
-                if (valid) sv = p.src_real ? make_float2(reinterpret_cast<const float *>(p.x)[i], 0.f) : p.x[i];
-                v[m] = cmul(sv, p.inv_c);
-            }
-        } else {
-#pragma unroll
-            for (int m = 0; m < G::N2; ++m)
-                v[m] = valid ? p.work[base + (long long)G::N1 * m] : make_float2(0.f, 0.f);
-            fft_line<N, true>(v, lay, j, p.tw);   // x inverse: v = (L+1)^-1 u
-            float lacc = 0.f;
-#pragma unroll
-            for (int m = 0; m < G::N2; ++m) {
-                const long long i = base + (long long)G::N1 * m;
-                const float2 b = valid ? p.B[i] : make_float2(0.f, 0.f);
-                float2 dn;
-                if (MODE == X_SRC_EPI) {
-                    dn = cmul(b, v[m]);                       // Delta_0 = B (L+1)^-1 s
-                    if (valid) {
-                        p.x[i] = make_float2(0.f, 0.f);       // x_0 = 0 (L83)
-                        p.delta[i] = dn;
-                    }
-                } else {
-                    const float2 d = valid ? p.delta[i] : make_float2(0.f, 0.f);
-                    const float2 xx = valid ? p.x[i] : make_float2(0.f, 0.f);
-                    // x_{k+1} = x_k + alpha Delta_k ; Delta_{k+1} = Delta_k + alpha B (y - Delta_k)
-                    const float2 t = cmul(b, csub(v[m], d));
-                    dn = make_float2(fmaf(alpha, t.x, d.x), fmaf(alpha, t.y, d.y));
-                    if (valid) {
-                        p.x[i] = make_float2(fmaf(alpha, d.x, xx.x), fmaf(alpha, d.y, xx.y));
-                        p.delta[i] = dn;
-                    }
-                }
-                lacc += cabs2(dn);
-                v[m] = cmul(b, dn);                           // next chain: u = B Delta
-            }
-            acc += (double)lacc;
-        }
-        fft_line<N, false>(v, lay, j, p.tw);   // x forward
-        if (valid) {
-#pragma unroll
-            for (int m = 0; m < G::N2; ++m) p.work[base + (long long)G::N1 * m] = v[m];
-        }
-    }
-
-    if (MODE == X_SRC_FWD) return;
-    double total;
-    const double mine = block_sum_d<XG::NT>(acc, sh_red);
-    if (!last_block_total<XG::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
-    if (threadIdx.x != 0) return;
-    if (p.red.chunk_acc) {   // chunked schedule: z-chunks reduce in launch order (deterministic)
-        if (!p.red.chunk_first) total += *p.red.chunk_acc;
-        if (!p.red.chunk_last) {
-            *p.red.chunk_acc = total;
-            return;
-        }
-    }
-    if (p.red.local_sum) {   // slab-decomposed: k_finish sums the ranks' totals after the all-gather
-        *p.red.local_sum = total;
-        return;
-    }
-    finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red);
-}
 
 // ========================================================== strided pass ==
 // Strided axes (y: stride nx, z: stride nx*ny).  A CTA transforms tiles of
@@ -500,30 +386,6 @@ __global__ void k_set_state(IterState *st, double alpha, double tol, long long k
 
 bool supported_n(long long n) { return n >= 16 && n <= 2048 && (n & (n - 1)) == 0; }
 
-template <int N, int MODE>
-static cudaError_t xpass_t(const XParams &p, int grid, cudaStream_t s) {
-    constexpr int SM = XGeo<N>::SMEM;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_xpass<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    k_xpass<N, MODE><<<grid, XGeo<N>::NT, SM, s>>>(p);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStream_t s) {
-#define X_CASE(n)                                                  \
-    case n:                                                        \
-        if (mode == X_SRC_FWD) return xpass_t<n, X_SRC_FWD>(p, grid, s); \
-        if (mode == X_SRC_EPI) return xpass_t<n, X_SRC_EPI>(p, grid, s); \
-        return xpass_t<n, X_ITER>(p, grid, s);
-    switch (N) { USP_FOR_EACH_N(X_CASE) default: return cudaErrorInvalidValue; }
-#undef X_CASE
-}
-
-
 template <int N, int MODE, int COLS>
 static cudaError_t strided_t(const SParams &p, int grid, cudaStream_t s) {
     constexpr int SM = SGeo<N, COLS>::SMEM;
@@ -544,23 +406,16 @@ static cudaError_t strided_mode(SMode mode, const SParams &p, int grid, cudaStre
     return strided_t<N, S_FWD_MUL_INV, COLS>(p, grid, s);
 }
 
-// Columns per tile: 8 for N1 = 32 (N >= 1024: 256-thread CTAs, 2 per SM), else 16.
-int strided_cols_for(int N) { return N >= 1024 ? 8 : 16; }
-
-cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s, int cols) {
-    if (cols == 16 && N == 1024) return strided_mode<1024, 16>(mode, p, grid, s);
+// Register-staged passes for the short strided lines k_stile does not take
+// (N = 16, 32): 16-column tiles.
+cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s) {
     switch (N) {
     case 16: return strided_mode<16, 16>(mode, p, grid, s);
     case 32: return strided_mode<32, 16>(mode, p, grid, s);
-    case 64: return strided_mode<64, 16>(mode, p, grid, s);
-    case 128: return strided_mode<128, 16>(mode, p, grid, s);
-    case 256: return strided_mode<256, 16>(mode, p, grid, s);
-    case 512: return strided_mode<512, 16>(mode, p, grid, s);
-    case 1024: return strided_mode<1024, 8>(mode, p, grid, s);
-    case 2048: return strided_mode<2048, 8>(mode, p, grid, s);
     default: return cudaErrorInvalidValue;
     }
 }
+
 
 cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s) {
 #define O_CASE(n)                                                                   \
@@ -600,17 +455,26 @@ cudaError_t launch_set_form(IterState *st, int form, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+__global__ void k_put_blob(unsigned char *dst, Blob v, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = v.b[i];
+}
+
+cudaError_t launch_put_bytes(void *dst, const void *src, size_t n, cudaStream_t s) {
+    if (n > sizeof(Blob)) return cudaErrorInvalidValue;
+    Blob b;
+    memcpy(b.b, src, n);
+    k_put_blob<<<1, 128, 0, s>>>(static_cast<unsigned char *>(dst), b, (int)n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_put_state(IterState *st, const IterState &h, cudaStream_t s) {
+    return launch_put_bytes(st, &h, sizeof h, s);
+}
+
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s) {
     k_set_state<<<1, 1, 0, s>>>(st, alpha, tol, kmax);
     return cudaGetLastError();
 }
 
-int xpass_threads(int) { return 256; }
-int xpass_lines_per_cta(int N) { return 256 / (1 << (ilog2(N) / 2)); }
-size_t xpass_smem(int N) {
-    const int n1 = 1 << (ilog2(N) / 2), n2 = N / n1;
-    return (size_t)(256 / n1) * n1 * (n2 + 1) * sizeof(float2);
-}
-int strided_threads(int N) { return strided_cols_for(N) * (1 << (ilog2(N) / 2)); }
 
 }  // namespace usp

@@ -127,7 +127,6 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
         if (warp == T::XC) {
             // ------------------------------------------------ producer warp
             if (lane == 0) {
-                const uint64_t pol_first = policy_evict_first();
                 for (int i = 0; i < nloc; ++i) {
                     const int s = i % T::S;
                     if (i >= T::S && !mbar_wait(&empty[s], ((i / T::S) - 1) & 1)) {
@@ -146,12 +145,6 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
                         bulk_g2s(st, p.work + off, ub, &full[s]);
                         if (p.s) bulk_g2s(st + T::SD, slot1 + off, ub, &full[s]);
                         bulk_g2s(st + T::SB, p.B + off, ub, &full[s]);
-                    } else if (p.l2hint) {
-                        mbar_arrive_expect_tx(&full[s], 4 * ub);
-                        bulk_g2s(st, p.work + off, ub, &full[s]);
-                        bulk_g2s_hint(st + T::SD, slot1 + off, ub, &full[s], pol_first);
-                        bulk_g2s_hint(st + T::SX, p.x + off, ub, &full[s], pol_first);
-                        bulk_g2s_hint(st + T::SB, p.B + off, ub, &full[s], pol_first);
                     } else {
                         mbar_arrive_expect_tx(&full[s], (stage1 ? 4 : 3) * ub);
                         bulk_g2s(st, p.work + off, ub, &full[s]);
@@ -165,8 +158,6 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
         } else {
             // ------------------------------------------------ consumer warps
             const int lq = lane / G::N1, j = lane % G::N1;
-            // (the chunked schedule's L2 hints apply to the loads only: hinted
-            // stores cost a uniform-register move per store in this body)
             const LayRow<N> lay{xbufs + warp * T::XBUF + lq * LayRow<N>::kFloat2PerLine};
             for (int i = warp; i < nloc; i += T::XC) {
                 const int s = i % T::S;
@@ -222,7 +213,7 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
                                 lacc += cabs2(dk);
                                 v[m] = cmul(b, xn);
                             }
-                        } else if (XSPEC && !LEAN && MODE == X_ITER && act == ACT_X && need1 && !p.l2hint) {
+                        } else if (XSPEC && !LEAN && MODE == X_ITER && act == ACT_X && need1) {
                             // the dense-source x-form's dedicated body: u = B x_{k+1} + s
 #pragma unroll
                             for (int m = 0; m < G::N2; ++m) {
@@ -236,7 +227,7 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
                                 const float2 bx = cmul(b, xn);
                                 v[m] = make_float2(bx.x + sv.x, bx.y + sv.y);
                             }
-                        } else if (DSPEC && !LEAN && MODE == X_ITER && act == ACT_DELTA && !p.l2hint) {
+                        } else if (DSPEC && !LEAN && MODE == X_ITER && act == ACT_DELTA) {
                             // the Delta-form's dedicated body
 #pragma unroll
                             for (int m = 0; m < G::N2; ++m) {
@@ -307,13 +298,6 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p)
     const double mine = block_sum_d<T::NT>(acc, sh_red);
     if (!last_block_total<T::NT>(mine, p.st, p.red.partials, sh_red, &total)) return;
     if (threadIdx.x != 0) return;
-    if (p.red.chunk_acc) {   // chunked schedule: z-chunks reduce in launch order (deterministic)
-        if (!p.red.chunk_first) total += *p.red.chunk_acc;
-        if (!p.red.chunk_last) {
-            *p.red.chunk_acc = total;
-            return;
-        }
-    }
     if (p.red.local_sum) {   // slab-decomposed: k_finish sums the ranks' totals after the all-gather
         *p.red.local_sum = total;
         return;
@@ -406,10 +390,6 @@ static cudaError_t xpipe_t(const XParams &p, int grid, cudaStream_t s) {
     return launch_pdl(k_xpass_pipe<N, MODE, LEAN, DSPEC, XSPEC>, grid, T::NT, T::SMEM, s, p);
 }
 
-#ifndef USP_XSPEC
-#define USP_XSPEC 1
-#endif
-constexpr bool XSPEC_ON = USP_XSPEC != 0;
 
 // X_ITER variants by the form the host expects: lean (sparse-source x-form:
 // 3-slot stages, one more consumer warp; N <= 1024), x-form (general body),
@@ -421,7 +401,7 @@ cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cud
         if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD, false, false>(p, grid, s); \
         if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI, false, false>(p, grid, s); \
         if (lean && n <= 1024) return xpipe_t<n, X_ITER, true, false>(p, grid, s);    \
-        if (expect_x) return xpipe_t<n, X_ITER, false, false, XSPEC_ON>(p, grid, s);  \
+        if (expect_x) return xpipe_t<n, X_ITER, false, false, true>(p, grid, s);  \
         return xpipe_t<n, X_ITER, false, true>(p, grid, s);
     switch (N) { USP_PIPE_X_N(XP_CASE) default: return cudaErrorInvalidValue; }
 #undef XP_CASE

@@ -31,9 +31,6 @@ namespace usp {
 
 // Sense-reversing grid barrier over co-resident CTAs (cooperative launch).
 // A 4-second watchdog turns a scheduling failure into an error code.
-#ifndef USP_S2_SCOPED_BARRIER
-#define USP_S2_SCOPED_BARRIER 1
-#endif
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -57,7 +54,6 @@ __device__ __forceinline__ bool grid_barrier(unsigned *count, volatile unsigned 
     __shared__ int ok;
     if (threadIdx.x == 0) {
         ok = 1;
-#if USP_S2_SCOPED_BARRIER
         unsigned *genp = const_cast<unsigned *>(gen);
         const unsigned g = ld_acquire_gpu(genp);
         if (atom_add_acqrel_gpu(count, 1u) == gridDim.x - 1) {
@@ -74,26 +70,6 @@ __device__ __forceinline__ bool grid_barrier(unsigned *count, volatile unsigned 
                 }
             }
         }
-#else
-        const unsigned g = *gen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            *count = 0u;
-            __threadfence();
-            atomicAdd((unsigned *)gen, 1u);
-        } else {
-            const uint64_t t0 = globaltimer_ns();
-            unsigned n = 0;
-            while (*gen == g) {
-                if ((++n & 255u) == 0 && globaltimer_ns() - t0 > 4000000000ull) {
-                    if (atomicCAS(&st->err, 0, 10) == 0) st->err_info = blockIdx.x;
-                    ok = 0;
-                    break;
-                }
-            }
-        }
-        __threadfence();
-#endif
     }
     __syncthreads();
     return ok != 0;
@@ -310,19 +286,13 @@ static cudaError_t solve2d_t(const S2Params &p, int nsm, cudaStream_t s, int *gr
                                        s);
 }
 
-// CTA size (USP_S2NT = 64 / 128 / 256).  Default 128: twice the CTAs of the
-// 256-thread version, and the X phase's B, Delta, x fit the shared-memory
-// prefetch.  C2 (512^2, 1680 iterations to 1e-6): 256 threads 35.9 ms, 128
-// threads 25.5 ms (15.2 us per iteration), 64 threads 25.6 ms.
+// CTA size 128: twice the CTAs of the 256-thread version, and the X phase's
+// B, Delta, x fit the shared-memory prefetch.  C2 (512^2, 1680 iterations to
+// 1e-6): 256 threads 35.9 ms, 128 threads 25.5 ms (15.2 us per iteration),
+// 64 threads 25.6 ms.
 template <int NX, int NY>
 static cudaError_t solve2d_nt(const S2Params &p, int nsm, cudaStream_t s) {
-    static const int nt = [] {
-        const char *e = std::getenv("USP_S2NT");
-        return e ? std::atoi(e) : 128;
-    }();
-    if (nt == 64) return solve2d_t<NX, NY, 64>(p, nsm, s, nullptr);
-    if (nt == 128) return solve2d_t<NX, NY, 128>(p, nsm, s, nullptr);
-    return solve2d_t<NX, NY, 256>(p, nsm, s, nullptr);
+    return solve2d_t<NX, NY, 128>(p, nsm, s, nullptr);
 }
 
 bool solve2d_supported(long long nx, long long ny) {

@@ -169,21 +169,11 @@ __device__ __forceinline__ void stile_fft(float2 (&v)[LineGeo<N>::N2], float2 *x
     }
 }
 
-// USP_ST128: 0 = 64-bit stores everywhere, 1 = paired 128-bit stores
-// everywhere, 2 (default) = paired stores in the inverse y pass (K_D) only.
-// Measured at 1024^3 (tools/gpu/kab.py, medians of 5): K_D 3.30 -> 2.77 ms with
-// paired stores, while K_B (2.67 -> 2.82) and K_C (4.45 -> 4.51) are faster
-// with 64-bit stores.
-// diagnostics only (timing ablations of K_C; results wrong when changed)
-#ifndef USP_DIAG_PASSES
-#define USP_DIAG_PASSES 2
-#endif
-#ifndef USP_DIAG_NOMUL
-#define USP_DIAG_NOMUL 0
-#endif
-#ifndef USP_ST128
-#define USP_ST128 2
-#endif
+// Stores from registers: 64-bit stores, except the inverse y pass (K_D),
+// where adjacent-column lanes pair up into 128-bit stores.  Measured at
+// 1024^3 (medians of 5, one process): K_D 3.30 -> 2.77 ms with paired
+// stores, while K_B (2.67 -> 2.82) and K_C (4.45 -> 4.51) are faster with
+// 64-bit stores.
 // Store register slots m in [M0, M1) (rows j + N1 m of column c) of a tile.
 // Paired stores: adjacent-column lane pairs swap one value per slot pair with
 // a shuffle so each lane writes two columns of one row with one 128-bit store
@@ -193,7 +183,7 @@ __device__ __forceinline__ void store_slots(const float2 (&v)[LineGeo<N>::N2], f
                                             int j, int c) {
     using G = LineGeo<N>;
     auto val = [&](int m) { return (MODE == S_FWD) ? v[m] : cconj(v[m]); };
-    constexpr bool paired = USP_ST128 == 1 || (USP_ST128 == 2 && MODE == S_INV);
+    constexpr bool paired = MODE == S_INV;
     if constexpr (paired && STile<N>::COLS == 16 && ((M1 - M0) % 2) == 0) {
         const bool odd = c & 1;
         float2 *b = base - (odd ? 1 : 0) + (long long)(j + (odd ? G::N1 : 0)) * stride;
@@ -235,11 +225,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     pdl_trigger();
     if (tid == 0) prefetch_tmap(&tmap);
     pdl_wait();
-    if (p.check_state) {
-        const bool running = iter_running(p.st);
-        if (p.check_state == 3 && blockIdx.x == 0 && threadIdx.x == 0) p.st->full_iter = running;
-        if (!((p.check_state == 2) ? (p.st->full_iter != 0) : running)) return;
-    }
+    if (p.check_state && !iter_running(p.st)) return;
     const int c = tl % T::COLS, j = tl / T::COLS;
     const long long tpo = p.ncols / T::COLS;
     const long long ntiles = tpo * p.nouter;
@@ -249,7 +235,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
 
     auto issue = [&](int i) {   // thread 0 of the group: TMA boxes of local tile i
         const long long t = vb + (long long)i * vg;
-        const long long ol = t / tpo, o = p.o0 + ol;
+        const long long ol = t / tpo, o = ol;
         const int c0 = (int)((t - ol * tpo) * T::COLS);
         mbar_arrive_expect_tx(full, T::TILE * 8);
         if (p.map_rank == 5) {
@@ -329,9 +315,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 base = fmaf(p.mp.D, pt2, p.mp.sc.x);
             }
 #pragma unroll 1
-            for (int pass = 0; pass < USP_DIAG_PASSES; ++pass) {
+            for (int pass = 0; pass < 2; ++pass) {
                 stile_fft<N>(v, xb, sm_tw, c, j, bar);
-                if (pass == 0 && !USP_DIAG_NOMUL) {
+                if (pass == 0) {
                     // (L+1)^-1 symbol (Eq. 12) at the signed frequency of k = j + N1 m:
                     //   g = cn (dr - i di) / (dr^2 + di^2),  dr = D |p|^2 + Re(sigma + c),
                     //   di = Im(sigma + c);  then conj so the second forward DFT inverts.
@@ -360,7 +346,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         }
         long long t = vb + (long long)i * vg;
         asm volatile("" : "+l"(t));
-        const long long ol = t / tpo, o = p.o0 + ol;
+        const long long ol = t / tpo, o = ol;
         const long long col = (t - ol * tpo) * T::COLS + c;
         long long stride = p.stride;
         asm volatile("" : "+l"(stride));
@@ -425,18 +411,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 bulk_commit();
             }
         } else {
-            float2 *sb = p.dst + (o * p.ostride + col) + (long long)j * stride;
-            const long long step = (long long)G::N1 * stride;
-            if (p.store_hint) {
-                const uint64_t pol = p.store_hint == 1 ? policy_evict_last() : policy_evict_first();
-#pragma unroll
-                for (int m = 0; m < G::N2; ++m) {
-                    st_hint(sb, (MODE == S_FWD) ? v[m] : cconj(v[m]), pol);
-                    sb += step;
-                }
-            } else {
-                store_slots<N, MODE, 0, G::N2>(v, p.dst + (o * p.ostride + col), stride, j, c);
-            }
+            store_slots<N, MODE, 0, G::N2>(v, p.dst + (o * p.ostride + col), stride, j, c);
         }
     }
     if (TST && tl == 0) bulk_wait0();   // the exchange buffer outlives the last bulk store

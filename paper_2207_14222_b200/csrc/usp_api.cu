@@ -140,7 +140,7 @@ struct Timed {
 
 }  // namespace
 
-constexpr size_t kHostMapBytes = 64 * 1024;   // mapped pinned scratch for small read-backs
+constexpr size_t kHostMapBytes = 1024 * 1024;   // mapped pinned scratch for small read-backs
 
 struct usp_plan_s {
     usp_plan_desc d{};
@@ -166,7 +166,7 @@ struct usp_plan_s {
     size_t ws_bytes = 0;
     float2 *x = nullptr, *delta = nullptr, *B = nullptr, *work = nullptr;
     float2 *sendb = nullptr, *recvb = nullptr;   // P > 1
-    // transposes fused into the K_B / K_C stores (peer memory; USP_FUSED=0 -> NCCL all-to-all)
+    // transposes fused into the K_B / K_C stores (peer memory; desc.separate_transposes -> NCCL all-to-all)
     bool fused = false;
     float2 *peer_recv[kMaxPeers] = {}, *peer_send[kMaxPeers] = {};
     std::vector<void *> ipc_bases;   // peer allocations mapped with cudaIpcOpenMemHandle
@@ -188,13 +188,13 @@ struct usp_plan_s {
     int ncomp = 1;                 // components of the fields (1; 2 anti; d + 1 tdiff)
     float *td_vu = nullptr, *td_vf = nullptr, *td_dinv = nullptr, *td_red = nullptr;
     TDParams td{};
-    // persistent 2-D solve (kernels_small.cu; USP_SOLVE2D=0 disables)
+    // persistent 2-D solve (kernels_small.cu; desc.launch_per_pass disables)
     bool solve2d = false;
-    // x-form passes while r >= r_sw (reading R-30; USP_XFORM=0 disables,
-    // USP_XSWITCH sets r_sw): s = S / c kept in its own field
+    // x-form passes while r >= r_sw (reading R-30; desc.delta_form disables,
+    // desc.r_switch sets r_sw): s = S / c kept in its own field
     bool xform_cap = false, xform = false, probe_needed = false;
-    bool force_finish = false;   // USP_FORCE_FINISH=1 (test hook, see rank_finish)
-    // sparse source (R-31; USP_SPARSE_S=0 disables): <= kSparseMaxLines x-lines carry
+    bool force_finish = false;   // desc.test_hooks & USP_HOOK_RANK_FINISH (see rank_finish)
+    // sparse source (R-31; desc.dense_source disables): <= kSparseMaxLines x-lines carry
     // the source; their x-transforms live in the s field (list, then lines)
     unsigned char *s_flag = nullptr;
     unsigned *s_ctr = nullptr;
@@ -202,20 +202,25 @@ struct usp_plan_s {
     int s_count = 0;
     // expect_x: the host's view of the device-side form (x-form or not),
     // refreshed at call start and batch boundaries; it picks the x-pass
-    // instance (lean 3-slot pass for sparse-source x-form passes unless
-    // USP_LEAN=0, general body, Delta-form body) and whether the sparse
-    // source lines are added after a pass
-    bool lean_ok = true, expect_x = false;
+    // instance (lean 3-slot pass for sparse-source x-form passes, general
+    // body, Delta-form body) and whether the sparse source lines are added
+    // after a pass
+    bool expect_x = false;
     // mapped pinned scratch for small read-backs (see readback) and the
     // device view of st_host
     void *hmap = nullptr, *hmap_dev = nullptr, *st_host_dev = nullptr;
     // asynchronous input staging (usp_stage_inputs): caller-owned area, copy
-    // stream, "copies done" and "staging area consumed" events
+    // streams, "copies done" event
     char *stg = nullptr;
     size_t stg_bytes = 0;
     cudaStream_t cstream = nullptr, dstream = nullptr;   // H2D staging, D2H results
-    cudaEvent_t ev_staged = nullptr, ev_consumed = nullptr, ev_snap = nullptr, ev_out = nullptr;
-    bool staged = false, consumed_recorded = false, out_pending = false;
+    // per slot "consumed by the plan stream" events: the copy stream refills a
+    // slot only after them; medium_taken = set_potential(STAGED) ran, its
+    // source not yet consumed (usp_stage_inputs refuses meanwhile)
+    cudaEvent_t ev_staged = nullptr, ev_med_used = nullptr, ev_src_used = nullptr, ev_snap = nullptr,
+                ev_out = nullptr;
+    bool staged = false, med_used_rec = false, src_used_rec = false, medium_taken = false, out_pending = false;
+    bool stg_result = false;   // the staging area has the read-back slot
     double r_sw = 1e-2;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
@@ -230,29 +235,21 @@ struct usp_plan_s {
     double *far_d = nullptr;
     long long *far_i = nullptr;
     int far_cap = 0;
-    double *coll = nullptr;         // collective scratch: [0] local x-pass total, [1] chunk sum, [8..15]
+    double *coll = nullptr;         // collective scratch: [0] local x-pass total, [8..15]
                                     // all-gathered totals, [16..] IPC records, [64..] / [128..] host gathers
     IterState *st_host = nullptr;   // pinned mirror
     // split
     usp_c128 sigma{}, c{}, centre{};
     double radius = 0.0, vmax = 0.0;
     bool have_potential = false, have_source = false;
-    // launch configuration
-    int grid_x = 0, grid_y = 0, grid_z = 0;
-    // TMA-pipelined x pass (default); USP_LEGACY=1 selects the register-staged kernels
-    bool pipe = true, pipe_xk = true;
+    // launch configuration: the TMA-pipelined x pass (one CTA per SM), the
+    // TMA-prefetched strided passes (kernels_stile.cu, lines of 64..2048;
+    // shorter lines take the register-staged k_strided)
     int gridp_x = 0;
-    // TMA-prefetched 16-column strided passes (kernels_stile.cu; default, USP_STILE=0 disables)
-    bool stile = true, stile_y = false, stile_z = false;
+    int grid_y = 0, grid_z = 0;   // k_strided (N = 16, 32)
+    bool stile_y = false, stile_z = false;
     int grids_y = 0, grids_z = 0;
     CUtensorMap smap_y{}, smap_z{}, smap_kd{};
-    // chunked schedule (1 GPU, 3-D; experimental, off by default): per
-    // iteration K_C over the volume, then K_D, K_A, K_B chunk by chunk of G
-    // z-planes so the chunk's work array can stay in L2 between the three
-    // (USP_CHUNK = G).  Measured slower at 1024^3.
-    bool chunked = false;
-    long long chunk_g = 0;
-    bool l2hint = true;   // USP_L2HINT=0 disables the eviction-priority hints
     // profiling
     bool prof = false;
     std::vector<Timed> timed;
@@ -377,6 +374,8 @@ int occ_grid(usp_plan_s *p, long long units, int per_sm) {
 
 // ------------------------------------------------------- collectives --
 // Gather `n` host doubles from every rank (rank order) into out[P*n].
+usp_status readback(usp_plan_s *p, void *host, const void *dev, size_t bytes);
+
 usp_status gather_host(usp_plan_s *p, const double *mine, int n, std::vector<double> &out) {
     out.assign((size_t)p->P * n, 0.0);
     if (!multi_rank(p)) {
@@ -385,11 +384,9 @@ usp_status gather_host(usp_plan_s *p, const double *mine, int n, std::vector<dou
     }
     if (n > 64 || (size_t)p->P * n > 1920) return fail(USP_ERR_ARG, "gather of %d doubles x %d ranks too large", n, p->P);
     double *snd = p->coll + 64, *rcv = p->coll + 128;
-    CU(cudaMemcpyAsync(snd, mine, sizeof(double) * n, cudaMemcpyHostToDevice, p->stream));
+    CU(launch_put_bytes(snd, mine, sizeof(double) * n, p->stream));
     NC(nccl().AllGather(snd, rcv, (size_t)n, ncclDouble, p->comm, p->stream));
-    CU(cudaMemcpyAsync(out.data(), rcv, sizeof(double) * n * p->P, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
-    return USP_OK;
+    return readback(p, out.data(), rcv, sizeof(double) * n * p->P);
 }
 
 // ---------------------------------------------------------------- MEC --
@@ -448,7 +445,7 @@ void mec_small(const std::vector<P2> &pts, P2 &c, double &r) {
 // the copy engines (usp_stage_inputs / usp_get_field_async).
 usp_status readback(usp_plan_s *p, void *host, const void *dev, size_t bytes) {
     if (bytes > kHostMapBytes) return fail(USP_ERR_ARG, "read-back of %zu bytes exceeds the mapped scratch", bytes);
-    CU(launch_copy_bytes(p->hmap_dev, dev, bytes, 4, p->stream));
+    CU(launch_copy_bytes(p->hmap_dev, dev, bytes, bytes > 65536 ? 64 : 4, p->stream));
     CU(cudaStreamSynchronize(p->stream));
     std::memcpy(host, p->hmap, bytes);
     return USP_OK;
@@ -520,9 +517,33 @@ usp_status device_mec(usp_plan_s *p, const void *medium_dev, P2 &centre, double 
     return fail(USP_ERR_CUDA, "smallest-circle search did not converge");
 }
 
+// Copy a caller's input into the workspace.  Device inputs are copied by an
+// SM kernel (not a copy engine, so the plan stream never queues behind bulk
+// staging transfers); a pointer the device cannot dereference is refused
+// here instead of faulting in the kernel.
 usp_status stage(usp_plan_s *p, void *dst, const void *src, size_t bytes, usp_where where) {
-    if (where == USP_HOST) CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
-    else CU(launch_copy_bytes(dst, src, bytes, 4 * p->nsm, p->stream));   // SMs, not a copy engine
+    if (where == USP_HOST) {
+        CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, p->stream));
+        return USP_OK;
+    }
+    if (where != USP_DEVICE) return fail(USP_ERR_ARG, "bad where (%d)", (int)where);
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, src) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(USP_ERR_ARG, "input pointer is not device memory (where = USP_DEVICE)");
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged &&
+        !(at.type == cudaMemoryTypeHost && at.devicePointer))
+        return fail(USP_ERR_ARG, "input pointer is not device memory (where = USP_DEVICE)");
+    const void *dsrc = at.type == cudaMemoryTypeHost ? at.devicePointer : src;   // mapped pinned host memory
+    CU(launch_copy_bytes(dst, dsrc, bytes, 4 * p->nsm, p->stream));
+    return USP_OK;
+}
+
+// Write the device iteration state from the host without a copy engine (the
+// state travels as a kernel argument).
+usp_status put_state(usp_plan_s *p, const IterState &h) {
+    CU(launch_put_state(p->st, h, p->stream));
     return USP_OK;
 }
 
@@ -546,8 +567,8 @@ MulParams mul_params(const usp_plan_s *p) {
 }
 
 // The x pass's residual goes through the all-gather + k_finish path: with
-// P > 1 ranks, or (test hook USP_FORCE_FINISH=1) on a one-rank communicator,
-// so the rank-ordered finish is exercised on one GPU.
+// P > 1 ranks, or (desc.test_hooks & USP_HOOK_RANK_FINISH) on a one-rank
+// communicator, so the rank-ordered finish is exercised on one GPU.
 bool rank_finish(const usp_plan_s *p) { return multi_rank(p) || (p->comm && p->force_finish); }
 
 Red red_params(usp_plan_s *p) {
@@ -581,11 +602,9 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
     {
         Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
         if (p->real) CU(launch_xpass_real((int)p->nx, mode, xp, p->gridp_x, p->stream));
-        else if (p->pipe_xk)
+        else
             CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream,
-                                 mode == X_ITER && p->s_sparse && p->expect_x && p->lean_ok,
-                                 p->xform && p->expect_x));
-        else CU(launch_xpass((int)p->nx, mode, xp, p->grid_x, p->stream));
+                                 mode == X_ITER && p->s_sparse && p->expect_x, p->xform && p->expect_x));
     }
     if (mode != X_SRC_FWD && rank_finish(p)) {
         {
@@ -618,26 +637,21 @@ usp_status sparse_add(usp_plan_s *p) {
 }
 
 usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, const SParams &sp, const CUtensorMap &map,
-                       bool use_stile, int grid_legacy) {
+                       bool use_stile, int grid_short) {
     Tick t(p, cls);
     if (use_stile) {
-        // half-tile tensor-map stores: only where the load map describes the
-        // destination (in place, natural layout).  Default on for the z pass
-        // (K_C: 4.59 -> 4.48 ms at 1024^3); the y passes measured slower with
-        // them (2.69 -> 2.94 ms), USP_TSTORE=2 turns them on everywhere, 0 off.
-        static const char *ts = std::getenv("USP_TSTORE");
-        const int tsm = ts ? std::atoi(ts) : 1;
+        // half-tile tensor-map stores where the load map describes the
+        // destination (in place, natural layout), in the z pass only (K_C
+        // 4.59 -> 4.48 ms at 1024^3; the y passes measured slower with them,
+        // 2.69 -> 2.94 ms)
         SParams q = sp;
-        q.tma_store = (tsm == 2 || (tsm == 1 && mode == S_FWD_MUL_INV)) && sp.dst == sp.data &&
-                      (sp.map_rank == 2 || sp.map_rank == 3) && !sp.peer_mode && !sp.send_layout && !sp.store_hint;
+        q.tma_store = mode == S_FWD_MUL_INV && sp.dst == sp.data && (sp.map_rank == 2 || sp.map_rank == 3) &&
+                      !sp.peer_mode && !sp.send_layout;
         CU(launch_stile(n, mode, map, q, cls == KC_ZMUL ? p->grids_z : p->grids_y, p->stream));
         return USP_OK;
     }
-    // legacy register-staged passes (line lengths the TMA tiles do not cover):
-    // the z pass (two FFTs + multiplier) runs 16-column tiles of 512 threads
-    static const char *zc = std::getenv("USP_ZCOLS");
-    const int cols = (cls == KC_ZMUL) ? (zc ? std::atoi(zc) : 16) : 0;
-    CU(launch_strided(n, mode, sp, cols == 16 ? p->nsm : grid_legacy, p->stream, cols));
+    // register-staged passes for the short lines (N = 16, 32) the TMA tiles do not take
+    CU(launch_strided(n, mode, sp, grid_short, p->stream));
     return USP_OK;
 }
 
@@ -692,8 +706,7 @@ void close_peers(usp_plan_s *p) {
 // all-to-alls if any rank cannot map its peers).
 usp_status setup_peers(usp_plan_s *p) {
     close_peers(p);
-    const char *fz = std::getenv("USP_FUSED");
-    const bool want = p->P > 1 && p->P <= kMaxPeers && !(fz && fz[0] == '0');
+    const bool want = p->P > 1 && p->P <= kMaxPeers && !p->d.separate_transposes;
     const long long bk = p->nzs * p->nyl * p->rp;
     if (!want) return USP_OK;
     if (p->virt) {   // rank q's region of the one-GPU buffers
@@ -956,49 +969,6 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
     return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_kd, true, 0);
 }
 
-// Chunked schedule (P = 1, 3-D).  Invariant between iterations: `work`
-// holds the x- and y-forward transforms of B Delta_k.  One iteration:
-//   K_C over the volume (z forward, multiplier, z inverse; snapshots the
-//   "full iteration" test into st->full_iter), then for each chunk of G
-//   z-planes: K_D (y inverse), K_A (x inverse, update, residual partial,
-//   x forward), K_B (y forward).  The chunk's 8 G nx ny bytes of `work`
-//   written by K_D are re-read by K_A and K_B straight from L2, so only
-//   Delta, x, B and the K_C/K_D/K_B endpoints touch HBM: 72 B/voxel instead
-//   of 104 B/voxel per iteration.  K_A's residual partials are summed over
-//   the chunks in launch order (deterministic).
-usp_status chunk_kb_all(usp_plan_s *p) {
-    SParams yb = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, p->nz, p->rp * p->ny, 1, 0, 3);
-    return run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0);
-}
-
-usp_status chunked_iteration(usp_plan_s *p) {
-    usp_status s;
-    SParams zm = sparams(p, p->work, p->work, p->tw[2], p->rp * p->ny, p->rp * p->ny, 1, 0, 2, 3, 2);
-    if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, true, 0))) return s;
-    const long long G = p->chunk_g, nch = p->nz / G, plane = p->rp * p->ny;
-    for (long long ch = 0; ch < nch; ++ch) {
-        SParams yc = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, G, plane, 1, 2, 3);
-        yc.o0 = ch * G;
-        yc.store_hint = p->l2hint ? 1 : 0;   // K_A re-reads the chunk from L2
-        if ((s = run_strided(p, KC_YINV, (int)p->ny, S_INV, yc, p->smap_y, true, 0))) return s;
-        yc.store_hint = 0;
-        XParams xp = x_params(p);
-        const long long off = ch * G * plane;
-        xp.work += off;
-        xp.delta += off;
-        xp.x += off;
-        xp.B += off;
-        xp.nlines = G * p->ny;
-        xp.red.chunk_acc = p->coll + 1;
-        xp.red.chunk_first = ch == 0;
-        xp.red.chunk_last = ch == nch - 1;
-        xp.l2hint = p->l2hint;
-        if ((s = run_xpass(p, X_ITER, xp))) return s;
-        if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yc, p->smap_y, true, 0))) return s;
-    }
-    return USP_OK;
-}
-
 usp_status chain_mid(usp_plan_s *p, int check_state);
 usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp);
 
@@ -1021,8 +991,7 @@ usp_status sync_state(usp_plan_s *p) {
 // Tensor maps of the strided passes (they embed the workspace addresses).
 void build_maps(usp_plan_s *p) {
     p->stile_y = p->stile_z = false;
-    p->chunked = false;
-    if (!p->stile || p->ndim < 2 || !stile_supported(p->ny)) return;
+    if (p->ndim < 2 || !stile_supported(p->ny)) return;
     const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
     if (p->ndim == 2) {
         const cuuint64_t dims[2] = {(cuuint64_t)p->rp, (cuuint64_t)(p->ny * p->ncomp)};
@@ -1045,7 +1014,6 @@ void build_maps(usp_plan_s *p) {
         const cuuint64_t str[1] = {(cuuint64_t)(p->rp * p->ny) * 8};
         const cuuint32_t box[2] = {cz, bz};
         p->stile_z = make_map(&p->smap_z, p->work, 2, dims, str, box);
-        p->chunked = p->stile_y && p->stile_z && p->pipe_xk && p->chunk_g > 0 && p->chunk_g < p->nz;
         return;
     }
     const long long pv = p->virt ? p->P : 1;
@@ -1075,7 +1043,7 @@ extern "C" {
 
 const char *usp_last_error(void) { return g_err.c_str(); }
 
-const char *usp_version(void) { return "0.2 sm_100a"; }
+const char *usp_version(void) { return "0.3 sm_100a"; }
 
 usp_status usp_comm_unique_id(unsigned char id[128]) {
     if (!id) return fail(USP_ERR_ARG, "NULL argument");
@@ -1178,12 +1146,10 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     p->nzh = (P > 1 && !virt) ? p->nzs : p->nz;
     p->nyl = p->ny / P;
     p->nloc = p->nx * p->ny * p->nzh;
-    {
-        const char *rl = std::getenv("USP_REAL");
-        p->real = !p->anti && !p->tdiff && !(rl && rl[0] == '0') && desc->dtype == USP_R32 && desc->medium == USP_MEDIUM_W &&
-                  desc->ndim == 3 && xreal_supported(p->nx) && stile_supported(p->ny) && stile_supported(p->nz);
-        p->rp = p->real ? xreal_row_pitch((int)p->nx) : p->nx;
-    }
+    p->real = !p->anti && !p->tdiff && !desc->complex_path && desc->dtype == USP_R32 &&
+              desc->medium == USP_MEDIUM_W && desc->ndim == 3 && xreal_supported(p->nx) && stile_supported(p->ny) &&
+              stile_supported(p->nz);
+    p->rp = p->real ? xreal_row_pitch((int)p->nx) : p->nx;
     p->stream = (cudaStream_t)desc->stream;
     p->sigma = desc->sigma;
     p->c = desc->c;
@@ -1197,24 +1163,9 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     // launch grids: one resident wave, persistent grid-stride loops
     {
         const long long xl = p->ny * p->nzh;
-        p->grid_x = occ_grid(p, (xl + xpass_lines_per_cta((int)p->nx) - 1) / xpass_lines_per_cta((int)p->nx), 2);
-        auto sgrid = [&](long long n, long long ncol_units) {
-            const int per_sm = strided_threads((int)n) <= 256 ? 2 : 1;
-            return occ_grid(p, ncol_units, per_sm);
-        };
-        if (p->ndim >= 2) p->grid_y = sgrid(p->ny, (p->nx / strided_cols_for((int)p->ny)) * p->nzh);
-        if (p->ndim >= 3) p->grid_z = sgrid(p->nz, (p->nx * p->ny) / strided_cols_for((int)p->nz));
-        const char *leg = std::getenv("USP_LEGACY");
-        p->pipe = !(leg && leg[0] == '1');
-        const char *px = std::getenv("USP_PIPE_X");
-        p->pipe_xk = p->pipe && !(px && px[0] == '0');
-        const char *l2h = std::getenv("USP_L2HINT");
-        p->l2hint = !(l2h && l2h[0] == '0');
-        const char *chk = std::getenv("USP_CHUNK");
-        if (chk) p->chunk_g = std::atoll(chk);
-        while (p->chunk_g > 0 && (p->nz % p->chunk_g)) p->chunk_g >>= 1;
-        const char *stl = std::getenv("USP_STILE");
-        p->stile = (P > 1) || p->real || p->anti || p->tdiff || (p->pipe && !(stl && stl[0] == '0'));
+        // short strided lines (k_strided, 16-column tiles of 64 threads, 2 CTAs per SM)
+        if (p->ndim >= 2) p->grid_y = occ_grid(p, (p->nx / 16) * p->nzh * p->ncomp, 2);
+        if (p->ndim >= 3) p->grid_z = occ_grid(p, (p->nx * p->ny) / 16 * p->ncomp, 2);
         const long long comps = p->ncomp;
         if (p->ndim >= 2 && stile_supported(p->ny))
             p->grids_y = occ_grid(p, (p->rp / stile_cols((int)p->ny)) * p->nzh * comps, stile_ctas_per_sm((int)p->ny));
@@ -1226,7 +1177,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         p->gridp_x = occ_grid(p, xl / u, 1);   // one CTA per SM, persistent over the warp units
     }
     // reduction partials: <= 3 doubles per CTA of the largest reducing grid
-    p->partials_cap = 3 * std::max(std::max(p->grid_x, p->gridp_x), p->nsm * 8);
+    p->partials_cap = 3 * std::max(p->gridp_x, p->nsm * 8);
     p->far_cap = p->nsm * 8;
     std::vector<float2> twh[3];
     const long long ext[3] = {p->nx, p->ny, p->nz};
@@ -1248,19 +1199,10 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->ks, sizeof(KState)));
     TRY(cudaMalloc(&p->bar, sizeof(unsigned) * 2));
     TRY(cudaMemset(p->bar, 0, sizeof(unsigned) * 2));
-    {
-        const char *s2 = std::getenv("USP_SOLVE2D");
-        p->solve2d = !p->anti && !p->tdiff && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !(s2 && s2[0] == '0');
-        const char *xf = std::getenv("USP_XFORM");
-        p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && (p->pipe_xk || p->real) &&
-                       !(xf && xf[0] == '0');
-        const char *xs = std::getenv("USP_XSWITCH");
-        if (xs) p->r_sw = std::atof(xs);
-        const char *ff = std::getenv("USP_FORCE_FINISH");
-        p->force_finish = ff && ff[0] == '1';
-        const char *ln = std::getenv("USP_LEAN");
-        p->lean_ok = !(ln && ln[0] == '0');
-    }
+    p->solve2d = !p->anti && !p->tdiff && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !desc->launch_per_pass;
+    p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && !desc->delta_form;
+    if (desc->r_switch > 0.0) p->r_sw = desc->r_switch;
+    p->force_finish = (desc->test_hooks & USP_HOOK_RANK_FINISH) != 0;
     TRY(cudaHostAlloc(&p->st_host, sizeof(IterState), cudaHostAllocMapped));
     TRY(cudaHostGetDevicePointer(&p->st_host_dev, p->st_host, 0));
     TRY(cudaHostAlloc(&p->hmap, kHostMapBytes, cudaHostAllocMapped));
@@ -1369,7 +1311,7 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     bool from_stage = false;
     if (where == USP_STAGED) {   // the medium staged by usp_stage_inputs
-        if (!p->staged) return fail(USP_ERR_STATE, "nothing staged (usp_stage_inputs)");
+        if (!p->staged || p->medium_taken) return fail(USP_ERR_STATE, "no staged medium (usp_stage_inputs)");
         CU(cudaStreamWaitEvent(p->stream, p->ev_staged, 0));
         medium = p->stg;
         where = USP_DEVICE;
@@ -1382,9 +1324,10 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
     // stage the medium in the chain buffer (the source resets it later)
     usp_status s = stage(p, p->work, medium, (size_t)p->nloc * elem_bytes(p), where);
     if (s) return s;
-    if (from_stage) {   // (set_source records it again after the source copy)
-        CU(cudaEventRecord(p->ev_consumed, p->stream));
-        p->consumed_recorded = true;
+    if (from_stage) {   // the medium slot may be refilled once this copy has run
+        CU(cudaEventRecord(p->ev_med_used, p->stream));
+        p->med_used_rec = true;
+        p->medium_taken = true;
     }
     p->have_source = false;
     p->have_potential = false;
@@ -1469,8 +1412,7 @@ usp_status usp_set_tensor_medium(usp_plan_t p, const float *mu, const float *D, 
     t.red = p->td_red;
     CU(launch_tdiff_pot(t, 0, grid, p->stream));
     std::vector<float> red((size_t)16 * grid);
-    CU(cudaMemcpyAsync(red.data(), p->td_red, sizeof(float) * red.size(), cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    if ((s = readback(p, red.data(), p->td_red, sizeof(float) * red.size()))) return s;
     double lo[7], hi[7], bad = 0.0;
     for (int q = 0; q < 7; ++q) { lo[q] = 3e38; hi[q] = -3e38; }
     for (int c = 0; c < grid; ++c) {
@@ -1496,8 +1438,7 @@ usp_status usp_set_tensor_medium(usp_plan_t p, const float *mu, const float *D, 
         t.inv_cu = (float)(1.0 / (c * s_u));
         t.inv_cf = (float)(1.0 / (c * s_F));
         CU(launch_tdiff_pot(t, pass == 0 ? 1 : 2, grid, p->stream));
-        CU(cudaMemcpyAsync(red.data(), p->td_red, sizeof(float) * red.size(), cudaMemcpyDeviceToHost, p->stream));
-        CU(cudaStreamSynchronize(p->stream));
+        if ((s = readback(p, red.data(), p->td_red, sizeof(float) * red.size()))) return s;
         double vmax = 0.0;
         for (int q = 0; q < grid; ++q) vmax = std::max(vmax, (double)red[(size_t)q * 16 + 14]);
         if (pass == 0) {
@@ -1560,6 +1501,7 @@ usp_status usp_get_split(usp_plan_t p, usp_c128 *sigma, usp_c128 *c, usp_c128 *c
 usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     const bool from_stage = where == USP_STAGED;
+    if (where != USP_HOST && where != USP_DEVICE && !from_stage) return fail(USP_ERR_ARG, "bad where");
     if (from_stage) {   // the source staged by usp_stage_inputs
         if (!p->staged) return fail(USP_ERR_STATE, "nothing staged (usp_stage_inputs)");
         CU(cudaStreamWaitEvent(p->stream, p->ev_staged, 0));
@@ -1570,20 +1512,21 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
     if (!p->have_potential) return fail(USP_ERR_STATE, "set_potential must succeed first");
     usp_status s = stage(p, p->x, src, (size_t)p->nloc * elem_bytes(p), where);
     if (s) return s;
-    if (from_stage) {   // the staging area may be refilled once this copy has run
-        CU(cudaEventRecord(p->ev_consumed, p->stream));
-        p->consumed_recorded = true;
+    if (from_stage) {   // the source slot may be refilled once this copy has run
+        CU(cudaEventRecord(p->ev_src_used, p->stream));
+        p->src_used_rec = true;
         p->staged = false;
+        p->medium_taken = false;
     }
     IterState s0{};
     s0.status = ST_NO_SOURCE;
     s0.alpha = 0.75;
-    p->xform = p->xform_cap && !p->chunked;
+    p->xform = p->xform_cap;
     p->probe_needed = false;
     s0.xform = p->xform ? 1 : 0;
     s0.r_sw = p->r_sw;
     s0.form = FORM_DELTA;   // the source setup's finish sets FORM_X on x-form plans
-    CU(cudaMemcpyAsync(p->st, &s0, sizeof s0, cudaMemcpyHostToDevice, p->stream));
+    if ((s = put_state(p, s0))) return s;
     if (p->ndim == 1) {
         OneParams op{};
         op.delta = p->delta;
@@ -1613,8 +1556,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         p->s_sparse = false;
         p->expect_x = false;
         XParams xp = x_params(p);
-        const char *sps = std::getenv("USP_SPARSE_S");
-        const bool try_sparse = p->xform && !p->real && !(sps && sps[0] == '0');
+        const bool try_sparse = p->xform && !p->real && !p->d.dense_source;
         if (try_sparse) {
             if (!p->s_flag) CU(cudaMalloc(&p->s_flag, (size_t)p->ny * p->nzh));
             if (!p->s_ctr) CU(cudaMalloc(&p->s_ctr, sizeof(unsigned)));
@@ -1627,7 +1569,6 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         if (s) return s;
         s = run_xpass(p, X_SRC_EPI, xp);
         if (s) return s;
-        if (p->chunked && (s = chunk_kb_all(p))) return s;   // establish the chunked invariant
         if (try_sparse) {
             // reading R-31: few source lines -> keep FFT_x(s) of those lines only
             // (work holds FFT_x(u_0) = FFT_x(s) after the x-form setup)
@@ -1743,10 +1684,6 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
                     if ((s = run_anti_x(p, X_ITER))) return s;
                     continue;
                 }
-                if (p->chunked) {
-                    if ((s = chunked_iteration(p))) return s;
-                    continue;
-                }
                 s = chain_mid(p, 1);
                 if (s) return s;
                 s = run_xpass(p, X_ITER, xp);
@@ -1802,49 +1739,59 @@ usp_status usp_residual_history(usp_plan_t p, double *host, int64_t cap, int64_t
     *n = avail;
     if (host && cap > 0) {
         std::vector<double> all(p->hist_cap);
-        CU(cudaMemcpy(all.data(), p->hist, sizeof(double) * p->hist_cap, cudaMemcpyDeviceToHost));
+        if ((s = readback(p, all.data(), p->hist, sizeof(double) * p->hist_cap))) return s;
         const long long first = p->st_host->k + 1 - avail;
         for (long long i = 0; i < std::min<long long>(cap, avail); ++i) host[i] = all[(first + i) % p->hist_cap];
     }
     return USP_OK;
 }
 
-usp_status usp_staging_size(usp_plan_t p, size_t *bytes) {
+usp_status usp_staging_size(usp_plan_t p, int with_readback, size_t *bytes) {
     if (!p || !bytes) return fail(USP_ERR_ARG, "NULL argument");
-    *bytes = 3 * align256((size_t)p->nloc * elem_bytes(p));   // medium, source, result
+    *bytes = (with_readback ? 3 : 2) * align256((size_t)p->nloc * elem_bytes(p));   // medium, source[, result]
     return USP_OK;
 }
 
 usp_status usp_plan_set_staging(usp_plan_t p, void *dev, size_t bytes) {
     if (!p || !dev) return fail(USP_ERR_ARG, "NULL argument");
     if (((uintptr_t)dev) & 255) return fail(USP_ERR_ARG, "staging area must be 256-byte aligned");
-    size_t need = 0;
-    usp_staging_size(p, &need);
+    size_t need = 0, need_rb = 0;
+    usp_staging_size(p, 0, &need);
+    usp_staging_size(p, 1, &need_rb);
     if (bytes < need) return fail(USP_ERR_NOMEM, "staging area %zu bytes < required %zu", bytes, need);
     if (p->tdiff) return fail(USP_ERR_UNSUPPORTED, "tensor-diffusion plans do not stage inputs");
     if (!p->cstream) {
         CU(cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking));
         CU(cudaStreamCreateWithFlags(&p->dstream, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&p->ev_staged, cudaEventDisableTiming));
-        CU(cudaEventCreateWithFlags(&p->ev_consumed, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&p->ev_med_used, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&p->ev_src_used, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&p->ev_snap, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
     }
+    CU(cudaStreamSynchronize(p->stream));   // nothing on the plan stream still reads the old area
     CU(cudaStreamSynchronize(p->cstream));
     CU(cudaStreamSynchronize(p->dstream));
     p->out_pending = false;
     p->stg = (char *)dev;
     p->stg_bytes = bytes;
-    p->staged = false;
+    p->stg_result = bytes >= need_rb;
+    p->staged = p->medium_taken = false;
+    p->med_used_rec = p->src_used_rec = false;
     return USP_OK;
 }
 
 usp_status usp_stage_inputs(usp_plan_t p, const void *medium, const void *source) {
     if (!p || !medium || !source) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->stg) return fail(USP_ERR_STATE, "usp_plan_set_staging must be called first");
+    if (p->medium_taken)
+        return fail(USP_ERR_STATE, "the staged medium was taken by set_potential; consume its source with "
+                                   "set_source(USP_STAGED) before staging the next problem");
     const size_t nb = (size_t)p->nloc * elem_bytes(p);
-    if (p->consumed_recorded) CU(cudaStreamWaitEvent(p->cstream, p->ev_consumed, 0));
+    // each slot is refilled only after the plan stream has consumed its previous contents
+    if (p->med_used_rec) CU(cudaStreamWaitEvent(p->cstream, p->ev_med_used, 0));
     CU(cudaMemcpyAsync(p->stg, medium, nb, cudaMemcpyHostToDevice, p->cstream));
+    if (p->src_used_rec) CU(cudaStreamWaitEvent(p->cstream, p->ev_src_used, 0));
     CU(cudaMemcpyAsync(p->stg + align256(nb), source, nb, cudaMemcpyHostToDevice, p->cstream));
     CU(cudaEventRecord(p->ev_staged, p->cstream));
     p->staged = true;
@@ -1857,6 +1804,8 @@ usp_status usp_get_field_async(usp_plan_t p, void *out) {
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
     if (p->tdiff || (p->d.dtype != USP_C64 && !p->real))
         return fail(USP_ERR_UNSUPPORTED, "asynchronous read-back of this field layout");
+    if (!p->stg_result)
+        return fail(USP_ERR_NOMEM, "staging area sized without the read-back slot (usp_staging_size(plan, 1, ..))");
     const size_t nb = (size_t)p->nloc * elem_bytes(p);
     char *res = p->stg + 2 * align256(nb);
     // the previous read-back must have left the result slot
@@ -1930,7 +1879,7 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->k_rh) return fail(USP_ERR_STATE, "usp_krylov_set_workspace must be called first");
     if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
-    if (p->ndim < 2 || p->real || p->anti || p->tdiff || multi_rank(p) || !p->pipe_xk)
+    if (p->ndim < 2 || p->real || p->anti || p->tdiff || multi_rank(p))
         return fail(USP_ERR_UNSUPPORTED, "BiCGSTAB runs on 2-D / 3-D complex64 plans on one GPU");
     usp_status s = sync_state(p);
     if (s) return s;
@@ -1938,7 +1887,7 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
         return fail(USP_ERR_STATE, "BiCGSTAB starts from x_0 = 0: call usp_set_source again first");
     const long long nvb = (long long)p->nloc * sizeof(float2);
     // r = b = Delta_0 (the fixed-point setup left it in `delta`), rhat = r, p = v = 0
-    CU(cudaMemcpyAsync(p->k_rh, p->delta, nvb, cudaMemcpyDeviceToDevice, p->stream));
+    CU(launch_copy_bytes(p->k_rh, p->delta, nvb, 4 * p->nsm, p->stream));
     CU(cudaMemsetAsync(p->k_p, 0, nvb, p->stream));
     CU(cudaMemsetAsync(p->k_v, 0, nvb, p->stream));
     KState k0{};
@@ -1946,7 +1895,7 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
     k0.rho = make_double2(nb * nb, 0.0);
     k0.omega = make_double2(1.0, 0.0);
     k0.nb = nb;
-    CU(cudaMemcpyAsync(p->ks, &k0, sizeof k0, cudaMemcpyHostToDevice, p->stream));
+    CU(launch_put_bytes(p->ks, &k0, sizeof k0, p->stream));
     {
         Tick t(p, KC_SETSTATE);
         CU(launch_set_state(p->st, 1.0, tol, n_max, p->stream));
@@ -2038,13 +1987,6 @@ typedef std::complex<double> zd;
 // Gram-Schmidt over basis vectors U[0..nv) in blocks of 8: GS_DOT returns
 // d_j = (U_j, z) (+ ||z||^2 in *nrm); GS_AXPY applies z <- scale (z - sum c_j U_j)
 // and returns ||z||^2 of the result.  Partial rows summed on the host in CTA order.
-bool gm_always_cgs2() {   // USP_GMRES_CGS2=1: always two passes (the previous behaviour)
-    static const bool v = [] {
-        const char *e = std::getenv("USP_GMRES_CGS2");
-        return e && e[0] == '1';
-    }();
-    return v;
-}
 
 usp_status gs_dots(usp_plan_s *p, int nv, float2 *z, std::vector<zd> &d, double *nrm) {
     d.assign(nv, zd(0.0, 0.0));
@@ -2063,8 +2005,8 @@ usp_status gs_dots(usp_plan_s *p, int nv, float2 *z, std::vector<zd> &d, double 
         CU(launch_gs(GS_DOT, nb, g, p->gm_grid, p->stream));
     }
     std::vector<double> h(region * nblk);
-    CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * region * nblk, cudaMemcpyDeviceToHost, p->stream));
-    CU(cudaStreamSynchronize(p->stream));
+    usp_status rs = readback(p, h.data(), p->gm_part, sizeof(double) * region * nblk);
+    if (rs) return rs;
     for (int bi = 0; bi < nblk; ++bi) {
         const int b0 = 8 * bi, nb = std::min(8, nv - b0);
         const int K = 2 * nb + 1;
@@ -2108,8 +2050,8 @@ usp_status gs_axpy(usp_plan_s *p, int nv, const std::vector<float2 *> &U, const 
             CU(launch_gs(GS_AXPY, nb, g, p->gm_grid, p->stream));
         }
         if (last && nrm) {
-            CU(cudaMemcpyAsync(h.data(), p->gm_part, sizeof(double) * p->gm_grid, cudaMemcpyDeviceToHost, p->stream));
-            CU(cudaStreamSynchronize(p->stream));
+            usp_status rs = readback(p, h.data(), p->gm_part, sizeof(double) * p->gm_grid);
+            if (rs) return rs;
             for (int q = 0; q < p->gm_grid; ++q) s2 += h[q];
             std::vector<double> all;   // slab-decomposed: ranks' norms in rank order
             usp_status st = gather_host(p, &s2, 1, all);
@@ -2149,7 +2091,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->gm_b) return fail(USP_ERR_STATE, "usp_gmres_set_workspace must be called first");
     if (n_max < 0) return fail(USP_ERR_ARG, "need n_max >= 0");
-    if (p->ndim < 2 || p->real || p->anti || p->tdiff || !p->pipe_xk)
+    if (p->ndim < 2 || p->real || p->anti || p->tdiff)
         return fail(USP_ERR_UNSUPPORTED, "GMRES runs on 2-D / 3-D complex64 plans");
     usp_status s = sync_state(p);
     if (s) return s;
@@ -2162,7 +2104,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
     const int m = p->gm_m;
     const long long nvb = (long long)p->nloc * sizeof(float2);
     const double nb = p->st_host->n0;   // ||b||, b = Delta_0 = B (L+1)^-1 s
-    CU(cudaMemcpyAsync(p->gm_b, p->delta, nvb, cudaMemcpyDeviceToDevice, p->stream));
+    CU(launch_copy_bytes(p->gm_b, p->delta, nvb, 4 * p->nsm, p->stream));
     std::vector<double> hist;
     long long steps = 0;
     double est = nb > 0.0 ? 1.0 : 0.0;
@@ -2174,7 +2116,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
         // r = b - M x  (x = 0 on the first cycle: r = b)
         double b2 = 0.0;
         if (first) {
-            CU(cudaMemcpyAsync(p->gm_U[0], p->gm_b, nvb, cudaMemcpyDeviceToDevice, p->stream));
+            CU(launch_copy_bytes(p->gm_U[0], p->gm_b, nvb, 4 * p->nsm, p->stream));
             b2 = nb * nb;
         } else {
             if ((s = apply_M_dev(p, p->x, p->gm_U[0]))) return s;
@@ -2207,7 +2149,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
                 }
                 std::vector<float2 *> Ub(p->gm_U.begin(), p->gm_U.begin() + j + 1);
                 if ((s = gs_axpy(p, j + 1, Ub, c, p->gm_U[j + 1], zd(1.0, 0.0), &z2))) return s;
-                if (round == 0 && z2 >= 0.5 * w2 && !gm_always_cgs2()) break;
+                if (round == 0 && z2 >= 0.5 * w2) break;
             }
             nu[j + 1] = std::sqrt(z2);
             hcol[j + 1] = nu[j + 1] / nu[j];
@@ -2250,11 +2192,15 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
     h.k = steps;
     h.r = est;
     h.status = status == ST_RUNNING ? ST_RUNNING : status;
-    CU(cudaMemcpyAsync(p->st, &h, sizeof h, cudaMemcpyHostToDevice, p->stream));
-    for (size_t i = 0; i < hist.size(); ++i) {
-        const long long kk = (long long)i + 1;
-        CU(cudaMemcpyAsync(p->hist + (kk % p->hist_cap), &hist[i], sizeof(double), cudaMemcpyHostToDevice,
-                           p->stream));
+    if ((s = put_state(p, h))) return s;
+    // history r_1 .. r_steps into the ring through the mapped scratch (contiguous segments)
+    for (size_t i0 = 0; i0 < hist.size();) {
+        const long long pos = (long long)(i0 + 1) % p->hist_cap;
+        const size_t seg = std::min<size_t>({hist.size() - i0, (size_t)(p->hist_cap - pos), kHostMapBytes / 8});
+        CU(cudaStreamSynchronize(p->stream));   // the previous segment's copy has read the scratch
+        std::memcpy(p->hmap, hist.data() + i0, seg * sizeof(double));
+        CU(launch_copy_bytes(p->hist + pos, p->hmap_dev, seg * sizeof(double), 4, p->stream));
+        i0 += seg;
     }
     if ((s = sync_state(p))) return s;
     drain_timing(p);
@@ -2302,7 +2248,7 @@ usp_status usp_iteration_form(usp_plan_t p, int *xform, int *form, double *r_swi
     usp_status s = sync_state(p);
     if (s) return s;
     if (source_lines) *source_lines = p->s_sparse ? p->s_count : 0;
-    if (xform) *xform = (p->xform_cap && !p->chunked) ? 1 : 0;
+    if (xform) *xform = p->xform_cap ? 1 : 0;
     if (form) *form = (p->st_host->form == FORM_DELTA) ? 0 : 1;
     if (r_switch) *r_switch = p->r_sw;
     return USP_OK;
@@ -2323,7 +2269,8 @@ void usp_plan_destroy(usp_plan_t p) {
         cudaStreamDestroy(p->cstream);
         cudaStreamDestroy(p->dstream);
         cudaEventDestroy(p->ev_staged);
-        cudaEventDestroy(p->ev_consumed);
+        cudaEventDestroy(p->ev_med_used);
+        cudaEventDestroy(p->ev_src_used);
         cudaEventDestroy(p->ev_snap);
         cudaEventDestroy(p->ev_out);
     }

@@ -28,7 +28,6 @@ struct IterState {
     unsigned int counter;  // last-block-done counter (reset by the last block)
     int err;               // pipeline watchdog: non-zero = a kernel gave up waiting (see tma.cuh)
     int err_info;
-    int full_iter;         // chunked schedule: the running iteration does the full chain (snapshot by K_C)
     // Algebraic form of the x pass (reading R-30): FORM_DELTA = Delta-form
     // recurrence; FORM_X = Algorithm 1 literally (needs s,
     // 8 fewer bytes per voxel); FORM_PROBE = one pass that computes Delta_k
@@ -50,8 +49,6 @@ struct Red {             // reduction scratch (device)
     double *hist;        // residual ring
     int hist_cap;
     double *local_sum;   // slab-decomposed: the x pass stores its total here (else nullptr)
-    double *chunk_acc;   // chunked schedule: running total over the z-chunk launches (else nullptr)
-    int chunk_first, chunk_last;
 };
 
 // Fourier multiplier data of (L+1)^-1 = F^-1 [c/(D|p|^2 + sigma + c)] F (Eq. 12),
@@ -81,7 +78,6 @@ struct XParams {
     float2 inv_c;        // 1/c (s = S/c)
     IterState *st;
     Red red;
-    int l2hint;          // chunked schedule: stream Delta/x/B evict_first, keep work evict_last
     float2 *s;           // x-form plans: s = S / c (else nullptr)
     // sparse source (R-31): the x pass forms u = B x and k_sadd adds the
     // x-transformed source lines afterwards; X_SRC_FWD flags the source lines
@@ -146,9 +142,7 @@ struct SParams {
     long long nouter;    // outer slabs
     long long ostride;   // elements between outer slabs
     int line_axis;       // 1 = y (2-D, columns = x), 2 = z (3-D, columns = (y, x))
-    int check_state;     // 0: always run; 1: skip unless status == RUNNING && k < kmax;
-                         // 3: as 1, and block 0 snapshots that test into st->full_iter;
-                         // 2: skip unless st->full_iter (chunked schedule, see usp_api.cu)
+    int check_state;     // 0: always run; 1: skip unless status == RUNNING && k < kmax
     MulParams mp;
     IterState *st;
     // slab decomposition (k_stile only; P = 1: natural layout everywhere)
@@ -158,8 +152,6 @@ struct SParams {
     int nz_loc;          // z planes per slab
     int nyl_lg;          // log2(ny / P)
     long long y0;        // global y of this rank's y block (z pass multiplier)
-    long long o0;        // first outer index (plane) of this launch (chunked schedule)
-    int store_hint;      // 0: plain stores; 1: evict_last (K_D: K_A re-reads from L2); 2: evict_first
     int tma_store;       // k_stile: store the upper half of each tile (rows >= N/2; all rows for
                          // N <= 256) through the exchange buffer with tensor-map stores on the
                          // load map (in-place passes whose map describes dst only)
@@ -288,13 +280,16 @@ int xreal_row_pitch(int N);
 int xreal_lines_per_unit(int N);
 
 // launchers (kernels.cu); all return cudaGetLastError()
-cudaError_t launch_xpass(int N, XMode mode, const XParams &p, int grid, cudaStream_t s);
-cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s, int cols = 0);
+cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaStream_t s);   // N = 16, 32
 cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s);
 cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s);
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
+// small host -> device writes as kernel arguments (no copy engine, no pageable-memory copy)
+struct Blob { unsigned char b[512]; };
+cudaError_t launch_put_bytes(void *dst, const void *src, size_t n, cudaStream_t s);
+cudaError_t launch_put_state(IterState *st, const IterState &h, cudaStream_t s);
 cudaError_t launch_set_form(IterState *st, int form, cudaStream_t s);
 cudaError_t launch_copy_bytes(void *dst, const void *src, size_t n, int grid, cudaStream_t s);
 cudaError_t launch_sparse_count(const unsigned char *flag, long long nlines, unsigned *count, cudaStream_t s);
@@ -305,9 +300,6 @@ cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s);
 // TMA-pipelined variants (kernels_pipe.cu)
 cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean = false,
                               bool expect_x = false);
-cudaError_t launch_strided_pipe(int N, SMode mode, int rank, const CUtensorMap &map, const SParams &p, int grid,
-                                cudaStream_t s);
-bool strided_pipe_supported(long long n);
 
 // TMA-prefetched 16-column strided passes (kernels_stile.cu)
 cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s);
@@ -315,14 +307,7 @@ bool stile_supported(long long n);
 int stile_cols(int N);
 int stile_box(int N);
 int stile_ctas_per_sm(int N);
-int strided_pipe_cols(int N);
-int strided_pipe_box(int N);
 
-int xpass_threads(int N);          // threads per CTA of the x pass
-int xpass_lines_per_cta(int N);
-int strided_threads(int N);
-int strided_cols_for(int N);
-size_t xpass_smem(int N);
 bool supported_n(long long n);
 
 }  // namespace usp

@@ -25,6 +25,10 @@ class Split:
     max_abs_V: float
 
 
+def _numel(a) -> int:
+    return int(a.numel()) if hasattr(a, "numel") and callable(a.numel) else int(np.asarray(a).size)
+
+
 def _ptr_where(a, want_dtype):
     """(pointer, where, keepalive) for a torch tensor or numpy array."""
     try:
@@ -60,12 +64,23 @@ class Plan:
 
     ``antisymmetric=True`` solves the antisymmetrised system of Eq. 9-10
     (accretive for any problem, e.g. gain media); ``get_field`` returns x.
+
+    Options (usp_plan_desc; the defaults are the library's):
+    ``delta_form`` (Delta-form recurrence from the first iteration instead of
+    the x-form while r >= ``r_switch``, R-30), ``dense_source`` (no
+    sparse-source x pass, R-31), ``separate_transposes`` (NCCL all-to-all
+    transposes of the slab decomposition instead of the fused peer stores),
+    ``complex_path`` (float32 diffusion data on the complex path),
+    ``launch_per_pass`` (2-D: one launch per pass instead of the persistent
+    solver), ``test_hooks`` (USP_HOOK_* bits; tests only).
     """
 
     def __init__(self, shape: Sequence[int], kind: str = "helmholtz", h: Optional[Sequence[float]] = None,
                  D: float = 1.0, sigma: complex = 0j, c: complex = 1 + 0j, dtype: str = "c64",
                  stream=None, device=None, comm=None, virtual_ranks: int = 0, antisymmetric: bool = False,
-                 tensor_diffusion: bool = False):
+                 tensor_diffusion: bool = False, delta_form: bool = False, r_switch: float = 0.0,
+                 dense_source: bool = False, separate_transposes: bool = False, complex_path: bool = False,
+                 launch_per_pass: bool = False, test_hooks: int = 0):
         import torch
 
         self.lib = L.load()
@@ -93,6 +108,13 @@ class Plan:
         d.virtual_ranks = int(virtual_ranks)
         d.antisymmetric = int(bool(antisymmetric))
         d.tensor_diffusion = int(bool(tensor_diffusion))
+        d.delta_form = int(bool(delta_form))
+        d.r_switch = float(r_switch)
+        d.dense_source = int(bool(dense_source))
+        d.separate_transposes = int(bool(separate_transposes))
+        d.complex_path = int(bool(complex_path))
+        d.launch_per_pass = int(bool(launch_per_pass))
+        d.test_hooks = int(test_hooks)
         if tensor_diffusion:
             d.dtype = L.R32
             self.dtype = "r32"
@@ -110,6 +132,9 @@ class Plan:
         L.check(self.lib.usp_local_extent(self.handle, ctypes.byref(z0), ctypes.byref(nzl)))
         self.z0 = int(z0.value)
         self.local_shape = ((int(nzl.value),) + self.shape[1:]) if self.ndim == 3 else self.shape
+        self.staging = None
+        self._staged_keep = []   # host inputs of pending stage_inputs copies (until set_source("staged"))
+        self._out_keep = []      # host outputs of pending get_field_async copies (until wait_field)
 
     # -- setup ---------------------------------------------------------------
     def stage_inputs(self, medium, source):
@@ -123,15 +148,18 @@ class Plan:
         ps, ws, ks = _ptr_where(source, self.dtype)
         if wm != L.HOST or ws != L.HOST:
             raise ValueError("stage_inputs takes host buffers")
-        self._staged_keep = (km, ks)   # the copies read them asynchronously
+        n = int(np.prod(self.local_shape))
+        if _numel(km) != n or _numel(ks) != n:
+            raise ValueError(f"stage_inputs needs {n} elements per array")
         L.check(self.lib.usp_stage_inputs(self.handle, pm, ps))
+        self._staged_keep.append((km, ks))   # the copies read them asynchronously
 
     def _ensure_staging(self):
-        if getattr(self, "staging", None) is None:
+        if self.staging is None:
             import torch
 
             nbytes = ctypes.c_size_t()
-            L.check(self.lib.usp_staging_size(self.handle, ctypes.byref(nbytes)))
+            L.check(self.lib.usp_staging_size(self.handle, 1, ctypes.byref(nbytes)))   # with the read-back slot
             self.staging = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
             L.check(self.lib.usp_plan_set_staging(self.handle, ctypes.c_void_p(self.staging.data_ptr()),
                                                   int(nbytes.value)))
@@ -144,11 +172,15 @@ class Plan:
         ptr, where, keep = _ptr_where(out, self.dtype)
         if where != L.HOST:
             raise ValueError("get_field_async writes host memory")
-        self._out_keep = keep
+        n = int(np.prod(self.local_shape))
+        if _numel(keep) != n:
+            raise ValueError(f"get_field_async needs a host array of {n} elements, got {_numel(keep)}")
         L.check(self.lib.usp_get_field_async(self.handle, ptr))
+        self._out_keep.append(keep)   # alive until wait_field()
 
     def wait_field(self):
         L.check(self.lib.usp_wait_field(self.handle))
+        self._out_keep.clear()
 
     def set_potential(self, medium, target_norm: float = 0.95):
         if isinstance(medium, str) and medium == "staged":
@@ -189,6 +221,10 @@ class Plan:
     def set_source(self, src):
         if isinstance(src, str) and src == "staged":
             L.check(self.lib.usp_set_source(self.handle, None, L.STAGED))
+            # usp_set_source returns after its setup ran on the plan stream: the
+            # oldest staged pair has been copied from the host
+            if self._staged_keep:
+                self._staged_keep.pop(0)
             return
         ptr, where, keep = _ptr_where(src, self.dtype)
         L.check(self.lib.usp_set_source(self.handle, ptr, where))

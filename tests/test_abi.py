@@ -37,7 +37,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_version_and_error_strings(lib):
-    assert lib.usp_version().startswith(b"0.2")
+    assert lib.usp_version().startswith(b"0.3")
     assert isinstance(lib.usp_last_error(), bytes)
 
 
@@ -75,3 +75,25 @@ def test_product_does_not_touch_oracle():
     for f in os.listdir(os.path.join(ROOT, "oracle")):
         if f.endswith((".py", ".c", ".h")):
             assert not bad_orc.search(open(os.path.join(ROOT, "oracle", f)).read()), f
+
+
+def test_no_environment_switches_in_the_product():
+    """What a plan computes is chosen by usp_plan_desc fields, not by the
+    environment: the only getenv in the library is the NCCL path hint."""
+    csrc = os.path.join(ROOT, "paper_2207_14222_b200", "csrc")
+    hits = []
+    for f in sorted(os.listdir(csrc)):
+        txt = open(os.path.join(csrc, f), errors="replace").read()
+        hits += [(f, m) for m in re.findall(r"getenv\(\s*\"([A-Z0-9_]+)\"", txt)]
+    assert hits == [("usp_api.cu", "USP_NCCL_LIB")], hits
+
+
+def test_desc_binding_matches_header():
+    """The ctypes PlanDesc mirrors usp_plan_desc field by field."""
+    from paper_2207_14222_b200 import _lib
+
+    src = open(os.path.join(ROOT, "include", "usp.h")).read()
+    body = src[src.index("typedef struct {\n    int ndim;"):src.index("} usp_plan_desc;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = re.findall(r"\b([A-Za-z_0-9]+)(?:\[\d\])?;", body)
+    assert names == [f[0] for f in _lib.PlanDesc._fields_]

@@ -4,7 +4,7 @@ float32 data (BASELINE.json config C4, §3.2) runs on half spectra
 instead of 104 B per voxel and iteration.
 
 * vs the oracle (complex128) after the same count: relative L2 <= 1e-4;
-* vs the complex path on the same input (USP_REAL=0): same iterate to fp32
+* vs the complex path on the same input (desc.complex_path): same iterate to fp32
   rounding;
 * closed form for constant mu_a (every Fourier mode decouples);
 * the slab decomposition of the real path (virtual slabs) is bit-identical
@@ -25,13 +25,13 @@ def _cuda():
         pytest.fail("CUDA GPU required for -m gpu tests")
 
 
-def _run(p, n, virtual_ranks=0, tol=0.0):
+def _run(p, n, virtual_ranks=0, tol=0.0, **opts):
     import torch
     from paper_2207_14222_b200 import Plan
 
     med, src, dtype = rounded_inputs(p)
     assert dtype == "r32"
-    plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype, virtual_ranks=virtual_ranks)
+    plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype, virtual_ranks=virtual_ranks, **opts)
     plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
     plan.set_source(torch.from_numpy(src).cuda())
     nd, term = plan.iterate(n, p.alpha, tol)
@@ -60,14 +60,13 @@ def test_real_path_matches_oracle(orc, shape, n):
     assert np.allclose(plan.history()[:n], res.hist[:n], rtol=1e-3, atol=0.0)
 
 
-def test_real_path_equals_complex_path(monkeypatch):
+def test_real_path_equals_complex_path():
     from synth import make
 
     p = make("C4", (64, 128, 64))
-    monkeypatch.setenv("USP_XFORM", "0")   # the same (Delta-form) arithmetic on both paths
-    xr, _, _, pr = _run(p, 50)
-    monkeypatch.setenv("USP_REAL", "0")
-    xc, _, _, pc = _run(p, 50)
+    # the same (Delta-form) arithmetic on both paths
+    xr, _, _, pr = _run(p, 50, delta_form=True)
+    xc, _, _, pc = _run(p, 50, delta_form=True, complex_path=True)
     assert _ws_bytes(pr) < 0.7 * _ws_bytes(pc)
     assert rel_l2(xr.astype(np.float64), xc.astype(np.float64)) <= 2e-6
     assert np.allclose(pr.history(), pc.history(), rtol=1e-5, atol=0.0)

@@ -26,12 +26,12 @@ def _cuda():
         pytest.fail("CUDA GPU required for -m gpu tests")
 
 
-def _run(p, n, virtual_ranks, tol=0.0):
+def _run(p, n, virtual_ranks, tol=0.0, **opts):
     import torch
     from paper_2207_14222_b200 import Plan
 
     med, src, dtype = rounded_inputs(p)
-    plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype, virtual_ranks=virtual_ranks)
+    plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype, virtual_ranks=virtual_ranks, **opts)
     plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
     plan.set_source(torch.from_numpy(src).cuda())
     nd, term = plan.iterate(n, p.alpha, tol)
@@ -43,16 +43,15 @@ def _run(p, n, virtual_ranks, tol=0.0):
                                             ("C5", (64, 128, 64), 8, 20), ("C4", (64, 64, 128), 2, 30),
                                             ("C3", (256, 128, 64), 2, 10), ("C3", (64, 64, 64), 16, 10),
                                             ("C5", (2048, 64, 32), 8, 6)])
-def test_virtual_slabs_bit_identical_to_one_slab(name, shape, P, n, fused, monkeypatch):
+def test_virtual_slabs_bit_identical_to_one_slab(name, shape, P, n, fused):
     """fused = transposes in the K_B / K_C stores (peer-memory path; P <= 8);
     0 = separate transposes (device copies standing in for the NCCL
     all-to-alls)."""
     from synth import make
 
-    monkeypatch.setenv("USP_FUSED", fused)
     p = make(name, shape)
     x1, n1, _, pl1 = _run(p, n, 0)
-    xp, n_p, _, plp = _run(p, n, P)
+    xp, n_p, _, plp = _run(p, n, P, separate_transposes=fused == "0")
     assert n1 == n_p == n
     assert plp.local_shape == tuple(shape) and plp.z0 == 0
     assert np.array_equal(x1.view(np.uint8), xp.view(np.uint8)), rel_l2(xp.astype(np.complex128), x1.astype(np.complex128))
@@ -183,8 +182,7 @@ def test_rank_finish_path_with_xform_switch(monkeypatch):
         med, src, _ = rounded_inputs(p)
         x1, n1, t1, pl1 = _run(p, 2000, 0, tol=1e-6)
         comm = comm_init()
-        monkeypatch.setenv("USP_FORCE_FINISH", "1")
-        plan = Plan(p.shape, comm=comm)
+        plan = Plan(p.shape, comm=comm, test_hooks=1)   # USP_HOOK_RANK_FINISH
         plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
         plan.set_source(torch.from_numpy(src).cuda())
         n, term = plan.iterate(7, p.alpha, 0.0)
@@ -201,27 +199,3 @@ def test_rank_finish_path_with_xform_switch(monkeypatch):
     finally:
         if own:
             dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("G", [4, 16])
-def test_chunked_schedule_matches_four_pass(G, monkeypatch):
-    """The experimental chunked schedule (USP_CHUNK=G: K_C, then K_D/K_A/K_B
-    per z-chunk) computes the same iterate as the 4-pass schedule up to the
-    residual summation order, across resumed iterate() calls."""
-    from synth import make
-
-    p = make("C3", (64, 64, 64))
-    x0, _, _, pl0 = _run(p, 25, 0)
-    monkeypatch.setenv("USP_CHUNK", str(G))
-    import torch
-    from paper_2207_14222_b200 import Plan
-
-    med, src, dtype = rounded_inputs(p)
-    plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype)
-    plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
-    plan.set_source(torch.from_numpy(src).cuda())
-    for k in (1, 9, 15):
-        plan.iterate(k, p.alpha, 0.0)
-    x = plan.get_field().cpu().numpy()
-    assert rel_l2(x.astype(np.complex128), x0.astype(np.complex128)) <= 1e-6
-    assert np.allclose(plan.history(), pl0.history(), rtol=1e-6, atol=0.0)

@@ -24,12 +24,11 @@ def orc():
     return O
 
 
-def _plan(p, monkeypatch, xform):
+def _plan(p, monkeypatch, xform, **opts):
     from paper_2207_14222_b200 import Plan
 
-    monkeypatch.setenv("USP_XFORM", "1" if xform else "0")
     _, _, dtype = rounded_inputs(p)
-    return Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype)
+    return Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype=dtype, delta_form=not xform, **opts)
 
 
 @pytest.mark.parametrize("shape,n", [((32, 32, 32), 40), ((64, 32, 128), 25)])
@@ -141,8 +140,7 @@ def test_sparse_source_xform(monkeypatch):
     pa = _plan(p, monkeypatch, True)
     xa, na, _, _ = run_gpu(p, n_iter=30, tol=0.0, plan=pa)
     assert pa.source_lines() == 1
-    monkeypatch.setenv("USP_SPARSE_S", "0")
-    pb = _plan(p, monkeypatch, True)
+    pb = _plan(p, monkeypatch, True, dense_source=True)
     xb, nb, _, _ = run_gpu(p, n_iter=30, tol=0.0, plan=pb)
     assert pb.source_lines() == 0
     pd = _plan(p, monkeypatch, False)
@@ -154,7 +152,6 @@ def test_sparse_source_xform(monkeypatch):
     xu, nu, tu, _ = run_gpu(p, n_iter=3000, tol=1e-6, plan=pd)
     assert tt == tu == "converged" and abs(nt - nu) <= TOL_COUNT and rel_l2(xt, xu) <= 1e-4
     # a source on many lines stays dense
-    monkeypatch.delenv("USP_SPARSE_S")
     rng = np.random.default_rng(5)
     med, src, _ = rounded_inputs(p)
     src = (rng.standard_normal(src.shape) + 1j * rng.standard_normal(src.shape)).astype(np.complex64)

@@ -1,14 +1,13 @@
-"""In-process A/B of library builds (and env switches) on the C5 1024^3 iteration.
+"""In-process A/B of library builds on the C5 1024^3 iteration.
 
-    python tools/gpu/kab.py LIB_A.so[:ENV=V,...] LIB_B.so[:ENV=V,...] ... [--rounds 4] [--iters 20] [--size 1024]
+    python tools/gpu/kab.py LIB_A.so LIB_B.so ... [--rounds 4] [--iters 20] [--size 1024]
 
 Each variant gets its own plan (own copy of the library: ctypes handles and
 static state are per file, so copy a build to a distinct name first);
 variants are run round-robin `--rounds` times so clock/thermal drift hits
 them alike, and per-kernel device times (usp_profile_read) are reported as
-the median over rounds.  Env switches are set before each variant's
-iterate() (the library reads USP_* switches it caches on first use, so only
-per-call switches can differ between variants sharing a file).
+the median over rounds.  (Builds come from tools/build_variant.py, e.g.
+from another git revision of csrc/.)
 """
 import argparse
 import ctypes
