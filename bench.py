@@ -40,34 +40,38 @@ sys.path.insert(0, ROOT)
 METRIC = "voxel-iterations/s (device-timed) and % of HBM roofline at 1/2/4/8 B200"
 UNIT = "voxel-iterations/s"
 
-# Algorithmic HBM bytes per voxel and launch of each kernel class (DESIGN.md
-# "Kernels and their rooflines"): complex64 = 8 B per value.
-KERNEL_BYTES = {
-    "xpass": 56,            # read work, Delta, x, B; write Delta, x, work
-    "y_fwd": 16,            # read + write work
-    "z_fwd_mul_inv": 16,
-    "y_inv": 16,
-    "y_fwd_mul_inv": 16,
-}
-ITER_BYTES_3D = 104         # 56 + 3 * 16 (SURVEY.md §8 geometry table)
-# x-form plans (reading R-30): Algorithm 1 literally; the x pass
-# reads work, s, x, B and writes x, work (its end-of-call probe moves the
-# same bytes: writes Delta instead of x)
-XFORM_XPASS_BYTES = 48
-ITER_BYTES_3D_XFORM = 96
-XFORM_XPASS_BYTES_REAL = 24     # real path: Delta (4 B) neither read nor written, s (4 B) read
-ITER_BYTES_REAL_XFORM = 48
-# sparse source (reading R-31: the source on <= 64 x-lines): the x-form pass
-# does not read s at all -- reads work, x, B, writes x, work
-XFORM_XPASS_BYTES_SPARSE = 40
-ITER_BYTES_3D_XFORM_SPARSE = 88
-# Real path (C4 diffusion, float32 fields, half spectra; SURVEY.md §8 geometry
-# table): x pass reads x, Delta, B (4 B each) + half spectrum (4) and writes
-# x, Delta (4 each) + half spectrum (4); each strided pass moves the half
-# spectrum once each way (8).  (The 16 padding columns per spectrum row add
-# 16/(nx/2) to the spectrum bytes; they are counted as overhead, not work.)
-KERNEL_BYTES_REAL = {"xpass": 28, "y_fwd": 8, "z_fwd_mul_inv": 8, "y_inv": 8}
-ITER_BYTES_REAL = 52
+# Algorithmic HBM bytes per voxel and iteration of each kernel class
+# (complex64 = 8 B, float32 = 4 B
+# per value), by the algebraic form the x pass ran (reading R-30 / R-31):
+#   x_sparse  Algorithm 1 literally, source on <= 64 x-lines (s not read)
+#   x_dense   Algorithm 1 literally, s read densely
+#   delta     the Delta-form recurrence
+# x pass (K_A): read work + x + B (+ s | + Delta), write x + work (+ Delta).
+# Each strided pass (K_B, K_C, K_D) reads and writes work once (16 B).
+# The plane-chained pass (kernels_plane.cu, NEXT-4) runs K_D, K_A and K_B
+# with work L2-resident in between: HBM sees K_D's read and K_B's write of
+# work (16 B) plus the x pass's operands.
+XPASS_BYTES = {"x_sparse": 40, "x_dense": 48, "delta": 56}
+PLANE_BYTES = {"x_sparse": 40, "x_dense": 48, "delta": 56}
+STRIDED_BYTES = 16
+# real path (C4 diffusion, float32 fields, half spectra; the 16 padding
+# columns per spectrum row are overhead, not work)
+XPASS_BYTES_REAL = {"x_sparse": 24, "x_dense": 24, "delta": 28}
+STRIDED_BYTES_REAL = 8
+
+
+def bytes_model(schedule, real):
+    """(kernel -> {form -> B/voxel}, iteration {form -> B/voxel})."""
+    if real:
+        k = {"xpass": XPASS_BYTES_REAL, "y_fwd": STRIDED_BYTES_REAL, "z_fwd_mul_inv": STRIDED_BYTES_REAL,
+             "y_inv": STRIDED_BYTES_REAL}
+    elif schedule == "plane":
+        k = {"plane_dab": PLANE_BYTES, "z_fwd_mul_inv": STRIDED_BYTES}
+    else:
+        k = {"xpass": XPASS_BYTES, "y_fwd": STRIDED_BYTES, "z_fwd_mul_inv": STRIDED_BYTES, "y_inv": STRIDED_BYTES}
+    forms = ("x_sparse", "x_dense", "delta")
+    it = {f: sum(v[f] if isinstance(v, dict) else v for v in k.values()) for f in forms}
+    return k, it
 
 
 def env_int(name, default):
@@ -308,6 +312,122 @@ def slab_selfcheck(comm, world, rank, dev, separate, n_iter=8, shape=(128, 128, 
     return float(err.item())
 
 
+def host_cpu():
+    """CPU model and core count of the host (lscpu), for the cpu_baseline."""
+    model, cores = None, os.cpu_count()
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return model, cores
+
+
+def timed_iterations(plan, stream, n, alpha=0.75, warm=3):
+    """Device time per iteration of n iterations (after `warm`), kernel-class
+    profile, and the form summary of the plan."""
+    import torch
+
+    plan.iterate(warm, alpha, 0.0)
+    plan.profile(True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    nd, _ = plan.iterate(n, alpha, 0.0)
+    b.record(stream)
+    torch.cuda.synchronize()
+    prof = plan.profile_read()
+    plan.profile(False)
+    return a.elapsed_time(b) / nd, prof
+
+
+def variant_rooflines(dev, stream, med, src, p, hbm, n=20):
+    """The same C5 problem on other plan options, each timed over n
+    iterations: the general case (Delta-form, s read densely: what a dense
+    source or a converging solve runs), and the 4-pass schedule (SURVEY.md
+    §8 geometry table) next to the default plane-chained pass."""
+    import torch
+    from paper_2207_14222_b200 import Plan
+
+    nloc = med.numel()
+    out = {}
+    for key, opts, form, desc in (
+            ("general_delta_dense", {"delta_form": True, "dense_source": True}, "delta",
+             "Delta-form (P:L613), s read densely"),
+            ("four_pass_xform_sparse", {"four_pass": True}, "x_sparse",
+             "x-form, sparse source, 4-pass schedule (K_B, K_C, K_D, K_A)"),
+            ("four_pass_general", {"four_pass": True, "delta_form": True, "dense_source": True}, "delta",
+             "Delta-form, s read densely, 4-pass schedule")):
+        with torch.cuda.stream(stream):
+            plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev, **opts)
+            plan.set_potential(med, 0.95)
+            plan.set_source(src)
+            ms, prof = timed_iterations(plan, stream, n)
+            plan.close()
+            del plan
+            torch.cuda.empty_cache()
+        sched = "plane" if "plane_dab" in prof else "4-pass"
+        kmodel, itmodel = bytes_model(sched, False)
+        bpv = itmodel[form]
+        kern = {k: round(v[0] / v[1], 4) for k, v in prof.items() if k in kmodel}
+        dk = max(kern, key=lambda k: kern[k] * prof[k][1])
+        kb = kmodel[dk] if not isinstance(kmodel[dk], dict) else kmodel[dk][form]
+        out[key] = {"form": desc, "schedule": sched, "bytes_per_voxel": bpv, "iter_ms": ms,
+                    "achieved_gbs": bpv * nloc / (ms / 1e3) / 1e9, "frac": bpv * nloc / (ms / 1e3) / 1e9 / hbm,
+                    "value": nloc / (ms / 1e3), "kernel_ms_per_launch": kern,
+                    "dominant": {"kernel": dk, "bytes_per_voxel": kb, "ms": kern[dk],
+                                 "frac": kb * nloc / (kern[dk] / 1e3) / 1e9 / hbm}}
+    return out
+
+
+def c4_line(dev, hbm, n_iter=200):
+    """BASELINE.json C4 (512^3 float32 diffusion, the real half-spectrum
+    path), one step of 200 iterations after a warm-up step, device-timed."""
+    import torch
+    from paper_2207_14222_b200 import Plan
+    from synth import make
+
+    p = make("C4", None, device=str(dev))
+    med, src = p.medium.to(torch.float32), p.source.to(torch.float32)
+    p.medium = p.source = None
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, dtype="r32", stream=stream, device=dev)
+        for rep in range(2):
+            plan.set_potential(med, 0.95)
+            plan.set_source(src)
+            if rep == 1:
+                plan.profile(True)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            nd, _ = plan.iterate(n_iter, p.alpha, 0.0)
+            b.record(stream)
+            torch.cuda.synchronize()
+        prof = plan.profile_read()
+        h = plan.history()
+        xf_plan, _, r_sw = plan.iteration_form()
+        plan.close()
+    ms = a.elapsed_time(b)
+    nvox = med.numel()
+    below = [k for k, r in enumerate(h[:n_iter]) if r < r_sw]
+    n_x = (min(n_iter, below[0] + 1) if below else n_iter) if xf_plan else 0
+    fx = n_x / n_iter
+    kmodel, itmodel = bytes_model("4-pass", True)
+    bpv = fx * itmodel["x_dense"] + (1 - fx) * itmodel["delta"]
+    it_ms = ms / n_iter
+    kx = fx * kmodel["xpass"]["x_dense"] + (1 - fx) * kmodel["xpass"]["delta"]
+    xms = prof["xpass"][0] / n_iter
+    return {"workload": "C4 3-D diffusion 512x512x512 float32 (half-spectrum real path), 200 iterations",
+            "value": nvox * n_iter / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "iteration_form": f"x-form for {n_x} of {n_iter} iterations, then Delta-form",
+            "iteration_roofline": {"bytes_per_voxel": bpv, "iter_ms": it_ms,
+                                   "achieved_gbs": bpv * nvox / (it_ms / 1e3) / 1e9,
+                                   "frac": bpv * nvox / (it_ms / 1e3) / 1e9 / hbm},
+            "xpass_roofline": {"bytes_per_voxel": kx, "ms": xms, "frac": kx * nvox / (xms / 1e3) / 1e9 / hbm},
+            "kernel_ms_per_launch": {k: round(v[0] / v[1], 4) for k, v in prof.items()}}
+
+
 def run_usp(args, world, rank, local):
     import numpy as np
     import torch
@@ -410,8 +530,8 @@ def run_usp(args, world, rank, local):
     # its device time per iteration
     hbm, peak_kind = peaks()
     n_it_total = n_iter * args.steps
-    schedule = "4-pass"
-    kbytes = dict(KERNEL_BYTES_REAL if real else KERNEL_BYTES)
+    schedule = "plane" if "plane_dab" in prof else "4-pass"
+    kmodel, itmodel = bytes_model(schedule, real)
     # which algebraic form ran: every timed step starts from set_source (x-form
     # on x-form plans) and ends still in the x-form unless r fell below r_switch
     xform_plan, xform_now, r_switch = plan.iteration_form()
@@ -426,13 +546,17 @@ def run_usp(args, world, rank, local):
         n_x = min(n_iter, below[0] + 1) if below else n_iter
     fx = n_x / n_iter
     sparse_lines = plan.source_lines()
-    xb = XFORM_XPASS_BYTES_REAL if real else (XFORM_XPASS_BYTES_SPARSE if sparse_lines else XFORM_XPASS_BYTES)
-    kbytes["xpass"] = fx * xb + (1 - fx) * kbytes["xpass"]
+    xf = "x_sparse" if sparse_lines else "x_dense"
+
+    def mix(v):
+        return v if not isinstance(v, dict) else fx * v[xf] + (1 - fx) * v["delta"]
+
+    kbytes = {k: mix(v) for k, v in kmodel.items()}
     form_desc = ("x-form (Algorithm 1 literally) throughout" +
                  (f", source on {sparse_lines} x-line(s) (s not streamed)" if sparse_lines else "") if xform_all else
                  (f"x-form for {n_x} of {n_iter} iterations, then Delta-form below r_switch = {r_switch:g}"
                   if xform_plan else "Delta-form"))
-    dname = "xpass" if "xpass" in prof else max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
+    dname = max((k for k in prof if k in kbytes), key=lambda k: prof[k][0])
     dms, dcount = prof[dname]
     d_ms_per_iter = dms / n_it_total
     dbytes = int(kbytes[dname] * nloc)              # per iteration (= per launch)
@@ -443,6 +567,10 @@ def run_usp(args, world, rank, local):
     # iteration time: device time of the iterate() calls / iterations
     iter_ms = sum(a.elapsed_time(b) for a, b in it_events) / n_it_total
     kernel_share = {k: round(v[0] / sum(x[0] for x in prof.values()), 4) for k, v in prof.items()}
+
+    variants = None
+    if world == 1 and not args.no_variants and name == "C5" and mode == "1 GPU" and args.size is None:
+        variants = variant_rooflines(dev, stream, med, src, p, hbm)
 
     # ------------------------------------------------ e2e (host buffers)
     e2e = None
@@ -509,21 +637,24 @@ def run_usp(args, world, rank, local):
 
     if rank != 0:
         return 0
+    plan.close()   # the remaining measurements allocate their own plans
+    del plan
+    torch.cuda.empty_cache()
     solvers = None
     if world == 1 and not args.no_solvers and name == "C5":
-        del plan
-        torch.cuda.empty_cache()
         solvers = solver_comparison(dev)
+    c4 = None
+    if world == 1 and not args.no_variants and name == "C5" and args.size is None:
+        c4 = c4_line(dev, hbm)
     cpu = None
     if world == 1 and not args.no_cpu:
         v, dt, thr, desc = cpu_oracle_sample()
-        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2)}
+        model, ncpu = host_cpu()
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": desc, "seconds": round(dt, 2),
+               "cpu_model": model, "nproc": ncpu}
     # separate transposes (NCCL all-to-all / device copies) add their staging
     # reads and writes; the fused (peer-store) transposes add nothing to HBM
-    base_bpv = ITER_BYTES_REAL if real else ITER_BYTES_3D
-    xform_bpv = ITER_BYTES_REAL_XFORM if real else (ITER_BYTES_3D_XFORM_SPARSE if sparse_lines else ITER_BYTES_3D_XFORM)
-    iter_bpv = fx * xform_bpv + (1 - fx) * base_bpv + \
-        ((16 if real else 32) if "all_to_all" in prof else 0)
+    iter_bpv = mix(itmodel) + ((16 if real else 32) if "all_to_all" in prof else 0)
     it_bytes = iter_bpv * nloc
     parallelism = {"1 GPU": "1 GPU", "replicas": f"{world} independent replicas",
                    "slabs": f"{world} z-slabs, transposes: {transposes} (self-check first)",
@@ -556,6 +687,8 @@ def run_usp(args, world, rank, local):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "solvers_to_tol": solvers,
+        "variants": variants,
+        "c4_real_path": c4,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -575,6 +708,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of slabs")
     ap.add_argument("--no-solvers", action="store_true", help="skip the C3 fixed-point vs BiCGSTAB comparison")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the general-case / 4-pass rooflines and the C4 line")
     ap.add_argument("--separate-transposes", action="store_true",
                     help="slab decomposition: NCCL all-to-all transposes instead of the fused peer stores")
     ap.add_argument("--virtual-ranks", type=int, default=0,

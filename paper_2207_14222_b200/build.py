@@ -12,8 +12,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libusp.so")
-SOURCES = ["kernels.cu", "kernels_pipe.cu", "kernels_stile.cu", "kernels_real.cu", "kernels_krylov.cu", "kernels_small.cu", "kernels_anti.cu", "kernels_tdiff.cu", "usp_api.cu"]
-HEADERS = ["fft_core.cuh", "kcommon.cuh", "tma.cuh", "usp_internal.h", "tw64.h"]
+SOURCES = ["kernels.cu", "kernels_pipe.cu", "kernels_stile.cu", "kernels_real.cu", "kernels_krylov.cu", "kernels_small.cu", "kernels_anti.cu", "kernels_tdiff.cu", "kernels_plane.cu", "usp_api.cu"]
+HEADERS = ["fft_core.cuh", "kcommon.cuh", "stile_core.cuh", "tma.cuh", "usp_internal.h", "tw64.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <complex>
@@ -127,11 +128,11 @@ Nccl &nccl() {
 
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
               KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_BARRIER, KC_XOP,
-              KC_KUPD, KC_SOLVE2D, KC_SADD, KC_N };
+              KC_KUPD, KC_SOLVE2D, KC_SADD, KC_PLANE, KC_N };
 const char *kc_names[KC_N] = {"xpass", "y_fwd", "z_fwd_mul_inv", "y_inv", "y_fwd_mul_inv",
                               "solve1d", "potential", "farthest", "set_state", "xpass_setup",
                               "all_to_all", "finish", "allgather", "rank_barrier", "krylov_xop",
-                              "krylov_update", "solve2d", "sparse_source_add"};
+                              "krylov_update", "solve2d", "sparse_source_add", "plane_dab"};
 
 struct Timed {
     int cls;
@@ -190,6 +191,13 @@ struct usp_plan_s {
     TDParams td{};
     // persistent 2-D solve (kernels_small.cu; desc.launch_per_pass disables)
     bool solve2d = false;
+    // plane-chained pass (kernels_plane.cu, NEXT-4; desc.four_pass disables): an
+    // iteration is K_C + one persistent K_D -> K_A -> K_B kernel; unit counter,
+    // per-plane done counters, per-unit residual partials
+    bool plane = false;
+    unsigned long long *pl_ctr = nullptr;
+    unsigned *pl_done = nullptr;
+    double *pl_part = nullptr;
     // x-form passes while r >= r_sw (reading R-30; desc.delta_form disables,
     // desc.r_switch sets r_sw): s = S / c kept in its own field
     bool xform_cap = false, xform = false, probe_needed = false;
@@ -274,11 +282,20 @@ cudaEvent_t get_event(usp_plan_s *p) {
     return e;
 }
 
-struct Tick {   // brackets one launch with events when profiling
+// NVTX range over a host-side scope (an ABI call, a launch): a timeline tool
+// (nsys, ncu --nvtx) shows which call / kernel class issued what; without a
+// tool attached a push/pop is a no-op call.
+struct Range {
+    explicit Range(const char *name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
+
+struct Tick {   // brackets one launch with events when profiling, and with an NVTX range
     usp_plan_s *p;
     int cls;
     cudaEvent_t a = nullptr;
     Tick(usp_plan_s *pl, int c, bool count = true) : p(pl), cls(c) {
+        nvtxRangePushA(kc_names[c]);
         if (count) ++p->launches;
         if (p->prof) {
             a = get_event(p);
@@ -286,6 +303,7 @@ struct Tick {   // brackets one launch with events when profiling
         }
     }
     ~Tick() {
+        nvtxRangePop();
         if (p->prof) {
             cudaEvent_t b = get_event(p);
             cudaEventRecord(b, p->stream);
@@ -633,6 +651,40 @@ usp_status sparse_add(usp_plan_s *p) {
     sa.st = p->st;
     Tick t(p, KC_SADD);
     CU(launch_sparse_add(sa, p->stream));
+    return USP_OK;
+}
+
+SParams sparams(usp_plan_s *p, float2 *data, float2 *dst, const float2 *tw, long long stride, long long ncols,
+                long long nouter, long long ostride, int line_axis, int check_state, int map_rank);
+usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, const SParams &sp, const CUtensorMap &map,
+                       bool use_stile, int grid_short);
+
+// plane-chained schedule: K_C over the volume (z forward, g(p), z inverse),
+// then the persistent K_D -> K_A -> K_B kernel (kernels_plane.cu)
+usp_status plane_iteration(usp_plan_s *p) {
+    SParams zm = sparams(p, p->work, p->work, p->tw[2], p->rp * p->ny, p->rp * p->ny, 1, 0, 2, 1, 2);
+    usp_status s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, p->stile_z, p->grid_z);
+    if (s) return s;
+    PParams pp{};
+    pp.work = p->work;
+    pp.x = p->x;
+    pp.delta = p->delta;
+    pp.B = p->B;
+    pp.s = p->xform ? p->s : nullptr;
+    pp.tw = p->tw[0];
+    pp.nz = p->nz;
+    pp.s_sparse = p->s_sparse ? 1 : 0;
+    pp.s_list = reinterpret_cast<const int *>(p->s);
+    pp.s_comp = p->s ? p->s + 256 : nullptr;
+    pp.s_count = p->s_count;
+    pp.ctr = p->pl_ctr;
+    pp.d_done = p->pl_done;
+    pp.a_done = p->pl_done + p->nz;
+    pp.upart = p->pl_part;
+    pp.st = p->st;
+    pp.red = red_params(p);
+    Tick t(p, KC_PLANE);
+    CU(launch_plane(p->smap_y, pp, p->nsm, p->stream, p->s_sparse && p->expect_x, p->xform && p->expect_x));
     return USP_OK;
 }
 
@@ -991,9 +1043,10 @@ usp_status sync_state(usp_plan_s *p) {
 // Tensor maps of the strided passes (they embed the workspace addresses).
 void build_maps(usp_plan_s *p) {
     p->stile_y = p->stile_z = false;
-    if (p->ndim < 2 || !stile_supported(p->ny)) return;
+    if (p->ndim < 2) return;
     const cuuint32_t cy = (cuuint32_t)stile_cols((int)p->ny), by = (cuuint32_t)stile_box((int)p->ny);
     if (p->ndim == 2) {
+        if (!stile_supported(p->ny)) return;
         const cuuint64_t dims[2] = {(cuuint64_t)p->rp, (cuuint64_t)(p->ny * p->ncomp)};
         const cuuint64_t str[1] = {(cuuint64_t)p->rp * 8};
         const cuuint32_t box[2] = {cy, by};
@@ -1001,7 +1054,7 @@ void build_maps(usp_plan_s *p) {
         return;
     }
     const long long comps = p->ncomp;   // multi-component fields: the components as extra planes
-    {   // y pass over the planes held here: {x, y, z}
+    if (stile_supported(p->ny)) {   // y pass over the planes held here: {x, y, z}
         const cuuint64_t dims[3] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny, (cuuint64_t)(p->nzh * comps)};
         const cuuint64_t str[2] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->rp * p->ny) * 8};
         const cuuint32_t box[3] = {cy, by, 1};
@@ -1200,6 +1253,15 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->bar, sizeof(unsigned) * 2));
     TRY(cudaMemset(p->bar, 0, sizeof(unsigned) * 2));
     p->solve2d = !p->anti && !p->tdiff && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !desc->launch_per_pass;
+    p->plane = !desc->four_pass && P == 1 && p->ndim == 3 && !p->real && !p->anti && !p->tdiff && p->nx == kPlaneN &&
+               p->ny == kPlaneN && stile_supported(p->nz);
+    if (p->plane) {
+        TRY(cudaMalloc(&p->pl_ctr, sizeof(unsigned long long)));
+        TRY(cudaMemset(p->pl_ctr, 0, sizeof(unsigned long long)));
+        TRY(cudaMalloc(&p->pl_done, sizeof(unsigned) * 2 * p->nz));
+        TRY(cudaMemset(p->pl_done, 0, sizeof(unsigned) * 2 * p->nz));
+        TRY(cudaMalloc(&p->pl_part, sizeof(double) * 64 * p->nz));
+    }
     p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && !desc->delta_form;
     if (desc->r_switch > 0.0) p->r_sw = desc->r_switch;
     p->force_finish = (desc->test_hooks & USP_HOOK_RANK_FINISH) != 0;
@@ -1308,6 +1370,7 @@ usp_status usp_local_extent(usp_plan_t p, int64_t *z0, int64_t *nz_local) {
 }
 
 usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, double target_norm) {
+    Range nvtx_range("usp_set_potential");
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     bool from_stage = false;
     if (where == USP_STAGED) {   // the medium staged by usp_stage_inputs
@@ -1393,6 +1456,7 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
 }
 
 usp_status usp_set_tensor_medium(usp_plan_t p, const float *mu, const float *D, usp_where where, double target_norm) {
+    Range nvtx_range("usp_set_tensor_medium");
     if (!p || !mu || !D) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->tdiff) return fail(USP_ERR_STATE, "the plan was not created with desc.tensor_diffusion");
     if (!p->ws) return fail(USP_ERR_STATE, "workspace not set");
@@ -1499,6 +1563,7 @@ usp_status usp_get_split(usp_plan_t p, usp_c128 *sigma, usp_c128 *c, usp_c128 *c
 }
 
 usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
+    Range nvtx_range("usp_set_source");
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     const bool from_stage = where == USP_STAGED;
     if (where != USP_HOST && where != USP_DEVICE && !from_stage) return fail(USP_ERR_ARG, "bad where");
@@ -1586,6 +1651,10 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
                 p->expect_x = true;
             }
         }
+        if (p->plane) {   // the plane-chained invariant: work = FFT_y FFT_x (u_0)
+            SParams yf = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, p->nz, p->rp * p->ny, 1, 0, 3);
+            if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, p->stile_y, p->grid_y))) return s;
+        }
     }
     s = sync_state(p);
     if (s) return s;
@@ -1607,6 +1676,7 @@ usp_status probe_xform(usp_plan_s *p) {
         Tick t(p, KC_SETSTATE);
         CU(launch_set_form(p->st, FORM_PROBE, p->stream));
     }
+    if (p->plane) return plane_iteration(p);
     if ((s = chain_mid(p, 1))) return s;
     if ((s = run_xpass(p, X_ITER, x_params(p)))) return s;
     return sparse_add(p);
@@ -1616,6 +1686,7 @@ usp_status probe_xform(usp_plan_s *p) {
 extern "C" {
 
 usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, int64_t *n_done, usp_term *term) {
+    Range nvtx_range("usp_iterate");
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (n_max < 0 || !(alpha > 0.0)) return fail(USP_ERR_ARG, "need n_max >= 0 and alpha > 0");
@@ -1684,6 +1755,10 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
                     if ((s = run_anti_x(p, X_ITER))) return s;
                     continue;
                 }
+                if (p->plane) {
+                    if ((s = plane_iteration(p))) return s;
+                    continue;
+                }
                 s = chain_mid(p, 1);
                 if (s) return s;
                 s = run_xpass(p, X_ITER, xp);
@@ -1716,6 +1791,7 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
 }
 
 usp_status usp_residual(usp_plan_t p, double *rel, double *abs_norm, int64_t *k) {
+    Range nvtx_range("usp_residual");
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
     usp_status s = probe_xform(p);
@@ -1729,6 +1805,7 @@ usp_status usp_residual(usp_plan_t p, double *rel, double *abs_norm, int64_t *k)
 }
 
 usp_status usp_residual_history(usp_plan_t p, double *host, int64_t cap, int64_t *n) {
+    Range nvtx_range("usp_residual_history");
     if (!p || !n) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
     usp_status s = probe_xform(p);
@@ -1782,6 +1859,7 @@ usp_status usp_plan_set_staging(usp_plan_t p, void *dev, size_t bytes) {
 }
 
 usp_status usp_stage_inputs(usp_plan_t p, const void *medium, const void *source) {
+    Range nvtx_range("usp_stage_inputs");
     if (!p || !medium || !source) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->stg) return fail(USP_ERR_STATE, "usp_plan_set_staging must be called first");
     if (p->medium_taken)
@@ -1799,6 +1877,7 @@ usp_status usp_stage_inputs(usp_plan_t p, const void *medium, const void *source
 }
 
 usp_status usp_get_field_async(usp_plan_t p, void *out) {
+    Range nvtx_range("usp_get_field_async");
     if (!p || !out) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->stg) return fail(USP_ERR_STATE, "usp_plan_set_staging must be called first");
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
@@ -1826,6 +1905,7 @@ usp_status usp_wait_field(usp_plan_t p) {
 }
 
 usp_status usp_get_field(usp_plan_t p, void *out, usp_where where) {
+    Range nvtx_range("usp_get_field");
     if (!p || !out) return fail(USP_ERR_ARG, "NULL argument");
     if (!p->have_source) return fail(USP_ERR_STATE, "no source");
     const cudaMemcpyKind kind = where == USP_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
@@ -1875,6 +1955,7 @@ usp_status usp_krylov_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
 }
 
 usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, usp_term *term) {
+    Range nvtx_range("usp_bicgstab");
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->k_rh) return fail(USP_ERR_STATE, "usp_krylov_set_workspace must be called first");
@@ -2087,6 +2168,7 @@ usp_status apply_M_dev(usp_plan_s *p, float2 *u, float2 *z) {
 }  // namespace
 
 usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, usp_term *term) {
+    Range nvtx_range("usp_gmres");
     if (!p) return fail(USP_ERR_ARG, "NULL plan");
     if (!p->have_source) return fail(USP_ERR_STATE, "set_source must succeed first");
     if (!p->gm_b) return fail(USP_ERR_STATE, "usp_gmres_set_workspace must be called first");
@@ -2284,6 +2366,9 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->gm_part);
     cudaFree(p->td_red);
     cudaFree(p->bar);
+    cudaFree(p->pl_ctr);
+    cudaFree(p->pl_done);
+    cudaFree(p->pl_part);
     for (int a = 0; a < 3; ++a) cudaFree(p->tw[a]);
     cudaFree(p->twr);
     cudaFreeHost(p->st_host);

@@ -166,6 +166,29 @@ struct SParams {
     float2 *peer[kMaxPeers];
 };
 
+// ------------------------------------------- plane-chained pass (NEXT-4) --
+// K_D -> K_A -> K_B of one iteration in one persistent kernel, plane by
+// plane, `work` L2-resident in between (kernels_plane.cu); nx = ny = kPlaneN.
+constexpr int kPlaneN = 1024;
+struct PParams {
+    float2 *work, *x, *delta;
+    const float2 *B;
+    const float2 *s;             // x-form plans: s = S / c (dense); else nullptr
+    const float2 *tw;            // four-step twiddles of kPlaneN (x and y)
+    long long nz;                // planes
+    int s_sparse;                // sparse source (R-31): add s_comp lines instead of reading s
+    const int *s_list;
+    const float2 *s_comp;
+    int s_count;
+    unsigned long long *ctr;     // unit counter (reset by the last CTA)
+    unsigned *d_done, *a_done;   // per plane: finished y-inverse tiles / x units
+    double *upart;               // per x unit: residual partial (nz * 64)
+    IterState *st;
+    Red red;
+};
+cudaError_t launch_plane(const CUtensorMap &mapy, const PParams &p, int grid, cudaStream_t s, bool lean,
+                         bool expect_x);
+
 // ------------------------------------------------------------------ 1-D --
 enum OneMode : int { O_SETUP = 0, O_ITER = 1 };
 struct OneParams {

@@ -107,7 +107,7 @@ def test_real_path_async_readback():
     from paper_2207_14222_b200 import Plan
     from synth import make
 
-    p = make("C4", (32, 64, 64))
+    p = make("C4", (64, 64, 64))   # the real path needs y, z extents >= 64
     med, src, dtype = rounded_inputs(p)
     assert dtype == "r32"
     ref, _, _, _ = run_gpu(p, n_iter=12, tol=0.0)
