@@ -345,8 +345,8 @@ def timed_iterations(plan, stream, n, alpha=0.75, warm=3):
 def variant_rooflines(dev, stream, med, src, p, hbm, n=20):
     """The same C5 problem on other plan options, each timed over n
     iterations: the general case (Delta-form, s read densely: what a dense
-    source or a converging solve runs), and the 4-pass schedule (SURVEY.md
-    §8 geometry table) next to the default plane-chained pass."""
+    source or a converging solve runs), and the plane-chained pass (NEXT-4)
+    next to the default 4-pass schedule."""
     import torch
     from paper_2207_14222_b200 import Plan
 
@@ -355,10 +355,10 @@ def variant_rooflines(dev, stream, med, src, p, hbm, n=20):
     for key, opts, form, desc in (
             ("general_delta_dense", {"delta_form": True, "dense_source": True}, "delta",
              "Delta-form (P:L613), s read densely"),
-            ("four_pass_xform_sparse", {"four_pass": True}, "x_sparse",
-             "x-form, sparse source, 4-pass schedule (K_B, K_C, K_D, K_A)"),
-            ("four_pass_general", {"four_pass": True, "delta_form": True, "dense_source": True}, "delta",
-             "Delta-form, s read densely, 4-pass schedule")):
+            ("plane_xform_sparse", {"plane_chain": True}, "x_sparse",
+             "x-form, sparse source, plane-chained pass (K_C + one K_D/K_A/K_B kernel)"),
+            ("plane_general", {"plane_chain": True, "delta_form": True, "dense_source": True}, "delta",
+             "Delta-form, s read densely, plane-chained pass")):
         with torch.cuda.stream(stream):
             plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev, **opts)
             plan.set_potential(med, 0.95)

@@ -143,14 +143,14 @@ typedef struct {
     int launch_per_pass;  /* != 0: 2-D grids up to 512^2 launch one kernel per pass and
                              iteration; 0: one persistent cooperative launch per iterate
                              call (kernels_small.cu).                                    */
-    int four_pass;        /* != 0: one sweep per FFT pass (K_B, K_C, K_D, K_A) even where the
-                             plane-chained pass applies.  0: on one GPU with nx = ny = 1024
-                             (complex64, 3-D), each iteration is the z pass plus ONE
-                             persistent kernel that runs the y-inverse, x and y-forward
-                             passes plane by plane with the plane's work array L2-resident
-                             (56 instead of 88 HBM B/voxel for the
-                             sparse-source x-form).  Same arithmetic per element; only the
-                             residual's summation order differs.                     */
+    int plane_chain;      /* != 0: on one GPU with nx = ny = 1024 (complex64, 3-D), each
+                             iteration is the z pass plus ONE persistent kernel that runs
+                             the y-inverse, x and y-forward passes plane by plane with the
+                             plane's work array L2-resident (56
+                             instead of 88 HBM B/voxel for the sparse-source x-form).  Same
+                             arithmetic per element; only the residual's summation order
+                             differs.  0: one sweep per FFT pass (K_B, K_C, K_D, K_A),
+                             measured faster.                          */
     int test_hooks;       /* bit 0 (USP_HOOK_RANK_FINISH): on a one-rank communicator, reduce
                              the residual through the rank-ordered all-gather + k_finish
                              path of P > 1 plans (a test of that path on one GPU).  0 in

@@ -191,7 +191,7 @@ struct usp_plan_s {
     TDParams td{};
     // persistent 2-D solve (kernels_small.cu; desc.launch_per_pass disables)
     bool solve2d = false;
-    // plane-chained pass (kernels_plane.cu, NEXT-4; desc.four_pass disables): an
+    // plane-chained pass (kernels_plane.cu, NEXT-4; desc.plane_chain enables): an
     // iteration is K_C + one persistent K_D -> K_A -> K_B kernel; unit counter,
     // per-plane done counters, per-unit residual partials
     bool plane = false;
@@ -681,6 +681,12 @@ usp_status plane_iteration(usp_plan_s *p) {
     pp.d_done = p->pl_done;
     pp.a_done = p->pl_done + p->nz;
     pp.upart = p->pl_part;
+    // y role : x role CTAs (USP_PLANE_Y64 / 64 of the SMs run the y role;
+    // a build-time constant, tools/gpu/kab.py compares builds)
+#ifndef USP_PLANE_Y64
+#define USP_PLANE_Y64 31
+#endif
+    pp.ny_ctas = (p->nsm * USP_PLANE_Y64 + 32) / 64;
     pp.st = p->st;
     pp.red = red_params(p);
     Tick t(p, KC_PLANE);
@@ -1253,14 +1259,14 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     TRY(cudaMalloc(&p->bar, sizeof(unsigned) * 2));
     TRY(cudaMemset(p->bar, 0, sizeof(unsigned) * 2));
     p->solve2d = !p->anti && !p->tdiff && p->ndim == 2 && solve2d_supported(p->nx, p->ny) && !desc->launch_per_pass;
-    p->plane = !desc->four_pass && P == 1 && p->ndim == 3 && !p->real && !p->anti && !p->tdiff && p->nx == kPlaneN &&
+    p->plane = desc->plane_chain && P == 1 && p->ndim == 3 && !p->real && !p->anti && !p->tdiff && p->nx == kPlaneN &&
                p->ny == kPlaneN && stile_supported(p->nz);
     if (p->plane) {
         TRY(cudaMalloc(&p->pl_ctr, sizeof(unsigned long long)));
         TRY(cudaMemset(p->pl_ctr, 0, sizeof(unsigned long long)));
         TRY(cudaMalloc(&p->pl_done, sizeof(unsigned) * 2 * p->nz));
         TRY(cudaMemset(p->pl_done, 0, sizeof(unsigned) * 2 * p->nz));
-        TRY(cudaMalloc(&p->pl_part, sizeof(double) * 64 * p->nz));
+        TRY(cudaMalloc(&p->pl_part, sizeof(double) * kPlaneN * p->nz));
     }
     p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && !desc->delta_form;
     if (desc->r_switch > 0.0) p->r_sw = desc->r_switch;

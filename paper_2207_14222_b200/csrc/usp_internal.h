@@ -180,9 +180,10 @@ struct PParams {
     const int *s_list;
     const float2 *s_comp;
     int s_count;
-    unsigned long long *ctr;     // unit counter (reset by the last CTA)
-    unsigned *d_done, *a_done;   // per plane: finished y-inverse tiles / x units
-    double *upart;               // per x unit: residual partial (nz * 64)
+    unsigned long long *ctr;     // y unit counter (reset by the last CTA)
+    unsigned *d_done, *a_done;   // per plane: finished y-inverse tiles / x lines
+    double *upart;               // per x line: residual partial (nz * nx)
+    int ny_ctas;                 // CTAs in the y role (the rest run the x role)
     IterState *st;
     Red red;
 };

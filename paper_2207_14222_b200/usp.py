@@ -72,8 +72,8 @@ class Plan:
     transposes of the slab decomposition instead of the fused peer stores),
     ``complex_path`` (float32 diffusion data on the complex path),
     ``launch_per_pass`` (2-D: one launch per pass instead of the persistent
-    solver), ``four_pass`` (one sweep per FFT pass instead of the
-    plane-chained pass on 1024^2-plane grids), ``test_hooks`` (USP_HOOK_*
+    solver), ``plane_chain`` (the plane-chained pass on 1024^2-plane
+    grids instead of one sweep per FFT pass), ``test_hooks`` (USP_HOOK_*
     bits; tests only).
     """
 
@@ -82,7 +82,7 @@ class Plan:
                  stream=None, device=None, comm=None, virtual_ranks: int = 0, antisymmetric: bool = False,
                  tensor_diffusion: bool = False, delta_form: bool = False, r_switch: float = 0.0,
                  dense_source: bool = False, separate_transposes: bool = False, complex_path: bool = False,
-                 launch_per_pass: bool = False, four_pass: bool = False, test_hooks: int = 0):
+                 launch_per_pass: bool = False, plane_chain: bool = False, test_hooks: int = 0):
         import torch
 
         self.lib = L.load()
@@ -116,7 +116,7 @@ class Plan:
         d.separate_transposes = int(bool(separate_transposes))
         d.complex_path = int(bool(complex_path))
         d.launch_per_pass = int(bool(launch_per_pass))
-        d.four_pass = int(bool(four_pass))
+        d.plane_chain = int(bool(plane_chain))
         d.test_hooks = int(test_hooks)
         if tensor_diffusion:
             d.dtype = L.R32

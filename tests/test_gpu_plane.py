@@ -44,14 +44,14 @@ def test_plane_equals_four_pass(form):
         rng = np.random.default_rng(3)
         src = src + (1e-3 * (rng.standard_normal(src.shape) + 1j * rng.standard_normal(src.shape))).astype(np.complex64)
     opts = {"delta_form": form == "delta"}
-    pa = _plan(p, **opts)
+    pa = _plan(p, plane_chain=True, **opts)
     pa.profile(True)
     xa, na, _, _ = run_gpu(p, n_iter=12, tol=0.0, plan=pa, med=med, src=src, dtype=dtype)
     la = _launches(pa)
     # the setup runs the 4-pass chain once (its y-inverse and one y-forward
     # more); every iteration is K_C + the plane-chained kernel
     assert la.get("plane_dab", 0) >= 12 and "xpass" not in la and la.get("y_inv", 0) == 1
-    pb = _plan(p, four_pass=True, **opts)
+    pb = _plan(p, **opts)
     xb, nb, _, _ = run_gpu(p, n_iter=12, tol=0.0, plan=pb, med=med, src=src, dtype=dtype)
     assert na == nb == 12
     assert pa.source_lines() == (1 if form == "xform_sparse" else 0)
@@ -66,7 +66,7 @@ def test_plane_to_tolerance_matches_oracle(orc):
     from synth import make
 
     p = make("C5", (64, 1024, 1024))
-    pa = _plan(p, r_switch=0.3)
+    pa = _plan(p, plane_chain=True, r_switch=0.3)
     xg, ng, term, _ = run_gpu(p, n_iter=400, tol=0.1, plan=pa)
     assert term == "converged" and not pa.iteration_form()[1]
     res, _ = run_oracle(orc, p, n_iter=400, tol=0.1)
@@ -87,8 +87,8 @@ def test_plane_resume_probe_and_stop():
     p = make("C5", SHAPE)
     med, src, dtype = rounded_inputs(p)
     res = []
-    for four in (False, True):
-        pl = _plan(p, four_pass=four, r_switch=0.3)
+    for chain in (True, False):
+        pl = _plan(p, plane_chain=chain, r_switch=0.3)
         run_gpu(p, n_iter=3, tol=0.0, plan=pl, med=med, src=src, dtype=dtype)
         r3 = pl.residual()
         pl.iterate(5, p.alpha, 0.0)

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--config", default="C5")
+    ap.add_argument("--nz", type=int, default=None, help="planes (default: --size)")
     args = ap.parse_args()
     import torch
 
@@ -37,7 +38,7 @@ def main():
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(0)
-    p = make(args.config, (args.size,) * 3, device=str(dev))
+    p = make(args.config, (args.nz or args.size, args.size, args.size), device=str(dev))
     real = p.kind == "diffusion"   # C4: float32 data, the real (half-spectrum) path
     if real:
         med = p.medium.real.float().contiguous()
