@@ -684,7 +684,7 @@ usp_status plane_iteration(usp_plan_s *p) {
     // y role : x role CTAs (USP_PLANE_Y64 / 64 of the SMs run the y role;
     // a build-time constant, tools/gpu/kab.py compares builds)
 #ifndef USP_PLANE_Y64
-#define USP_PLANE_Y64 31
+#define USP_PLANE_Y64 27
 #endif
     pp.ny_ctas = (p->nsm * USP_PLANE_Y64 + 32) / 64;
     pp.st = p->st;
