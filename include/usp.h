@@ -250,7 +250,10 @@ usp_status usp_iterate(usp_plan_t plan, int64_t n_max, double alpha, double tol,
 usp_status usp_residual(usp_plan_t plan, double *rel, double *abs_norm, int64_t *k);
 
 /* Copy r_0 .. r_{n-1} (fp64) into host[0..cap); *n = number available
- * (ring of the most recent 65536 iterations). */
+ * (ring of the most recent 65536 iterations): n = k + 1 (r_k of the current
+ * x_k included, computed on demand for x-form plans), except after a
+ * converged stop of usp_iterate, where the final x_k's own residual is not
+ * computed (reading R-5) and n = k (r_0 .. r_{k-1}, the last below tol). */
 usp_status usp_residual_history(usp_plan_t plan, double *host, int64_t cap, int64_t *n);
 
 /* Asynchronous input staging (pipelining a sequence of problems).

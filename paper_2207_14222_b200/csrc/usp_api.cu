@@ -230,6 +230,9 @@ struct usp_plan_s {
     bool staged = false, med_used_rec = false, src_used_rec = false, medium_taken = false, out_pending = false;
     bool stg_result = false;   // the staging area has the read-back slot
     double r_sw = 1e-2;
+    // after a converged stop of usp_iterate the final iterate's own residual
+    // is not computed (reading R-5): the history then holds r_0 .. r_{k-1}
+    bool hist_conv = false;
     float2 *s = nullptr;
     unsigned *bar = nullptr;   // [0] count, [1] generation
     // plan-owned small device memory
@@ -1594,6 +1597,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
     s0.alpha = 0.75;
     p->xform = p->xform_cap;
     p->probe_needed = false;
+    p->hist_conv = false;
     s0.xform = p->xform ? 1 : 0;
     s0.r_sw = p->r_sw;
     s0.form = FORM_DELTA;   // the source setup's finish sets FORM_X on x-form plans
@@ -1787,6 +1791,7 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
     if (s) return s;
     drain_timing(p);
     const IterState &h = *p->st_host;
+    p->hist_conv = h.status == ST_DONE_CONV;
     if (n_done) *n_done = h.k - k0;
     if (term) {
         if (h.status == ST_DONE_CONV) *term = USP_CONVERGED;
@@ -1818,12 +1823,15 @@ usp_status usp_residual_history(usp_plan_t p, double *host, int64_t cap, int64_t
     if (s) return s;
     s = sync_state(p);
     if (s) return s;
-    const long long avail = std::min<long long>(p->st_host->k + 1, p->hist_cap);
+    // entries r_0 .. r_last: the last computed residual (after a converged
+    // fixed-point stop, r_{k-1}: the residual of x_k itself is not computed)
+    const long long last = p->st_host->k - ((p->hist_conv && p->st_host->k > 0) ? 1 : 0);
+    const long long avail = std::min<long long>(last + 1, p->hist_cap);
     *n = avail;
     if (host && cap > 0) {
         std::vector<double> all(p->hist_cap);
         if ((s = readback(p, all.data(), p->hist, sizeof(double) * p->hist_cap))) return s;
-        const long long first = p->st_host->k + 1 - avail;
+        const long long first = last + 1 - avail;
         for (long long i = 0; i < std::min<long long>(cap, avail); ++i) host[i] = all[(first + i) % p->hist_cap];
     }
     return USP_OK;

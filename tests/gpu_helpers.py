@@ -51,3 +51,9 @@ def run_oracle(orc, p, n_iter=None, tol=None, alpha=None):
 
 def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def monotone(h, rel=1e-5):
+    """Cor. 1: r_{k+1} <= r_k, up to fp32 rounding."""
+    h = np.asarray(h)
+    return bool(np.all(np.diff(h) <= rel * h[:-1]))

@@ -113,7 +113,8 @@ def one(O, name, n, tol, tag):
     rec["hist_max_rel_dev"] = float(np.max(np.abs(h[:m] - res.hist[:m]) / res.hist[:m]))
     rec["r_last_gpu"] = float(h[ng - 1])
     rec["r_last_oracle"] = float(res.hist[m - 1])
-    rec["monotone_gpu"] = bool(np.all(np.diff(h[: ng + 1]) <= 1e-5 * h[:ng]))
+    hh = h[: ng + 1]
+    rec["monotone_gpu"] = bool(np.all(np.diff(hh) <= 1e-5 * hh[:-1]))
     rec["pass"] = bool(rec["rel_l2_field"] <= 1e-4 and (tol <= 0 or abs(ng - rec["oracle_count"]) <= 1))
     del xg, res
     gc.collect()
