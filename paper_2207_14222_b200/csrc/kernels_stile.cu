@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         } else {
 #pragma unroll
             for (int bx = 0; bx < N / T::BOXN; ++bx) {
-                if (p.map_rank == 3) tma_load_3d(stage + bx * T::BOXN * T::COLS, &tmap, c0, bx * T::BOXN, (int)o, full);
-                else tma_load_2d(stage + bx * T::BOXN * T::COLS, &tmap, c0, (int)o * N + bx * T::BOXN, full);
+                if (p.map_rank == 3)
+                    tma_load_3d(stage + bx * T::BOXN * T::COLS, &tmap, c0 + p.col0, bx * T::BOXN, (int)o, full);
+                else tma_load_2d(stage + bx * T::BOXN * T::COLS, &tmap, c0 + p.col0, (int)o * N + bx * T::BOXN, full);
             }
         }
     };
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 if (p.line_axis == 2) {
                     // column (x, y) of the (possibly y-sliced) z pass; y global
                     const long long gc = o * p.ncols + col;
-                    const int ix = (int)(gc % p.mp.rowc), iy = (int)(p.y0 + gc / p.mp.rowc);
+                    const int ix = (int)(gc % p.mp.rowc) + p.x0, iy = (int)(p.y0 + gc / p.mp.rowc);
                     const float px = p.mp.kx * freq_m(ix, p.mp.nx), py = p.mp.ky * freq_m(iy, p.mp.ny);
                     pt2 = fmaf(px, px, py * py);
                 } else {

@@ -167,6 +167,16 @@ struct usp_plan_s {
     size_t ws_bytes = 0;
     float2 *x = nullptr, *delta = nullptr, *B = nullptr, *work = nullptr;
     float2 *sendb = nullptr, *recvb = nullptr;   // P > 1
+    // separate transposes, pipelined over x-chunks: chunk c of
+    // width chunk_w owns a contiguous region of the send / receive buffers
+    // ([c][r][q][z_loc][y_loc][chunk_w]); K_B(c) -> all-to-all(c) -> K_C(c) ->
+    // all-to-all back(c) -> K_D(c), the all-to-alls on xstream overlapping the
+    // other chunks' passes
+    int nchunk = 1;
+    long long chunk_w = 0;
+    std::vector<CUtensorMap> smap_zc, smap_kdc;
+    cudaStream_t xstream = nullptr;
+    std::vector<cudaEvent_t> ev_b, ev_x, ev_c, ev_y;
     // transposes fused into the K_B / K_C stores (peer memory; desc.separate_transposes -> NCCL all-to-all)
     bool fused = false;
     float2 *peer_recv[kMaxPeers] = {}, *peer_send[kMaxPeers] = {};
@@ -296,20 +306,21 @@ struct Range {
 struct Tick {   // brackets one launch with events when profiling, and with an NVTX range
     usp_plan_s *p;
     int cls;
+    cudaStream_t s;
     cudaEvent_t a = nullptr;
-    Tick(usp_plan_s *pl, int c, bool count = true) : p(pl), cls(c) {
+    Tick(usp_plan_s *pl, int c, bool count = true, cudaStream_t st = nullptr) : p(pl), cls(c), s(st ? st : pl->stream) {
         nvtxRangePushA(kc_names[c]);
         if (count) ++p->launches;
         if (p->prof) {
             a = get_event(p);
-            cudaEventRecord(a, p->stream);
+            cudaEventRecord(a, s);
         }
     }
     ~Tick() {
         nvtxRangePop();
         if (p->prof) {
             cudaEvent_t b = get_event(p);
-            cudaEventRecord(b, p->stream);
+            cudaEventRecord(b, s);
             p->timed.push_back({cls, a, b});
         }
     }
@@ -318,6 +329,7 @@ struct Tick {   // brackets one launch with events when profiling, and with an N
 void drain_timing(usp_plan_s *p) {
     if (p->timed.empty()) return;
     cudaStreamSynchronize(p->stream);
+    if (p->xstream) cudaStreamSynchronize(p->xstream);
     for (auto &t : p->timed) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, t.a, t.b);
@@ -845,26 +857,32 @@ usp_status rank_barrier(usp_plan_s *p) {
 // layout holds slab r's rows for y block q; block (r, q) of the receive
 // layout holds y block r's planes of slab q.  forward: recv(r,q) <- send(q,r);
 // back: send(q,r) <- recv(r,q).
-usp_status exchange(usp_plan_s *p, bool forward) {
-    const long long bk = p->nzs * p->nyl * p->rp;   // elements per block
+// The whole exchange (nchunk = 1) or that of x-chunk `chunk` (blocks of
+// width chunk_w in the chunk's region), on stream `st`.
+usp_status exchange(usp_plan_s *p, bool forward, int chunk = 0, cudaStream_t st = nullptr) {
+    if (!st) st = p->stream;
+    const long long w = p->nchunk > 1 ? p->chunk_w : p->rp;
+    const long long bk = p->nzs * p->nyl * w;   // elements per block
+    const long long pv = p->virt ? p->P : 1;
+    const long long base = (long long)chunk * pv * p->P * bk;
     const size_t bytes = (size_t)bk * sizeof(float2);
-    Tick t(p, KC_A2A, false);
+    Tick t(p, KC_A2A, false, st);
     if (p->virt) {
         for (int r = 0; r < p->P; ++r)
             for (int q = 0; q < p->P; ++q) {
-                float2 *rv = p->recvb + ((long long)r * p->P + q) * bk;
-                float2 *sd = p->sendb + ((long long)q * p->P + r) * bk;
-                if (forward) CU(cudaMemcpyAsync(rv, sd, bytes, cudaMemcpyDeviceToDevice, p->stream));
-                else CU(cudaMemcpyAsync(sd, rv, bytes, cudaMemcpyDeviceToDevice, p->stream));
+                float2 *rv = p->recvb + base + ((long long)r * p->P + q) * bk;
+                float2 *sd = p->sendb + base + ((long long)q * p->P + r) * bk;
+                if (forward) CU(cudaMemcpyAsync(rv, sd, bytes, cudaMemcpyDeviceToDevice, st));
+                else CU(cudaMemcpyAsync(sd, rv, bytes, cudaMemcpyDeviceToDevice, st));
             }
         return USP_OK;
     }
     Nccl &n = nccl();
-    float2 *from = forward ? p->sendb : p->recvb, *to = forward ? p->recvb : p->sendb;
+    float2 *from = (forward ? p->sendb : p->recvb) + base, *to = (forward ? p->recvb : p->sendb) + base;
     NC(n.GroupStart());
     for (int q = 0; q < p->P; ++q) {
-        NC(n.Send(from + q * bk, (size_t)bk * 2, ncclFloat, q, p->comm, p->stream));
-        NC(n.Recv(to + q * bk, (size_t)bk * 2, ncclFloat, q, p->comm, p->stream));
+        NC(n.Send(from + q * bk, (size_t)bk * 2, ncclFloat, q, p->comm, st));
+        NC(n.Recv(to + q * bk, (size_t)bk * 2, ncclFloat, q, p->comm, st));
     }
     NC(n.GroupEnd());
     return USP_OK;
@@ -979,6 +997,54 @@ usp_status td_upd(usp_plan_s *p, XMode mode) {
     return USP_OK;
 }
 
+// Separate transposes pipelined over x-chunks: the compute
+// stream runs B0 B1 C0 B2 C1 D0 ... (K_B(c), K_C(c - 1), K_D(c - 2)), the
+// exchange stream F0 F1 R0 F2 R1 ... (forward all-to-all of chunk c once
+// K_B(c) is done, the return of chunk c once K_C(c) is done), so each chunk's
+// transfer overlaps the other chunks' FFT passes.  Per element the same
+// arithmetic as the unchunked path (bit-identical results).
+usp_status chain_mid_chunked(usp_plan_s *p, int check_state) {
+    usp_status s;
+    const int C = p->nchunk;
+    const long long W = p->chunk_w, pv = p->virt ? p->P : 1;
+    const long long bkc = p->nzs * p->nyl * W, creg = pv * p->P * bkc;   // elements per block / chunk region
+    for (int st = 0; st < C + 2; ++st) {
+        if (st < C) {   // K_B(st): y forward of columns [st W, st W + W) into the chunk's send layout
+            SParams yb = sparams(p, p->work, p->sendb + st * creg, p->tw[1], W, W, p->nzh, p->rp * p->ny, 1,
+                                 check_state, 3);
+            yb.send_layout = 1;
+            yb.col0 = (int)(st * W);
+            if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0))) return s;
+            CU(cudaEventRecord(p->ev_b[st], p->stream));
+            CU(cudaStreamWaitEvent(p->xstream, p->ev_b[st], 0));
+            if ((s = exchange(p, true, st, p->xstream))) return s;
+            CU(cudaEventRecord(p->ev_x[st], p->xstream));
+        }
+        const int c = st - 1;
+        if (c >= 0 && c < C) {   // K_C(c) on the chunk's y-slab blocks, then the return transpose
+            CU(cudaStreamWaitEvent(p->stream, p->ev_x[c], 0));
+            SParams zm = sparams(p, p->recvb + c * creg, p->recvb + c * creg, p->tw[2], p->nyl * W, p->nyl * W, pv,
+                                 p->nz * p->nyl * W, 2, check_state, 2);
+            zm.y0 = p->virt ? 0 : (long long)p->rank * p->nyl;
+            zm.x0 = (int)(c * W);
+            zm.mp.rowc = (int)W;
+            if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_zc[c], true, 0))) return s;
+            CU(cudaEventRecord(p->ev_c[c], p->stream));
+            CU(cudaStreamWaitEvent(p->xstream, p->ev_c[c], 0));
+            if ((s = exchange(p, false, c, p->xstream))) return s;
+            CU(cudaEventRecord(p->ev_y[c], p->xstream));
+        }
+        const int d = st - 2;
+        if (d >= 0 && d < C) {   // K_D(d): y inverse from the chunk's send layout into work columns [d W, d W + W)
+            CU(cudaStreamWaitEvent(p->stream, p->ev_y[d], 0));
+            SParams yd = sparams(p, p->sendb + d * creg, p->work + d * W, p->tw[1], p->rp, W, p->nzh,
+                                 p->rp * p->ny, 1, check_state, 5);
+            if ((s = run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_kdc[d], true, 0))) return s;
+        }
+    }
+    return USP_OK;
+}
+
 // The middle of the chain: every FFT pass between the x forward and the x
 // inverse, with the (L+1)^-1 multiplier on the last axis (Eq. 12).
 usp_status chain_mid(usp_plan_s *p, int check_state) {
@@ -1017,6 +1083,7 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
         if ((s = rank_barrier(p))) return s;
         return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_kd, true, 0);
     }
+    if (p->nchunk > 1) return chain_mid_chunked(p, check_state);
     SParams yb = sparams(p, p->work, p->sendb, p->tw[1], p->rp, p->rp, p->nzh, p->rp * p->ny, 1, check_state, 3);
     yb.send_layout = 1;
     SParams zm = sparams(p, p->recvb, p->recvb, p->tw[2], p->nyl * p->rp, p->nyl * p->rp, pv,
@@ -1093,6 +1160,23 @@ void build_maps(usp_plan_s *p) {
         const cuuint64_t str[4] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->nyl * p->rp) * 8, bk, bk * p->P};
         const cuuint32_t box[5] = {cy, std::min<cuuint32_t>(by, (cuuint32_t)p->nyl), 1, 1, 1};
         ok = ok && make_map(&p->smap_kd, p->sendb, 5, dims, str, box);
+    }
+    if (p->nchunk > 1) {   // the x-chunked separate transposes: one pair of maps per chunk region
+        const long long W = p->chunk_w, bkc = p->nzs * p->nyl * W, creg = pv * p->P * bkc;
+        p->smap_zc.assign(p->nchunk, CUtensorMap{});
+        p->smap_kdc.assign(p->nchunk, CUtensorMap{});
+        for (int c = 0; c < p->nchunk && ok; ++c) {
+            const cuuint64_t dz[2] = {(cuuint64_t)(p->nyl * W), (cuuint64_t)(p->nz * pv)};
+            const cuuint64_t sz[1] = {(cuuint64_t)(p->nyl * W) * 8};
+            const cuuint32_t bxz[2] = {cz, bz};
+            ok = make_map(&p->smap_zc[c], p->recvb + c * creg, 2, dz, sz, bxz);
+            const cuuint64_t dd[5] = {(cuuint64_t)W, (cuuint64_t)p->nyl, (cuuint64_t)p->nzs, (cuuint64_t)p->P,
+                                      (cuuint64_t)pv};
+            const cuuint64_t sd[4] = {(cuuint64_t)W * 8, (cuuint64_t)(p->nyl * W) * 8, (cuuint64_t)bkc * 8,
+                                      (cuuint64_t)bkc * p->P * 8};
+            const cuuint32_t bxd[5] = {cy, std::min<cuuint32_t>(by, (cuuint32_t)p->nyl), 1, 1, 1};
+            ok = ok && make_map(&p->smap_kdc[c], p->sendb + c * creg, 5, dd, sd, bxd);
+        }
     }
     p->stile_z = ok;
     p->stile_y = p->stile_y && ok;
@@ -1212,6 +1296,10 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
               desc->medium == USP_MEDIUM_W && desc->ndim == 3 && xreal_supported(p->nx) && stile_supported(p->ny) &&
               stile_supported(p->nz);
     p->rp = p->real ? xreal_row_pitch((int)p->nx) : p->nx;
+    if (P > 1 && !p->real) {   // x-chunks of the separate transposes: 4 chunks of >= 16 columns
+        p->nchunk = (int)std::min<long long>(4, p->rp / 16);
+        p->chunk_w = p->rp / p->nchunk;
+    }
     p->stream = (cudaStream_t)desc->stream;
     p->sigma = desc->sigma;
     p->c = desc->c;
@@ -1363,7 +1451,16 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
     build_maps(p);
     if (p->P > 1 && !(p->stile_y && p->stile_z))
         return fail(USP_ERR_CUDA, "could not encode the tensor maps of the slab decomposition");
-    return setup_peers(p);
+    usp_status s = setup_peers(p);
+    if (s) return s;
+    if (p->P > 1 && !p->fused && p->nchunk > 1 && !p->xstream) {
+        CU(cudaStreamCreateWithFlags(&p->xstream, cudaStreamNonBlocking));
+        for (auto *v : {&p->ev_b, &p->ev_x, &p->ev_c, &p->ev_y}) {
+            v->assign(p->nchunk, nullptr);
+            for (auto &e : *v) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+    }
+    return USP_OK;
 }
 
 usp_status usp_local_extent(usp_plan_t p, int64_t *z0, int64_t *nz_local) {
@@ -2380,6 +2477,12 @@ void usp_plan_destroy(usp_plan_t p) {
     cudaFree(p->gm_part);
     cudaFree(p->td_red);
     cudaFree(p->bar);
+    if (p->xstream) {
+        cudaStreamSynchronize(p->xstream);
+        cudaStreamDestroy(p->xstream);
+        for (auto *v : {&p->ev_b, &p->ev_x, &p->ev_c, &p->ev_y})
+            for (auto e : *v) cudaEventDestroy(e);
+    }
     cudaFree(p->pl_ctr);
     cudaFree(p->pl_done);
     cudaFree(p->pl_part);

@@ -152,6 +152,9 @@ struct SParams {
     int nz_loc;          // z planes per slab
     int nyl_lg;          // log2(ny / P)
     long long y0;        // global y of this rank's y block (z pass multiplier)
+    int col0;            // x-chunked transposes: column offset of the load map's coordinates (K_B)
+    int x0;              // x-chunked transposes: global x of the chunk's column 0 (z pass multiplier;
+                         // mp.rowc is then the chunk width)
     int tma_store;       // k_stile: store the upper half of each tile (rows >= N/2; all rows for
                          // N <= 256) through the exchange buffer with tensor-map stores on the
                          // load map (in-place passes whose map describes dst only)

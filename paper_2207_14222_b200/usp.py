@@ -25,6 +25,19 @@ class Split:
     max_abs_V: float
 
 
+def _cuda_malloc(lib, nbytes: int):
+    """cudaMalloc through the CUDA runtime libusp links (resolved via its handle)."""
+    ptr = ctypes.c_void_p()
+    lib.cudaMalloc.restype = ctypes.c_int
+    lib.cudaMalloc.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t]
+    lib.cudaFree.restype = ctypes.c_int
+    lib.cudaFree.argtypes = [ctypes.c_void_p]
+    rc = lib.cudaMalloc(ctypes.byref(ptr), ctypes.c_size_t(nbytes))
+    if rc != 0 or not ptr.value:
+        raise MemoryError(f"cudaMalloc of {nbytes} bytes failed (cudaError {rc})")
+    return ptr
+
+
 def _numel(a) -> int:
     return int(a.numel()) if hasattr(a, "numel") and callable(a.numel) else int(np.asarray(a).size)
 
@@ -128,9 +141,19 @@ class Plan:
         self.handle = h_
         nbytes = ctypes.c_size_t()
         L.check(self.lib.usp_plan_workspace_size(self.handle, ctypes.byref(nbytes)))
-        self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
-        L.check(self.lib.usp_plan_set_workspace(self.handle, ctypes.c_void_p(self.workspace.data_ptr()),
-                                                int(nbytes.value)))
+        self._ws_raw = None
+        if comm is not None:
+            # slab decomposition over ranks: a workspace of its own cudaMalloc, so
+            # CUDA IPC can map it for the fused transposes whatever torch's
+            # allocator settings (expandable segments are not IPC-mappable)
+            with torch.cuda.device(self.device):
+                self._ws_raw = _cuda_malloc(self.lib, int(nbytes.value))
+            self.workspace = None
+            ws_ptr = self._ws_raw
+        else:
+            self.workspace = torch.empty(int(nbytes.value), dtype=torch.uint8, device=self.device)
+            ws_ptr = ctypes.c_void_p(self.workspace.data_ptr())
+        L.check(self.lib.usp_plan_set_workspace(self.handle, ws_ptr, int(nbytes.value)))
         z0, nzl = ctypes.c_int64(), ctypes.c_int64()
         L.check(self.lib.usp_local_extent(self.handle, ctypes.byref(z0), ctypes.byref(nzl)))
         self.z0 = int(z0.value)
@@ -337,6 +360,9 @@ class Plan:
         if getattr(self, "handle", None):
             self.lib.usp_plan_destroy(self.handle)
             self.handle = None
+        if getattr(self, "_ws_raw", None) is not None:
+            self.lib.cudaFree(self._ws_raw)
+            self._ws_raw = None
 
     def __del__(self):
         try:
