@@ -36,7 +36,7 @@ CASES = [
     ("C5", (64, 64, 32), 8, 0.0, {"virtual_ranks": 4, "separate_transposes": True}),
     ("C4", (64, 64, 64), 30, 0.0, {}),                         # real path across the form switch
     ("C5", (1024, 64, 16), 3, 0.0, {}),                        # k_stile<1024> two-round exchange, TMA stores
-    ("C5", (16, 1024, 1024), 4, 0.0, {"plane_chain": True}),   # plane-chained pass
+    ("C5", (64, 1024, 1024), 4, 0.0, {"plane_chain": True}),   # plane-chained pass
     ("C5", (64, 64, 64), 5, 0.0, {"antisymmetric": True}),
 ]
 

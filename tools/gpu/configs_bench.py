@@ -36,6 +36,9 @@ for name in only:
             elif solver == "bicgstab":
                 n, term = plan.bicgstab(20000, p.tol if p.tol > 0 else 1e-6)
             else:
+                if getattr(plan, "kworkspace", None) is not None:   # BiCGSTAB's 5 fields are not needed any more
+                    plan.kworkspace = None
+                    torch.cuda.empty_cache()
                 m = 20 if int(np.prod(p.shape)) <= 256 ** 3 else 5     # basis memory: (m + 2) fields
                 n, term = plan.gmres(m, 40000, p.tol if p.tol > 0 else 1e-6)
             b.record(stream)

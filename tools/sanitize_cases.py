@@ -69,8 +69,8 @@ def main(case):
     elif case == "z1024":
         solve("C5", (1024, 64, 16), 3)
     elif case == "plane":   # plane-chained pass (nx = ny = 1024), x-form then Delta-form
-        solve("C5", (16, 1024, 1024), 3, r_switch=0.9)
-        solve("C5", (16, 1024, 1024), 2, delta_form=True)
+        solve("C5", (64, 1024, 1024), 3, r_switch=0.9, plane_chain=True)
+        solve("C5", (64, 1024, 1024), 2, delta_form=True, plane_chain=True)
     elif case == "krylov":
         from paper_2207_14222_b200 import Plan
 
