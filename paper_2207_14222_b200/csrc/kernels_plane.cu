@@ -323,7 +323,7 @@ __device__ __noinline__ void y_role(const CUtensorMap &mapy, const PParams &p, u
 }
 
 // ---------------------------------------------------------------- x role --
-template <bool LEAN, bool DSPEC, bool XSPEC>
+template <bool LEAN, bool DSPEC>
 __device__ __noinline__ void x_role(const PParams &p, unsigned char *smem_raw, float alpha, int act) {
     using PG = PlaneGeo;
     using X = XRole<LEAN>;
@@ -511,7 +511,7 @@ __device__ __noinline__ void x_role(const PParams &p, unsigned char *smem_raw, f
     }
 }
 
-template <bool LEAN, bool DSPEC, bool XSPEC>
+template <bool LEAN, bool DSPEC>
 __global__ void __launch_bounds__(PlaneGeo::NT, 1) k_plane(const __grid_constant__ CUtensorMap mapy, const __grid_constant__ PParams p) {
     using PG = PlaneGeo;
     constexpr int N = PG::N;
@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(PlaneGeo::NT, 1) k_plane(const __grid_constant
         if (USP_PLANE_TRACE && tid != 0) tr.k = TR_N;   // one thread per CTA counts the role time
     } else {
         TraceT tr(TR_X_ROLE);
-        x_role<LEAN, DSPEC, XSPEC>(p, smem_raw, alpha, act);
+        x_role<LEAN, DSPEC>(p, smem_raw, alpha, act);
         if (USP_PLANE_TRACE && tid != 0) tr.k = TR_N;
     }
 
@@ -587,13 +587,13 @@ __global__ void __launch_bounds__(PlaneGeo::NT, 1) k_plane(const __grid_constant
     }
 }
 
-template <bool LEAN, bool DSPEC, bool XSPEC>
+template <bool LEAN, bool DSPEC>
 static cudaError_t plane_t(const CUtensorMap &mapy, const PParams &p, int grid, cudaStream_t s) {
     constexpr int SM = plane_smem<LEAN>();
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
-            cudaFuncSetAttribute(k_plane<LEAN, DSPEC, XSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+            cudaFuncSetAttribute(k_plane<LEAN, DSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -611,15 +611,16 @@ static cudaError_t plane_t(const CUtensorMap &mapy, const PParams &p, int grid, 
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, k_plane<LEAN, DSPEC, XSPEC>, mapy, p);
+    return cudaLaunchKernelEx(&cfg, k_plane<LEAN, DSPEC>, mapy, p);
 }
 
 // instance by the form the host expects (as launch_xpass_pipe): lean
 // (sparse-source x-form), dense x-form, Delta-form
 cudaError_t launch_plane(const CUtensorMap &mapy, const PParams &p, int grid, cudaStream_t s, bool lean, bool expect_x) {
-    if (lean) return plane_t<true, false, false>(mapy, p, grid, s);
-    if (expect_x) return plane_t<false, false, false>(mapy, p, grid, s);   // the general body
-    return plane_t<false, true, false>(mapy, p, grid, s);
+    if (lean) return plane_t<true, false>(mapy, p, grid, s);
+    if (expect_x) return plane_t<false, false>(mapy, p, grid, s);   // the general body (a dedicated
+                                                                     // dense x-form body spills at 128 registers)
+    return plane_t<false, true>(mapy, p, grid, s);
 }
 
 }  // namespace usp
