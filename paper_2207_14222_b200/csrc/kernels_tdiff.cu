@@ -23,6 +23,7 @@
 
 #include "fft_core.cuh"
 #include "kcommon.cuh"
+#include "tma.cuh"
 #include "usp_internal.h"
 
 namespace usp {
@@ -155,9 +156,10 @@ __global__ void __launch_bounds__(256) k_tdiff_pot(TDParams p, int mode) {
 }
 
 // ------------------------------------------------------ per-mode symbol --
+// (templated on d so every component loop unrolls into registers)
+template <int d>
 __global__ void __launch_bounds__(256) k_tdiff_mul(TDParams p, int check_state) {
     if (check_state && (p.st->status != ST_RUNNING || p.st->k >= p.st->kmax)) return;
-    const int d = p.d;
     const long long n = p.n;
     const MulParams &mp = p.mp;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -168,14 +170,17 @@ __global__ void __launch_bounds__(256) k_tdiff_mul(TDParams p, int check_state) 
                       d == 3 ? mp.kz * freq_m(iz, mp.nz) * p.qs : 0.f};
         float w[3];
         float sig = p.a;
+#pragma unroll
         for (int k = 0; k < d; ++k) {
             w[k] = 0.f;
+#pragma unroll
             for (int m = 0; m < d; ++m) w[k] = fmaf(p.dm_inv[k * 3 + m], q[m], w[k]);
             sig = fmaf(q[k], w[k], sig);
         }
         const float is = p.inv_n / sig;
         const float2 u = p.work[i];
         float2 F[3], wF = make_float2(0.f, 0.f);
+#pragma unroll
         for (int k = 0; k < d; ++k) {
             F[k] = p.work[(k + 1) * n + i];
             wF = make_float2(fmaf(w[k], F[k].x, wF.x), fmaf(w[k], F[k].y, wF.y));
@@ -183,8 +188,10 @@ __global__ void __launch_bounds__(256) k_tdiff_mul(TDParams p, int check_state) 
         // out_u = (u - i wF) / sig ;  out_F = Dm^-1 F - i w out_u  (1/N_vox folded in)
         const float2 ou = make_float2((u.x + wF.y) * is, (u.y - wF.x) * is);
         p.work[i] = ou;
+#pragma unroll
         for (int k = 0; k < d; ++k) {
             float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
             for (int m = 0; m < d; ++m)
                 acc = make_float2(fmaf(p.dm_inv[k * 3 + m], F[m].x, acc.x), fmaf(p.dm_inv[k * 3 + m], F[m].y, acc.y));
             acc = cscale(acc, p.inv_n);
@@ -197,23 +204,22 @@ __global__ void __launch_bounds__(256) k_tdiff_mul(TDParams p, int check_state) 
 // mode X_SRC_FWD: work = s = [S / (c sqrt s_u); 0]        (no reduction)
 // mode X_SRC_EPI: Delta_0 = B y, x_0 = 0, n0, work = B Delta_0
 // mode X_ITER:    Delta <- Delta + alpha B (y - Delta), x <- x + alpha Delta, work = B Delta
-__device__ __forceinline__ void tdiff_B(const TDParams &p, long long i, const float2 *in, float2 *out) {
-    const int d = p.d, np = d * (d + 1) / 2;
-    float Vf[3][3];
-    sym_get(p.vf + i * np, d, Vf);
-    const float bu = 1.f - p.vu[i];
+template <int d>
+__device__ __forceinline__ void tdiff_B(const float (&Vf)[3][3], float bu, const float2 *in, float2 *out) {
     out[0] = cscale(in[0], bu);
+#pragma unroll
     for (int k = 0; k < d; ++k) {
         float2 acc = in[k + 1];
+#pragma unroll
         for (int m = 0; m < d; ++m) acc = make_float2(fmaf(-Vf[k][m], in[m + 1].x, acc.x), fmaf(-Vf[k][m], in[m + 1].y, acc.y));
         out[k + 1] = acc;
     }
 }
 
-template <int MODE>
+template <int d, int MODE>
 __global__ void __launch_bounds__(256) k_tdiff_upd(TDParams p) {
     __shared__ double sh_red[8];
-    const int d = p.d;
+    constexpr int np = d * (d + 1) / 2;
     const long long n = p.n;
     bool xonly = false;
     float alpha = 0.f;
@@ -229,39 +235,50 @@ __global__ void __launch_bounds__(256) k_tdiff_upd(TDParams p) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         if (MODE == X_SRC_FWD) {
             p.work[i] = make_float2(p.Sraw[i] * p.s_scale, 0.f);
+#pragma unroll
             for (int k = 1; k <= d; ++k) p.work[k * n + i] = make_float2(0.f, 0.f);
             continue;
         }
         float2 y[4], dl[4], t[4];
         if (MODE == X_ITER && xonly) {
+#pragma unroll
             for (int k = 0; k <= d; ++k) {
                 const float2 dd = p.delta[k * n + i], xx = p.x[k * n + i];
                 p.x[k * n + i] = make_float2(fmaf(alpha, dd.x, xx.x), fmaf(alpha, dd.y, xx.y));
             }
             continue;
         }
+        float Vf[3][3];
+        sym_get(p.vf + i * np, d, Vf);
+        const float bu = 1.f - p.vu[i];
+#pragma unroll
         for (int k = 0; k <= d; ++k) y[k] = p.work[k * n + i];
         if (MODE == X_SRC_EPI) {
-            tdiff_B(p, i, y, dl);
+            tdiff_B<d>(Vf, bu, y, dl);
+#pragma unroll
             for (int k = 0; k <= d; ++k) p.x[k * n + i] = make_float2(0.f, 0.f);
         } else {
             float2 od[4];
+#pragma unroll
             for (int k = 0; k <= d; ++k) {
                 od[k] = p.delta[k * n + i];
                 t[k] = csub(y[k], od[k]);
             }
-            tdiff_B(p, i, t, dl);
+            tdiff_B<d>(Vf, bu, t, dl);
+#pragma unroll
             for (int k = 0; k <= d; ++k) {
                 const float2 xx = p.x[k * n + i];
                 p.x[k * n + i] = make_float2(fmaf(alpha, od[k].x, xx.x), fmaf(alpha, od[k].y, xx.y));
                 dl[k] = make_float2(fmaf(alpha, dl[k].x, od[k].x), fmaf(alpha, dl[k].y, od[k].y));
             }
         }
+#pragma unroll
         for (int k = 0; k <= d; ++k) {
             p.delta[k * n + i] = dl[k];
             la += cabs2(dl[k]);
         }
-        tdiff_B(p, i, dl, t);                      // next chain input: u = B Delta
+        tdiff_B<d>(Vf, bu, dl, t);                 // next chain input: u = B Delta
+#pragma unroll
         for (int k = 0; k <= d; ++k) p.work[k * n + i] = t[k];
         if (++cnt == 64) { acc += (double)la; la = 0.f; cnt = 0; }
     }
@@ -272,6 +289,205 @@ __global__ void __launch_bounds__(256) k_tdiff_upd(TDParams p) {
     if (!last_block_total<256>(mine, p.st, p.red_d.partials, sh_red, &total)) return;
     if (threadIdx.x != 0) return;
     finish_xpass(MODE == X_SRC_EPI, xonly, total, p.st, p.red_d);
+}
+
+// ------------------------------------- fused x pass (TMA-pipelined) ------
+// The iteration's x inverse FFT -> k_tdiff_upd's update -> x forward FFT in
+// one pass (k_anti_pipe's structure): a producer warp bulk-copies a unit's
+// work, Delta and x of every component plus v_u and V_F into the consumer
+// warp's stage; the consumer transforms the components one at a time (each
+// y_c parked back in its own slot), runs the update element by element (x,
+// Delta stored, u = B Delta parked in the work slots) and forward-transforms
+// u.  Saves the two k_xfft passes (2 x 16 (d + 1) B/voxel).  The stage is
+// (3 (d + 1) + 1 + d (d + 1) / 2) x 8 B per element of the unit; where fewer
+// than two stages fit (x extent >= 512) the three-kernel sequence runs.
+constexpr int kTdSmemBudget = 232448 - 2048;
+
+template <int N, int d>
+struct TPipe {
+    using G = LineGeo<N>;
+    static constexpr int C = d + 1, NP = d * (d + 1) / 2;
+    static constexpr int U = 32 / G::N1;
+    static constexpr int UE = 32 * G::N2;
+    static constexpr int VU = 3 * C * UE;                // float2 offset of v_u (UE floats)
+    static constexpr int VF = VU + UE / 2;               // float2 offset of V_F (NP UE floats)
+    static constexpr int STAGE = VF + NP * UE / 2;
+    static constexpr int XBUF = U * LayRow<N>::kFloat2PerLine;
+    static constexpr int XC0 = (kTdSmemBudget - N * 8) / ((STAGE + XBUF) * 8);
+    static constexpr int XC = XC0 > 6 ? 6 : XC0;
+    static constexpr bool FITS = XC >= 2;
+    static constexpr int S = XC;
+    static constexpr int NT = 32 * (XC + 1);
+    static constexpr int SMEM = (S * STAGE + XC * XBUF + N) * 8 + 2 * S * 8;
+};
+
+template <int N, int d>
+__global__ void __launch_bounds__(TPipe<N, d>::NT, 1) k_tdiff_pipe(TDParams p) {
+    using G = LineGeo<N>;
+    using T = TPipe<N, d>;
+    constexpr int C = T::C;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float2 *stages = reinterpret_cast<float2 *>(smem_raw);
+    float2 *xbufs = stages + T::S * T::STAGE;
+    float2 *sm_tw = xbufs + T::XC * T::XBUF;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm_tw + N);
+    uint64_t *empty = full + T::S;
+    __shared__ double sh_red[T::NT / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int status = p.st->status;
+    if (p.st->k >= p.st->kmax || (status != ST_RUNNING && status != ST_STOP_PENDING)) return;
+    const bool xonly = status == ST_STOP_PENDING;
+    const float alpha = (float)p.st->alpha;
+    const long long n = p.n;
+    double acc = 0.0;
+    if (xonly) {   // the final x += alpha Delta after the stop test (R-5)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < C * n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const float2 dd = p.delta[i], xx = p.x[i];
+            p.x[i] = make_float2(fmaf(alpha, dd.x, xx.x), fmaf(alpha, dd.y, xx.y));
+        }
+    } else {
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < T::S; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], 1);
+            }
+            fence_mbar_init();
+        }
+        load_twiddles<N>(sm_tw, p.twx);
+        __syncthreads();
+        const long long nunits = n / T::UE;
+        const int nloc = (int)((nunits - blockIdx.x + gridDim.x - 1) / gridDim.x);
+        const uint32_t ub = T::UE * 8u;
+        if (warp == T::XC) {
+            if (lane == 0) {   // producer
+                for (int i = 0; i < nloc; ++i) {
+                    const int s = i % T::S;
+                    if (i >= T::S && !mbar_wait(&empty[s], ((i / T::S) - 1) & 1)) {
+                        if (atomicCAS(&p.st->err, 0, 33) == 0) p.st->err_info = i;
+                        break;
+                    }
+                    const long long off = (blockIdx.x + (long long)i * gridDim.x) * T::UE;
+                    float2 *st = stages + s * T::STAGE;
+                    mbar_arrive_expect_tx(&full[s], 3 * C * ub + T::UE * 4u * (1 + T::NP));
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        bulk_g2s(st + c * T::UE, p.work + c * n + off, ub, &full[s]);
+                        bulk_g2s(st + (C + c) * T::UE, p.delta + c * n + off, ub, &full[s]);
+                        bulk_g2s(st + (2 * C + c) * T::UE, p.x + c * n + off, ub, &full[s]);
+                    }
+                    bulk_g2s(st + T::VU, p.vu + off, T::UE * 4u, &full[s]);
+                    bulk_g2s(st + T::VF, p.vf + off * T::NP, T::UE * 4u * T::NP, &full[s]);
+                }
+            }
+            __syncwarp();
+        } else {
+            const int lq = lane / G::N1, j = lane % G::N1;
+            const LayRow<N> lay{xbufs + warp * T::XBUF + lq * LayRow<N>::kFloat2PerLine};
+            for (int i = warp; i < nloc; i += T::XC) {
+                const int s = i % T::S;
+                if (!mbar_wait(&full[s], (i / T::S) & 1)) {
+                    if (lane == 0 && atomicCAS(&p.st->err, 0, 34) == 0) p.st->err_info = i;
+                    break;
+                }
+                float2 *st = stages + s * T::STAGE;
+                const float *svu = reinterpret_cast<const float *>(st + T::VU);
+                const float *svf = reinterpret_cast<const float *>(st + T::VF);
+                const long long gb = (blockIdx.x + (long long)i * gridDim.x) * T::UE + lq * N + j;
+                const int sb = lq * N + j;
+                float2 v[G::N2];
+#pragma unroll 1
+                for (int c = 0; c < C; ++c) {   // x inverse (conj trick); y_c parked in its slot
+                    float2 *w = st + c * T::UE + sb;
+#pragma unroll
+                    for (int m = 0; m < G::N2; ++m) v[m] = cconj(w[G::N1 * m]);
+                    fft_line<N, false, LayRow<N>, true>(v, lay, j, sm_tw);
+#pragma unroll
+                    for (int m = 0; m < G::N2; ++m) w[G::N1 * m] = cconj(v[m]);
+                }
+                float lacc = 0.f;
+#pragma unroll 2
+                for (int m = 0; m < G::N2; ++m) {
+                    const int e = sb + G::N1 * m;
+                    const long long gi = gb + G::N1 * m;
+                    float Vf[3][3];
+                    sym_get(svf + e * T::NP, d, Vf);
+                    const float bu = 1.f - svu[e];
+                    float2 od[C], t[C], dl[C];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        od[c] = st[(C + c) * T::UE + e];
+                        t[c] = csub(st[c * T::UE + e], od[c]);
+                    }
+                    tdiff_B<d>(Vf, bu, t, dl);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        const float2 xx = st[(2 * C + c) * T::UE + e];
+                        p.x[c * n + gi] = make_float2(fmaf(alpha, od[c].x, xx.x), fmaf(alpha, od[c].y, xx.y));
+                        dl[c] = make_float2(fmaf(alpha, dl[c].x, od[c].x), fmaf(alpha, dl[c].y, od[c].y));
+                        p.delta[c * n + gi] = dl[c];
+                        lacc += cabs2(dl[c]);
+                    }
+                    tdiff_B<d>(Vf, bu, dl, t);   // next chain input: u = B Delta
+#pragma unroll
+                    for (int c = 0; c < C; ++c) st[c * T::UE + e] = t[c];
+                }
+                acc += (double)lacc;
+                __syncwarp();
+#pragma unroll 1
+                for (int c = 0; c < C; ++c) {   // x forward of u
+#pragma unroll
+                    for (int m = 0; m < G::N2; ++m) v[m] = st[c * T::UE + sb + G::N1 * m];
+                    if (c == C - 1) {            // the stage is consumed: let it refill
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&empty[s]);
+                    }
+                    fft_line<N, false, LayRow<N>, true>(v, lay, j, sm_tw);
+#pragma unroll
+                    for (int m = 0; m < G::N2; ++m) p.work[c * n + gb + G::N1 * m] = v[m];
+                }
+            }
+        }
+    }
+    double total;
+    const double mine = block_sum_d<T::NT>(acc, sh_red);
+    if (!last_block_total<T::NT>(mine, p.st, p.red_d.partials, sh_red, &total)) return;
+    if (threadIdx.x != 0) return;
+    finish_xpass(false, xonly, total, p.st, p.red_d);
+}
+
+template <int N, int d>
+static cudaError_t tdiff_pipe_t(const TDParams &p, int grid, cudaStream_t s) {
+    if constexpr (!TPipe<N, d>::FITS) {
+        return cudaErrorInvalidValue;
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(k_tdiff_pipe<N, d>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 TPipe<N, d>::SMEM);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        k_tdiff_pipe<N, d><<<grid, TPipe<N, d>::NT, TPipe<N, d>::SMEM, s>>>(p);
+        return cudaGetLastError();
+    }
+}
+
+cudaError_t launch_tdiff_pipe(int N, const TDParams &p, int grid, cudaStream_t s) {
+#define TP_CASE(n) \
+    case n: return p.d == 2 ? tdiff_pipe_t<n, 2>(p, grid, s) : tdiff_pipe_t<n, 3>(p, grid, s);
+    switch (N) { TP_CASE(64) TP_CASE(128) TP_CASE(256) TP_CASE(512) TP_CASE(1024)
+    default: return cudaErrorInvalidValue; }
+#undef TP_CASE
+}
+
+int tdiff_pipe_units(int N, int d) {   // lines per warp unit; 0: the stage does not fit
+#define TU_CASE(n) \
+    case n: return (d == 2 ? TPipe<n, 2>::FITS : TPipe<n, 3>::FITS) ? TPipe<n, 2>::U : 0;
+    switch (N) { TU_CASE(64) TU_CASE(128) TU_CASE(256) TU_CASE(512) TU_CASE(1024)
+    default: return 0; }
+#undef TU_CASE
 }
 
 // u = E_0 / sqrt(s_u) as float32 (the solution of A_raw, reading R-29)
@@ -301,13 +517,19 @@ cudaError_t launch_tdiff_pot(const TDParams &p, int mode, int grid, cudaStream_t
     return cudaGetLastError();
 }
 cudaError_t launch_tdiff_mul(const TDParams &p, int check_state, int grid, cudaStream_t s) {
-    k_tdiff_mul<<<grid, 256, 0, s>>>(p, check_state);
+    if (p.d == 2) k_tdiff_mul<2><<<grid, 256, 0, s>>>(p, check_state);
+    else k_tdiff_mul<3><<<grid, 256, 0, s>>>(p, check_state);
     return cudaGetLastError();
 }
+template <int d>
+static void tdiff_upd_t(XMode mode, const TDParams &p, int grid, cudaStream_t s) {
+    if (mode == X_SRC_FWD) k_tdiff_upd<d, X_SRC_FWD><<<grid, 256, 0, s>>>(p);
+    else if (mode == X_SRC_EPI) k_tdiff_upd<d, X_SRC_EPI><<<grid, 256, 0, s>>>(p);
+    else k_tdiff_upd<d, X_ITER><<<grid, 256, 0, s>>>(p);
+}
 cudaError_t launch_tdiff_upd(XMode mode, const TDParams &p, int grid, cudaStream_t s) {
-    if (mode == X_SRC_FWD) k_tdiff_upd<X_SRC_FWD><<<grid, 256, 0, s>>>(p);
-    else if (mode == X_SRC_EPI) k_tdiff_upd<X_SRC_EPI><<<grid, 256, 0, s>>>(p);
-    else k_tdiff_upd<X_ITER><<<grid, 256, 0, s>>>(p);
+    if (p.d == 2) tdiff_upd_t<2>(mode, p, grid, s);
+    else tdiff_upd_t<3>(mode, p, grid, s);
     return cudaGetLastError();
 }
 cudaError_t launch_tdiff_out(const float2 *E0, float *out, float scale, long long n, int grid, cudaStream_t s) {

@@ -198,6 +198,7 @@ struct usp_plan_s {
     bool tdiff = false;
     int ncomp = 1;                 // components of the fields (1; 2 anti; d + 1 tdiff)
     float *td_vu = nullptr, *td_vf = nullptr, *td_dinv = nullptr, *td_red = nullptr;
+    int td_pipe = 0;   // lines per unit of the fused x pass (k_tdiff_pipe), 0: k_xfft + k_tdiff_upd
     TDParams td{};
     // persistent 2-D solve (kernels_small.cu; desc.launch_per_pass disables)
     bool solve2d = false;
@@ -909,6 +910,11 @@ AParams anti_params(usp_plan_s *p) {
 
 usp_status run_anti_x(usp_plan_s *p, XMode mode) {
     Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
+    if (mode == X_ITER) {   // TMA-pipelined, one CTA per SM
+        const long long units = p->ny * p->nz / anti_pipe_units((int)p->nx);
+        CU(launch_anti_pipe((int)p->nx, anti_params(p), occ_grid(p, units, 1), p->stream));
+        return USP_OK;
+    }
     const int grid = occ_grid(p, (p->ny * p->nz + anti_lines_per_cta((int)p->nx) - 1) / anti_lines_per_cta((int)p->nx), 4);
     CU(launch_anti_x((int)p->nx, mode, anti_params(p), grid, p->stream));
     return USP_OK;
@@ -953,6 +959,7 @@ TDParams td_params(usp_plan_s *p) {
     t.red = p->td_red;
     t.inv_n = (float)(1.0 / (double)p->nvox);
     t.mp = mul_params(p);
+    t.twx = p->tw[0];
     t.st = p->st;
     t.red_d = Red{p->partials, p->hist, p->hist_cap, nullptr};
     return t;
@@ -993,6 +1000,11 @@ usp_status chain_tdiff(usp_plan_s *p, int check_state) {
 
 usp_status td_upd(usp_plan_s *p, XMode mode) {
     Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
+    if (mode == X_ITER && p->td_pipe) {   // x inverse FFT + update + x forward FFT in one TMA-pipelined pass
+        const long long units = p->ny * p->nz / p->td_pipe;
+        CU(launch_tdiff_pipe((int)p->nx, td_params(p), occ_grid(p, units, 1), p->stream));
+        return USP_OK;
+    }
     CU(launch_tdiff_upd(mode, td_params(p), occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
     return USP_OK;
 }
@@ -1278,6 +1290,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     p->anti = desc->antisymmetric != 0;
     p->tdiff = desc->tensor_diffusion != 0;
     p->ncomp = p->anti ? 2 : (p->tdiff ? desc->ndim + 1 : 1);
+    p->td_pipe = p->tdiff ? tdiff_pipe_units((int)desc->n[0], desc->ndim) : 0;
     p->ndim = desc->ndim;
     p->nx = desc->n[0];
     p->ny = desc->ndim >= 2 ? desc->n[1] : 1;
@@ -1720,6 +1733,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
         if ((s = chain_tdiff(p, 0))) return s;
         if ((s = td_xfft(p, true))) return s;
         if ((s = td_upd(p, X_SRC_EPI))) return s;
+        if (p->td_pipe && (s = td_xfft(p, false))) return s;   // the fused pass expects x-transformed input
     } else if (p->anti) {
         if ((s = run_anti_x(p, X_SRC_FWD))) return s;
         if ((s = chain_anti(p, 0))) return s;
@@ -1851,9 +1865,9 @@ usp_status usp_iterate(usp_plan_t p, int64_t n_max, double alpha, double tol, in
             }
             for (long long i = 0; i < nb; ++i) {
                 if (p->tdiff) {
-                    if ((s = td_xfft(p, false))) return s;
+                    if (!p->td_pipe && (s = td_xfft(p, false))) return s;
                     if ((s = chain_tdiff(p, 1))) return s;
-                    if ((s = td_xfft(p, true))) return s;
+                    if (!p->td_pipe && (s = td_xfft(p, true))) return s;
                     if ((s = td_upd(p, X_ITER))) return s;
                     continue;
                 }

@@ -237,6 +237,7 @@ struct TDParams {
     float s_scale;               // 1/(c sqrt(s_u))
     float *red;                  // setup reductions: 16 floats per CTA
     MulParams mp;
+    const float2 *twx;           // x-line twiddles (the fused x pass)
     IterState *st;
     Red red_d;
 };
@@ -283,11 +284,15 @@ struct FarParams {       // farthest medium value from a centre (smallest circle
 cudaError_t launch_anti_x(int N, XMode mode, const AParams &p, int grid, cudaStream_t s);
 cudaError_t launch_anti_mul(const AParams &p, int check_state, int grid, cudaStream_t s);
 int anti_lines_per_cta(int N);
+cudaError_t launch_anti_pipe(int N, const AParams &p, int grid, cudaStream_t s);   // the iterations' x pass
+int anti_pipe_units(int N);                                                        // lines per warp unit
 
 // tensor diffusion (kernels_tdiff.cu)
 cudaError_t launch_xfft(int N, bool inv, float2 *data, const float2 *tw, long long nlines, int grid, cudaStream_t s);
 cudaError_t launch_tdiff_pot(const TDParams &p, int mode, int grid, cudaStream_t s);
 cudaError_t launch_tdiff_mul(const TDParams &p, int check_state, int grid, cudaStream_t s);
+cudaError_t launch_tdiff_pipe(int N, const TDParams &p, int grid, cudaStream_t s);   // fused x pass; Invalid if the stage does not fit
+int tdiff_pipe_units(int N, int d);                                                  // 0: falls back to k_xfft + k_tdiff_upd
 cudaError_t launch_tdiff_upd(XMode mode, const TDParams &p, int grid, cudaStream_t s);
 cudaError_t launch_tdiff_out(const float2 *E0, float *out, float scale, long long n, int grid, cudaStream_t s);
 

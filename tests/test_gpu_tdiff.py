@@ -50,8 +50,11 @@ def _orc(orc, shape, mu, D, S, n, tol=0.0):
     return r, sp
 
 
+# x extents 64-256 (and 2-D 512) run the fused TMA-pipelined x pass
+# (k_tdiff_pipe); 3-D with x extent 512 the k_xfft + k_tdiff_upd sequence
 @pytest.mark.parametrize("shape,aniso,n", [((64, 64), True, 150), ((64, 128), False, 100), ((64, 64, 64), True, 60),
-                                           ((128, 64, 64), True, 30)])
+                                           ((128, 64, 64), True, 30), ((64, 256), True, 80), ((64, 512), True, 60),
+                                           ((64, 64, 256), True, 20), ((64, 64, 512), True, 10)])
 def test_tdiff_matches_oracle(orc, shape, aniso, n):
     mu, D, S = _medium(shape, 3, aniso)
     u, nd, term, plan = _gpu(shape, mu, D, S, n)
@@ -65,6 +68,20 @@ def test_tdiff_matches_oracle(orc, shape, aniso, n):
     k = r.hist[:n] > 1e-10        # above the oracle's x-form floor (the GPU Delta-form has none, R-17)
     assert np.allclose(h[:n][k], r.hist[:n][k], rtol=1e-3, atol=0.0)
     assert np.all(np.diff(h[: n + 1]) <= 1e-5 * h[:n])          # Cor. 1: monotone
+
+
+@pytest.mark.parametrize("shape", [(64, 256), (64, 64, 128)])
+def test_tdiff_split_iterate_equals_one_call(shape):
+    """iterate(a) + iterate(b) == iterate(a + b) bit for bit: the state the
+    fused x pass leaves between calls (x-transformed work) is complete."""
+    mu, D, S = _medium(shape, 6, True)
+    u1, _, _, p1 = _gpu(shape, mu, D, S, 25)
+    mu2, D2, S2 = _medium(shape, 6, True)
+    u2, n2, _, p2 = _gpu(shape, mu2, D2, S2, 10)
+    n3, _ = p2.iterate(15, 0.75, 0.0)
+    u2 = p2.get_field().cpu().numpy().astype(np.float64)
+    assert n2 + n3 == 25 and np.array_equal(u1, u2)
+    assert np.array_equal(p1.history()[:26], p2.history()[:26])
 
 
 def test_tdiff_converges_like_oracle(orc):

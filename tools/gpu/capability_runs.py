@@ -27,8 +27,13 @@ def timed(fn):
 
 
 def main():
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     torch.cuda.set_device(0)
     res = {}
+    if only == "tdiff":
+        tdiff(res)
+        print(json.dumps(res), flush=True)
+        return
     # antisymmetrised system (Eq. 9-10) on the C3 recipe at 256^3
     p = make("C3", device="cuda")
     med, src = p.medium.to(torch.complex64), p.source.to(torch.complex64)
@@ -57,7 +62,24 @@ def main():
     plan.close()
     del med, src
     torch.cuda.empty_cache()
-    # tensor diffusion, 3-D 256^3, anisotropic D
+    tdiff(res)
+    # C2 persistent 2-D solver and C1 1-D solver
+    for name in ("C2", "C1"):
+        q = make(name)
+        m2, s2 = (torch.from_numpy(np.asarray(q.medium).astype(np.complex64)).cuda(),
+                  torch.from_numpy(np.asarray(q.source).astype(np.complex64)).cuda())
+        plan = Plan(q.shape)
+        plan.set_potential(m2, 0.95)
+        plan.set_source(s2)
+        plan.iterate(5, 0.75, 0.0)
+        ms, _ = timed(lambda: plan.iterate(200, 0.75, 0.0))
+        res[name] = {"ms_per_iteration": ms / 200}
+        plan.close()
+    print(json.dumps(res), flush=True)
+
+
+def tdiff(res):
+    """tensor diffusion, 3-D 256^3, anisotropic D"""
     shape = (256, 256, 256)
     rng = np.random.default_rng(3)
     mu = torch.from_numpy((0.02 + 0.08 * rng.random(shape)).astype(np.float32)).cuda()
@@ -76,19 +98,6 @@ def main():
     plan.close()
     del mu, D, S
     torch.cuda.empty_cache()
-    # C2 persistent 2-D solver and C1 1-D solver
-    for name in ("C2", "C1"):
-        q = make(name)
-        m2, s2 = (torch.from_numpy(np.asarray(q.medium).astype(np.complex64)).cuda(),
-                  torch.from_numpy(np.asarray(q.source).astype(np.complex64)).cuda())
-        plan = Plan(q.shape)
-        plan.set_potential(m2, 0.95)
-        plan.set_source(s2)
-        plan.iterate(5, 0.75, 0.0)
-        ms, _ = timed(lambda: plan.iterate(200, 0.75, 0.0))
-        res[name] = {"ms_per_iteration": ms / 200}
-        plan.close()
-    print(json.dumps(res), flush=True)
 
 
 if __name__ == "__main__":
