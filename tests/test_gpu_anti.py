@@ -40,8 +40,10 @@ def _gpu(shape, k2, S, n, tol=0.0):
     return plan.get_field().cpu().numpy().astype(np.complex128), nd, term, plan
 
 
+# every x extent of the TMA-pipelined x pass (k_anti_pipe<64 .. 1024>)
 @pytest.mark.parametrize("shape,gain,n", [((64, 64), 0.0, 200), ((64, 128), 0.05, 150), ((64, 64, 64), 0.05, 60),
-                                          ((128, 64, 64), 0.0, 40)])
+                                          ((128, 64, 64), 0.0, 40), ((64, 256), 0.05, 80), ((64, 512), 0.0, 60),
+                                          ((64, 1024), 0.05, 40), ((64, 64, 256), 0.05, 20)])
 def test_anti_matches_oracle(orc, shape, gain, n):
     k2, S = _medium(shape, 5, gain)
     x, nd, term, plan = _gpu(shape, k2, S, n)
@@ -58,6 +60,19 @@ def test_anti_matches_oracle(orc, shape, gain, n):
     h = plan.history()
     assert np.allclose(h[:n], res.hist[:n], rtol=1e-3, atol=0.0)          # r_0 .. r_{n-1}
     assert np.all(np.diff(h[: n + 1]) <= 1e-5 * h[:n])       # Cor. 1: monotone
+
+
+@pytest.mark.parametrize("shape", [(64, 1024), (64, 64, 128)])
+def test_anti_split_iterate_equals_one_call(shape):
+    """iterate(a) + iterate(b) == iterate(a + b) bit for bit (the state the
+    pipelined x pass leaves between calls is complete)."""
+    k2, S = _medium(shape, 7, 0.05)
+    x1, _, _, p1 = _gpu(shape, k2, S, 25)
+    x2, n2, _, p2 = _gpu(shape, k2, S, 10)
+    n3, _ = p2.iterate(15, 0.75, 0.0)
+    x2 = p2.get_field().cpu().numpy().astype(np.complex128)
+    assert n2 + n3 == 25 and np.array_equal(x1, x2)
+    assert np.array_equal(p1.history()[:26], p2.history()[:26])
 
 
 def test_gain_medium_rejected_by_standard_form_solved_by_anti():

@@ -38,6 +38,7 @@ CASES = [
     ("C5", (1024, 64, 16), 3, 0.0, {}),                        # k_stile<1024> two-round exchange, TMA stores
     ("C5", (64, 1024, 1024), 4, 0.0, {"plane_chain": True}),   # plane-chained pass
     ("C5", (64, 64, 64), 5, 0.0, {"antisymmetric": True}),
+    ("C5", (64, 64, 1024), 3, 0.0, {"antisymmetric": True}),  # k_anti_pipe<1024>, 3 stages
 ]
 
 
@@ -122,3 +123,32 @@ def test_krylov_repeat_and_poison():
     for xb, xg in outs[1:]:
         assert np.array_equal(xb.view(np.uint8), outs[0][0].view(np.uint8))
         assert np.array_equal(xg.view(np.uint8), outs[0][1].view(np.uint8))
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 128), (64, 512)])
+def test_tdiff_repeat_and_poison(shape):
+    """Tensor diffusion: the fused pipelined x pass (3-D) and its 2-D
+    two-stage instance, zero / NaN / zero workspace: bit-identical."""
+    import torch
+    from paper_2207_14222_b200 import Plan
+
+    rng = np.random.default_rng(12)
+    d = len(shape)
+    mu = (0.02 + 0.08 * rng.random(shape)).astype(np.float32)
+    A = rng.standard_normal(shape + (d, d)) * 0.3
+    D = (np.einsum("...ij,...kj->...ik", A, A) + np.eye(d)).astype(np.float32)
+    S = np.zeros(shape, dtype=np.float32)
+    S[tuple(s // 2 for s in shape)] = 1.0
+    outs = []
+    for fill in (0, 255, 0):
+        plan = Plan(shape, kind="diffusion", tensor_diffusion=True)
+        _refill(plan, fill)
+        plan.set_tensor_medium(torch.from_numpy(mu).cuda(), torch.from_numpy(D).cuda(), 0.95)
+        plan.set_source(torch.from_numpy(S).cuda())
+        plan.iterate(12, 0.75, 0.0)
+        outs.append((plan.get_field().cpu().numpy(), plan.history()[:13].copy()))
+        plan.close()
+    assert np.isfinite(outs[1][0]).all()
+    for u, h in outs[1:]:
+        assert np.array_equal(u.view(np.uint8), outs[0][0].view(np.uint8))
+        assert np.array_equal(h, outs[0][1])
