@@ -345,7 +345,7 @@ cudaError_t launch_anti_x(int N, XMode mode, const AParams &p, int grid, cudaStr
 }
 
 cudaError_t launch_anti_mul(const AParams &p, int check_state, int grid, cudaStream_t s) {
-    k_anti_mul<<<grid, 256, 0, s>>>(p, check_state);
+    k_anti_mul<<<resident_grid<k_anti_mul>(grid, 256), 256, 0, s>>>(p, check_state);
     return cudaGetLastError();
 }
 

@@ -347,44 +347,76 @@ __global__ void __launch_bounds__(256) k_kupd(KParams p) {
 // GMRES(m) Gram-Schmidt blocks (NB <= 8 basis vectors per launch):
 //   GS_DOT:  partials of (U_j, z), j < NB (and ||z||^2 when want_norm)
 //   GS_AXPY: z <- scale (z - sum_j c_j U_j)  (and ||z||^2 of the result)
-// Per-thread fp32 over chunks of 64 elements, fp64 across chunks, fixed-order
+// Per-thread fp32 over chunks of 64 steps, fp64 across chunks, fixed-order
 // CTA sums -> one row of partials per CTA (the host sums them in order).
+// The axpy moves two complex values per thread and access (128-bit; n is
+// even: power-of-two extents).
+// Launched with kGsCtasPerSm = 3 CTAs per SM and a grid of 3 x SMs, so every
+// CTA is resident at once (the grid-stride loop gives all CTAs equal work;
+// before, a 4 x SMs grid of an 80-register kernel ran its last quarter as a
+// second wave: the dot at 62 % of the copy peak), and the register budget
+// (85) lets ptxas keep the NB + 1 loads back to back.
 template <int NB, int MODE>
-__global__ void __launch_bounds__(256) k_gs(GSParams p) {
+__global__ void __launch_bounds__(256, kGsCtasPerSm) k_gs(GSParams p) {
     constexpr int K = (MODE == GS_DOT) ? 2 * NB + 1 : 1;
-    double acc[K];
+    // the fp64 accumulators live in shared memory (the dot's 2 NB + 1 of them
+    // would take 34 registers)
+    __shared__ double acc_sh[K][256];
     float la[K];
 #pragma unroll
-    for (int q = 0; q < K; ++q) { acc[q] = 0.0; la[q] = 0.f; }
-    const long long n = p.n, stride = (long long)gridDim.x * blockDim.x;
+    for (int q = 0; q < K; ++q) { acc_sh[q][threadIdx.x] = 0.0; la[q] = 0.f; }
+    const long long stride = (long long)gridDim.x * blockDim.x;
     int cnt = 0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride) {
-        float2 z = p.z[i];
-        if (MODE == GS_DOT) {
+    if (MODE == GS_DOT) {
+        // one complex per thread and step (2 NB + 1 fp32 partials and NB + 1
+        // 64-bit loads in flight)
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n; i += stride) {
+            const float2 z = p.z[i];
+            float2 u[NB];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) u[b] = p.U[b][i];
 #pragma unroll
             for (int b = 0; b < NB; ++b) {
-                const float2 u = p.U[b][i];
-                la[2 * b] += u.x * z.x + u.y * z.y;
-                la[2 * b + 1] += u.x * z.y - u.y * z.x;
+                la[2 * b] += u[b].x * z.x + u[b].y * z.y;
+                la[2 * b + 1] += u[b].x * z.y - u[b].y * z.x;
             }
             la[2 * NB] += cabs2(z);
-        } else {
+            if (++cnt == 64) {
 #pragma unroll
-            for (int b = 0; b < NB; ++b) z = csub(z, cmul(p.c[b], p.U[b][i]));
-            z = cmul(p.scale, z);
-            p.z[i] = z;
-            la[0] += cabs2(z);
+                for (int q = 0; q < K; ++q) { acc_sh[q][threadIdx.x] += (double)la[q]; la[q] = 0.f; }
+                cnt = 0;
+            }
         }
-        if (++cnt == 64) {
+    } else {
+        // two complex values per thread and step (128-bit accesses)
+        const long long n2 = p.n / 2;
+        float4 *Z = reinterpret_cast<float4 *>(p.z);
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += stride) {
+            const float4 z4 = Z[i];
+            float4 u4[NB];
 #pragma unroll
-            for (int q = 0; q < K; ++q) { acc[q] += (double)la[q]; la[q] = 0.f; }
-            cnt = 0;
+            for (int b = 0; b < NB; ++b) u4[b] = reinterpret_cast<const float4 *>(p.U[b])[i];
+            float2 z[2] = {make_float2(z4.x, z4.y), make_float2(z4.z, z4.w)};
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                z[0] = csub(z[0], cmul(p.c[b], make_float2(u4[b].x, u4[b].y)));
+                z[1] = csub(z[1], cmul(p.c[b], make_float2(u4[b].z, u4[b].w)));
+            }
+            z[0] = cmul(p.scale, z[0]);
+            z[1] = cmul(p.scale, z[1]);
+            Z[i] = make_float4(z[0].x, z[0].y, z[1].x, z[1].y);
+            la[0] += cabs2(z[0]) + cabs2(z[1]);
+            if (++cnt == 64) {
+                acc_sh[0][threadIdx.x] += (double)la[0];
+                la[0] = 0.f;
+                cnt = 0;
+            }
         }
     }
     __shared__ double sh[8][K];
 #pragma unroll
     for (int q = 0; q < K; ++q) {
-        double v = warp_sum_d(acc[q] + (double)la[q]);
+        double v = warp_sum_d(acc_sh[q][threadIdx.x] + (double)la[q]);
         if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5][q] = v;
     }
     __syncthreads();
@@ -439,7 +471,7 @@ cudaError_t launch_gs(int mode, int nb, const GSParams &p, int grid, cudaStream_
 }
 
 cudaError_t launch_kupd(const KParams &p, int grid, cudaStream_t s) {
-    k_kupd<<<grid, 256, 0, s>>>(p);
+    k_kupd<<<resident_grid<k_kupd>(grid, 256), 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -517,15 +517,15 @@ cudaError_t launch_tdiff_pot(const TDParams &p, int mode, int grid, cudaStream_t
     return cudaGetLastError();
 }
 cudaError_t launch_tdiff_mul(const TDParams &p, int check_state, int grid, cudaStream_t s) {
-    if (p.d == 2) k_tdiff_mul<2><<<grid, 256, 0, s>>>(p, check_state);
-    else k_tdiff_mul<3><<<grid, 256, 0, s>>>(p, check_state);
+    if (p.d == 2) k_tdiff_mul<2><<<resident_grid<k_tdiff_mul<2>>(grid, 256), 256, 0, s>>>(p, check_state);
+    else k_tdiff_mul<3><<<resident_grid<k_tdiff_mul<3>>(grid, 256), 256, 0, s>>>(p, check_state);
     return cudaGetLastError();
 }
 template <int d>
 static void tdiff_upd_t(XMode mode, const TDParams &p, int grid, cudaStream_t s) {
-    if (mode == X_SRC_FWD) k_tdiff_upd<d, X_SRC_FWD><<<grid, 256, 0, s>>>(p);
-    else if (mode == X_SRC_EPI) k_tdiff_upd<d, X_SRC_EPI><<<grid, 256, 0, s>>>(p);
-    else k_tdiff_upd<d, X_ITER><<<grid, 256, 0, s>>>(p);
+    if (mode == X_SRC_FWD) k_tdiff_upd<d, X_SRC_FWD><<<resident_grid<k_tdiff_upd<d, X_SRC_FWD>>(grid, 256), 256, 0, s>>>(p);
+    else if (mode == X_SRC_EPI) k_tdiff_upd<d, X_SRC_EPI><<<resident_grid<k_tdiff_upd<d, X_SRC_EPI>>(grid, 256), 256, 0, s>>>(p);
+    else k_tdiff_upd<d, X_ITER><<<resident_grid<k_tdiff_upd<d, X_ITER>>(grid, 256), 256, 0, s>>>(p);
 }
 cudaError_t launch_tdiff_upd(XMode mode, const TDParams &p, int grid, cudaStream_t s) {
     if (p.d == 2) tdiff_upd_t<2>(mode, p, grid, s);

@@ -2305,7 +2305,7 @@ usp_status usp_gmres(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done, u
     if (p->st_host->k != 0)
         return fail(USP_ERR_STATE, "GMRES starts from x_0 = 0: call usp_set_source again first");
     if (!p->gm_part) {
-        p->gm_grid = p->nsm * 4;
+        p->gm_grid = p->nsm * kGsCtasPerSm;   // every CTA resident at once (k_gs)
         CU(cudaMalloc(&p->gm_part, sizeof(double) * 17 * p->gm_grid * 9));   // (m + 1 <= 65 vectors) / 8 blocks
     }
     const int m = p->gm_m;

@@ -303,6 +303,7 @@ cudaError_t launch_solve2d(int nx, int ny, const S2Params &p, int nsm, cudaStrea
 // BiCGSTAB (kernels_krylov.cu)
 cudaError_t launch_xop(int N, KMode mode, const KParams &p, int grid, cudaStream_t s);
 cudaError_t launch_kupd(const KParams &p, int grid, cudaStream_t s);
+constexpr int kGsCtasPerSm = 3;   // k_gs: __launch_bounds__(256, 3), grid = 3 x SMs
 cudaError_t launch_gs(int mode, int nb, const GSParams &p, int grid, cudaStream_t s);
 
 // real path (kernels_real.cu)

@@ -7,9 +7,15 @@ residual) the complex64 and complex128 runs drift apart after a few passes
 (measured 1.9e-2 after 20 passes at 128^2) while both converge to the same
 solution.  So the iterate-level bar (1e-4 after the same count) is applied
 where the recurrence is well conditioned (C3, all passes) and to the first
-passes of C2; on C2 the bar is the CONVERGED field (unique: A^-1 s) and a
-pass count within 5 % (measured 639 vs 619 passes to 1e-6 at 512^2).  On
-C3 the pass counts to 1e-4..1e-6 are identical (R-25)."""
+passes of C2; on C2 the bar is the CONVERGED solve: its TRUE residual
+||M x - b|| / ||b||, evaluated by the oracle's fp64 operator on the GPU's
+field, within tol + the complex64 residual gap (_gap32), a pass count within 5 % (measured 639 vs 619 passes
+to 1e-6 at 512^2), and the field within the distance two solutions of
+residual <= tol can have: ||x - x'|| <= ||M^-1|| (r + r') ||x||, with
+||M^-1|| ~ 1 / lambda_min ~ 90 on C2 (its fixed-point rate: 1680 iterations
+per 1e-6 at alpha = 0.75, lambda_min ~ (1 - 1e-6^(1/1680)) / 0.75 = 0.011),
+i.e. <= 5e-4 at tol = 1e-6 (R-25).  On C3 the pass counts to
+1e-4..1e-6 are identical and the field bar is 1e-4."""
 import math
 
 import numpy as np
@@ -47,6 +53,28 @@ def _orc(orc, p, n, tol):
                         tol, n)
 
 
+def _true_residual(orc, p, x):
+    """||M x - b|| / ||b|| with M = B[1 - (L+1)^-1 B], b = B (L+1)^-1 s
+    (R-25), evaluated in fp64 by the oracle's setup and (L+1)^-1."""
+    med, src, _ = rounded_inputs(p)
+    med64 = med.astype(np.complex128)
+    sp = orc.canonical(p.kind, med64, 0.95, D=p.D)
+    _, B, s = orc.setup(orc.medium_to_w(p.kind, med64), src.astype(np.complex128), sp.sigma, sp.c)
+    b = B * orc.apply_Linv(s, p.h, sp.D, sp.sigma, sp.c)
+    r = B * (x - orc.apply_Linv(B * x, p.h, sp.D, sp.sigma, sp.c)) - b
+    return float(np.linalg.norm(r) / np.linalg.norm(b))
+
+
+def _gap32(hist, n, per_pass):
+    """Bound on the gap between the recurrence residual and the true
+    residual of a complex64 Krylov run: rounding errors of ~eps32 relative
+    to the largest residual seen, committed by each of the per_pass operator
+    applications of the n passes (the classical residual-gap estimate,
+    ||b - M x_k - r_k|| <~ eps sum_j ||r_j||), with a factor 2 of slack."""
+    eps32 = float(np.finfo(np.float32).eps)
+    return 2.0 * eps32 * per_pass * max(n, 1) * float(np.max(hist))
+
+
 @pytest.mark.parametrize("name,shape,n", [("C3", (64, 64, 64), 20), ("C2", (128, 128), 3),
                                           ("C2", (512, 512), 3), ("C5", (32, 64, 128), 12),
                                           ("C3", (64, 32, 16), 20)])
@@ -71,11 +99,13 @@ def test_bicgstab_converges_like_oracle(orc, name, shape, tol):
     x, nd, term, plan = _gpu(p, 3000, tol)
     ref = _orc(orc, p, 3000, tol)
     assert term == "converged" and ref.rc == 0
+    assert _true_residual(orc, p, x) <= tol + _gap32(plan.history()[: nd + 1], nd, 2)
     if name == "C3":
         assert abs(nd - ref.n_done) <= 1, (nd, ref.n_done)
+        assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)
     else:
         assert abs(nd - ref.n_done) <= 0.05 * ref.n_done, (nd, ref.n_done)
-    assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)
+        assert rel_l2(x, ref.x) <= 500 * tol, rel_l2(x, ref.x)     # ||M^-1|| (r + r'), see the module doc
 
 
 def test_bicgstab_virtual_slabs_bit_identical():
@@ -177,6 +207,7 @@ def test_gmres_converges_like_oracle(orc, name, shape, m):
     x, nd, term, plan = _gpu_gmres(p, m, 5000, 1e-5)
     ref = _orc_gmres(orc, p, m, 5000, 1e-5)
     assert term == "converged" and ref.rc == 0
+    assert _true_residual(orc, p, x) <= 1e-5 + _gap32(plan.history()[: nd + 1], nd, 1)
     assert abs(nd - ref.n_done) <= max(1, 0.03 * ref.n_done), (nd, ref.n_done)
     assert rel_l2(x, ref.x) <= TOL_FIELD, rel_l2(x, ref.x)
 
