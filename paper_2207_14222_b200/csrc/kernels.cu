@@ -428,9 +428,11 @@ cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t
 }
 
 cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s) {
-    k_potential<<<grid, 256, 0, s>>>(p);
+    k_potential<<<resident_grid<k_potential>(grid, 256), 256, 0, s>>>(p);
     return cudaGetLastError();
 }
+
+int farthest_grid(int grid) { return resident_grid<k_farthest>(grid, 256); }
 
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s) {
     k_farthest<<<grid, 256, 0, s>>>(p);

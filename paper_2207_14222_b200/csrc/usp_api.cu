@@ -520,7 +520,7 @@ usp_status device_mec(usp_plan_s *p, const void *medium_dev, P2 &centre, double 
     sup.push_back(q);
     centre = q;
     radius = 0.0;
-    const int grid = std::min(p->far_cap, occ_grid(p, (p->nloc + 255) / 256, 8));
+    const int grid = farthest_grid(std::min(p->far_cap, occ_grid(p, (p->nloc + 255) / 256, 8)));
     std::vector<double> bd(grid);
     std::vector<long long> bi(grid);
     for (int it = 0; it < 200; ++it) {

@@ -317,6 +317,7 @@ cudaError_t launch_strided(int N, SMode mode, const SParams &p, int grid, cudaSt
 cudaError_t launch_solve1d(int N, OneMode mode, const OneParams &p, cudaStream_t s);
 cudaError_t launch_potential(const PotParams &p, int grid, cudaStream_t s);
 cudaError_t launch_farthest(const FarParams &p, int grid, cudaStream_t s);
+int farthest_grid(int grid);   // grid clamped to the CTAs resident at once (one partial per CTA)
 cudaError_t launch_finish(IterState *st, const double *sums, int P, int src_epi, const Red &red, cudaStream_t s);
 cudaError_t launch_set_state(IterState *st, double alpha, double tol, long long kmax, cudaStream_t s);
 // small host -> device writes as kernel arguments (no copy engine, no pageable-memory copy)
