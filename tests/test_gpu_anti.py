@@ -43,7 +43,8 @@ def _gpu(shape, k2, S, n, tol=0.0):
 # every x extent of the TMA-pipelined x pass (k_anti_pipe<64 .. 1024>)
 @pytest.mark.parametrize("shape,gain,n", [((64, 64), 0.0, 200), ((64, 128), 0.05, 150), ((64, 64, 64), 0.05, 60),
                                           ((128, 64, 64), 0.0, 40), ((64, 256), 0.05, 80), ((64, 512), 0.0, 60),
-                                          ((64, 1024), 0.05, 40), ((64, 64, 256), 0.05, 20)])
+                                          ((64, 1024), 0.05, 40), ((64, 64, 256), 0.05, 20),
+                                          ((128, 128, 256), 0.05, 8)])
 def test_anti_matches_oracle(orc, shape, gain, n):
     k2, S = _medium(shape, 5, gain)
     x, nd, term, plan = _gpu(shape, k2, S, n)

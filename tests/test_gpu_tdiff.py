@@ -55,7 +55,7 @@ def _orc(orc, shape, mu, D, S, n, tol=0.0):
 @pytest.mark.parametrize("shape,aniso,n", [((64, 64), True, 150), ((64, 128), False, 100), ((64, 64, 64), True, 60),
                                            ((128, 64, 64), True, 30), ((64, 256), True, 80), ((64, 512), True, 60),
                                            ((64, 1024), True, 40), ((64, 64, 256), True, 20),
-                                           ((64, 64, 512), True, 10)])
+                                           ((64, 64, 512), True, 10), ((64, 128, 256), True, 6)])
 def test_tdiff_matches_oracle(orc, shape, aniso, n):
     mu, D, S = _medium(shape, 3, aniso)
     u, nd, term, plan = _gpu(shape, mu, D, S, n)
