@@ -9,6 +9,7 @@
 //      exchange syncs only its group (named barrier), the stage is released
 //      by whichever group copies it last -- groups drift apart, so one
 //      group's FMA blocks can overlap the other's exchanges
+//   C  see k_c (swizzled stage, conflict-free group reads, TMA stores)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o zgroups zgroups.cu -lcuda && ./zgroups
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -149,6 +150,144 @@ __global__ void __launch_bounds__(NT, 1) k_g(const __grid_constant__ CUtensorMap
     }
 }
 
+
+// C  two groups of 8 warps on 8 columns each, like B, plus: the stage is
+//    loaded with the 128-byte swizzle and a warp reads rows {a, a+1, a+4,
+//    a+5} (+32m) of its 8 columns, so the four rows fall on both bank halves
+//    (2 wavefronts per 64-bit read, as in A); results leave through the
+//    group's exchange buffer by TMA stores ({8, 256} boxes, two halves per
+//    tile), never as 4-row x 64-byte register stores.
+// SM_: 0 no stores, 1 per-group {8, 256} TMA stores (64-byte rows), 2 both
+// groups meet, stash 16-column rows, {16, 256} TMA stores (128-byte rows)
+template <int R, int SM_ = 1>
+__global__ void __launch_bounds__(NT, 1) k_c(const __grid_constant__ CUtensorMap map,
+                                             const __grid_constant__ CUtensorMap smap8, float f) {
+    constexpr int GC = 8, GT = 256, XP = 16 * GC + 8, XBG = 32 * XP;
+    extern __shared__ __align__(1024) unsigned char sm[];
+    float2 *stage = (float2 *)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
+    const int g = threadIdx.x / GT, tl = threadIdx.x % GT;
+    float2 *xb = stage + 16 * NN + g * XBG;
+    uint64_t *full = (uint64_t *)(stage + 16 * NN + 2 * XBG);
+    unsigned *taken = (unsigned *)(full + 1);
+    const int w = tl / 32, l = tl % 32;
+    const int cl = l & 7, jr = l >> 3;
+    const int j = (w >> 1) * 8 + (w & 1) * 2 + (jr & 1) + (jr >> 1) * 4;
+    const int c = g * GC + cl;
+    const int bar = 1 + g;
+    const long long ntiles = NN * NN / 16;
+    const long long t0 = blockIdx.x, tstep = gridDim.x;
+    const int nloc = (int)((ntiles - t0 + tstep - 1) / tstep);
+    auto issue = [&](int i) {
+        const long long t = t0 + (long long)i * tstep;
+        mbar_expect(full, 16 * NN * 8);
+        for (int b = 0; b < 4; ++b) tma2d(stage + b * 256 * 16, &map, (int)(t * 16), b * 256, full);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        *taken = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (nloc > 0) issue(0);
+    }
+    __syncthreads();
+    for (int i = 0; i < nloc; ++i) {
+        mbar_wait(full, i & 1);
+        float2 v[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+            const int r = j + 32 * m;   // r & 7 == j & 7
+            v[m] = stage[r * 16 + (((c >> 1) ^ (r & 7)) << 1) + (c & 1)];
+        }
+        fence_async();
+        if (SM_ == 2) {
+            if (threadIdx.x == 0) bulk_wait_read0();
+        } else if (tl == 0) bulk_wait_read0();   // previous tile's stash stores have left xb
+        nbar(bar, GT);
+        if (tl == 0) {
+            if (atomicAdd(taken, 1u) % 2 == 1)
+                if (i + 1 < nloc) issue(i + 1);
+        }
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            fma_block<R>(v, f);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                float2 *wb = xb + j * XP + cl;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) wb[q * GC] = v[r * 16 + q];
+                nbar(bar, GT);
+                const float2 *rb = xb + (16 * r) * XP + (j & 15) * GC + cl;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) v[r * 16 + q] = rb[q * XP];
+                nbar(bar, GT);
+            }
+            fma_block<R>(v, f);
+            if (pass == 0) fma_block<R>(v, f);
+        }
+        const long long t = t0 + (long long)i * tstep;
+        if (SM_ == 0) {
+            if (v[0].x == 1.2345f) stage[tl] = v[1];
+            continue;
+        }
+        if (SM_ == 2) {
+            float2 *xs = stage + 16 * NN;   // both groups' exchange buffers
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (threadIdx.x == 0) bulk_wait_read0();
+                __syncthreads();
+#pragma unroll
+                for (int m = 16 * h; m < 16 * h + 16; ++m) xs[(j + 32 * (m - 16 * h)) * 16 + c] = v[m];
+                fence_async();
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    for (int b = 0; b < 2; ++b)
+                        tma2d_store(&smap8, (int)(t * 16), 512 * h + 256 * b, xs + 256 * b * 16);
+                    bulk_commit();
+                }
+            }
+            continue;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1) {
+                if (tl == 0) bulk_wait_read0();
+                nbar(bar, GT);
+            }
+#pragma unroll
+            for (int m = 16 * h; m < 16 * h + 16; ++m) xb[(j + 32 * (m - 16 * h)) * GC + cl] = v[m];
+            fence_async();
+            nbar(bar, GT);
+            if (tl == 0) {
+                // rows j + 32 m for m in [16h, 16h+16) = rows [512 h, 512 h + 512)
+                for (int b = 0; b < 2; ++b)
+                    tma2d_store(&smap8, (int)(t * 16 + g * GC), 512 * h + 256 * b, xb + 256 * b * GC);
+                bulk_commit();
+            }
+        }
+    }
+    if (tl == 0) bulk_wait0();
+}
+
+template <int R, int SM_ = 1>
+float run_c(const CUtensorMap &m, const CUtensorMap &s8, int nsm) {
+    constexpr int XP = 16 * 8 + 8;
+    const int smem = 1024 + 16 * NN * 8 + 2 * 32 * XP * 8 + 64;
+    cudaFuncSetAttribute(k_c<R, SM_>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float best = 1e9f;
+    for (int r = 0; r < 4; ++r) {
+        cudaEventRecord(e0);
+        k_c<R, SM_><<<nsm, NT, smem>>>(m, s8, 1.0000001f);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (r > 0 && ms < best) best = ms;
+    }
+    return best;
+}
+
 typedef CUresult (*EncFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *, const cuuint64_t *,
                           const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
                           CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -192,11 +331,24 @@ int main() {
     const cuuint32_t b16[2] = {16, 256}, es[2] = {1, 1};
     enc(&m16, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a, dims, str, b16, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUtensorMap m16s, s8;
+    enc(&m16s, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a, dims, str, b16, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const cuuint32_t b8[2] = {8, 256};
+    enc(&s8, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a, dims, str, b8, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUtensorMap s16;
+    enc(&s16, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, a, dims, str, b16, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     for (int rep = 0; rep < 2; ++rep) {
-        printf("R=0: A %.3f ms  B %.3f ms\n", run<1, 0>(m16, a, nsm), run<2, 0>(m16, a, nsm));
-        printf("R=3: A %.3f ms  B %.3f ms\n", run<1, 3>(m16, a, nsm), run<2, 3>(m16, a, nsm));
-        printf("R=6: A %.3f ms  B %.3f ms\n", run<1, 6>(m16, a, nsm), run<2, 6>(m16, a, nsm));
-        printf("R=9: A %.3f ms  B %.3f ms\n", run<1, 9>(m16, a, nsm), run<2, 9>(m16, a, nsm));
+        printf("C no stores: R=0 %.3f  R=6 %.3f ms;  C coupled 128-B TMA stores: R=0 %.3f  R=6 %.3f ms\n",
+               run_c<0, 0>(m16s, s8, nsm), run_c<6, 0>(m16s, s8, nsm), run_c<0, 2>(m16s, s16, nsm), run_c<6, 2>(m16s, s16, nsm));
+    }
+    for (int rep = 0; rep < 2; ++rep) {
+        printf("R=0: A %.3f ms  B %.3f ms  C %.3f ms\n", run<1, 0>(m16, a, nsm), run<2, 0>(m16, a, nsm), run_c<0>(m16s, s8, nsm));
+        printf("R=3: A %.3f ms  B %.3f ms  C %.3f ms\n", run<1, 3>(m16, a, nsm), run<2, 3>(m16, a, nsm), run_c<3>(m16s, s8, nsm));
+        printf("R=6: A %.3f ms  B %.3f ms  C %.3f ms\n", run<1, 6>(m16, a, nsm), run<2, 6>(m16, a, nsm), run_c<6>(m16s, s8, nsm));
+        printf("R=9: A %.3f ms  B %.3f ms  C %.3f ms\n", run<1, 9>(m16, a, nsm), run<2, 9>(m16, a, nsm), run_c<9>(m16s, s8, nsm));
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
