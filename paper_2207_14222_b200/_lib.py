@@ -34,7 +34,7 @@ class PlanDesc(ctypes.Structure):
                 ("tensor_diffusion", ctypes.c_int), ("delta_form", ctypes.c_int), ("r_switch", ctypes.c_double),
                 ("dense_source", ctypes.c_int), ("separate_transposes", ctypes.c_int),
                 ("complex_path", ctypes.c_int), ("launch_per_pass", ctypes.c_int), ("plane_chain", ctypes.c_int),
-                ("test_hooks", ctypes.c_int)]
+                ("test_hooks", ctypes.c_int), ("zpair_work", ctypes.c_int)]
 
 
 HOOK_RANK_FINISH = 1
@@ -81,6 +81,7 @@ SIGNATURES = {
     "usp_launch_count": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)]),
     "usp_iteration_form": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
                                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]),
+    "usp_work_layout": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "usp_plan_destroy": (None, [ctypes.c_void_p]),
     "usp_comm_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
     "usp_comm_init": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int, ctypes.c_int,

@@ -42,11 +42,17 @@
 
 namespace usp {
 
-template <int N, int MODE>
+// ZP (K_C on the z-pair layout of work, usp_internal.h WLayout): the tile's
+// N z-rows of 16 columns are N/2 pair rows of 32 columns (16 x of planes 2zp
+// and 2zp + 1 side by side), loaded as {32, BP} boxes and stored as 256-byte
+// rows; the FFT, the multiplier and the exchange are unchanged.
+template <int N, int MODE, bool ZP = false>
 __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     k_stile(const __grid_constant__ CUtensorMap tmap, SParams p) {
     using G = LineGeo<N>;
     using T = STile<N>;
+    static_assert(!ZP || (MODE == S_FWD_MUL_INV && T::COLS == 16 && G::N1 % 2 == 0), "z-pair tiles: K_C, N <= 1024");
+    constexpr int BP = (N / 4 < 256) ? N / 4 : 256;   // pair rows per box
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x;
     const int g = tid / T::NTG, tl = tid % T::NTG;     // thread group, thread in group
@@ -71,7 +77,10 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         const long long ol = t / tpo, o = ol;
         const int c0 = (int)((t - ol * tpo) * T::COLS);
         mbar_arrive_expect_tx(full, T::TILE * 8);
-        if (p.map_rank == 5) {
+        if constexpr (ZP) {
+#pragma unroll
+            for (int bx = 0; bx < N / 2 / BP; ++bx) tma_load_2d(stage + bx * BP * 32, &tmap, (int)(t * 32), bx * BP, full);
+        } else if (p.map_rank == 5) {
             // K_D after the return transpose: the line's rows live in P blocks of
             // the send layout [r][q][z_loc][y_loc][x] (5-D map {x, y_loc, z_loc, q, r})
             const int r = (int)(o / p.nz_loc), zl = (int)(o - (long long)r * p.nz_loc);
@@ -105,7 +114,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
     constexpr int SROWS = T::HALFX ? N / 2 : N;
     constexpr int SM0 = T::HALFX ? G::N2 / 2 : 0;
     static_assert(!T::HALFX || T::XB >= (N / 2) * T::COLS, "stash needs half a tile");
-    const bool TST = T::COLS == 16 && SROWS >= T::BOXN && p.tma_store;
+    const bool TST = T::COLS == 16 && (ZP || SROWS >= T::BOXN) && p.tma_store;
 
     for (int i = 0; i < nloc; ++i) {
         if (!mbar_wait(full, i & 1)) {
@@ -115,7 +124,9 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
         float2 v[G::N2];
 #pragma unroll
         for (int m = 0; m < G::N2; ++m) {
-            const float2 a = stage[(j + G::N1 * m) * T::COLS + c];
+            // z-pair: plane z = j + N1 m sits in pair row z / 2, half z % 2
+            const int z = j + G::N1 * m;
+            const float2 a = ZP ? stage[(z >> 1) * 32 + (z & 1) * 16 + c] : stage[z * T::COLS + c];
             v[m] = (MODE == S_INV) ? cconj(a) : a;
         }
         if (flip) {
@@ -188,7 +199,30 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
 #pragma unroll
             for (int m = 1; m < G::N2; m += 2) v[m] = cscale(v[m], -1.f);
         }
-        if (MODE == S_FWD && p.peer_mode == 1) {
+        if constexpr (ZP) {
+            // z-pair layout: register slot m = pair row (j >> 1) + (N1 / 2) m, half j & 1;
+            // a warp (16 columns x 2 rows j) writes one 256-byte pair row per slot
+            float2 *zb = p.dst + t * 32 + (j & 1) * 16 + c + (long long)(j >> 1) * stride;
+            const long long zstep = (long long)(G::N1 / 2) * stride;
+            if (TST) {
+#pragma unroll
+                for (int m = 0; m < SM0; ++m) zb[m * zstep] = cconj(v[m]);
+#pragma unroll
+                for (int m = SM0; m < G::N2; ++m)
+                    xb[((j >> 1) + (G::N1 / 2) * m - (N - SROWS) / 2) * 32 + (j & 1) * 16 + c] = cconj(v[m]);
+                fence_proxy_async_smem();
+                gsync<N>(bar);
+                if (tl == 0) {
+#pragma unroll
+                    for (int bx = 0; bx < SROWS / 2 / BP; ++bx)
+                        tma_store_2d(&tmap, (int)(t * 32), (N - SROWS) / 2 + bx * BP, xb + bx * BP * 32);
+                    bulk_commit();
+                }
+            } else {
+#pragma unroll
+                for (int m = 0; m < G::N2; ++m) zb[m * zstep] = cconj(v[m]);
+            }
+        } else if (MODE == S_FWD && p.peer_mode == 1) {
             // K_B with the forward transpose fused in: row y of plane (r, z_loc)
             // is stored straight into block r of the receive buffer of rank
             // q = y / ny_loc ([z][y_loc][x] there) -- over NVLink for q != r
@@ -257,22 +291,26 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
 }
 
 // ========================================================= launchers ====
-template <int N, int MODE>
+template <int N, int MODE, bool ZP = false>
 static cudaError_t stile_t(const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
-            cudaFuncSetAttribute(k_stile<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, STile<N>::SMEM);
+            cudaFuncSetAttribute(k_stile<N, MODE, ZP>, cudaFuncAttributeMaxDynamicSharedMemorySize, STile<N>::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_pdl(k_stile<N, MODE>, grid, STile<N>::NT, STile<N>::SMEM, s, map, p);
+    return launch_pdl(k_stile<N, MODE, ZP>, grid, STile<N>::NT, STile<N>::SMEM, s, map, p);
 }
 
 template <int N>
 static cudaError_t stile_mode(SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
     if (mode == S_FWD) return stile_t<N, S_FWD>(map, p, grid, s);
     if (mode == S_INV) return stile_t<N, S_INV>(map, p, grid, s);
+    if (p.zpair) {
+        if constexpr (N <= 1024) return stile_t<N, S_FWD_MUL_INV, true>(map, p, grid, s);
+        else return cudaErrorInvalidValue;
+    }
     return stile_t<N, S_FWD_MUL_INV>(map, p, grid, s);
 }
 

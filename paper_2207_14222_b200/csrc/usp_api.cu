@@ -272,6 +272,10 @@ struct usp_plan_s {
     bool stile_y = false, stile_z = false;
     int grids_y = 0, grids_z = 0;
     CUtensorMap smap_y{}, smap_z{}, smap_kd{};
+    // z-pair layout of work (usp_internal.h WLayout; desc.zpair_work enables):
+    // one-GPU complex 3-D plans; wmap = the x passes' 5-D load map of work
+    bool wpair = false;
+    CUtensorMap wmap{};
     // profiling
     bool prof = false;
     std::vector<Timed> timed;
@@ -611,6 +615,8 @@ Red red_params(usp_plan_s *p) {
     return r;
 }
 
+WLayout work_layout(const usp_plan_s *p) { return WLayout{p->wpair ? 1 : 0, (int)p->nx, log2ll(p->ny)}; }
+
 XParams x_params(usp_plan_s *p) {
     XParams xp{};
     xp.work = p->work;
@@ -627,6 +633,7 @@ XParams x_params(usp_plan_s *p) {
     xp.red = red_params(p);
     xp.s = p->xform ? p->s : nullptr;
     xp.s_sparse = p->s_sparse ? 1 : 0;
+    xp.wl = work_layout(p);
     return xp;
 }
 
@@ -637,7 +644,7 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
         Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
         if (p->real) CU(launch_xpass_real((int)p->nx, mode, xp, p->gridp_x, p->stream));
         else
-            CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream,
+            CU(launch_xpass_pipe((int)p->nx, mode, xp, p->wmap, p->gridp_x, p->stream,
                                  mode == X_ITER && p->s_sparse && p->expect_x, p->xform && p->expect_x));
     }
     if (mode != X_SRC_FWD && rank_finish(p)) {
@@ -665,6 +672,7 @@ usp_status sparse_add(usp_plan_s *p) {
     sa.count = p->s_count;
     sa.n = (int)p->nx;
     sa.st = p->st;
+    sa.wl = work_layout(p);
     Tick t(p, KC_SADD);
     CU(launch_sparse_add(sa, p->stream));
     return USP_OK;
@@ -1068,6 +1076,14 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
     if (p->P == 1) {
         SParams yf = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, p->nz, p->rp * p->ny, 1, check_state, 3);
         SParams zm = sparams(p, p->work, p->work, p->tw[2], p->rp * p->ny, p->rp * p->ny, 1, 0, 2, check_state, 2);
+        if (p->wpair) {
+            // z-pair layout: the y passes see [nz/2][ny][2 nx] (columns = (x, z parity));
+            // K_C steps over pair rows of 2 nx ny elements
+            yf = sparams(p, p->work, p->work, p->tw[1], 2 * p->nx, 2 * p->nx, p->nz / 2, 2 * p->nx * p->ny, 1,
+                         check_state, 3);
+            zm.stride = 2 * p->nx * p->ny;
+            zm.zpair = 1;
+        }
         if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, p->stile_y, p->grid_y))) return s;
         if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, p->stile_z, p->grid_z))) return s;
         return run_strided(p, KC_YINV, (int)p->ny, S_INV, yf, p->smap_y, p->stile_y, p->grid_y);
@@ -1150,6 +1166,42 @@ void build_maps(usp_plan_s *p) {
     }
     if (!stile_supported(p->nz)) return;
     const cuuint32_t cz = (cuuint32_t)stile_cols((int)p->nz), bz = (cuuint32_t)stile_box((int)p->nz);
+    if (p->wpair) {
+        // z-pair layout (usp_internal.h WLayout): y passes on [nz/2][ny][2 nx],
+        // K_C on pair rows {2 nx ny, nz/2} with {32, BP} boxes, x passes through
+        // {16, 2, nx/16, ny, nz/2} with {16, 1, nx/16, U, 1} boxes (one unit of U lines)
+        const long long nx = p->nx, ny = p->ny, nz = p->nz;
+        bool ok = true;
+        {
+            const cuuint64_t dims[3] = {(cuuint64_t)(2 * nx), (cuuint64_t)ny, (cuuint64_t)(nz / 2)};
+            const cuuint64_t str[2] = {(cuuint64_t)(2 * nx) * 8, (cuuint64_t)(2 * nx * ny) * 8};
+            const cuuint32_t box[3] = {cy, by, 1};
+            ok = make_map(&p->smap_y, p->work, 3, dims, str, box);
+        }
+        {
+            const cuuint64_t dims[2] = {(cuuint64_t)(2 * nx * ny), (cuuint64_t)(nz / 2)};
+            const cuuint64_t str[1] = {(cuuint64_t)(2 * nx * ny) * 8};
+            const cuuint32_t box[2] = {32, (cuuint32_t)std::min<long long>(256, nz / 4)};
+            ok = ok && make_map(&p->smap_z, p->work, 2, dims, str, box);
+        }
+        {
+            const long long n1 = 1LL << (log2ll(nx) / 2), u = 32 / n1;   // LineGeo<nx>::N1, lines per unit
+            const cuuint64_t dims[5] = {16, 2, (cuuint64_t)(nx / 16), (cuuint64_t)ny, (cuuint64_t)(nz / 2)};
+            const cuuint64_t str[4] = {16 * 8, 32 * 8, (cuuint64_t)(2 * nx) * 8, (cuuint64_t)(2 * nx * ny) * 8};
+            const cuuint32_t box[5] = {16, 1, (cuuint32_t)(nx / 16), (cuuint32_t)u, 1};
+            ok = ok && make_map(&p->wmap, p->work, 5, dims, str, box);
+        }
+        p->stile_y = p->stile_z = ok;
+        if (!ok) p->wpair = false;   // (plain layout then, maps rebuilt below)
+        else return;
+        p->stile_y = stile_supported(p->ny);
+        if (p->stile_y) {
+            const cuuint64_t dims[3] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny, (cuuint64_t)(p->nzh * comps)};
+            const cuuint64_t str[2] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->rp * p->ny) * 8};
+            const cuuint32_t box[3] = {cy, by, 1};
+            p->stile_y = make_map(&p->smap_y, p->work, 3, dims, str, box);
+        }
+    }
     if (p->P == 1) {   // z pass: {x*y columns, z}
         const cuuint64_t dims[2] = {(cuuint64_t)(p->rp * p->ny), (cuuint64_t)(p->nz * comps)};
         const cuuint64_t str[1] = {(cuuint64_t)(p->rp * p->ny) * 8};
@@ -1201,7 +1253,7 @@ extern "C" {
 
 const char *usp_last_error(void) { return g_err.c_str(); }
 
-const char *usp_version(void) { return "0.3 sm_100a"; }
+const char *usp_version(void) { return "0.4 sm_100a"; }
 
 usp_status usp_comm_unique_id(unsigned char id[128]) {
     if (!id) return fail(USP_ERR_ARG, "NULL argument");
@@ -1372,6 +1424,10 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         TRY(cudaMemset(p->pl_done, 0, sizeof(unsigned) * 2 * p->nz));
         TRY(cudaMalloc(&p->pl_part, sizeof(double) * kPlaneN * p->nz));
     }
+    // z-pair layout of work where every pass that touches it supports it (one
+    // GPU, complex 3-D, x lines of 256..2048 points, TMA tiles on y and z)
+    p->wpair = desc->zpair_work && P == 1 && p->ndim == 3 && !p->real && !p->anti && !p->tdiff && !p->plane &&
+               p->nx >= 256 && stile_supported(p->ny) && stile_supported(p->nz) && p->nz <= 1024;
     p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && !desc->delta_form;
     if (desc->r_switch > 0.0) p->r_sw = desc->r_switch;
     p->force_finish = (desc->test_hooks & USP_HOOK_RANK_FINISH) != 0;
@@ -1765,7 +1821,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
             // the list (2 KiB) and the lines must fit in the s field
             const long long cap = std::min<long long>(kSparseMaxLines, ((long long)p->nloc - 256) / p->nx);
             if (cnt > 0 && (long long)cnt <= cap) {
-                CU(launch_sparse_gather(p->s_flag, nlines, p->work, (int)p->nx, reinterpret_cast<int *>(p->s),
+                CU(launch_sparse_gather(p->s_flag, nlines, p->work, work_layout(p), reinterpret_cast<int *>(p->s),
                                         p->s + 256, p->s_ctr, p->stream));
                 p->s_sparse = true;
                 p->s_count = (int)cnt;
@@ -2124,10 +2180,11 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
     kp.partials = p->partials;
     kp.hist = p->hist;
     kp.hist_cap = p->hist_cap;
+    kp.wl = work_layout(p);
     const int gx = p->gridp_x, gu = occ_grid(p, (p->nloc + 255) / 256, 8);
     auto xop = [&](KMode m) -> usp_status {
         Tick t(p, KC_XOP);
-        CU(launch_xop((int)p->nx, m, kp, gx, p->stream));
+        CU(launch_xop((int)p->nx, m, kp, p->wmap, gx, p->stream));
         return USP_OK;
     };
     const long long batch = 8;
@@ -2280,14 +2337,15 @@ usp_status apply_M_dev(usp_plan_s *p, float2 *u, float2 *z) {
     kp.tw = p->tw[0];
     kp.nlines = p->ny * p->nzh;
     kp.st = p->st;
+    kp.wl = work_layout(p);
     usp_status s;
     {
         Tick t(p, KC_XOP);
-        CU(launch_xop((int)p->nx, K_OFWD, kp, p->gridp_x, p->stream));
+        CU(launch_xop((int)p->nx, K_OFWD, kp, p->wmap, p->gridp_x, p->stream));
     }
     if ((s = chain_mid(p, 0))) return s;
     Tick t(p, KC_XOP);
-    CU(launch_xop((int)p->nx, K_OINV, kp, p->gridp_x, p->stream));
+    CU(launch_xop((int)p->nx, K_OINV, kp, p->wmap, p->gridp_x, p->stream));
     return USP_OK;
 }
 }  // namespace
@@ -2458,6 +2516,12 @@ usp_status usp_iteration_form(usp_plan_t p, int *xform, int *form, double *r_swi
     if (xform) *xform = p->xform_cap ? 1 : 0;
     if (form) *form = (p->st_host->form == FORM_DELTA) ? 0 : 1;
     if (r_switch) *r_switch = p->r_sw;
+    return USP_OK;
+}
+
+usp_status usp_work_layout(usp_plan_t p, int *zpair) {
+    if (!p || !zpair) return fail(USP_ERR_ARG, "NULL argument");
+    *zpair = p->wpair ? 1 : 0;
     return USP_OK;
 }
 

@@ -86,8 +86,9 @@ class Plan:
     ``complex_path`` (float32 diffusion data on the complex path),
     ``launch_per_pass`` (2-D: one launch per pass instead of the persistent
     solver), ``plane_chain`` (the plane-chained pass on 1024^2-plane
-    grids instead of one sweep per FFT pass), ``test_hooks`` (USP_HOOK_*
-    bits; tests only).
+    grids instead of one sweep per FFT pass), ``zpair_work`` (the z-pair layout
+    of the FFT chain buffer instead of plain [z][y][x], where it applies),
+    ``test_hooks`` (USP_HOOK_* bits; tests only).
     """
 
     def __init__(self, shape: Sequence[int], kind: str = "helmholtz", h: Optional[Sequence[float]] = None,
@@ -95,7 +96,8 @@ class Plan:
                  stream=None, device=None, comm=None, virtual_ranks: int = 0, antisymmetric: bool = False,
                  tensor_diffusion: bool = False, delta_form: bool = False, r_switch: float = 0.0,
                  dense_source: bool = False, separate_transposes: bool = False, complex_path: bool = False,
-                 launch_per_pass: bool = False, plane_chain: bool = False, test_hooks: int = 0):
+                 launch_per_pass: bool = False, plane_chain: bool = False, test_hooks: int = 0,
+                 zpair_work: bool = False):
         import torch
 
         self.lib = L.load()
@@ -131,6 +133,7 @@ class Plan:
         d.launch_per_pass = int(bool(launch_per_pass))
         d.plane_chain = int(bool(plane_chain))
         d.test_hooks = int(test_hooks)
+        d.zpair_work = int(bool(zpair_work))
         if tensor_diffusion:
             d.dtype = L.R32
             self.dtype = "r32"
@@ -347,6 +350,12 @@ class Plan:
         L.check(self.lib.usp_iteration_form(self.handle, ctypes.byref(xf), ctypes.byref(fm), ctypes.byref(rs),
                                             ctypes.byref(sl)))
         return bool(xf.value), bool(fm.value), float(rs.value)
+
+    def work_layout(self) -> str:
+        """"z-pair" or "flat": the layout of the plan's FFT chain buffer (usp_work_layout)."""
+        zp = ctypes.c_int()
+        L.check(self.lib.usp_work_layout(self.handle, ctypes.byref(zp)))
+        return "z-pair" if zp.value else "flat"
 
     def source_lines(self) -> int:
         """Number of x-lines carrying the source when the x-form skips the

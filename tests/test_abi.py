@@ -37,7 +37,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 
 def test_version_and_error_strings(lib):
-    assert lib.usp_version().startswith(b"0.3")
+    assert lib.usp_version().startswith(b"0.4")
     assert isinstance(lib.usp_last_error(), bytes)
 
 
