@@ -672,6 +672,7 @@ def run_usp(args, world, rank, local):
                                f"{n_iter} iterations of Alg. 1 per step (setup + iterations), alpha=0.75",
                    "grid": list(shape), "iterations_per_step": n_iter, "iteration_form": form_desc,
                    "parallelism": parallelism, "slab_check_rel_l2": slab_check,
+                   "z_pass_buffer": plan.work_layout(),
                    "l2": "inputs (8 GiB fields) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,

@@ -155,16 +155,15 @@ typedef struct {
                              the residual through the rank-ordered all-gather + k_finish
                              path of P > 1 plans (a test of that path on one GPU).  0 in
                              production.                                                  */
-    int zpair_work;       /* != 0: on one GPU (complex64, 3-D, nx in [256, 2048], ny and nz
-                             in [64, 1024]) keep the FFT chain buffer in the z-pair layout:
-                             planes 2zp and 2zp+1 interleaved in 128-byte x blocks, so the
-                             z pass (K_C) moves 256-byte rows (K_C 4.86
-                             -> 4.61 ms at 1024^3, but the x pass then moves 128-byte
-                             halves, 6.16 -> 6.32 ms; net -0.4 % per x-form iteration,
-                             +0.6 % per Delta-form iteration).  0: plain [z][y][x].
-                             Internal to the plan: the arrays the caller passes and
-                             receives are [z][y][x] either way, and the fields are
-                             bit-identical.                                               */
+    int flat_work;        /* != 0: the z pass works in place on the chain buffer ([z][y][x],
+                             16-column tiles of 128-byte rows).  0: on one GPU (complex64,
+                             3-D, nx in [256, 2048], ny and nz in [64, 1024]) the y-forward
+                             pass writes a second chain buffer in the z-pair layout --
+                             planes 2zp and 2zp+1 interleaved in 128-byte x blocks -- so
+                             the z pass (K_C) moves 256-byte rows, and the y-inverse pass
+                             reads it back (K_C 4.81 -> 4.58 ms at
+                             1024^3, iteration -0.9 %; one more field of workspace).
+                             Internal to the plan: fields are bit-identical either way.  */
 } usp_plan_desc;
 
 #define USP_HOOK_RANK_FINISH 1
@@ -372,8 +371,8 @@ usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
  * the ranks of a slab-decomposed plan.  Errors: USP_ERR_ARG. */
 usp_status usp_iteration_form(usp_plan_t plan, int *xform, int *form, double *r_switch, int *source_lines);
 
-/* *zpair = 1 if the plan keeps its FFT chain buffer in the z-pair layout
- * (desc.zpair_work and the plan qualifies), else 0.  Diagnostic; no device work.  Errors: USP_ERR_ARG. */
+/* *zpair = 1 if the plan's z pass runs on the z-pair chain buffer
+ * (desc.flat_work), else 0.  Diagnostic; no device work.  Errors: USP_ERR_ARG. */
 usp_status usp_work_layout(usp_plan_t plan, int *zpair);
 
 /* NCCL communicator for the slab decomposition (one process per GPU).

@@ -34,7 +34,7 @@ class PlanDesc(ctypes.Structure):
                 ("tensor_diffusion", ctypes.c_int), ("delta_form", ctypes.c_int), ("r_switch", ctypes.c_double),
                 ("dense_source", ctypes.c_int), ("separate_transposes", ctypes.c_int),
                 ("complex_path", ctypes.c_int), ("launch_per_pass", ctypes.c_int), ("plane_chain", ctypes.c_int),
-                ("test_hooks", ctypes.c_int), ("zpair_work", ctypes.c_int)]
+                ("test_hooks", ctypes.c_int), ("flat_work", ctypes.c_int)]
 
 
 HOOK_RANK_FINISH = 1

@@ -101,7 +101,7 @@ struct XOp {
 //   K_SFWD: r, v, B        K_TINV: work, s, B
 //   K_OFWD: p, B           K_OINV: work, p, B      (plain M p -> v, for GMRES)
 template <int N, int MODE>
-__global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p, const __grid_constant__ CUtensorMap wmap) {
+__global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p) {
     using G = LineGeo<N>;
     using T = XOp<N>;
     constexpr int NSLOT = (MODE == K_OFWD) ? 2 : ((MODE == K_SFWD || MODE == K_TINV || MODE == K_OINV) ? 3 : 4);
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p, const __grid_c
     load_twiddles<N>(sm_tw, p.tw);
     __syncthreads();
     const long long nunits = p.nlines / T::U;
-    const int nloc = xunits_local(p.wl, nunits, blockIdx.x, gridDim.x);
+    const int nloc = (int)((nunits - blockIdx.x + gridDim.x - 1) / gridDim.x);
     const uint32_t ub = T::UE * 8u;
     const float2 *src[4];
     if (MODE == K_PFWD) { src[0] = p.r; src[1] = p.p; src[2] = p.v; src[3] = p.B; }
@@ -154,20 +154,11 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p, const __grid_c
                     if (atomicCAS(&p.st->err, 0, 8) == 0) p.st->err_info = i;
                     break;
                 }
-                const long long l0 = xunit_line0(p.wl, T::U, i, blockIdx.x, gridDim.x);
-                const long long off = l0 * N;
+                const long long off = (blockIdx.x + (long long)i * gridDim.x) * T::UE;
                 float2 *st = stages + s * T::STAGE;
                 mbar_arrive_expect_tx(&full[s], NSLOT * ub);
 #pragma unroll
-                for (int q = 0; q < NSLOT; ++q) {
-                    if (INV && q == 0 && p.wl.pair) {   // work on the z-pair layout: 5-D box
-                        const long long z = l0 >> p.wl.nylg;
-                        tma_load_5d(st, &wmap, 0, (int)(z & 1), 0, (int)(l0 & ((1LL << p.wl.nylg) - 1)),
-                                    (int)(z >> 1), &full[s]);
-                    } else {
-                        bulk_g2s(st + q * T::UE, src[q] + off, ub, &full[s]);
-                    }
-                }
+                for (int q = 0; q < NSLOT; ++q) bulk_g2s(st + q * T::UE, src[q] + off, ub, &full[s]);
             }
         }
         __syncwarp();
@@ -181,8 +172,7 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p, const __grid_c
                 break;
             }
             const float2 *st = stages + s * T::STAGE;
-            const long long l0 = xunit_line0(p.wl, T::U, i, blockIdx.x, gridDim.x);
-            const long long gb = l0 * N + lq * N + j;
+            const long long gb = (blockIdx.x + (long long)i * gridDim.x) * T::UE + lq * N + j;
             const int sb = lq * N + j;
             float2 v[G::N2];
             float la[4] = {0.f, 0.f, 0.f, 0.f};
@@ -210,13 +200,8 @@ __global__ void __launch_bounds__(XOp<N>::NT, 1) k_xop(KParams p, const __grid_c
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[s]);
                 fft_line<N, false, LayRow<N>, true>(v, lay, j, sm_tw);
-                long long wb = gb, ws = G::N1;   // work stores (z-pair layout: see k_xpass_pipe)
-                if (p.wl.pair) {
-                    wb = wpair_line(p.wl, l0 + lq) + (j >> 4) * 32 + (j & 15);
-                    ws = 2 * G::N1;
-                }
 #pragma unroll
-                for (int m = 0; m < G::N2; ++m) p.work[wb + ws * m] = v[m];
+                for (int m = 0; m < G::N2; ++m) p.work[gb + G::N1 * m] = v[m];
             } else {
                 // x inverse (conj trick) -> y = (L+1)^-1 B u; out = B (u - y) + inner products
 #pragma unroll
@@ -444,26 +429,26 @@ __global__ void __launch_bounds__(256, kGsCtasPerSm) k_gs(GSParams p) {
 
 // ========================================================= launchers ====
 template <int N, int MODE>
-static cudaError_t xop_t(const KParams &p, const CUtensorMap &wmap, int grid, cudaStream_t s) {
+static cudaError_t xop_t(const KParams &p, int grid, cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_xop<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, XOp<N>::SMEM);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_xop<N, MODE><<<grid, XOp<N>::NT, XOp<N>::SMEM, s>>>(p, wmap);
+    k_xop<N, MODE><<<grid, XOp<N>::NT, XOp<N>::SMEM, s>>>(p);
     return cudaGetLastError();
 }
 
-cudaError_t launch_xop(int N, KMode mode, const KParams &p, const CUtensorMap &wmap, int grid, cudaStream_t s) {
-#define XO_CASE(n)                                                         \
-    case n:                                                                \
-        if (mode == K_PFWD) return xop_t<n, K_PFWD>(p, wmap, grid, s);     \
-        if (mode == K_VINV) return xop_t<n, K_VINV>(p, wmap, grid, s);     \
-        if (mode == K_SFWD) return xop_t<n, K_SFWD>(p, wmap, grid, s);     \
-        if (mode == K_OFWD) return xop_t<n, K_OFWD>(p, wmap, grid, s);     \
-        if (mode == K_OINV) return xop_t<n, K_OINV>(p, wmap, grid, s);     \
-        return xop_t<n, K_TINV>(p, wmap, grid, s);
+cudaError_t launch_xop(int N, KMode mode, const KParams &p, int grid, cudaStream_t s) {
+#define XO_CASE(n)                                                   \
+    case n:                                                          \
+        if (mode == K_PFWD) return xop_t<n, K_PFWD>(p, grid, s);     \
+        if (mode == K_VINV) return xop_t<n, K_VINV>(p, grid, s);     \
+        if (mode == K_SFWD) return xop_t<n, K_SFWD>(p, grid, s);     \
+        if (mode == K_OFWD) return xop_t<n, K_OFWD>(p, grid, s);     \
+        if (mode == K_OINV) return xop_t<n, K_OINV>(p, grid, s);     \
+        return xop_t<n, K_TINV>(p, grid, s);
     switch (N) { XO_CASE(16) XO_CASE(32) XO_CASE(64) XO_CASE(128) XO_CASE(256) XO_CASE(512) XO_CASE(1024)
                  XO_CASE(2048) default: return cudaErrorInvalidValue; }
 #undef XO_CASE

@@ -61,8 +61,7 @@ struct XPipe {
 // 10.3 ms next to a Delta-form body, the Delta-form 13.4 vs 9.7 ms the other
 // way round -- so each expected form gets its own instantiation.
 template <int N, int MODE, bool LEAN, bool DSPEC, bool XSPEC = false>
-__global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1)
-    k_xpass_pipe(XParams p, const __grid_constant__ CUtensorMap wmap) {
+__global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1) k_xpass_pipe(XParams p) {
     using G = LineGeo<N>;
     using T = XPipe<N, LEAN>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -123,7 +122,7 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1)
         load_twiddles<N>(sm_tw, p.tw);
         __syncthreads();
         const long long nunits = p.nlines / T::U;
-        const int nloc = xunits_local(p.wl, nunits, blockIdx.x, gridDim.x);
+        const int nloc = (int)((nunits - blockIdx.x + gridDim.x - 1) / gridDim.x);
         const uint32_t ub = T::UE * 8u;                       // bytes per complex slot
         if (warp == T::XC) {
             // ------------------------------------------------ producer warp
@@ -134,20 +133,8 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1)
                         if (atomicCAS(&p.st->err, 0, 1) == 0) p.st->err_info = i;
                         break;
                     }
-                    const long long l0 = xunit_line0(p.wl, T::U, i, blockIdx.x, gridDim.x);
-                    const long long off = l0 * N;
+                    const long long off = (blockIdx.x + (long long)i * gridDim.x) * T::UE;
                     float2 *st = stages + s * T::STAGE;
-                    // the unit's work lines: one bulk copy (plain layout) or one
-                    // 5-D tensor-map box {16, 1, nx/16, U, 1} (z-pair layout)
-                    auto work_g2s = [&]() {
-                        if (p.wl.pair) {
-                            const long long z = l0 >> p.wl.nylg;
-                            tma_load_5d(st, &wmap, 0, (int)(z & 1), 0, (int)(l0 & ((1LL << p.wl.nylg) - 1)),
-                                        (int)(z >> 1), &full[s]);
-                        } else {
-                            bulk_g2s(st, p.work + off, ub, &full[s]);
-                        }
-                    };
                     if (MODE == X_SRC_FWD) {
                         const uint32_t sb = p.src_real ? ub / 2 : ub;
                         mbar_arrive_expect_tx(&full[s], sb);
@@ -155,12 +142,12 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1)
                         bulk_g2s(st, src, sb, &full[s]);
                     } else if (MODE == X_SRC_EPI) {
                         mbar_arrive_expect_tx(&full[s], (p.s ? 3 : 2) * ub);
-                        work_g2s();
+                        bulk_g2s(st, p.work + off, ub, &full[s]);
                         if (p.s) bulk_g2s(st + T::SD, slot1 + off, ub, &full[s]);
                         bulk_g2s(st + T::SB, p.B + off, ub, &full[s]);
                     } else {
                         mbar_arrive_expect_tx(&full[s], (stage1 ? 4 : 3) * ub);
-                        work_g2s();
+                        bulk_g2s(st, p.work + off, ub, &full[s]);
                         if (stage1) bulk_g2s(st + T::SD, slot1 + off, ub, &full[s]);
                         bulk_g2s(st + T::SX, p.x + off, ub, &full[s]);
                         bulk_g2s(st + T::SB, p.B + off, ub, &full[s]);
@@ -179,8 +166,7 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1)
                     break;
                 }
                 const float2 *st = stages + s * T::STAGE;
-                const long long l0 = xunit_line0(p.wl, T::U, i, blockIdx.x, gridDim.x);
-                const long long gb = l0 * N + lq * N + j;
+                const long long gb = (blockIdx.x + (long long)i * gridDim.x) * T::UE + lq * N + j;
                 const int sbase = lq * N + j;
                 float2 v[G::N2];
                 if (MODE == X_SRC_FWD) {
@@ -198,7 +184,7 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1)
                         for (int m = 0; m < G::N2; ++m) nz |= (v[m].x != 0.f) || (v[m].y != 0.f);
                         const unsigned bal = __ballot_sync(0xffffffffu, nz);
                         const unsigned lmask = (G::N1 >= 32) ? 0xffffffffu : (((1u << G::N1) - 1u) << (lq * G::N1));
-                        if (j == 0) p.s_flag[l0 + lq] = (bal & lmask) != 0u;
+                        if (j == 0) p.s_flag[(blockIdx.x + (long long)i * gridDim.x) * T::U + lq] = (bal & lmask) != 0u;
                     }
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -301,15 +287,8 @@ __global__ void __launch_bounds__(XPipe<N, LEAN>::NT, 1)
                         if (lane == 0) mbar_arrive(&empty[s]);
                     }
                 }
-                // work stores: x = j + N1 m of the line; z-pair layout: 16-element blocks
-                // 32 apart, so N1 = 16 / 32 lanes keep writing 128-byte runs
-                long long wb = gb, ws = G::N1;
-                if (p.wl.pair) {
-                    wb = wpair_line(p.wl, l0 + lq) + (j >> 4) * 32 + (j & 15);
-                    ws = 2 * G::N1;
-                }
 #pragma unroll
-                for (int m = 0; m < G::N2; ++m) p.work[wb + ws * m] = v[m];
+                for (int m = 0; m < G::N2; ++m) p.work[gb + G::N1 * m] = v[m];
             }
         }
     }
@@ -340,9 +319,8 @@ __global__ void k_sparse_count(const unsigned char *flag, long long nlines, unsi
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
-__global__ void k_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, WLayout wl,
-                                int *list, float2 *comp, unsigned *count) {
-    const int n = wl.nx;
+__global__ void k_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, int n, int *list,
+                                float2 *comp, unsigned *count) {
     for (long long l = blockIdx.x; l < nlines; l += gridDim.x) {
         if (!flag[l]) continue;   // uniform per CTA
         __shared__ unsigned idx;
@@ -351,7 +329,7 @@ __global__ void k_sparse_gather(const unsigned char *flag, long long nlines, con
             list[idx] = (int)l;
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) comp[(long long)idx * n + i] = work[work_off(wl, l, i)];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) comp[(long long)idx * n + i] = work[l * n + i];
         __syncthreads();
     }
 }
@@ -360,12 +338,11 @@ __global__ void k_sparse_add(SAddParams p) {
     pdl_wait();
     if (!p.st->add_s) return;
     for (int q = blockIdx.x; q < p.count; q += gridDim.x) {
-        const long long l = p.list[q];
+        float2 *w = p.work + (long long)p.list[q] * p.n;
         const float2 *c = p.comp + (long long)q * p.n;
         for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
-            float2 *w = p.work + work_off(p.wl, l, i);
-            const float2 a = *w, b = c[i];
-            *w = make_float2(a.x + b.x, a.y + b.y);
+            const float2 a = w[i], b = c[i];
+            w[i] = make_float2(a.x + b.x, a.y + b.y);
         }
     }
 }
@@ -379,11 +356,11 @@ cudaError_t launch_sparse_count(const unsigned char *flag, long long nlines, uns
     return cudaGetLastError();
 }
 
-cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, const WLayout &wl,
-                                 int *list, float2 *comp, unsigned *count, cudaStream_t s) {
+cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, int n, int *list,
+                                 float2 *comp, unsigned *count, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
-    k_sparse_gather<<<592, 256, 0, s>>>(flag, nlines, work, wl, list, comp, count);
+    k_sparse_gather<<<592, 256, 0, s>>>(flag, nlines, work, n, list, comp, count);
     return cudaGetLastError();
 }
 
@@ -401,7 +378,7 @@ cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s) {
 #define USP_PIPE_X_N(X) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
 
 template <int N, int MODE, bool LEAN, bool DSPEC, bool XSPEC = false>
-static cudaError_t xpipe_t(const XParams &p, const CUtensorMap &wmap, int grid, cudaStream_t s) {
+static cudaError_t xpipe_t(const XParams &p, int grid, cudaStream_t s) {
     using T = XPipe<N, LEAN>;
     static bool attr = false;
     if (!attr) {
@@ -410,22 +387,22 @@ static cudaError_t xpipe_t(const XParams &p, const CUtensorMap &wmap, int grid, 
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_pdl(k_xpass_pipe<N, MODE, LEAN, DSPEC, XSPEC>, grid, T::NT, T::SMEM, s, p, wmap);
+    return launch_pdl(k_xpass_pipe<N, MODE, LEAN, DSPEC, XSPEC>, grid, T::NT, T::SMEM, s, p);
 }
 
 
 // X_ITER variants by the form the host expects: lean (sparse-source x-form:
 // 3-slot stages, one more consumer warp; N <= 1024), x-form (general body),
 // Delta-form (dedicated body)
-cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, const CUtensorMap &wmap, int grid, cudaStream_t s,
-                              bool lean, bool expect_x) {
-#define XP_CASE(n)                                                                          \
-    case n:                                                                                 \
-        if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD, false, false>(p, wmap, grid, s); \
-        if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI, false, false>(p, wmap, grid, s); \
-        if (lean && n <= 1024) return xpipe_t<n, X_ITER, true, false>(p, wmap, grid, s);    \
-        if (expect_x) return xpipe_t<n, X_ITER, false, false, true>(p, wmap, grid, s);      \
-        return xpipe_t<n, X_ITER, false, true>(p, wmap, grid, s);
+cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean,
+                              bool expect_x) {
+#define XP_CASE(n)                                                                    \
+    case n:                                                                           \
+        if (mode == X_SRC_FWD) return xpipe_t<n, X_SRC_FWD, false, false>(p, grid, s); \
+        if (mode == X_SRC_EPI) return xpipe_t<n, X_SRC_EPI, false, false>(p, grid, s); \
+        if (lean && n <= 1024) return xpipe_t<n, X_ITER, true, false>(p, grid, s);    \
+        if (expect_x) return xpipe_t<n, X_ITER, false, false, true>(p, grid, s);  \
+        return xpipe_t<n, X_ITER, false, true>(p, grid, s);
     switch (N) { USP_PIPE_X_N(XP_CASE) default: return cudaErrorInvalidValue; }
 #undef XP_CASE
 }

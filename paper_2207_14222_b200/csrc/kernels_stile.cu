@@ -89,10 +89,14 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
             for (int y0 = 0; y0 < N; y0 += (1 << lg))
                 tma_load_5d(stage + y0 * T::COLS, &tmap, c0, y0 & nyl_mask, zl, y0 >> p.nyl_lg, r, full);
         } else {
+            // K_D on the z-pair buffer: plane o = half o & 1 of pair plane o >> 1 of the
+            // [nz/2][ny][2 nx] view, its 16-column block at 32 (c0 / 16) + 16 (o & 1)
+            const int cx = p.pair_src ? (c0 >> 4) * 32 + (int)(o & 1) * 16 : c0 + p.col0;
+            const int ox = p.pair_src ? (int)(o >> 1) : (int)o;
 #pragma unroll
             for (int bx = 0; bx < N / T::BOXN; ++bx) {
                 if (p.map_rank == 3)
-                    tma_load_3d(stage + bx * T::BOXN * T::COLS, &tmap, c0 + p.col0, bx * T::BOXN, (int)o, full);
+                    tma_load_3d(stage + bx * T::BOXN * T::COLS, &tmap, cx, bx * T::BOXN, ox, full);
                 else tma_load_2d(stage + bx * T::BOXN * T::COLS, &tmap, c0 + p.col0, (int)o * N + bx * T::BOXN, full);
             }
         }
@@ -279,7 +283,10 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 bulk_commit();
             }
         } else {
-            store_slots<N, MODE, 0, G::N2>(v, p.dst + (o * p.ostride + col), stride, j, c);
+            // K_B into the z-pair buffer: plane o -> pair plane o >> 1, half o & 1
+            const long long ob = p.pair_dst ? (o >> 1) * p.ostride + (o & 1) * 16 + ((col >> 4) << 5) + (col & 15)
+                                            : o * p.ostride + col;
+            store_slots<N, MODE, 0, G::N2>(v, p.dst + ob, stride, j, c);
         }
     }
     if (TST && tl == 0) bulk_wait0();   // the exchange buffer outlives the last bulk store

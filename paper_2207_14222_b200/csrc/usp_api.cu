@@ -272,10 +272,12 @@ struct usp_plan_s {
     bool stile_y = false, stile_z = false;
     int grids_y = 0, grids_z = 0;
     CUtensorMap smap_y{}, smap_z{}, smap_kd{};
-    // z-pair layout of work (usp_internal.h WLayout; desc.zpair_work enables):
-    // one-GPU complex 3-D plans; wmap = the x passes' 5-D load map of work
+    // z-pair chain buffer of the z pass (usp_internal.h; desc.flat_work
+    // disables): work2 (one more field of workspace), smap_z on it, smap_yp =
+    // K_D's map of its [nz/2][ny][2 nx] view
     bool wpair = false;
-    CUtensorMap wmap{};
+    float2 *work2 = nullptr;
+    CUtensorMap smap_yp{};
     // profiling
     bool prof = false;
     std::vector<Timed> timed;
@@ -615,8 +617,6 @@ Red red_params(usp_plan_s *p) {
     return r;
 }
 
-WLayout work_layout(const usp_plan_s *p) { return WLayout{p->wpair ? 1 : 0, (int)p->nx, log2ll(p->ny)}; }
-
 XParams x_params(usp_plan_s *p) {
     XParams xp{};
     xp.work = p->work;
@@ -633,7 +633,6 @@ XParams x_params(usp_plan_s *p) {
     xp.red = red_params(p);
     xp.s = p->xform ? p->s : nullptr;
     xp.s_sparse = p->s_sparse ? 1 : 0;
-    xp.wl = work_layout(p);
     return xp;
 }
 
@@ -644,7 +643,7 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
         Tick t(p, mode == X_ITER ? KC_XPASS : KC_XSETUP);
         if (p->real) CU(launch_xpass_real((int)p->nx, mode, xp, p->gridp_x, p->stream));
         else
-            CU(launch_xpass_pipe((int)p->nx, mode, xp, p->wmap, p->gridp_x, p->stream,
+            CU(launch_xpass_pipe((int)p->nx, mode, xp, p->gridp_x, p->stream,
                                  mode == X_ITER && p->s_sparse && p->expect_x, p->xform && p->expect_x));
     }
     if (mode != X_SRC_FWD && rank_finish(p)) {
@@ -672,7 +671,6 @@ usp_status sparse_add(usp_plan_s *p) {
     sa.count = p->s_count;
     sa.n = (int)p->nx;
     sa.st = p->st;
-    sa.wl = work_layout(p);
     Tick t(p, KC_SADD);
     CU(launch_sparse_add(sa, p->stream));
     return USP_OK;
@@ -1077,12 +1075,19 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
         SParams yf = sparams(p, p->work, p->work, p->tw[1], p->rp, p->rp, p->nz, p->rp * p->ny, 1, check_state, 3);
         SParams zm = sparams(p, p->work, p->work, p->tw[2], p->rp * p->ny, p->rp * p->ny, 1, 0, 2, check_state, 2);
         if (p->wpair) {
-            // z-pair layout: the y passes see [nz/2][ny][2 nx] (columns = (x, z parity));
-            // K_C steps over pair rows of 2 nx ny elements
-            yf = sparams(p, p->work, p->work, p->tw[1], 2 * p->nx, 2 * p->nx, p->nz / 2, 2 * p->nx * p->ny, 1,
-                         check_state, 3);
-            zm.stride = 2 * p->nx * p->ny;
-            zm.zpair = 1;
+            // z-pair buffer (usp_internal.h): K_B stores work -> work2 (planes 2zp, 2zp+1
+            // interleaved), K_C runs on work2's 256-byte pair rows, K_D reads work2
+            // through the [nz/2][ny][2 nx] view and stores work back in [z][y][x]
+            const long long nx = p->nx, ny = p->ny;
+            SParams yb = sparams(p, p->work, p->work2, p->tw[1], 2 * nx, nx, p->nz, 2 * nx * ny, 1, check_state, 3);
+            yb.pair_dst = 1;
+            SParams zp = sparams(p, p->work2, p->work2, p->tw[2], 2 * nx * ny, nx * ny, 1, 0, 2, check_state, 2);
+            zp.zpair = 1;
+            SParams yd = sparams(p, p->work2, p->work, p->tw[1], nx, nx, p->nz, nx * ny, 1, check_state, 3);
+            yd.pair_src = 1;
+            if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0))) return s;
+            if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zp, p->smap_z, true, 0))) return s;
+            return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_yp, true, 0);
         }
         if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, p->stile_y, p->grid_y))) return s;
         if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, p->stile_z, p->grid_z))) return s;
@@ -1167,40 +1172,22 @@ void build_maps(usp_plan_s *p) {
     if (!stile_supported(p->nz)) return;
     const cuuint32_t cz = (cuuint32_t)stile_cols((int)p->nz), bz = (cuuint32_t)stile_box((int)p->nz);
     if (p->wpair) {
-        // z-pair layout (usp_internal.h WLayout): y passes on [nz/2][ny][2 nx],
-        // K_C on pair rows {2 nx ny, nz/2} with {32, BP} boxes, x passes through
-        // {16, 2, nx/16, ny, nz/2} with {16, 1, nx/16, U, 1} boxes (one unit of U lines)
+        // z-pair buffer (usp_internal.h): K_C on pair rows {2 nx ny, nz/2} with {32, BP}
+        // boxes, K_D on the [nz/2][ny][2 nx] view with {16, by, 1} boxes (K_B loads work
+        // through the plain y map above)
         const long long nx = p->nx, ny = p->ny, nz = p->nz;
-        bool ok = true;
-        {
-            const cuuint64_t dims[3] = {(cuuint64_t)(2 * nx), (cuuint64_t)ny, (cuuint64_t)(nz / 2)};
-            const cuuint64_t str[2] = {(cuuint64_t)(2 * nx) * 8, (cuuint64_t)(2 * nx * ny) * 8};
-            const cuuint32_t box[3] = {cy, by, 1};
-            ok = make_map(&p->smap_y, p->work, 3, dims, str, box);
+        const cuuint64_t dz[2] = {(cuuint64_t)(2 * nx * ny), (cuuint64_t)(nz / 2)};
+        const cuuint64_t sz[1] = {(cuuint64_t)(2 * nx * ny) * 8};
+        const cuuint32_t bxz[2] = {32, (cuuint32_t)std::min<long long>(256, nz / 4)};
+        const cuuint64_t dy[3] = {(cuuint64_t)(2 * nx), (cuuint64_t)ny, (cuuint64_t)(nz / 2)};
+        const cuuint64_t sy[2] = {(cuuint64_t)(2 * nx) * 8, (cuuint64_t)(2 * nx * ny) * 8};
+        const cuuint32_t bxy[3] = {cy, by, 1};
+        if (p->stile_y && make_map(&p->smap_z, p->work2, 2, dz, sz, bxz) &&
+            make_map(&p->smap_yp, p->work2, 3, dy, sy, bxy)) {
+            p->stile_z = true;
+            return;
         }
-        {
-            const cuuint64_t dims[2] = {(cuuint64_t)(2 * nx * ny), (cuuint64_t)(nz / 2)};
-            const cuuint64_t str[1] = {(cuuint64_t)(2 * nx * ny) * 8};
-            const cuuint32_t box[2] = {32, (cuuint32_t)std::min<long long>(256, nz / 4)};
-            ok = ok && make_map(&p->smap_z, p->work, 2, dims, str, box);
-        }
-        {
-            const long long n1 = 1LL << (log2ll(nx) / 2), u = 32 / n1;   // LineGeo<nx>::N1, lines per unit
-            const cuuint64_t dims[5] = {16, 2, (cuuint64_t)(nx / 16), (cuuint64_t)ny, (cuuint64_t)(nz / 2)};
-            const cuuint64_t str[4] = {16 * 8, 32 * 8, (cuuint64_t)(2 * nx) * 8, (cuuint64_t)(2 * nx * ny) * 8};
-            const cuuint32_t box[5] = {16, 1, (cuuint32_t)(nx / 16), (cuuint32_t)u, 1};
-            ok = ok && make_map(&p->wmap, p->work, 5, dims, str, box);
-        }
-        p->stile_y = p->stile_z = ok;
-        if (!ok) p->wpair = false;   // (plain layout then, maps rebuilt below)
-        else return;
-        p->stile_y = stile_supported(p->ny);
-        if (p->stile_y) {
-            const cuuint64_t dims[3] = {(cuuint64_t)p->rp, (cuuint64_t)p->ny, (cuuint64_t)(p->nzh * comps)};
-            const cuuint64_t str[2] = {(cuuint64_t)p->rp * 8, (cuuint64_t)(p->rp * p->ny) * 8};
-            const cuuint32_t box[3] = {cy, by, 1};
-            p->stile_y = make_map(&p->smap_y, p->work, 3, dims, str, box);
-        }
+        p->wpair = false;   // (plain chain then)
     }
     if (p->P == 1) {   // z pass: {x*y columns, z}
         const cuuint64_t dims[2] = {(cuuint64_t)(p->rp * p->ny), (cuuint64_t)(p->nz * comps)};
@@ -1424,9 +1411,9 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         TRY(cudaMemset(p->pl_done, 0, sizeof(unsigned) * 2 * p->nz));
         TRY(cudaMalloc(&p->pl_part, sizeof(double) * kPlaneN * p->nz));
     }
-    // z-pair layout of work where every pass that touches it supports it (one
+    // the z pass on the z-pair buffer where the passes around it support it (one
     // GPU, complex 3-D, x lines of 256..2048 points, TMA tiles on y and z)
-    p->wpair = desc->zpair_work && P == 1 && p->ndim == 3 && !p->real && !p->anti && !p->tdiff && !p->plane &&
+    p->wpair = !desc->flat_work && P == 1 && p->ndim == 3 && !p->real && !p->anti && !p->tdiff && !p->plane &&
                p->nx >= 256 && stile_supported(p->ny) && stile_supported(p->nz) && p->nz <= 1024;
     p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && !desc->delta_form;
     if (desc->r_switch > 0.0) p->r_sw = desc->r_switch;
@@ -1474,7 +1461,8 @@ usp_status usp_plan_workspace_size(usp_plan_t p, size_t *bytes) {
         *bytes = 3 * (size_t)p->ncomp * f + align256((size_t)p->nloc * 4) * (1 + 2 * np);
         return USP_OK;
     }
-    *bytes = 3 * f + w * (p->P > 1 ? 3 : 1) + (p->xform_cap ? f : 0);   // + s for the x-form
+    *bytes = 3 * f + w * (p->P > 1 ? 3 : 1) + (p->xform_cap ? f : 0)   // + s for the x-form
+             + (p->wpair ? w : 0);                                        // + the z-pair buffer
     return USP_OK;
 }
 
@@ -1514,6 +1502,7 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
         p->recvb = (float2 *)(p->ws + 3 * f + 2 * w);
     }
     p->s = p->xform_cap ? (float2 *)(p->ws + 3 * f + w * (p->P > 1 ? 3 : 1)) : nullptr;
+    p->work2 = p->wpair ? (float2 *)(p->ws + 3 * f + w * (p->P > 1 ? 3 : 1) + (p->xform_cap ? f : 0)) : nullptr;
     if (p->real)   // the spectrum rows' padding columns are never written by the x pass: keep them 0
         CU(cudaMemsetAsync(p->work, 0, w * (p->P > 1 ? 3 : 1), p->stream));
     p->have_potential = p->have_source = false;
@@ -1821,7 +1810,7 @@ usp_status usp_set_source(usp_plan_t p, const void *src, usp_where where) {
             // the list (2 KiB) and the lines must fit in the s field
             const long long cap = std::min<long long>(kSparseMaxLines, ((long long)p->nloc - 256) / p->nx);
             if (cnt > 0 && (long long)cnt <= cap) {
-                CU(launch_sparse_gather(p->s_flag, nlines, p->work, work_layout(p), reinterpret_cast<int *>(p->s),
+                CU(launch_sparse_gather(p->s_flag, nlines, p->work, (int)p->nx, reinterpret_cast<int *>(p->s),
                                         p->s + 256, p->s_ctr, p->stream));
                 p->s_sparse = true;
                 p->s_count = (int)cnt;
@@ -2180,11 +2169,10 @@ usp_status usp_bicgstab(usp_plan_t p, int64_t n_max, double tol, int64_t *n_done
     kp.partials = p->partials;
     kp.hist = p->hist;
     kp.hist_cap = p->hist_cap;
-    kp.wl = work_layout(p);
     const int gx = p->gridp_x, gu = occ_grid(p, (p->nloc + 255) / 256, 8);
     auto xop = [&](KMode m) -> usp_status {
         Tick t(p, KC_XOP);
-        CU(launch_xop((int)p->nx, m, kp, p->wmap, gx, p->stream));
+        CU(launch_xop((int)p->nx, m, kp, gx, p->stream));
         return USP_OK;
     };
     const long long batch = 8;
@@ -2337,15 +2325,14 @@ usp_status apply_M_dev(usp_plan_s *p, float2 *u, float2 *z) {
     kp.tw = p->tw[0];
     kp.nlines = p->ny * p->nzh;
     kp.st = p->st;
-    kp.wl = work_layout(p);
     usp_status s;
     {
         Tick t(p, KC_XOP);
-        CU(launch_xop((int)p->nx, K_OFWD, kp, p->wmap, p->gridp_x, p->stream));
+        CU(launch_xop((int)p->nx, K_OFWD, kp, p->gridp_x, p->stream));
     }
     if ((s = chain_mid(p, 0))) return s;
     Tick t(p, KC_XOP);
-    CU(launch_xop((int)p->nx, K_OINV, kp, p->wmap, p->gridp_x, p->stream));
+    CU(launch_xop((int)p->nx, K_OINV, kp, p->gridp_x, p->stream));
     return USP_OK;
 }
 }  // namespace

@@ -64,48 +64,16 @@ struct MulParams {
 };
 
 // ------------------------------------------------- chain-buffer layout --
-// Layout of `work`.  Plain: work[z][y][x].  z-pair (one-GPU
-// complex 3-D plans, nx in [256, 2048], ny, nz in [64, 1024]): planes 2zp and
-// 2zp + 1 interleaved in 16-element (128-byte) x blocks,
-//   work[((zp * ny + y) * (nx / 16) + x / 16) * 32 + (z % 2) * 16 + x % 16],
-// so a 16-column z tile (K_C) reads and writes 256-byte rows -- the z pass's
-// DRAM efficiency depends on the row width (tools/micro/zwrite.cu,
-// zpairlay.cu) -- while the y passes see a plain [zp][y][2 nx] array (rows
-// of 2 nx columns, each a (x, z parity) pair) and the x passes load a line
-// through a 5-D tensor map that undoes the interleave.
-struct WLayout {
-    int pair;            // 0: plain [z][y][x]; 1: z-pair
-    int nx;
-    int nylg;            // log2(ny)
-};
-// offset of element x = 0 of line (y + ny z) in the z-pair layout
-__host__ __device__ __forceinline__ long long wpair_line(const WLayout &w, long long line) {
-    const long long z = line >> w.nylg, y = line & ((1LL << w.nylg) - 1);
-    return (((z >> 1) << w.nylg) + y) * (2LL * w.nx) + (z & 1) * 16;
-}
-__host__ __device__ __forceinline__ long long work_off(const WLayout &w, long long line, int x) {
-    return w.pair ? wpair_line(w, line) + (x >> 4) * 32 + (x & 15) : line * w.nx + x;
-}
-// Work units of the x passes (U consecutive lines of one plane each), dealt
-// to CTA b of a grid of g.  Plain: units b, b + g, ...  z-pair: units come
-// in pairs -- the same U lines of planes 2zp and 2zp + 1, whose 128-byte x
-// blocks share 256-byte chunks -- a CTA takes pairs b, b + g, ... and the
-// two units of a pair back to back, so both halves of every chunk are
-// loaded and stored by one SM at nearly the same time.
-__host__ __device__ __forceinline__ int xunits_local(const WLayout &w, long long nunits, long long b, long long g) {
-    if (!w.pair) return (int)((nunits - b + g - 1) / g);
-    return 2 * (int)((nunits / 2 - b + g - 1) / g);
-}
-// first line (y + ny z) of local unit i
-__host__ __device__ __forceinline__ long long xunit_line0(const WLayout &w, int U, long long i, long long b,
-                                                          long long g) {
-    if (!w.pair) return (b + i * g) * U;
-    // pair q = (zp, y block): ny / U (a power of two) y blocks per plane pair
-    const long long q = b + (i >> 1) * g;
-    const int ylg = w.nylg - (U == 2 ? 1 : 0);
-    const long long zp = q >> ylg, yb = q & ((1LL << ylg) - 1);
-    return ((2 * zp + (i & 1)) << w.nylg) + yb * U;
-}
+// z-pair layout (default; desc.flat_work disables; one-GPU complex 3-D plans, nx in [256,
+// 2048], ny, nz in [64, 1024]): the z pass runs on a second
+// chain buffer `work2` in which planes 2zp and 2zp + 1 are interleaved in
+// 16-element (128-byte) x blocks,
+//   work2[((zp * ny + y) * (nx / 16) + x / 16) * 32 + (z % 2) * 16 + x % 16],
+// so its 16-column tiles read and write 256-byte rows (the z pattern's DRAM
+// efficiency depends on the row width: tools/micro/zwrite.cu, zpairlay.cu).
+// K_B writes work -> work2 in that layout, K_D reads work2 through the
+// [nz/2][ny][2 nx] view and writes work back in [z][y][x]; the x pass never
+// sees it.
 
 // ---------------------------------------------------------------- x pass --
 enum XMode : int { X_SRC_FWD = 0, X_SRC_EPI = 1, X_ITER = 2 };
@@ -127,7 +95,6 @@ struct XParams {
     // x-transformed source lines afterwards; X_SRC_FWD flags the source lines
     unsigned char *s_flag;   // per x-line: s != 0 (written by X_SRC_FWD when non-null)
     int s_sparse;            // X_ITER: do not read s (its x-transform is added by k_sadd)
-    WLayout wl;              // layout of work (z-pair: loads through the kernel's 5-D map)
 };
 
 // sparse source lines (R-31): line l = list[i] of the local grid gets comp[i*N .. +N) added
@@ -136,9 +103,8 @@ struct SAddParams {
     const float2 *comp;
     const int *list;
     int count;
-    int n;               // line length
+    int n;               // line length (row pitch of work)
     IterState *st;
-    WLayout wl;          // layout of work
 };
 
 // ------------------------------------------------------- BiCGSTAB (NEXT-2) --
@@ -173,7 +139,6 @@ struct KParams {
     double *partials;    // >= 3 doubles per CTA
     double *hist;
     int hist_cap;
-    WLayout wl;          // layout of work (z-pair: loads through the kernel's 5-D map)
 };
 
 // ---------------------------------------------------------- strided pass --
@@ -202,8 +167,11 @@ struct SParams {
     int col0;            // x-chunked transposes: column offset of the load map's coordinates (K_B)
     int x0;              // x-chunked transposes: global x of the chunk's column 0 (z pass multiplier;
                          // mp.rowc is then the chunk width)
-    int zpair;           // K_C on the z-pair layout of work: a tile row is 32 columns (16 x of
-                         // planes 2zp, 2zp + 1), rows = plane pairs, stride = pair-row pitch
+    int zpair;           // K_C on the z-pair buffer: a tile row is 32 columns (16 x of planes
+                         // 2zp, 2zp + 1), rows = plane pairs, stride = pair-row pitch
+    int pair_dst;        // K_B: store plane o into the z-pair buffer (stride = 2 nx, ostride =
+                         // 2 nx ny per plane pair)
+    int pair_src;        // K_D: load plane o through the map of the [nz/2][ny][2 nx] view
     int tma_store;       // k_stile: store the upper half of each tile (rows >= N/2; all rows for
                          // N <= 256) through the exchange buffer with tensor-map stores on the
                          // load map (in-place passes whose map describes dst only)
@@ -350,7 +318,7 @@ bool solve2d_supported(long long nx, long long ny);
 cudaError_t launch_solve2d(int nx, int ny, const S2Params &p, int nsm, cudaStream_t s);
 
 // BiCGSTAB (kernels_krylov.cu)
-cudaError_t launch_xop(int N, KMode mode, const KParams &p, const CUtensorMap &wmap, int grid, cudaStream_t s);
+cudaError_t launch_xop(int N, KMode mode, const KParams &p, int grid, cudaStream_t s);
 cudaError_t launch_kupd(const KParams &p, int grid, cudaStream_t s);
 constexpr int kGsCtasPerSm = 3;   // k_gs: __launch_bounds__(256, 3), grid = 3 x SMs
 cudaError_t launch_gs(int mode, int nb, const GSParams &p, int grid, cudaStream_t s);
@@ -376,14 +344,13 @@ cudaError_t launch_put_state(IterState *st, const IterState &h, cudaStream_t s);
 cudaError_t launch_set_form(IterState *st, int form, cudaStream_t s);
 cudaError_t launch_copy_bytes(void *dst, const void *src, size_t n, int grid, cudaStream_t s);
 cudaError_t launch_sparse_count(const unsigned char *flag, long long nlines, unsigned *count, cudaStream_t s);
-cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, const WLayout &wl,
-                                 int *list, float2 *comp, unsigned *count, cudaStream_t s);
+cudaError_t launch_sparse_gather(const unsigned char *flag, long long nlines, const float2 *work, int n, int *list,
+                                 float2 *comp, unsigned *count, cudaStream_t s);
 cudaError_t launch_sparse_add(const SAddParams &p, cudaStream_t s);
 
 // TMA-pipelined variants (kernels_pipe.cu)
-// wmap: the 5-D load map of work when p.wl.pair (unused otherwise)
-cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, const CUtensorMap &wmap, int grid, cudaStream_t s,
-                              bool lean = false, bool expect_x = false);
+cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cudaStream_t s, bool lean = false,
+                              bool expect_x = false);
 
 // TMA-prefetched 16-column strided passes (kernels_stile.cu)
 cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s);

@@ -86,8 +86,8 @@ class Plan:
     ``complex_path`` (float32 diffusion data on the complex path),
     ``launch_per_pass`` (2-D: one launch per pass instead of the persistent
     solver), ``plane_chain`` (the plane-chained pass on 1024^2-plane
-    grids instead of one sweep per FFT pass), ``zpair_work`` (the z-pair layout
-    of the FFT chain buffer instead of plain [z][y][x], where it applies),
+    grids instead of one sweep per FFT pass), ``flat_work`` (the z pass in place
+    on the [z][y][x] chain buffer instead of the z-pair buffer),
     ``test_hooks`` (USP_HOOK_* bits; tests only).
     """
 
@@ -97,7 +97,7 @@ class Plan:
                  tensor_diffusion: bool = False, delta_form: bool = False, r_switch: float = 0.0,
                  dense_source: bool = False, separate_transposes: bool = False, complex_path: bool = False,
                  launch_per_pass: bool = False, plane_chain: bool = False, test_hooks: int = 0,
-                 zpair_work: bool = False):
+                 flat_work: bool = False):
         import torch
 
         self.lib = L.load()
@@ -133,7 +133,7 @@ class Plan:
         d.launch_per_pass = int(bool(launch_per_pass))
         d.plane_chain = int(bool(plane_chain))
         d.test_hooks = int(test_hooks)
-        d.zpair_work = int(bool(zpair_work))
+        d.flat_work = int(bool(flat_work))
         if tensor_diffusion:
             d.dtype = L.R32
             self.dtype = "r32"
@@ -352,7 +352,7 @@ class Plan:
         return bool(xf.value), bool(fm.value), float(rs.value)
 
     def work_layout(self) -> str:
-        """"z-pair" or "flat": the layout of the plan's FFT chain buffer (usp_work_layout)."""
+        """"z-pair" or "flat": the chain buffer the z pass runs on (usp_work_layout)."""
         zp = ctypes.c_int()
         L.check(self.lib.usp_work_layout(self.handle, ctypes.byref(zp)))
         return "z-pair" if zp.value else "flat"

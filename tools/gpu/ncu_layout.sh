@@ -5,7 +5,7 @@
 # k_xpass_pipe launch (after the two setup passes and iteration 1's).
 set -e
 mkdir -p gpurun_out
-for v in "zpair:zpair_work=1" "flat:"; do
+for v in "zpair:" "flat:flat_work=1"; do
   n=${v%%:*}
   if [ "${1:-all}" != "xpass" ]; then
     ncu --set full --clock-control none -k regex:"k_stile" --launch-skip 9 --launch-count 3 \

@@ -1,6 +1,6 @@
 """In-process A/B of plan options (usp_plan_desc fields) on one library build.
 
-    python tools/gpu/opt_ab.py "zpair:zpair_work=1" "flat:" [--rounds 5] [--iters 20] [--config C5] [--size 1024]
+    python tools/gpu/opt_ab.py "zpair:" "flat:flat_work=1" [--rounds 5] [--iters 20] [--config C5] [--size 1024]
 
 Each variant is NAME:opt=val,opt=val (Plan keyword arguments); every variant
 gets its own plan and workspace on the same inputs, variants run round-robin
