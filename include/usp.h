@@ -156,8 +156,8 @@ typedef struct {
                              path of P > 1 plans (a test of that path on one GPU).  0 in
                              production.                                                  */
     int flat_work;        /* != 0: the z pass works in place on the chain buffer ([z][y][x],
-                             16-column tiles of 128-byte rows).  0: on one GPU (complex64,
-                             3-D, nx in [256, 2048], ny and nz in [64, 1024]) the y-forward
+                             16-column tiles of 128-byte rows).  0: on one GPU (3-D, ny and
+                             nz in [64, 1024], not antisymmetric / tensor) the y-forward
                              pass writes a second chain buffer in the z-pair layout --
                              planes 2zp and 2zp+1 interleaved in 128-byte x blocks -- so
                              the z pass (K_C) moves 256-byte rows, and the y-inverse pass

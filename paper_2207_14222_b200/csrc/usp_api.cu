@@ -1078,7 +1078,7 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
             // z-pair buffer (usp_internal.h): K_B stores work -> work2 (planes 2zp, 2zp+1
             // interleaved), K_C runs on work2's 256-byte pair rows, K_D reads work2
             // through the [nz/2][ny][2 nx] view and stores work back in [z][y][x]
-            const long long nx = p->nx, ny = p->ny;
+            const long long nx = p->rp, ny = p->ny;   // row pitch (nx; nx/2 + 16 on the real path)
             SParams yb = sparams(p, p->work, p->work2, p->tw[1], 2 * nx, nx, p->nz, 2 * nx * ny, 1, check_state, 3);
             yb.pair_dst = 1;
             SParams zp = sparams(p, p->work2, p->work2, p->tw[2], 2 * nx * ny, nx * ny, 1, 0, 2, check_state, 2);
@@ -1175,7 +1175,7 @@ void build_maps(usp_plan_s *p) {
         // z-pair buffer (usp_internal.h): K_C on pair rows {2 nx ny, nz/2} with {32, BP}
         // boxes, K_D on the [nz/2][ny][2 nx] view with {16, by, 1} boxes (K_B loads work
         // through the plain y map above)
-        const long long nx = p->nx, ny = p->ny, nz = p->nz;
+        const long long nx = p->rp, ny = p->ny, nz = p->nz;   // row pitch: nx, or nx/2 + 16 (real path)
         const cuuint64_t dz[2] = {(cuuint64_t)(2 * nx * ny), (cuuint64_t)(nz / 2)};
         const cuuint64_t sz[1] = {(cuuint64_t)(2 * nx * ny) * 8};
         const cuuint32_t bxz[2] = {32, (cuuint32_t)std::min<long long>(256, nz / 4)};
@@ -1412,9 +1412,9 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
         TRY(cudaMalloc(&p->pl_part, sizeof(double) * kPlaneN * p->nz));
     }
     // the z pass on the z-pair buffer where the passes around it support it (one
-    // GPU, complex 3-D, x lines of 256..2048 points, TMA tiles on y and z)
-    p->wpair = !desc->flat_work && P == 1 && p->ndim == 3 && !p->real && !p->anti && !p->tdiff && !p->plane &&
-               p->nx >= 256 && stile_supported(p->ny) && stile_supported(p->nz) && p->nz <= 1024;
+    // GPU, 3-D, one component, 16-column TMA tiles on y and z)
+    p->wpair = !desc->flat_work && P == 1 && p->ndim == 3 && !p->anti && !p->tdiff && !p->plane &&
+               stile_supported(p->ny) && p->ny <= 1024 && stile_supported(p->nz) && p->nz <= 1024;
     p->xform_cap = !p->anti && !p->tdiff && p->ndim >= 2 && !p->solve2d && !desc->delta_form;
     if (desc->r_switch > 0.0) p->r_sw = desc->r_switch;
     p->force_finish = (desc->test_hooks & USP_HOOK_RANK_FINISH) != 0;

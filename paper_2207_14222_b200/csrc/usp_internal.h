@@ -64,16 +64,17 @@ struct MulParams {
 };
 
 // ------------------------------------------------- chain-buffer layout --
-// z-pair layout (default; desc.flat_work disables; one-GPU complex 3-D plans, nx in [256,
-// 2048], ny, nz in [64, 1024]): the z pass runs on a second
-// chain buffer `work2` in which planes 2zp and 2zp + 1 are interleaved in
-// 16-element (128-byte) x blocks,
-//   work2[((zp * ny + y) * (nx / 16) + x / 16) * 32 + (z % 2) * 16 + x % 16],
+// z-pair layout (default; desc.flat_work disables; one-GPU 3-D plans with
+// ny, nz in [64, 1024]): the z pass runs on a second chain
+// buffer `work2` in which planes 2zp and 2zp + 1 are interleaved in
+// 16-element (128-byte) blocks of the row (rp = nx, or nx/2 + 16 on the
+// real path),
+//   work2[((zp * ny + y) * (rp / 16) + x / 16) * 32 + (z % 2) * 16 + x % 16],
 // so its 16-column tiles read and write 256-byte rows (the z pattern's DRAM
 // efficiency depends on the row width: tools/micro/zwrite.cu, zpairlay.cu).
 // K_B writes work -> work2 in that layout, K_D reads work2 through the
-// [nz/2][ny][2 nx] view and writes work back in [z][y][x]; the x pass never
-// sees it.
+// [nz/2][ny][2 rp] view and writes work back in [z][y][rp]; the x pass
+// never sees it.
 
 // ---------------------------------------------------------------- x pass --
 enum XMode : int { X_SRC_FWD = 0, X_SRC_EPI = 1, X_ITER = 2 };

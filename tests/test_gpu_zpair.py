@@ -34,11 +34,10 @@ def _dense(src):
     return src + (1e-3 * (rng.standard_normal(src.shape) + 1j * rng.standard_normal(src.shape))).astype(np.complex64)
 
 
-# (nz, ny, nx): every x extent the layout takes (U = 2 / 1 lines per x unit,
-# N1 = 16 / 32 lanes per line), y / z tiles of 64 .. 1024 rows, the HALFX
-# two-round exchange (nz >= 512) and the full one (nz <= 256)
+# (nz, ny, nx): x extents 32 .. 2048, y / z tiles of 64 .. 1024 rows, the
+# HALFX two-round exchange (nz >= 512) and the full one (nz <= 256)
 SHAPES = [(64, 64, 256), (128, 64, 512), (64, 128, 1024), (512, 64, 256), (1024, 64, 256), (64, 64, 2048),
-          (256, 256, 256)]
+          (256, 256, 256), (64, 64, 32), (128, 1024, 64)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -132,10 +131,29 @@ def test_zpair_where_it_applies():
 
     assert Plan((64, 64, 256)).work_layout() == "z-pair"
     assert Plan((64, 64, 256), flat_work=True).work_layout() == "flat"
-    assert Plan((64, 64, 128)).work_layout() == "flat"            # x lines < 256 points
+    assert Plan((64, 64, 16)).work_layout() == "z-pair"           # any x extent
+    assert Plan((64, 64, 256), kind="diffusion", dtype="r32").work_layout() == "z-pair"   # real path
     assert Plan((32, 64, 256)).work_layout() == "flat"            # z lines of 32: register-staged pass
     assert Plan((2048, 64, 256)).work_layout() == "flat"          # z tiles of 8 columns
+    assert Plan((64, 2048, 256)).work_layout() == "flat"          # y tiles of 8 columns
     assert Plan((64, 256)).work_layout() == "flat"                # 2-D
     assert Plan((64, 64, 256), virtual_ranks=2).work_layout() == "flat"
-    assert Plan((64, 64, 256), kind="diffusion", dtype="r32").work_layout() == "flat"   # real path
     assert Plan((64, 64, 256), antisymmetric=True).work_layout() == "flat"
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 128), (128, 64, 512), (512, 64, 64)])
+def test_zpair_real_path_identical(shape):
+    """The half-spectrum real path (rows of nx/2 + 16 columns) on the z-pair
+    buffer: bit-identical to the in-place z pass (C4 recipe)."""
+    from synth import make
+
+    p = make("C4", shape)
+    med, src, dtype = rounded_inputs(p)
+    assert dtype == "r32"
+    out = []
+    for flat in (False, True):
+        pl = _plan(p, dtype, flat_work=flat, r_switch=0.3)
+        assert pl.work_layout() == ("flat" if flat else "z-pair")
+        x, n, _, _ = run_gpu(p, n_iter=12, tol=0.0, plan=pl, med=med, src=src, dtype=dtype)
+        out.append((x, pl.history()))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
