@@ -638,7 +638,7 @@ def run_usp(args, world, rank, local):
 
     if rank != 0:
         return 0
-    z_pass_buffer = plan.work_layout()
+    z_pass_buffer, transport = plan.work_layout(), plan.transport()
     plan.close()   # the remaining measurements allocate their own plans
     del plan
     torch.cuda.empty_cache()
@@ -673,7 +673,7 @@ def run_usp(args, world, rank, local):
                                f"{n_iter} iterations of Alg. 1 per step (setup + iterations), alpha=0.75",
                    "grid": list(shape), "iterations_per_step": n_iter, "iteration_form": form_desc,
                    "parallelism": parallelism, "slab_check_rel_l2": slab_check,
-                   "z_pass_buffer": z_pass_buffer,
+                   "z_pass_buffer": z_pass_buffer, "transposes": transport,
                    "l2": "inputs (8 GiB fields) larger than L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,

@@ -167,6 +167,21 @@ typedef struct {
 } usp_plan_desc;
 
 #define USP_HOOK_RANK_FINISH 1
+#define USP_HOOK_WINDOW 2   /* one-rank communicator, workspace from usp_shared_alloc: register the
+                               workspace as an NCCL window at usp_plan_set_workspace, write through
+                               ncclGetPeerPointer's mapping and check the bytes through the plain
+                               pointer (the NEXT-1 transport's machinery on one GPU; tests only) */
+
+/* How the slab decomposition's transposes move data (usp_transport). */
+typedef enum {
+    USP_TRANSPORT_NONE = 0,          /* one slab: no transposes                                  */
+    USP_TRANSPORT_VIRTUAL = 1,       /* virtual slabs, fused into the K_B / K_C stores           */
+    USP_TRANSPORT_VIRTUAL_COPY = 2,  /* virtual slabs, separate device-copy transposes            */
+    USP_TRANSPORT_NCCL_WINDOW = 3,   /* fused stores into the peers' buffers through an NCCL 2.28
+                                        window (ncclCommWindowRegister + ncclGetPeerPointer)     */
+    USP_TRANSPORT_CUDA_IPC = 4,      /* fused stores into CUDA-IPC-mapped peer buffers            */
+    USP_TRANSPORT_NCCL_ALLTOALL = 5  /* separate transposes: grouped ncclSend / ncclRecv          */
+} usp_transport_kind;
 
 /* Create a plan for the grid and problem described by *desc (copied).
  *
@@ -370,6 +385,19 @@ usp_status usp_launch_count(usp_plan_t plan, int64_t *launches);
  * probe pass: x unchanged); those two calls are therefore collective over
  * the ranks of a slab-decomposed plan.  Errors: USP_ERR_ARG. */
 usp_status usp_iteration_form(usp_plan_t plan, int *xform, int *form, double *r_switch, int *source_lines);
+
+/* Workspace memory for slab-decomposed plans over a communicator: ncclMemAlloc
+ * (symmetric memory NCCL can register as a window, so the fused transposes
+ * reach the peers' buffers through ncclGetPeerPointer -- SURVEY.md §8(f)
+ * NEXT-1) when libnccl.so.2 (>= 2.28) provides it, else cudaMalloc.  The
+ * caller owns it and frees it with usp_shared_free after usp_plan_destroy.
+ * Errors: USP_ERR_ARG, USP_ERR_NOMEM. */
+usp_status usp_shared_alloc(size_t bytes, void **ptr);
+usp_status usp_shared_free(void *ptr);
+
+/* *kind = the usp_transport_kind the plan's transposes use (decided at
+ * usp_plan_set_workspace; collectively for NCCL plans).  Errors: USP_ERR_ARG. */
+usp_status usp_transport(usp_plan_t plan, int *kind);
 
 /* *zpair = 1 if the plan's z pass runs on the z-pair chain buffer
  * (desc.flat_work), else 0.  Diagnostic; no device work.  Errors: USP_ERR_ARG. */

@@ -20,9 +20,12 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nccl_device.h>   // ncclGetPeerPointer (device side of the NCCL 2.28 window API)
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <complex>
 #include <cstdlib>
 #include <cmath>
@@ -78,9 +81,15 @@ struct Nccl {
     ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
     const char *(*GetErrorString)(ncclResult_t);
+    // NCCL >= 2.28 (optional): symmetric memory and windows
+    bool win = false;
+    ncclResult_t (*MemAlloc)(void **, size_t);
+    ncclResult_t (*MemFree)(void *);
+    ncclResult_t (*CommWindowRegister)(ncclComm_t, void *, size_t, ncclWindow_t *, int);
+    ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t);
 };
 
-Nccl &nccl() {
+Nccl &nccl_api() {
     static Nccl n;
     static bool tried = false;
     if (tried) return n;
@@ -113,6 +122,11 @@ Nccl &nccl() {
     n.AllGather = (decltype(n.AllGather))sym("ncclAllGather");
     n.AllReduce = (decltype(n.AllReduce))sym("ncclAllReduce");
     n.GetErrorString = (decltype(n.GetErrorString))sym("ncclGetErrorString");
+    n.MemAlloc = (decltype(n.MemAlloc))dlsym(h, "ncclMemAlloc");
+    n.MemFree = (decltype(n.MemFree))dlsym(h, "ncclMemFree");
+    n.CommWindowRegister = (decltype(n.CommWindowRegister))dlsym(h, "ncclCommWindowRegister");
+    n.CommWindowDeregister = (decltype(n.CommWindowDeregister))dlsym(h, "ncclCommWindowDeregister");
+    n.win = n.MemAlloc && n.MemFree && n.CommWindowRegister && n.CommWindowDeregister;
     n.ok = all;
     if (!all) n.why = "libnccl.so.2 lacks an entry point";
     return n;
@@ -122,9 +136,51 @@ Nccl &nccl() {
     do {                                                                                           \
         ncclResult_t r_ = (call);                                                                  \
         if (r_ != ncclSuccess)                                                                     \
-            return fail(USP_ERR_NCCL, "%s failed: %s (%s:%d)", #call, nccl().GetErrorString(r_), __FILE__, \
+            return fail(USP_ERR_NCCL, "%s failed: %s (%s:%d)", #call, nccl_api().GetErrorString(r_), __FILE__, \
                         __LINE__);                                                                 \
     } while (0)
+
+// usp_shared_alloc's allocations: base -> (bytes, from ncclMemAlloc)
+struct SharedAlloc {
+    size_t bytes;
+    bool nccl;
+};
+std::mutex g_shared_mu;
+std::map<char *, SharedAlloc> g_shared;
+
+// the ncclMemAlloc allocation holding [p, p + bytes), if any
+bool shared_range(const void *p, size_t bytes, char **base, size_t *size) {
+    std::lock_guard<std::mutex> g(g_shared_mu);
+    auto it = g_shared.upper_bound((char *)p);
+    if (it == g_shared.begin()) return false;
+    --it;
+    if (!it->second.nccl || (char *)p + bytes > it->first + it->second.bytes) return false;
+    *base = it->first;
+    *size = it->second.bytes;
+    return true;
+}
+
+// peer q's address of the window's byte 0, for q < P (the window spans one
+// LSA team: every rank of a single-node communicator)
+__global__ void k_win_peers(ncclWindow_t w, int P, void **out) {
+    const int q = threadIdx.x;
+    if (q < P) out[q] = ncclGetPeerPointer(w, 0, q);
+}
+// window self-test on a one-rank communicator: write through the window's
+// mapping, read through the plain pointer
+__global__ void k_win_write(float2 *dst, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = make_float2((float)i, -(float)(i & 1023));
+    __threadfence_system();
+}
+__global__ void k_win_check(const float2 *src, long long n, unsigned *bad) {
+    unsigned b = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float2 v = src[i];
+        b += (v.x != (float)i || v.y != -(float)(i & 1023)) ? 1u : 0u;
+    }
+    if (b) atomicAdd(bad, b);
+}
 
 enum KClass { KC_XPASS = 0, KC_YFWD, KC_ZMUL, KC_YINV, KC_YMUL2D, KC_SOLVE1D, KC_POTENTIAL,
               KC_FARTHEST, KC_SETSTATE, KC_XSETUP, KC_A2A, KC_FINISH, KC_ALLGATHER, KC_BARRIER, KC_XOP,
@@ -181,6 +237,10 @@ struct usp_plan_s {
     bool fused = false;
     float2 *peer_recv[kMaxPeers] = {}, *peer_send[kMaxPeers] = {};
     std::vector<void *> ipc_bases;   // peer allocations mapped with cudaIpcOpenMemHandle
+    // NCCL window over the workspace (ncclMemAlloc'd by usp_shared_alloc): the
+    // peers' send / receive buffers through ncclGetPeerPointer (NEXT-1)
+    ncclWindow_t win = nullptr;
+    int transport = USP_TRANSPORT_NONE;
     // BiCGSTAB (caller-owned Krylov workspace: rhat, p, v, s, t)
     float2 *k_rh = nullptr, *k_p = nullptr, *k_v = nullptr, *k_s = nullptr, *k_t = nullptr;
     KState *ks = nullptr;
@@ -425,7 +485,7 @@ usp_status gather_host(usp_plan_s *p, const double *mine, int n, std::vector<dou
     if (n > 64 || (size_t)p->P * n > 1920) return fail(USP_ERR_ARG, "gather of %d doubles x %d ranks too large", n, p->P);
     double *snd = p->coll + 64, *rcv = p->coll + 128;
     CU(launch_put_bytes(snd, mine, sizeof(double) * n, p->stream));
-    NC(nccl().AllGather(snd, rcv, (size_t)n, ncclDouble, p->comm, p->stream));
+    NC(nccl_api().AllGather(snd, rcv, (size_t)n, ncclDouble, p->comm, p->stream));
     return readback(p, out.data(), rcv, sizeof(double) * n * p->P);
 }
 
@@ -649,7 +709,7 @@ usp_status run_xpass(usp_plan_s *p, XMode mode, const XParams &xp) {
     if (mode != X_SRC_FWD && rank_finish(p)) {
         {
             Tick t(p, KC_ALLGATHER, false);
-            NC(nccl().AllGather(p->coll, p->coll + 8, 1, ncclDouble, p->comm, p->stream));
+            NC(nccl_api().AllGather(p->coll, p->coll + 8, 1, ncclDouble, p->comm, p->stream));
         }
         Tick t(p, KC_FINISH);
         CU(launch_finish(p->st, p->coll + 8, p->P, mode == X_SRC_EPI, red_params(p), p->stream));
@@ -777,7 +837,34 @@ AddrRangeFn addr_range_fn() {
 void close_peers(usp_plan_s *p) {
     for (void *b : p->ipc_bases) cudaIpcCloseMemHandle(b);
     p->ipc_bases.clear();
+    if (p->win) {   // collective, like the registration
+        nccl_api().CommWindowDeregister(p->comm, p->win);
+        p->win = nullptr;
+    }
     p->fused = false;
+    p->transport = USP_TRANSPORT_NONE;
+}
+
+// every rank's flag (1/0) -> the minimum over the ranks (on the plan stream)
+usp_status all_agree(usp_plan_s *p, bool mine, bool *all) {
+    double good = mine ? 1.0 : 0.0;
+    CU(cudaMemcpyAsync(p->coll + 2, &good, sizeof(double), cudaMemcpyHostToDevice, p->stream));
+    NC(nccl_api().AllReduce(p->coll + 2, p->coll + 2, 1, ncclDouble, ncclMin, p->comm, p->stream));
+    CU(cudaMemcpyAsync(&good, p->coll + 2, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    *all = good == 1.0;
+    return USP_OK;
+}
+
+// NCCL window over the workspace allocation (collective): on success the P
+// ranks' addresses of byte 0 of that allocation in peer[0..P)
+usp_status window_peers(usp_plan_s *p, char *base, size_t size, char **peer) {
+    Nccl &n = nccl_api();
+    NC(n.CommWindowRegister(p->comm, base, size, &p->win, NCCL_WIN_COLL_SYMMETRIC));
+    void **d = reinterpret_cast<void **>(p->coll + 176);   // scratch: 8 pointers (past the IPC records)
+    k_win_peers<<<1, 32, 0, p->stream>>>(p->win, p->P, d);
+    CU(cudaGetLastError());
+    return readback(p, peer, d, sizeof(void *) * p->P);
 }
 
 // Map every rank's send / receive buffer for the fused transposes (collective
@@ -795,8 +882,37 @@ usp_status setup_peers(usp_plan_s *p) {
             p->peer_send[q] = p->sendb + (long long)q * p->P * bk;
         }
         p->fused = true;
+        p->transport = USP_TRANSPORT_VIRTUAL;
         return USP_OK;
     }
+    // 1. NCCL window (the workspace came from usp_shared_alloc = ncclMemAlloc on
+    //    every rank): peers' buffers through ncclGetPeerPointer
+    {
+        char *base = nullptr;
+        size_t size = 0;
+        const bool can = nccl_api().win && shared_range(p->ws, p->ws_bytes, &base, &size);
+        bool all = false;
+        usp_status s = all_agree(p, can, &all);
+        if (s) return s;
+        if (all) {
+            char *peer[kMaxPeers] = {};
+            s = window_peers(p, base, size, peer);
+            bool ok = s == USP_OK;
+            for (int q = 0; ok && q < p->P; ++q) ok = peer[q] != nullptr;
+            if ((s = all_agree(p, ok, &all))) return s;
+            if (all) {
+                for (int q = 0; q < p->P; ++q) {
+                    p->peer_recv[q] = (float2 *)(peer[q] + ((char *)p->recvb - base));
+                    p->peer_send[q] = (float2 *)(peer[q] + ((char *)p->sendb - base));
+                }
+                p->fused = true;
+                p->transport = USP_TRANSPORT_NCCL_WINDOW;
+                return USP_OK;
+            }
+            close_peers(p);
+        }
+    }
+    // 2. CUDA IPC handles of the workspace allocations, all-gathered
     struct Rec {
         cudaIpcMemHandle_t h;
         long long off_recv, off_send;
@@ -814,7 +930,7 @@ usp_status setup_peers(usp_plan_s *p) {
     cudaGetLastError();   // clear a failed IPC query
     Rec *d = reinterpret_cast<Rec *>(p->coll + 16);   // scratch: 8 x 88 bytes fits the 192 doubles
     CU(cudaMemcpyAsync(d, &mine, sizeof(Rec), cudaMemcpyHostToDevice, p->stream));
-    NC(nccl().AllGather(d, d + 1, sizeof(Rec), ncclChar, p->comm, p->stream));
+    NC(nccl_api().AllGather(d, d + 1, sizeof(Rec), ncclChar, p->comm, p->stream));
     std::vector<Rec> all(p->P);
     CU(cudaMemcpyAsync(all.data(), d + 1, sizeof(Rec) * p->P, cudaMemcpyDeviceToHost, p->stream));
     CU(cudaStreamSynchronize(p->stream));
@@ -843,11 +959,15 @@ usp_status setup_peers(usp_plan_s *p) {
     }
     // consensus: fused only if every rank mapped every peer
     CU(cudaMemcpyAsync(p->coll + 2, &good, sizeof(double), cudaMemcpyHostToDevice, p->stream));
-    NC(nccl().AllReduce(p->coll + 2, p->coll + 2, 1, ncclDouble, ncclMin, p->comm, p->stream));
+    NC(nccl_api().AllReduce(p->coll + 2, p->coll + 2, 1, ncclDouble, ncclMin, p->comm, p->stream));
     CU(cudaMemcpyAsync(&good, p->coll + 2, sizeof(double), cudaMemcpyDeviceToHost, p->stream));
     CU(cudaStreamSynchronize(p->stream));
-    if (good == 1.0) p->fused = true;
-    else close_peers(p);
+    if (good == 1.0) {
+        p->fused = true;
+        p->transport = USP_TRANSPORT_CUDA_IPC;
+    } else {
+        close_peers(p);
+    }
     return USP_OK;
 }
 
@@ -856,7 +976,7 @@ usp_status setup_peers(usp_plan_s *p) {
 usp_status rank_barrier(usp_plan_s *p) {
     if (!multi_rank(p)) return USP_OK;
     Tick t(p, KC_BARRIER, false);
-    NC(nccl().AllReduce(p->coll + 3, p->coll + 3, 1, ncclDouble, ncclSum, p->comm, p->stream));
+    NC(nccl_api().AllReduce(p->coll + 3, p->coll + 3, 1, ncclDouble, ncclSum, p->comm, p->stream));
     return USP_OK;
 }
 
@@ -884,7 +1004,7 @@ usp_status exchange(usp_plan_s *p, bool forward, int chunk = 0, cudaStream_t st 
             }
         return USP_OK;
     }
-    Nccl &n = nccl();
+    Nccl &n = nccl_api();
     float2 *from = (forward ? p->sendb : p->recvb) + base, *to = (forward ? p->recvb : p->sendb) + base;
     NC(n.GroupStart());
     for (int q = 0; q < p->P; ++q) {
@@ -1244,7 +1364,7 @@ const char *usp_version(void) { return "0.4 sm_100a"; }
 
 usp_status usp_comm_unique_id(unsigned char id[128]) {
     if (!id) return fail(USP_ERR_ARG, "NULL argument");
-    Nccl &n = nccl();
+    Nccl &n = nccl_api();
     if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
     ncclUniqueId u;
     NC(n.GetUniqueId(&u));
@@ -1256,7 +1376,7 @@ usp_status usp_comm_unique_id(unsigned char id[128]) {
 usp_status usp_comm_init(const unsigned char id[128], int nranks, int rank, void **comm) {
     if (!id || !comm) return fail(USP_ERR_ARG, "NULL argument");
     if (nranks < 1 || rank < 0 || rank >= nranks) return fail(USP_ERR_ARG, "bad rank %d of %d", rank, nranks);
-    Nccl &n = nccl();
+    Nccl &n = nccl_api();
     if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
@@ -1268,7 +1388,7 @@ usp_status usp_comm_init(const unsigned char id[128], int nranks, int rank, void
 
 usp_status usp_comm_destroy(void *comm) {
     if (!comm) return USP_OK;
-    Nccl &n = nccl();
+    Nccl &n = nccl_api();
     if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
     NC(n.CommDestroy((ncclComm_t)comm));
     return USP_OK;
@@ -1292,7 +1412,7 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out) {
     if (desc->nccl_comm && desc->virtual_ranks > 1)
         return fail(USP_ERR_ARG, "nccl_comm and virtual_ranks are exclusive");
     if (desc->nccl_comm) {
-        Nccl &n = nccl();
+        Nccl &n = nccl_api();
         if (!n.ok) return fail(USP_ERR_NCCL, "%s", n.why.c_str());
         NC(n.CommCount((ncclComm_t)desc->nccl_comm, &P));
         NC(n.CommUserRank((ncclComm_t)desc->nccl_comm, &rank));
@@ -1511,6 +1631,27 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
         return fail(USP_ERR_CUDA, "could not encode the tensor maps of the slab decomposition");
     usp_status s = setup_peers(p);
     if (s) return s;
+    if (p->P > 1 && !p->fused) p->transport = p->virt ? USP_TRANSPORT_VIRTUAL_COPY : USP_TRANSPORT_NCCL_ALLTOALL;
+    if (p->comm && p->P == 1 && (p->d.test_hooks & USP_HOOK_WINDOW)) {
+        // the window machinery on one GPU: register, resolve rank 0's mapping,
+        // write through it, check through the plain pointer
+        char *base = nullptr, *peer[kMaxPeers] = {};
+        size_t size = 0;
+        if (!nccl_api().win || !shared_range(p->ws, p->ws_bytes, &base, &size))
+            return fail(USP_ERR_UNSUPPORTED, "window test: NCCL >= 2.28 and a usp_shared_alloc workspace needed");
+        if ((s = window_peers(p, base, size, peer))) return s;
+        if (!peer[0]) return fail(USP_ERR_NCCL, "ncclGetPeerPointer returned NULL");
+        const long long n = std::min<long long>(p->nloc, 1LL << 22);
+        unsigned *bad = reinterpret_cast<unsigned *>(p->coll + 184);
+        CU(cudaMemsetAsync(bad, 0, sizeof(unsigned), p->stream));
+        k_win_write<<<p->nsm, 256, 0, p->stream>>>((float2 *)(peer[0] + ((char *)p->work - base)), n);
+        k_win_check<<<p->nsm, 256, 0, p->stream>>>(p->work, n, bad);
+        CU(cudaGetLastError());
+        unsigned nbad = 0;
+        if ((s = readback(p, &nbad, bad, sizeof nbad))) return s;
+        if (nbad) return fail(USP_ERR_NCCL, "window test: %u of %lld values differ", nbad, n);
+        p->transport = USP_TRANSPORT_NCCL_WINDOW;
+    }
     if (p->P > 1 && !p->fused && p->nchunk > 1 && !p->xstream) {
         CU(cudaStreamCreateWithFlags(&p->xstream, cudaStreamNonBlocking));
         for (auto *v : {&p->ev_b, &p->ev_x, &p->ev_c, &p->ev_y}) {
@@ -1602,8 +1743,8 @@ usp_status usp_set_potential(usp_plan_t p, const void *medium, usp_where where, 
         CU(launch_potential(pp, occ_grid(p, (p->nloc + 255) / 256, 8), p->stream));
     }
     if (multi_rank(p)) {   // the Theorem 1 checks over the whole grid
-        NC(nccl().AllReduce(p->red_u, p->red_u, 1, ncclUint32, ncclMax, p->comm, p->stream));
-        NC(nccl().AllReduce(p->red_u + 1, p->red_u + 1, 2, ncclUint32, ncclSum, p->comm, p->stream));
+        NC(nccl_api().AllReduce(p->red_u, p->red_u, 1, ncclUint32, ncclMax, p->comm, p->stream));
+        NC(nccl_api().AllReduce(p->red_u + 1, p->red_u + 1, 2, ncclUint32, ncclSum, p->comm, p->stream));
     }
     unsigned red[4];
     if ((s = readback(p, red, p->red_u, sizeof red))) return s;
@@ -2503,6 +2644,52 @@ usp_status usp_iteration_form(usp_plan_t p, int *xform, int *form, double *r_swi
     if (xform) *xform = p->xform_cap ? 1 : 0;
     if (form) *form = (p->st_host->form == FORM_DELTA) ? 0 : 1;
     if (r_switch) *r_switch = p->r_sw;
+    return USP_OK;
+}
+
+usp_status usp_shared_alloc(size_t bytes, void **ptr) {
+    if (!ptr || !bytes) return fail(USP_ERR_ARG, "NULL argument or zero size");
+    *ptr = nullptr;
+    Nccl &n = nccl_api();
+    void *q = nullptr;
+    bool via = false;
+    if (n.ok && n.win && n.MemAlloc(&q, bytes) == ncclSuccess && q) {
+        via = true;
+    } else {
+        cudaGetLastError();
+        q = nullptr;
+        if (cudaMalloc(&q, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(USP_ERR_NOMEM, "could not allocate %zu bytes", bytes);
+        }
+    }
+    std::lock_guard<std::mutex> g(g_shared_mu);
+    g_shared[(char *)q] = SharedAlloc{bytes, via};
+    *ptr = q;
+    return USP_OK;
+}
+
+usp_status usp_shared_free(void *ptr) {
+    if (!ptr) return USP_OK;
+    SharedAlloc a{};
+    {
+        std::lock_guard<std::mutex> g(g_shared_mu);
+        auto it = g_shared.find((char *)ptr);
+        if (it == g_shared.end()) return fail(USP_ERR_ARG, "not a usp_shared_alloc pointer");
+        a = it->second;
+        g_shared.erase(it);
+    }
+    if (a.nccl) {
+        NC(nccl_api().MemFree(ptr));
+    } else {
+        CU(cudaFree(ptr));
+    }
+    return USP_OK;
+}
+
+usp_status usp_transport(usp_plan_t p, int *kind) {
+    if (!p || !kind) return fail(USP_ERR_ARG, "NULL argument");
+    *kind = p->transport;
     return USP_OK;
 }
 

@@ -25,19 +25,6 @@ class Split:
     max_abs_V: float
 
 
-def _cuda_malloc(lib, nbytes: int):
-    """cudaMalloc through the CUDA runtime libusp links (resolved via its handle)."""
-    ptr = ctypes.c_void_p()
-    lib.cudaMalloc.restype = ctypes.c_int
-    lib.cudaMalloc.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_size_t]
-    lib.cudaFree.restype = ctypes.c_int
-    lib.cudaFree.argtypes = [ctypes.c_void_p]
-    rc = lib.cudaMalloc(ctypes.byref(ptr), ctypes.c_size_t(nbytes))
-    if rc != 0 or not ptr.value:
-        raise MemoryError(f"cudaMalloc of {nbytes} bytes failed (cudaError {rc})")
-    return ptr
-
-
 def _numel(a) -> int:
     return int(a.numel()) if hasattr(a, "numel") and callable(a.numel) else int(np.asarray(a).size)
 
@@ -146,11 +133,14 @@ class Plan:
         L.check(self.lib.usp_plan_workspace_size(self.handle, ctypes.byref(nbytes)))
         self._ws_raw = None
         if comm is not None:
-            # slab decomposition over ranks: a workspace of its own cudaMalloc, so
-            # CUDA IPC can map it for the fused transposes whatever torch's
-            # allocator settings (expandable segments are not IPC-mappable)
+            # slab decomposition over ranks: a workspace of its own (usp_shared_alloc:
+            # ncclMemAlloc, so NCCL can register it as a window for the fused
+            # transposes, else cudaMalloc, which CUDA IPC can map whatever torch's
+            # allocator settings)
             with torch.cuda.device(self.device):
-                self._ws_raw = _cuda_malloc(self.lib, int(nbytes.value))
+                ptr = ctypes.c_void_p()
+                L.check(self.lib.usp_shared_alloc(int(nbytes.value), ctypes.byref(ptr)))
+                self._ws_raw = ptr
             self.workspace = None
             ws_ptr = self._ws_raw
         else:
@@ -357,6 +347,16 @@ class Plan:
         L.check(self.lib.usp_work_layout(self.handle, ctypes.byref(zp)))
         return "z-pair" if zp.value else "flat"
 
+    TRANSPORTS = ("none", "virtual", "virtual-copy", "nccl-window", "cuda-ipc", "nccl-alltoall")
+
+    def transport(self) -> str:
+        """How the slab transposes move data (usp_transport): "none" (one slab),
+        "virtual" / "virtual-copy" (virtual slabs, fused / device copies),
+        "nccl-window", "cuda-ipc" (fused peer stores) or "nccl-alltoall"."""
+        k = ctypes.c_int()
+        L.check(self.lib.usp_transport(self.handle, ctypes.byref(k)))
+        return self.TRANSPORTS[k.value]
+
     def source_lines(self) -> int:
         """Number of x-lines carrying the source when the x-form skips the
         dense s field (reading R-31), else 0."""
@@ -370,7 +370,7 @@ class Plan:
             self.lib.usp_plan_destroy(self.handle)
             self.handle = None
         if getattr(self, "_ws_raw", None) is not None:
-            self.lib.cudaFree(self._ws_raw)
+            L.check(self.lib.usp_shared_free(self._ws_raw))
             self._ws_raw = None
 
     def __del__(self):

@@ -199,3 +199,52 @@ def test_rank_finish_path_with_xform_switch(monkeypatch):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_nccl_window_machinery_one_rank():
+    """NEXT-1's transport on one GPU: the workspace of a
+    communicator plan comes from usp_shared_alloc (ncclMemAlloc), is
+    registered as an NCCL 2.28 window (ncclCommWindowRegister), and values
+    written through ncclGetPeerPointer's mapping of rank 0 read back through
+    the plain pointer (USP_HOOK_WINDOW); the solve on that memory is the
+    single-GPU one bit for bit."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+    from paper_2207_14222_b200 import Plan, comm_init
+    from synth import make
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29734")
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        p = make("C3", (64, 64, 128))
+        med, src, _ = rounded_inputs(p)
+        x1, n1, t1, pl1 = _run(p, 30, 0)
+        assert pl1.transport() == "none"
+        comm = comm_init()
+        plan = Plan(p.shape, comm=comm, test_hooks=2)   # USP_HOOK_WINDOW
+        assert plan.transport() == "nccl-window"
+        plan.set_potential(torch.from_numpy(med).cuda(), 0.95)
+        plan.set_source(torch.from_numpy(src).cuda())
+        n, term = plan.iterate(30, p.alpha, 0.0)
+        assert n == n1 == 30
+        assert np.array_equal(plan.get_field().cpu().numpy(), x1)
+        plan.close()
+        comm.close()
+    finally:
+        if own:
+            dist.destroy_process_group()
+
+
+def test_transport_reported():
+    """usp_transport: the mode the transposes run in."""
+    from synth import make
+
+    p = make("C3", (64, 64, 64))
+    assert _run(p, 2, 2)[3].transport() == "virtual"
+    assert _run(p, 2, 2, separate_transposes=True)[3].transport() == "virtual-copy"
+    assert _run(p, 2, 0)[3].transport() == "none"
