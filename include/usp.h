@@ -192,7 +192,9 @@ typedef enum {
  * of P doubles summed in rank order, so every rank takes the same stop
  * decision.  The transposes are fused into the stores of
  * the y-forward and z passes (each row goes straight to the buffer of the
- * rank that needs it: CUDA-IPC-mapped peer memory over NVLink, mapped at
+ * rank that needs it over NVLink: the peers' workspaces through an NCCL
+ * window -- ncclCommWindowRegister + ncclGetPeerPointer, when the workspaces
+ * come from usp_shared_alloc -- else CUDA-IPC mappings; resolved at
  * usp_plan_set_workspace, which is then collective), with a cross-rank
  * barrier after each; if any rank cannot map its peers (or P > 8, or
  * desc.separate_transposes) NCCL all-to-alls are used instead.  With nccl_comm, the arrays passed to
