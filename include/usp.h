@@ -170,7 +170,8 @@ typedef struct {
 #define USP_HOOK_WINDOW 2   /* one-rank communicator, workspace from usp_shared_alloc: register the
                                workspace as an NCCL window at usp_plan_set_workspace, write through
                                ncclGetPeerPointer's mapping and check the bytes through the plain
-                               pointer (the NEXT-1 transport's machinery on one GPU; tests only) */
+                               pointer, create the device communicator and run its LSA barrier
+                               (the NEXT-1 transport's machinery on one GPU; tests only) */
 
 /* How the slab decomposition's transposes move data (usp_transport). */
 typedef enum {

@@ -87,6 +87,9 @@ struct Nccl {
     ncclResult_t (*MemFree)(void *);
     ncclResult_t (*CommWindowRegister)(ncclComm_t, void *, size_t, ncclWindow_t *, int);
     ncclResult_t (*CommWindowDeregister)(ncclComm_t, ncclWindow_t);
+    bool devcomm = false;   // device communicators (LSA barrier)
+    ncclResult_t (*DevCommCreate)(ncclComm_t, const ncclDevCommRequirements_t *, ncclDevComm_t *);
+    ncclResult_t (*DevCommDestroy)(ncclComm_t, const ncclDevComm_t *);
 };
 
 Nccl &nccl_api() {
@@ -127,6 +130,9 @@ Nccl &nccl_api() {
     n.CommWindowRegister = (decltype(n.CommWindowRegister))dlsym(h, "ncclCommWindowRegister");
     n.CommWindowDeregister = (decltype(n.CommWindowDeregister))dlsym(h, "ncclCommWindowDeregister");
     n.win = n.MemAlloc && n.MemFree && n.CommWindowRegister && n.CommWindowDeregister;
+    n.DevCommCreate = (decltype(n.DevCommCreate))dlsym(h, "ncclDevCommCreate");
+    n.DevCommDestroy = (decltype(n.DevCommDestroy))dlsym(h, "ncclDevCommDestroy");
+    n.devcomm = n.DevCommCreate && n.DevCommDestroy;
     n.ok = all;
     if (!all) n.why = "libnccl.so.2 lacks an entry point";
     return n;
@@ -166,6 +172,15 @@ __global__ void k_win_peers(ncclWindow_t w, int P, void **out) {
     const int q = threadIdx.x;
     if (q < P) out[q] = ncclGetPeerPointer(w, 0, q);
 }
+// cross-rank barrier of the fused transposes over the LSA team (NVLink peers):
+// one CTA; acq_rel at system scope orders this rank's earlier peer stores
+// (performed by the preceding kernels, which end with a system fence) before
+// the peers' later reads, and theirs before ours
+__global__ void k_lsa_barrier(ncclDevComm dc) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
 // window self-test on a one-rank communicator: write through the window's
 // mapping, read through the plain pointer
 __global__ void k_win_write(float2 *dst, long long n) {
@@ -241,6 +256,10 @@ struct usp_plan_s {
     // peers' send / receive buffers through ncclGetPeerPointer (NEXT-1)
     ncclWindow_t win = nullptr;
     int transport = USP_TRANSPORT_NONE;
+    // device communicator with one LSA barrier: the cross-rank barrier after
+    // K_B / K_C (else an ncclAllReduce of one double)
+    ncclDevComm_t devcomm{};
+    bool lsa = false;
     // BiCGSTAB (caller-owned Krylov workspace: rhat, p, v, s, t)
     float2 *k_rh = nullptr, *k_p = nullptr, *k_v = nullptr, *k_s = nullptr, *k_t = nullptr;
     KState *ks = nullptr;
@@ -837,6 +856,10 @@ AddrRangeFn addr_range_fn() {
 void close_peers(usp_plan_s *p) {
     for (void *b : p->ipc_bases) cudaIpcCloseMemHandle(b);
     p->ipc_bases.clear();
+    if (p->lsa) {   // collective, like the creation
+        nccl_api().DevCommDestroy(p->comm, &p->devcomm);
+        p->lsa = false;
+    }
     if (p->win) {   // collective, like the registration
         nccl_api().CommWindowDeregister(p->comm, p->win);
         p->win = nullptr;
@@ -865,6 +888,27 @@ usp_status window_peers(usp_plan_s *p, char *base, size_t size, char **peer) {
     k_win_peers<<<1, 32, 0, p->stream>>>(p->win, p->P, d);
     CU(cudaGetLastError());
     return readback(p, peer, d, sizeof(void *) * p->P);
+}
+
+// device communicator with one LSA barrier (collective; p->lsa on success on
+// every rank, decided by consensus)
+usp_status setup_lsa(usp_plan_s *p) {
+    Nccl &n = nccl_api();
+    bool mine = false;
+    if (n.devcomm) {
+        ncclDevCommRequirements_t req{};
+        req.lsaBarrierCount = 1;
+        mine = n.DevCommCreate(p->comm, &req, &p->devcomm) == ncclSuccess;
+    }
+    bool all = false;
+    usp_status s = all_agree(p, mine, &all);
+    if (s) return s;
+    if (all) {
+        p->lsa = true;
+    } else if (mine) {
+        n.DevCommDestroy(p->comm, &p->devcomm);
+    }
+    return USP_OK;
 }
 
 // Map every rank's send / receive buffer for the fused transposes (collective
@@ -907,7 +951,7 @@ usp_status setup_peers(usp_plan_s *p) {
                 }
                 p->fused = true;
                 p->transport = USP_TRANSPORT_NCCL_WINDOW;
-                return USP_OK;
+                return setup_lsa(p);
             }
             close_peers(p);
         }
@@ -965,6 +1009,7 @@ usp_status setup_peers(usp_plan_s *p) {
     if (good == 1.0) {
         p->fused = true;
         p->transport = USP_TRANSPORT_CUDA_IPC;
+        return setup_lsa(p);
     } else {
         close_peers(p);
     }
@@ -976,6 +1021,11 @@ usp_status setup_peers(usp_plan_s *p) {
 usp_status rank_barrier(usp_plan_s *p) {
     if (!multi_rank(p)) return USP_OK;
     Tick t(p, KC_BARRIER, false);
+    if (p->lsa) {   // LSA barrier of the device communicator (NCCL 2.28 device API)
+        k_lsa_barrier<<<1, 32, 0, p->stream>>>(p->devcomm);
+        CU(cudaGetLastError());
+        return USP_OK;
+    }
     NC(nccl_api().AllReduce(p->coll + 3, p->coll + 3, 1, ncclDouble, ncclSum, p->comm, p->stream));
     return USP_OK;
 }
@@ -1651,6 +1701,12 @@ usp_status usp_plan_set_workspace(usp_plan_t p, void *dev, size_t bytes) {
         if ((s = readback(p, &nbad, bad, sizeof nbad))) return s;
         if (nbad) return fail(USP_ERR_NCCL, "window test: %u of %lld values differ", nbad, n);
         p->transport = USP_TRANSPORT_NCCL_WINDOW;
+        // and the device communicator's LSA barrier (one rank: returns at once)
+        if ((s = setup_lsa(p))) return s;
+        if (!p->lsa) return fail(USP_ERR_NCCL, "window test: ncclDevCommCreate failed");
+        k_lsa_barrier<<<1, 32, 0, p->stream>>>(p->devcomm);
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(p->stream));
     }
     if (p->P > 1 && !p->fused && p->nchunk > 1 && !p->xstream) {
         CU(cudaStreamCreateWithFlags(&p->xstream, cudaStreamNonBlocking));

@@ -50,9 +50,11 @@ def test_real_path_matches_oracle(orc, shape, n):
     p = make("C4", shape)
     x, nd, term, plan = _run(p, n)
     assert nd == n and term == "max_iter" and x.dtype == np.float32
-    # the real path's workspace: 3 float32 fields (+ s for the x-form, R-30) + the half spectrum
+    # the real path's workspace: 3 float32 fields (+ s for the x-form, R-30) + the half
+    # spectrum (twice with the z pass's plane-pair buffer)
     nz, ny, nx = shape
-    assert _ws_bytes(plan) < 4 * 4 * nz * ny * nx + 8 * nz * ny * (nx // 2 + 16) + 4096
+    spectra = 2 if plan.work_layout() == "z-pair" else 1
+    assert _ws_bytes(plan) < 4 * 4 * nz * ny * nx + spectra * 8 * nz * ny * (nx // 2 + 16) + 4096
     res, _ = run_oracle(orc, p, n_iter=n)
     assert np.abs(res.x.imag).max() <= 1e-12 * np.abs(res.x).max()
     err = rel_l2(x.astype(np.complex128), res.x)

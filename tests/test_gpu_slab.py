@@ -206,8 +206,9 @@ def test_nccl_window_machinery_one_rank():
     communicator plan comes from usp_shared_alloc (ncclMemAlloc), is
     registered as an NCCL 2.28 window (ncclCommWindowRegister), and values
     written through ncclGetPeerPointer's mapping of rank 0 read back through
-    the plain pointer (USP_HOOK_WINDOW); the solve on that memory is the
-    single-GPU one bit for bit."""
+    the plain pointer, and the device communicator's LSA barrier (the fused
+    transposes' cross-rank barrier) runs (USP_HOOK_WINDOW); the solve on that
+    memory is the single-GPU one bit for bit."""
     import os
 
     import torch
