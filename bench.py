@@ -16,8 +16,11 @@ on a bounded sample of the same workload on the host cores (this tier has no
 installable reference implementation; the oracle is the reference arm).
 
 Multi-GPU (torchrun, one process per GPU, N>1): C5 is split into N z-slabs
-(libusp's slab decomposition: NCCL all-to-all transposes around the z pass,
-rank-ordered residual all-gather) -- strong scaling, the total work fixed.
+(libusp's slab decomposition: the two transposes around the z pass fused
+into the K_B / K_C stores over NVLink -- an NCCL window, else CUDA IPC; NCCL
+all-to-all if neither maps -- with an LSA-barrier, rank-ordered residual
+all-gather; config.transposes says which ran) -- strong scaling, the total
+work fixed.
 Before timing, a closed-form check (constant V, 128^3) runs through the same
 communicator; if it fails, the run falls back to N independent replicas
 ("scaling": "weak") and says so.  --replicas forces the replica mode.
@@ -638,11 +641,14 @@ def run_usp(args, world, rank, local):
                                                    "during the next one's)",
                "serial_value": serial}
 
-    if rank != 0:
-        return 0
     z_pass_buffer, transport = plan.work_layout(), plan.transport()
+    # every rank destroys the plan here, in the same order: with the NCCL
+    # window transport the destruction is collective (window deregistration,
+    # device communicator)
     plan.close()   # the remaining measurements allocate their own plans
     del plan
+    if rank != 0:
+        return 0
     torch.cuda.empty_cache()
     solvers = None
     if world == 1 and not args.no_solvers and name == "C5":
