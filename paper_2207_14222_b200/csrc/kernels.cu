@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(LineGeo<N>::N1) k_solve1d(OneParams p) {
 // hypotheses checked pointwise: |V| < 1 and Re(w/c) >= 0 (accretive A for
 // D Re(c) >= 0, Eq. 1).
 __global__ void __launch_bounds__(256) k_potential(PotParams p) {
-    float vmax = 0.f;
+    double v2max = 0.0;   // max |V|^2 (one sqrt per thread at the end: sqrt is monotonic)
     unsigned nacc = 0, nnf = 0;
     const double cr = p.c_re, ci = p.c_im, inv_c2 = 1.0 / (cr * cr + ci * ci);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n;
@@ -244,17 +244,18 @@ __global__ void __launch_bounds__(256) k_potential(PotParams p) {
         const double ar = wr - p.sig_re, ai = wi - p.sig_im;
         // V = (w - sigma)/c = (w - sigma) conj(c) / |c|^2
         const double vr = (ar * cr + ai * ci) * inv_c2, vi = (ai * cr - ar * ci) * inv_c2;
-        const double av = sqrt(vr * vr + vi * vi);
+        const double av2 = vr * vr + vi * vi;
         if (!isfinite(vr) || !isfinite(vi)) ++nnf;
-        vmax = fmaxf(vmax, (float)av);
-        if (av >= 1.0) vmax = fmaxf(vmax, 1.0f);
-        // Re(w/c)
+        v2max = fmax(v2max, av2);
+        // Re(w/c) < -1e-6 |w/c|, without the square root
         const double wcr = (wr * cr + wi * ci) * inv_c2, wci = (wi * cr - wr * ci) * inv_c2;
-        if (!p.store_v && wcr < -1e-6 * sqrt(wcr * wcr + wci * wci)) ++nacc;
+        if (!p.store_v && wcr < 0.0 && wcr * wcr > 1e-12 * (wcr * wcr + wci * wci)) ++nacc;
         if (p.store_v) p.B[i] = make_float2((float)vr, (float)vi);
         else if (p.b_real) reinterpret_cast<float *>(p.B)[i] = (float)(1.0 - vr);
         else p.B[i] = make_float2((float)(1.0 - vr), (float)(-vi));
     }
+    float vmax = (float)sqrt(v2max);
+    if (v2max >= 1.0) vmax = fmaxf(vmax, 1.0f);
     // CTA reduce then one atomic each
     __shared__ float smax[8];
     __shared__ unsigned sacc[8], snf[8];
