@@ -209,7 +209,9 @@ usp_status usp_plan_create(const usp_plan_desc *desc, usp_plan_t *out);
 
 /* Bytes of device workspace the plan needs: 4 complex64 fields
  * (x, Delta, B, work) = 32 bytes per local voxel; 6 (+ send and receive
- * buffers of the transposes) = 48 bytes per local voxel when P > 1. */
+ * buffers of the transposes) = 48 bytes per local voxel when P > 1; + one
+ * more field for s on x-form plans (R-30) and for the z pass's plane-pair
+ * buffer (desc.flat_work; the real path: half-spectrum rows instead). */
 usp_status usp_plan_workspace_size(usp_plan_t plan, size_t *bytes);
 
 /* Attach caller-owned device memory (>= workspace_size bytes, 256-B aligned).
