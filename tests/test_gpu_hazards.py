@@ -35,7 +35,10 @@ CASES = [
     ("C5", (64, 64, 32), 8, 0.0, {"virtual_ranks": 2}),        # fused peer-store transposes
     ("C5", (64, 64, 32), 8, 0.0, {"virtual_ranks": 4, "separate_transposes": True}),
     ("C4", (64, 64, 64), 30, 0.0, {}),                         # real path across the form switch
-    ("C5", (1024, 64, 16), 3, 0.0, {}),                        # k_stile<1024> two-round exchange, TMA stores
+    ("C5", (1024, 64, 16), 3, 0.0, {}),                        # k_stile<1024> two-round exchange, TMA stores,
+                                                               # z pass on the plane-pair buffer
+    ("C5", (1024, 64, 16), 3, 0.0, {"flat_work": True}),       # the same z pass in place on work
+    ("C3", (128, 64, 256), 6, 0.0, {"delta_form": True}),      # plane-pair buffer, full exchange (N = 128)
     ("C5", (64, 1024, 1024), 4, 0.0, {"plane_chain": True}),   # plane-chained pass
     ("C5", (64, 64, 64), 5, 0.0, {"antisymmetric": True}),
     ("C5", (64, 64, 1024), 3, 0.0, {"antisymmetric": True}),  # k_anti_pipe<1024>, 3 stages
