@@ -48,7 +48,7 @@ namespace usp {
 // rows; the FFT, the multiplier and the exchange are unchanged.
 template <int N, int MODE, bool ZP = false>
 __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
-    k_stile(const __grid_constant__ CUtensorMap tmap, SParams p) {
+    k_stile(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap smap, SParams p) {
     using G = LineGeo<N>;
     using T = STile<N>;
     static_assert(!ZP || (MODE == S_FWD_MUL_INV && T::COLS == 16 && G::N1 % 2 == 0), "z-pair tiles: K_C, N <= 1024");
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
                 if (tl == 0) {
 #pragma unroll
                     for (int bx = 0; bx < SROWS / 2 / BP; ++bx)
-                        tma_store_2d(&tmap, (int)(t * 32), (N - SROWS) / 2 + bx * BP, xb + bx * BP * 32);
+                        tma_store_2d(&smap, (int)(t * 32), (N - SROWS) / 2 + bx * BP, xb + bx * BP * 32);
                     bulk_commit();
                 }
             } else {
@@ -277,8 +277,8 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
 #pragma unroll
                 for (int bx = 0; bx < SROWS / T::BOXN; ++bx) {
                     const int r0 = N - SROWS + bx * T::BOXN;
-                    if (p.map_rank == 3) tma_store_3d(&tmap, c0, r0, (int)o, xb + (r0 - (N - SROWS)) * T::COLS);
-                    else tma_store_2d(&tmap, c0, (int)o * N + r0, xb + (r0 - (N - SROWS)) * T::COLS);
+                    if (p.map_rank == 3) tma_store_3d(&smap, c0, r0, (int)o, xb + (r0 - (N - SROWS)) * T::COLS);
+                    else tma_store_2d(&smap, c0, (int)o * N + r0, xb + (r0 - (N - SROWS)) * T::COLS);
                 }
                 bulk_commit();
             }
@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(STile<N>::NT, STile<N>::MINB)
 
 // ========================================================= launchers ====
 template <int N, int MODE, bool ZP = false>
-static cudaError_t stile_t(const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
+static cudaError_t stile_t(const CUtensorMap &map, const CUtensorMap &smap, const SParams &p, int grid,
+                           cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
         cudaError_t e =
@@ -307,18 +308,19 @@ static cudaError_t stile_t(const CUtensorMap &map, const SParams &p, int grid, c
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    return launch_pdl(k_stile<N, MODE, ZP>, grid, STile<N>::NT, STile<N>::SMEM, s, map, p);
+    return launch_pdl(k_stile<N, MODE, ZP>, grid, STile<N>::NT, STile<N>::SMEM, s, map, smap, p);
 }
 
 template <int N>
-static cudaError_t stile_mode(SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
-    if (mode == S_FWD) return stile_t<N, S_FWD>(map, p, grid, s);
-    if (mode == S_INV) return stile_t<N, S_INV>(map, p, grid, s);
+static cudaError_t stile_mode(SMode mode, const CUtensorMap &map, const CUtensorMap &smap, const SParams &p, int grid,
+                              cudaStream_t s) {
+    if (mode == S_FWD) return stile_t<N, S_FWD>(map, smap, p, grid, s);
+    if (mode == S_INV) return stile_t<N, S_INV>(map, smap, p, grid, s);
     if (p.zpair) {
-        if constexpr (N <= 1024) return stile_t<N, S_FWD_MUL_INV, true>(map, p, grid, s);
+        if constexpr (N <= 1024) return stile_t<N, S_FWD_MUL_INV, true>(map, smap, p, grid, s);
         else return cudaErrorInvalidValue;
     }
-    return stile_t<N, S_FWD_MUL_INV>(map, p, grid, s);
+    return stile_t<N, S_FWD_MUL_INV>(map, smap, p, grid, s);
 }
 
 bool stile_supported(long long n) { return n >= 64 && n <= 2048 && (n & (n - 1)) == 0; }
@@ -336,14 +338,15 @@ int stile_ctas_per_sm(int N) {
     }
 }
 
-cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s) {
+cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const CUtensorMap &smap, const SParams &p, int grid,
+                         cudaStream_t s) {
     switch (N) {
-    case 64: return stile_mode<64>(mode, map, p, grid, s);
-    case 128: return stile_mode<128>(mode, map, p, grid, s);
-    case 256: return stile_mode<256>(mode, map, p, grid, s);
-    case 512: return stile_mode<512>(mode, map, p, grid, s);
-    case 1024: return stile_mode<1024>(mode, map, p, grid, s);
-    case 2048: return stile_mode<2048>(mode, map, p, grid, s);
+    case 64: return stile_mode<64>(mode, map, smap, p, grid, s);
+    case 128: return stile_mode<128>(mode, map, smap, p, grid, s);
+    case 256: return stile_mode<256>(mode, map, smap, p, grid, s);
+    case 512: return stile_mode<512>(mode, map, smap, p, grid, s);
+    case 1024: return stile_mode<1024>(mode, map, smap, p, grid, s);
+    case 2048: return stile_mode<2048>(mode, map, smap, p, grid, s);
     default: return cudaErrorInvalidValue;
     }
 }

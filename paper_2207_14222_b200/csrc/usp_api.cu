@@ -758,7 +758,7 @@ usp_status sparse_add(usp_plan_s *p) {
 SParams sparams(usp_plan_s *p, float2 *data, float2 *dst, const float2 *tw, long long stride, long long ncols,
                 long long nouter, long long ostride, int line_axis, int check_state, int map_rank);
 usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, const SParams &sp, const CUtensorMap &map,
-                       bool use_stile, int grid_short);
+                       bool use_stile, int grid_short, const CUtensorMap *smap = nullptr);
 
 // plane-chained schedule: K_C over the volume (z forward, g(p), z inverse),
 // then the persistent K_D -> K_A -> K_B kernel (kernels_plane.cu)
@@ -796,17 +796,18 @@ usp_status plane_iteration(usp_plan_s *p) {
 }
 
 usp_status run_strided(usp_plan_s *p, int cls, int n, SMode mode, const SParams &sp, const CUtensorMap &map,
-                       bool use_stile, int grid_short) {
+                       bool use_stile, int grid_short, const CUtensorMap *smap) {
     Tick t(p, cls);
     if (use_stile) {
-        // half-tile tensor-map stores where the load map describes the
-        // destination (in place, natural layout), in the z pass only (K_C
-        // 4.59 -> 4.48 ms at 1024^3; the y passes measured slower with them,
-        // 2.69 -> 2.94 ms)
+        // half-tile tensor-map stores (the upper half of each tile through the
+        // exchange buffer) where a map describes the destination (the load map of
+        // an in-place pass, or smap), in the z pass and the y-inverse pass: K_C
+        // 4.59 -> 4.48 ms, K_D 2.90 -> 2.70 ms at 1024^3; the y-forward pass
+        // measured slower with them (2.69 -> 2.94 ms)
         SParams q = sp;
-        q.tma_store = mode == S_FWD_MUL_INV && sp.dst == sp.data && (sp.map_rank == 2 || sp.map_rank == 3) &&
-                      !sp.peer_mode && !sp.send_layout;
-        CU(launch_stile(n, mode, map, q, cls == KC_ZMUL ? p->grids_z : p->grids_y, p->stream));
+        q.tma_store = (mode == S_FWD_MUL_INV || mode == S_INV) && (sp.dst == sp.data || smap) &&
+                      (sp.map_rank == 2 || sp.map_rank == 3) && !sp.peer_mode && !sp.send_layout;
+        CU(launch_stile(n, mode, map, smap ? *smap : map, q, cls == KC_ZMUL ? p->grids_z : p->grids_y, p->stream));
         return USP_OK;
     }
     // register-staged passes for the short lines (N = 16, 32) the TMA tiles do not take
@@ -1257,7 +1258,7 @@ usp_status chain_mid(usp_plan_s *p, int check_state) {
             yd.pair_src = 1;
             if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yb, p->smap_y, true, 0))) return s;
             if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zp, p->smap_z, true, 0))) return s;
-            return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_yp, true, 0);
+            return run_strided(p, KC_YINV, (int)p->ny, S_INV, yd, p->smap_yp, true, 0, &p->smap_y);
         }
         if ((s = run_strided(p, KC_YFWD, (int)p->ny, S_FWD, yf, p->smap_y, p->stile_y, p->grid_y))) return s;
         if ((s = run_strided(p, KC_ZMUL, (int)p->nz, S_FWD_MUL_INV, zm, p->smap_z, p->stile_z, p->grid_z))) return s;

@@ -354,7 +354,10 @@ cudaError_t launch_xpass_pipe(int N, XMode mode, const XParams &p, int grid, cud
                               bool expect_x = false);
 
 // TMA-prefetched 16-column strided passes (kernels_stile.cu)
-cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const SParams &p, int grid, cudaStream_t s);
+// smap: the map the half-tile tensor-map stores (SParams::tma_store) write through
+// (the load map for in-place passes)
+cudaError_t launch_stile(int N, SMode mode, const CUtensorMap &map, const CUtensorMap &smap, const SParams &p, int grid,
+                         cudaStream_t s);
 bool stile_supported(long long n);
 int stile_cols(int N);
 int stile_box(int N);

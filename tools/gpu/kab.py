@@ -29,7 +29,9 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--config", default="C5")
     ap.add_argument("--nz", type=int, default=None, help="planes (default: --size)")
+    ap.add_argument("--opts", default="", help="plan options for every variant, e.g. flat_work=1,delta_form=1")
     args = ap.parse_args()
+    popts = {k: int(v) for k, v in (o.split("=", 1) for o in args.opts.split(",") if o)}
     import torch
 
     from paper_2207_14222_b200 import _lib as L
@@ -59,7 +61,7 @@ def main():
         for key, val in env.items():
             os.environ[key] = val
         with torch.cuda.stream(stream):
-            plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev,
+            plan = Plan(p.shape, kind=p.kind, h=p.h, D=p.D, stream=stream, device=dev, **popts,
                         dtype="r32" if real else "c64")
         plan.set_potential(med, 0.95)
         plan.set_source(src)
