@@ -94,9 +94,9 @@ def main():
             eb.record(stream)
             torch.cuda.synchronize()
             res[v].setdefault("iter_ms", []).append(ea.elapsed_time(eb) / args.iters)
-            for name, (ms, cnt) in prof.items():
+            for name, (ms, cnt) in prof.items():   # ms per iteration (see opt_ab.py)
                 if cnt:
-                    res[v].setdefault(name, []).append(ms / cnt)
+                    res[v].setdefault(name, []).append(ms / args.iters)
     for v in res:
         out = {k: round(statistics.median(x), 4) for k, x in res[v].items()}
         out["iter_ms_all"] = [round(x, 3) for x in res[v]["iter_ms"]]

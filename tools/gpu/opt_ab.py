@@ -5,8 +5,8 @@
 Each variant is NAME:opt=val,opt=val (Plan keyword arguments); every variant
 gets its own plan and workspace on the same inputs, variants run round-robin
 `--rounds` times so clock / power-cap drift hits them alike, and per-kernel
-device times (usp_profile_read) and the iteration time are reported as
-medians over rounds, one JSON line per variant.
+device times per iteration (usp_profile_read) and the iteration time are
+reported as medians over rounds, one JSON line per variant.
 """
 import argparse
 import json
@@ -71,9 +71,12 @@ def main():
             eb.record(stream)
             torch.cuda.synchronize()
             res[name]["iter_ms"].append(ea.elapsed_time(eb) / args.iters)
+            # ms per ITERATION (an x-form plan launches one spare chain + x pass
+            # per iterate() call that skips itself: per-launch averages would
+            # read ~1/iters low)
             for k, (ms, n) in plan.profile_read().items():
                 if n:
-                    res[name].setdefault(k, []).append(ms / n)
+                    res[name].setdefault(k, []).append(ms / args.iters)
             plan.profile(False)
     for name, kw, plan in plans:
         out = {"variant": name, "options": kw, "work_layout": plan.work_layout(), "config": args.config,
