@@ -97,3 +97,46 @@ def test_desc_binding_matches_header():
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     names = re.findall(r"\b([A-Za-z_0-9]+)(?:\[\d\])?;", body)
     assert names == [f[0] for f in _lib.PlanDesc._fields_]
+
+
+C_CLIENT = r"""
+#include <stdio.h>
+#include <string.h>
+#include "usp.h"
+int main(void) {
+    usp_plan_desc d;
+    memset(&d, 0, sizeof d);
+    d.ndim = 3; d.n[0] = 64; d.n[1] = 64; d.n[2] = 100;   /* 100: not a power of two */
+    d.h[0] = d.h[1] = d.h[2] = 1.0; d.D = 1.0;
+    usp_plan_t p = 0;
+    usp_status s = usp_plan_create(&d, &p);
+    char msg[512];
+    strncpy(msg, usp_last_error(), sizeof msg - 1);
+    msg[sizeof msg - 1] = 0;
+    int kind = -1;
+    usp_status s2 = usp_transport(0, &kind);                /* NULL plan: an error status */
+    printf("%s|%d|%d|%s\n", usp_version(), (int)s, (int)s2, msg);
+    return (s == USP_ERR_UNSUPPORTED && p == 0 && s2 == USP_ERR_ARG) ? 0 : 1;
+}
+"""
+
+
+def test_plain_c_client(lib, tmp_path):
+    """The boundary is C: include/usp.h compiles as C99 and a C program
+    linked against libusp.so gets validation errors as statuses (no GPU)."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "client.c"
+    src.write_text(C_CLIENT)
+    exe = tmp_path / "client"
+    libdir = os.path.join(ROOT, "paper_2207_14222_b200")
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src), "-L", libdir,
+                    "-lusp", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    version, status, status2, msg = r.stdout.strip().split("|", 3)
+    assert version.startswith("0.4") and int(status) == 5 and int(status2) == 1 and "power of two" in msg
