@@ -189,7 +189,7 @@ def ncu_traffic(workload):
 
 
 # ----------------------------------------------------------------- oracle --
-def cpu_oracle_sample(shape=(256, 256, 256), iters=2):
+def cpu_oracle_sample(shape=(256, 256, 256), iters=40):
     """The oracle as it stands (x-form Alg. 1, c128) on a bounded sample of the
     C5 recipe; returns (vox-it/s, seconds, threads, description)."""
     from oracle import oracle as O
@@ -209,13 +209,30 @@ def cpu_oracle_sample(shape=(256, 256, 256), iters=2):
         f"(lambda=8, GRF ell=4, seed 3), {iters} iterations incl. its setup FFT round trip")
 
 
+REF_SAMPLE_ITERS = 10   # iterations of Alg. 1 per reference-arm step (256^3 sample)
+
+
+def c5_workload(n_iter=100, shape=(1024, 1024, 1024)):
+    """The usp arm's config.workload string for the default (C5, complex64) bench."""
+    return (f"C5 3-D Helmholtz {shape[2]}x{shape[1]}x{shape[0]} complex64, "
+            f"{n_iter} iterations of Alg. 1 per step (setup + iterations), alpha=0.75")
+
+
 def run_reference(args, world, rank):
+    """The reference arm: the CPU oracle as it stands on the box's host cores,
+    on the usp arm's config / metric / unit; each step is a bounded sample of
+    that workload (the C5 recipe at 256^3, setup + REF_SAMPLE_ITERS iterations
+    of Alg. 1), stated in config.sample and cpu_baseline.sample."""
     if rank != 0:
         return 0
-    cfg = {"workload": "C5 recipe sample for the CPU oracle", "grid": [256, 256, 256], "iterations_per_step": 1}
     from oracle import oracle as O
     from synth import make
 
+    n_it = REF_SAMPLE_ITERS
+    sample = (f"each step: the C5 recipe at 256^3 (lambda=8, GRF ell=4, seed 3), setup (n0 FFT round trip) + "
+              f"{n_it} iterations of Alg. 1 (x-form, complex128) on the host cores")
+    cfg = {"workload": c5_workload(), "grid": [1024, 1024, 1024], "iterations_per_step": 100,
+           "sample": sample, "sample_grid": [256, 256, 256], "sample_iterations_per_step": n_it}
     O.build()
     p = make("C5", (256, 256, 256))
     med = p.medium.astype("complex64").astype("complex128")
@@ -224,20 +241,20 @@ def run_reference(args, world, rank):
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        O.fixed_point(w, p.source, p.h, sp.D, sp.sigma, sp.c, 0.75, 0.0, 1)
+        O.fixed_point(w, p.source, p.h, sp.D, sp.sigma, sp.c, 0.75, 0.0, n_it)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
     tot = sum(times)
-    # one oracle call = setup round trip + 1 iteration = 2 applications of (L+1)^-1
-    value = p.n_vox * args.steps / tot
+    # like the usp arm: voxel-iterations advanced / time of setup + iterations
+    value = p.n_vox * n_it * args.steps / tot
+    model, nproc = host_cpu()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
-                             "sample": "1 iteration of Alg. 1 (x-form, complex128) incl. the n0 setup FFT round "
-                                       "trip on the C5 recipe at 256^3 per step"},
+                             "sample": sample, "seconds": round(tot, 2), "cpu_model": model, "nproc": nproc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
