@@ -189,7 +189,7 @@ def ncu_traffic(workload):
 
 
 # ----------------------------------------------------------------- oracle --
-def cpu_oracle_sample(shape=(256, 256, 256), iters=40):
+def cpu_oracle_sample(shape=(256, 256, 256), iters=100):
     """The oracle as it stands (x-form Alg. 1, c128) on a bounded sample of the
     C5 recipe; returns (vox-it/s, seconds, threads, description)."""
     from oracle import oracle as O
